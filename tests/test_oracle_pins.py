@@ -1,0 +1,467 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (SURVEY.md §8(c)
+"What pins each part").  CPU only, no GPU.
+
+P1 linearity, P2 injective-hash exactness, P3 unbiasedness, P4 paper worked values,
+P5 brute-force contraction, P6 fold identity, P7 hash statistics, P8 filter,
+P9 greedy hand traces, P10 C1 estimate vs exact join; plus the exact big-integer
+arithmetic against Python ints and published mixer test vectors.
+"""
+import json
+import math
+import os
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import K_MAT, K_MERGED, K_VEC, POINT, RANGE, SUBSET
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = json.load(open(os.path.join(HERE, "golden", "paper_pins.json")))
+P61 = (1 << 61) - 1
+
+
+# ---------------------------------------------------------------- P4 / published vectors
+def test_mixers_published_vectors():
+    L = oracle.lib()
+    assert L.or_splitmix64(0) == int(GOLD["splitmix64_first_output_seed0"]["expect"], 16)
+    for case in GOLD["fnv1a64"]:
+        assert L.or_fnv1a64(case["input"].encode()) == int(case["expect"], 16)
+
+
+@pytest.mark.parametrize("case", GOLD["merge_minabs"])
+def test_merge_rule_paper_values(case):
+    """PAPER.md:238, evaluated by the C oracle's merged-tensor path (brute + message passing)."""
+    a, b = case["values"]
+    tens = [(K_MERGED, [0, 1], [np.array([a]), np.array([b])]),
+            (K_VEC, [0], [np.array([1])]), (K_VEC, [1], [np.array([1])])]
+    assert oracle.contract_row(tens, [1, 1], brute=True) == case["expect"]
+    assert oracle.contract_row(tens, [1, 1]) == case["expect"]
+    assert oracle.merge_entry([a, b]) == case["expect"]
+
+
+def test_merge_tie_keeps_left():
+    """ties keep the left (earliest) constituent."""
+    tens = [(K_MERGED, [0, 1], [np.array([2]), np.array([-2])]),
+            (K_VEC, [0], [np.array([1])]), (K_VEC, [1], [np.array([1])])]
+    assert oracle.contract_row(tens, [1, 1], brute=True) == 2
+
+
+def test_l1_paper_example():
+    g = GOLD["l1_permutation"]
+    assert oracle.permutation_l1(g["estimates"], g["truths"]) == g["expect"]
+    assert oracle.permutation_l1([1, 2, 3], [1, 2, 3]) == 0
+    assert oracle.permutation_l1([3, 2, 1], [1, 2, 3]) == 4
+
+
+# ---------------------------------------------------------------- exact arithmetic
+def test_bignum_exact_vs_python_int():
+    L = oracle.lib()
+    rng = random.Random(7)
+    import ctypes
+    for trial in range(200):
+        n = rng.randint(1, 40)
+        xs = [rng.choice([rng.randint(-(1 << 63), (1 << 63) - 1), rng.randint(-9, 9), -(1 << 63)]) for _ in range(n)]
+        ys = [rng.randint(-(1 << 63), (1 << 63) - 1) for _ in range(n)]
+        a = np.array(xs, dtype=np.int64)
+        b = np.array(ys, dtype=np.int64)
+        buf = ctypes.create_string_buffer(256)
+        rc = L.or_bn_selftest_mul_add(n, a.ctypes.data, b.ctypes.data, buf, 256)
+        assert rc >= 0
+        assert int(buf.value.decode()) == sum(x * y * x for x, y in zip(xs, ys))
+
+
+def test_bignum_to_double_correctly_rounded():
+    L = oracle.lib()
+    rng = random.Random(11)
+    cases = [[(1 << 53) + 1, 1 << 20], [(1 << 53) + 3, 1 << 30], [-(1 << 53) - 1, 3], [(1 << 62) + 1, (1 << 62) + 1],
+             [-(1 << 63), -(1 << 63), -(1 << 63)], [0, 5], [1], [-1], [(1 << 54) - 1]]
+    for _ in range(300):
+        cases.append([rng.randint(-(1 << 63), (1 << 63) - 1) for _ in range(rng.randint(1, 7))])
+    for xs in cases:
+        a = np.array(xs, dtype=np.int64)
+        prod = 1
+        for x in xs:
+            prod *= x
+        assert L.or_bn_selftest_to_double(len(xs), a.ctypes.data) == float(prod)
+        assert L.or_dec_to_double(str(prod).encode()) == float(prod)
+
+
+def test_field_arithmetic_implementation():
+    """Implementation check (not a method pin): mod-p polynomial evaluation vs Python ints."""
+    for key in [0, 1, -1, 2**31 - 1, -2**31, 2**63 - 1, -2**63, P61, P61 + 5, 123456789]:
+        assert oracle.canon(key) == (key % (1 << 64)) % P61
+    for r in range(3):
+        e = "A.x|B.y"
+        a = [oracle.coef(42, e, r, 0, i) for i in range(4)]
+        b = [oracle.coef(42, e, r, 1, i) for i in range(2)]
+        assert all(0 <= c < P61 for c in a + b)
+        for key in [0, 5, -7, 10**12, 2**40 + 3]:
+            x = (key % (1 << 64)) % P61
+            v = (((a[3] * x + a[2]) * x + a[1]) * x + a[0]) % P61
+            assert oracle.xi(42, e, r, key) == (1 if v & 1 else -1)
+            assert oracle.bucket(42, e, r, key, 1024) == ((b[1] * x + b[0]) % P61) % 1024
+
+
+def test_seed_symmetry_and_distinctness():
+    """Both endpoints of an edge see identical seeds; 10^4 (edge,row) pairs have no duplicates."""
+    seen = set()
+    for e in range(100):
+        for r in range(100):
+            t = tuple(oracle.coef(42, f"E{e}.a|F{e}.b", r, role, i) for role, n in ((0, 4), (1, 2)) for i in range(n))
+            assert t not in seen
+            seen.add(t)
+    assert oracle.coef(42, "x|y", 3, 0, 1) == oracle.coef(42, "x|y", 3, 0, 1)
+
+
+# ---------------------------------------------------------------- P7 hash statistics
+def test_xi_sign_balance():
+    keys = np.arange(100_000, dtype=np.int64)
+    sk = oracle.build([keys], None, 9, [1], ["K.id|MK.kid"])      # w = 1 -> row sum = sum_k xi_r(k)
+    means = sk[:, 0] / len(keys)
+    assert np.all(np.abs(means) < 0.02), means
+
+
+def test_xi_four_wise_products():
+    rng = random.Random(3)
+    tuples = []
+    while len(tuples) < 200:
+        t = rng.sample(range(10**6), 4)
+        tuples.append(t)
+    tot4 = tot2 = 0
+    n = 0
+    for s in range(500):
+        for (a, b, c, d) in tuples:
+            xa, xb, xc, xd = (oracle.xi(1000 + s, "e|f", 0, k) for k in (a, b, c, d))
+            tot4 += xa * xb * xc * xd
+            tot2 += xa * xb
+            n += 1
+    assert abs(tot4 / n) < 0.02 and abs(tot2 / n) < 0.02
+
+
+def test_bucket_chi_square():
+    from scipy.stats import chi2
+    keys = range(100_000)
+    for r in range(2):
+        counts = np.zeros(1024, dtype=np.int64)
+        for k in keys:
+            counts[oracle.bucket(42, "R.key|S.key", r, k, 1024)] += 1
+        exp = len(keys) / 1024
+        stat = float(((counts - exp) ** 2 / exp).sum())
+        assert stat < chi2.ppf(0.999, 1023), stat
+
+
+# ---------------------------------------------------------------- P8 filter
+def test_filter_brute_force_and_prefiltered_build():
+    rng = np.random.default_rng(5)
+    n = 20_000
+    cols = {"a": rng.integers(0, 100, n).astype(np.int32), "b": rng.integers(-50, 50, n).astype(np.int64),
+            "c": rng.integers(0, 1000, n).astype(np.int32), "k": rng.integers(0, 500, n).astype(np.int64)}
+    S = [3, 7, 999, 500, 11]
+    preds = [("a", RANGE, 10, 59), ("b", RANGE, oracle.INT64_MIN, 20), ("c", SUBSET, 0, 0, None)]
+    preds[2] = ("c", SUBSET, 0, 0, S + list(range(100, 400)))
+    mask, cnt = oracle.filter_mask(cols, preds)
+    ref = (cols["a"] >= 10) & (cols["a"] <= 59) & (cols["b"] <= 20) & np.isin(cols["c"], S + list(range(100, 400)))
+    assert cnt == int(ref.sum()) and np.array_equal(mask.astype(bool), ref)
+    m2, c2 = oracle.filter_mask(cols, [("a", POINT, 42, 42, None)])
+    assert c2 == int((cols["a"] == 42).sum())
+    m3, c3 = oracle.filter_mask(cols, [])
+    assert c3 == n
+    m4, c4 = oracle.filter_mask(cols, [("c", SUBSET, 0, 0, [])])
+    assert c4 == 0
+    sk1 = oracle.build([cols["k"]], mask, 5, [64], ["F.k|G.k"])
+    sk2 = oracle.build([cols["k"][ref]], None, 5, [64], ["F.k|G.k"])
+    assert np.array_equal(sk1, sk2)
+    mk1 = oracle.build([cols["k"], cols["a"]], mask, 3, [16, 32], ["F.k|G.k", "F.a|H.a"])
+    mk2 = oracle.build([cols["k"][ref], cols["a"][ref]], None, 3, [16, 32], ["F.k|G.k", "F.a|H.a"])
+    assert np.array_equal(mk1, mk2)
+
+
+# ---------------------------------------------------------------- P1 linearity, P6 fold
+def test_linearity_random_shards():
+    rng = np.random.default_rng(9)
+    for trial in range(30):
+        n = int(rng.integers(1, 3000))
+        k0 = rng.integers(-10**9, 10**9, n).astype(np.int64)
+        k1 = rng.integers(0, 1000, n).astype(np.int32)
+        full = oracle.build([k0], None, 3, [128], ["a|b"])
+        fullm = oracle.build([k0, k1], None, 3, [16, 8], ["a|b", "c|d"])
+        G = int(rng.integers(1, 9))
+        cuts = np.sort(rng.integers(0, n + 1, G - 1))
+        parts = np.split(np.arange(n), cuts)
+        acc = np.zeros_like(full)
+        accm = np.zeros_like(fullm)
+        for p in parts:
+            oracle.build([k0[p]], None, 3, [128], ["a|b"], out=acc)
+            oracle.build([k0[p], k1[p]], None, 3, [16, 8], ["a|b", "c|d"], out=accm)
+        assert np.array_equal(acc, full) and np.array_equal(accm, fullm)
+        # each tuple moves exactly one counter per row by +-1
+        assert np.all(np.abs(full).sum(axis=1) <= n) and np.all(full.sum(axis=1) % 2 == n % 2)
+
+
+def test_fold_identity():
+    rng = np.random.default_rng(10)
+    for trial in range(10):
+        keys = rng.integers(0, 10**6, 5000).astype(np.int32)
+        b1024 = oracle.build([keys], None, 5, [1024], ["x|y"])
+        for wn in (512, 256, 64):
+            assert np.array_equal(oracle.fold(b1024, wn), oracle.build([keys], None, 5, [wn], ["x|y"]))
+        k2 = rng.integers(0, 10**6, 5000).astype(np.int32)
+        m = oracle.build([keys, k2], None, 3, [64, 32], ["x|y", "z|z2"])
+        m2 = oracle.build([keys, k2], None, 3, [16, 8], ["x|y", "z|z2"])
+        assert np.array_equal(oracle.fold(oracle.fold(m, 16, axis=1), 8, axis=2), m2)
+
+
+# ---------------------------------------------------------------- P2 exactness
+def _injective_seed(keys, edges_widths, d, start=42):
+    s = start
+    while True:
+        ok = True
+        for e, w in edges_widths:
+            for r in range(d):
+                if len({oracle.bucket(s, e, r, k, w) for k in keys}) != len(keys):
+                    ok = False
+                    break
+            if not ok:
+                break
+        if ok:
+            return s
+        s += 1
+
+
+def test_single_key_exactness():
+    """one key, frequencies fA, fB -> every row equals fA*fB."""
+    for fa in range(1, 21, 3):
+        for fb in range(1, 21, 4):
+            A = oracle.build([np.full(fa, 77, dtype=np.int64)], None, 5, [1024], ["A.k|B.k"])
+            B = oracle.build([np.full(fb, 77, dtype=np.int32)], None, 5, [1024], ["A.k|B.k"])
+            assert all(oracle.two_way_row(A[r], B[r]) == fa * fb for r in range(5))
+
+
+def test_injective_hash_two_way_and_chain_exact():
+    """North-star pin 2 / SURVEY P2: injective h on a tiny domain -> every row exact."""
+    rng = np.random.default_rng(12)
+    keys = list(range(100, 108))
+    e1, e2 = "A.k|B.k", "B.l|C.l"
+    d = 3
+    seed = _injective_seed(keys, [(e1, 1024), (e1, 64), (e2, 1024), (e2, 64)], d)
+    fA = rng.integers(0, 6, 8)
+    fC = rng.integers(0, 6, 8)
+    fB = rng.integers(0, 4, (8, 8))
+    kA = np.repeat(keys, fA).astype(np.int64)
+    kC = np.repeat(keys, fC).astype(np.int32)
+    pairs = [(keys[i], keys[j]) for i in range(8) for j in range(8) for _ in range(fB[i, j])]
+    kB1 = np.array([p[0] for p in pairs], dtype=np.int32)
+    kB2 = np.array([p[1] for p in pairs], dtype=np.int64)
+    A = oracle.build([kA], None, d, [1024], [e1], master=seed)
+    B1 = oracle.build([kB1], None, d, [1024], [e1], master=seed)
+    B2 = oracle.build([kB2], None, d, [1024], [e2], master=seed)
+    C = oracle.build([kC], None, d, [1024], [e2], master=seed)
+    M = oracle.build([kB1, kB2], None, d, [64, 64], [e1, e2], master=seed)
+    g = oracle.Graph({"A": len(kA), "B": len(kB1), "C": len(kC)}, [(e1, "A", "B"), (e2, "B", "C")],
+                     {("A", e1): A, ("B", e1): B1, ("B", e2): B2, ("C", e2): C}, {("B", (e1, e2)): M})
+    ab = oracle.estimate_rows(g, ("A", "B"))
+    assert ab == [int((fA * fB.sum(axis=1)).sum())] * d
+    abc = oracle.estimate_rows(g, ("A", "B", "C"))
+    assert abc == [int(fA @ fB @ fC)] * d
+    for r in range(d):   # message passing == literal definition on the chain
+        assert oracle.estimate_rows(g, ("A", "B", "C"), brute=False, rows=[r]) == [abc[r]]
+
+
+# ---------------------------------------------------------------- P3 unbiasedness
+def _mean_se(vals):
+    v = np.array(vals, dtype=np.float64)
+    return v.mean(), v.std(ddof=1) / math.sqrt(len(v))
+
+
+def test_two_way_unbiased():
+    rng = np.random.default_rng(21)
+    p = 1.0 / np.arange(1, 13) ** 1.1
+    p /= p.sum()
+    kA = rng.choice(12, 60, p=p).astype(np.int64)
+    kB = rng.choice(12, 60, p=p).astype(np.int64)
+    J = int((np.bincount(kA, minlength=12) * np.bincount(kB, minlength=12)).sum())
+    ests = []
+    for s in range(2000):
+        A = oracle.build([kA], None, 1, [4], ["A.k|B.k"], master=5000 + s)
+        B = oracle.build([kB], None, 1, [4], ["A.k|B.k"], master=5000 + s)
+        ests.append(oracle.two_way_row(A[0], B[0]))
+    m, se = _mean_se(ests)
+    assert abs(m - J) < 4 * se, (m, J, se)
+
+
+def test_partitioned_chain_unbiased():
+    rng = np.random.default_rng(22)
+    kA = rng.integers(0, 6, 40).astype(np.int64)
+    kB1 = rng.integers(0, 6, 40).astype(np.int64)
+    kB2 = rng.integers(0, 6, 40).astype(np.int64)
+    kC = rng.integers(0, 6, 40).astype(np.int64)
+    fA, fC = np.bincount(kA, minlength=6), np.bincount(kC, minlength=6)
+    fB = np.zeros((6, 6), dtype=np.int64)
+    np.add.at(fB, (kB1, kB2), 1)
+    J = int(fA @ fB @ fC)
+    e1, e2 = "A.k|B.k", "B.l|C.l"
+    ests = []
+    for s in range(2000):
+        A = oracle.build([kA], None, 1, [4], [e1], master=9000 + s)
+        C = oracle.build([kC], None, 1, [4], [e2], master=9000 + s)
+        M = oracle.build([kB1, kB2], None, 1, [4, 4], [e1, e2], master=9000 + s)
+        ests.append(int(A[0] @ M[0] @ C[0]))
+    m, se = _mean_se(ests)
+    assert abs(m - J) < 4 * se, (m, J, se)
+
+
+# ---------------------------------------------------------------- P5 contraction vs literal definition
+def _random_network(rng, topo, w, vmax=3):
+    """topo: list of edges (u, v) over tables 0..T-1 (canonical order = list order)."""
+    T = 1 + max(max(e) for e in topo)
+    widths = [int(rng.integers(1, w + 1)) for _ in topo]
+    tens = []
+    for t in range(T):
+        inc = [i for i, e in enumerate(topo) if t in e]
+        if len(inc) == 1:
+            tens.append((K_VEC, inc, [rng.integers(-vmax, vmax + 1, widths[inc[0]])]))
+        elif len(inc) == 2 and rng.random() < 0.4:
+            tens.append((K_MAT, inc, [rng.integers(-vmax, vmax + 1, widths[inc[0]] * widths[inc[1]])]))
+        else:
+            tens.append((K_MERGED, inc, [rng.integers(-vmax, vmax + 1, widths[e]) for e in inc]))
+    return tens, widths
+
+
+TOPOLOGIES = [
+    [(0, 1)],
+    [(0, 1), (1, 2)],
+    [(0, 1), (1, 2), (2, 3)],
+    [(0, 1), (1, 2), (0, 2)],                          # triangle
+    [(0, 1), (1, 2), (2, 0), (2, 3)],                  # triangle + tail
+    [(1, 0), (0, 2), (1, 2), (2, 3), (1, 4)],          # C3 shape (triangle 0-1-2, leaves 3, 4)
+    [(0, 1), (0, 2), (0, 3)],                          # star: 3-leg merged node
+    [(0, 1), (1, 2), (2, 3), (3, 0)],                  # 4-cycle
+    [(2, 1), (0, 1), (3, 1), (2, 0)],                  # triangle with 3-leg node + leaf
+]
+
+
+def test_message_passing_equals_literal_definition():
+    rng = np.random.default_rng(31)
+    for trial in range(400):
+        topo = TOPOLOGIES[trial % len(TOPOLOGIES)]
+        tens, widths = _random_network(rng, topo, 4)
+        assert oracle.contract_row(tens, widths) == oracle.contract_row(tens, widths, brute=True), (trial, topo)
+
+
+def _c3_graph(rng, w, d=3, vmax=3):
+    import datagen
+    ws = datagen.c3(scale=1e-4, w=w, d=d)
+    vec = {(s.table, s.edge_ids[0]): rng.integers(-vmax, vmax + 1, (d, w)).astype(np.int64) for s in ws.sketches}
+    return oracle.Graph({t.name: int(rng.integers(1, 50)) for t in ws.tables}, ws.edges, vec)
+
+
+def test_c3_subplans_all_14_equal_literal_definition():
+    """The C3 recipe with its canonical edge order: every connected sub-plan."""
+    rng = np.random.default_rng(41)
+    for trial in range(4):
+        g = _c3_graph(rng, w=3)
+        subs = oracle.connected_subplans(g)
+        assert len(subs) == 14
+        for s in subs:
+            assert oracle.estimate_rows(g, s) == oracle.estimate_rows(g, s, brute=True), s
+
+
+def test_merged_one_edge_equals_two_way():
+    """merged_estimate on one edge == fa_two_way_estimate."""
+    rng = np.random.default_rng(42)
+    g = _c3_graph(rng, w=64)
+    for s in [("K", "MK"), ("CI", "N"), ("MK", "T")]:
+        e = g.induced(s)[0][0]
+        a, b = s
+        assert oracle.estimate_rows(g, s) == [oracle.two_way_row(g.vec[(a, e)][r], g.vec[(b, e)][r]) for r in range(g.d)]
+
+
+def test_c5_cycle_small_equals_literal():
+    import datagen
+    rng = np.random.default_rng(43)
+    ws = datagen.c5(scale=1e-6, cycle=True, w=4, wm=2, d=1, n_tables=4)
+    vec, mat = {}, {}
+    for s in ws.sketches:
+        if len(s.key_cols) == 1:
+            vec[(s.table, s.edge_ids[0])] = rng.integers(-3, 4, (1, 4)).astype(np.int64)
+        else:
+            mat[(s.table, tuple(s.edge_ids))] = rng.integers(-3, 4, (1, 2, 2)).astype(np.int64)
+    g = oracle.Graph({t.name: 5 for t in ws.tables}, ws.edges, vec, mat)
+    for s in oracle.connected_subplans(g):
+        assert oracle.estimate_rows(g, s) == oracle.estimate_rows(g, s, brute=True), s
+
+
+# ---------------------------------------------------------------- P9 greedy
+class _FakeG(oracle.Graph):
+    def __init__(self, tables, edges):
+        self.tables, self.edges, self.vec, self.mat, self.d = dict(tables), sorted(edges), {}, {}, 1
+
+
+def test_greedy_hand_trace():
+    g = _FakeG({"a": 10, "b": 100, "c": 5}, [("a.x|b.x", "a", "b"), ("b.y|c.y", "b", "c")])
+    est = {("a", "b"): 50.0, ("b", "c"): 20.0, ("a", "b", "c"): 30.0}
+    order, prefix, cost = oracle.plan_greedy(g, est_fn=lambda S: est[tuple(sorted(S))])
+    assert order == ["c", "b", "a"] and prefix == [5.0, 20.0, 30.0] and cost == 55.0
+    # negative estimates are clamped to 0 for planning
+    est2 = {("a", "b"): -7.0, ("b", "c"): 20.0, ("a", "b", "c"): 1.0}
+    order, prefix, cost = oracle.plan_greedy(g, est_fn=lambda S: est2[tuple(sorted(S))])
+    assert order == ["a", "b", "c"] and prefix == [10.0, 0.0, 1.0] and cost == 11.0
+
+
+def test_greedy_ties_by_alias():
+    g = _FakeG({"a": 7, "b": 7, "c": 7}, [("a.x|b.x", "a", "b"), ("b.y|c.y", "b", "c"), ("a.z|c.z", "a", "c")])
+    est = {("a", "b"): 3.0, ("b", "c"): 3.0, ("a", "c"): 3.0, ("a", "b", "c"): 1.0}
+    order, _, _ = oracle.plan_greedy(g, est_fn=lambda S: est[tuple(sorted(S))])
+    assert order == ["a", "b", "c"]
+
+
+def test_greedy_cost_not_below_exhaustive_minimum():
+    """With exact cardinalities, greedy's cost >= min over all valid left-deep orders."""
+    import itertools
+    rng = np.random.default_rng(51)
+    for trial in range(20):
+        T = int(rng.integers(3, 6))
+        names = [f"t{i}" for i in range(T)]
+        edges = [(f"{names[i]}.k|{names[j]}.k", names[i], names[j]) for i in range(1, T) for j in [int(rng.integers(0, i))]]
+        card = {}
+        g = _FakeG({n: int(rng.integers(1, 100)) for n in names}, edges)
+
+        def est(S):
+            S = tuple(sorted(S))
+            if S not in card:
+                card[S] = float(rng.integers(0, 1000))
+            return card[S]
+        order, prefix, cost = oracle.plan_greedy(g, est_fn=est)
+        best = math.inf
+        for perm in itertools.permutations(names):
+            ok, c = True, 0.0
+            for i in range(1, len(perm) + 1):
+                if not oracle.connected(g, perm[:i]):
+                    ok = False
+                    break
+                c += float(g.tables[perm[0]]) if i == 1 else max(est(perm[:i]), 0.0)
+            if ok:
+                best = min(best, c)
+        assert cost >= best
+
+
+# ---------------------------------------------------------------- P10 C1 end to end
+def test_c1_estimate_vs_exact_join():
+    import datagen
+    ws = datagen.c1()
+    R = {k: v.numpy() for k, v in datagen.generate_table(ws, "R").items()}
+    S = {k: v.numpy() for k, v in datagen.generate_table(ws, "S").items()}
+    mask, nR = oracle.filter_mask(R, datagen.resolve_preds(ws, "R"))
+    assert abs(nR / len(mask) - 14 / 125) < 0.01       # attr uniform [1900,2025) > 2010 -> 14/125
+    e = ws.edges[0][0]
+    A = oracle.build([R["key"]], mask, 5, [1024], [e])
+    B = oracle.build([S["key"]], None, 5, [1024], [e])
+    fR = np.bincount(R["key"][mask.astype(bool)], minlength=10000)
+    fS = np.bincount(S["key"], minlength=10000)
+    J = int((fR * fS).sum())
+    rows = [oracle.two_way_row(A[r], B[r]) for r in range(5)]
+    est = oracle.median_odd(rows)
+    sigma = math.sqrt((float((fR ** 2).sum()) * float((fS ** 2).sum()) + J * J) / 1024)
+    assert abs(est - J) < 4 * sigma, (est, J, sigma)
