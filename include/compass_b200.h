@@ -1,0 +1,219 @@
+/*
+ * compass_b200.h — C-ABI of the B200-native COMPASS hot path (arXiv 2102.02440).
+ *
+ * The data-parallel hot path of COMPASS: an online Fast-AGMS sketch build fused
+ * with push-down selection, the merge of partial sketches, the sketch-composition
+ * estimates of join cardinality and the greedy join-order enumerator that consumes
+ * them.  Citations: PAPER.md / SPEC.md under /root/reference, SURVEY.md §8(b).
+ *
+ * Conventions (all entry points):
+ *   - Plain C types only.  "device" pointers are CUDA device pointers on the
+ *     sketch's device; "host" pointers are ordinary host memory.
+ *   - Asynchronous entry points enqueue work on `stream` (a cudaStream_t passed
+ *     as void*; NULL = legacy default stream) and return immediately.  Entry
+ *     points that return host values (estimate_*, plan_greedy) synchronise
+ *     `stream` before returning.
+ *   - Ownership: columns, survivor counters and caller-provided counter buffers
+ *     are owned by the caller and must stay valid until the stream work that
+ *     uses them completes.  The library owns only what it allocated.
+ *   - Errors: no exception crosses the ABI.  Every call returns an sk_status;
+ *     sk_last_error() gives a thread-local message for the last failure.
+ *   - Concurrency: a sketch must not be updated from two streams at once.
+ *   - There is no CPU fallback: if no CUDA device is usable, calls that need one
+ *     return SK_ECUDA.
+ */
+#ifndef COMPASS_B200_H
+#define COMPASS_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SK_API __attribute__((visibility("default")))
+#else
+#define SK_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SK_OK = 0,
+    SK_EINVAL = 1,       /* bad argument: arity/type, even d, non-power-of-two w */
+    SK_EMISMATCH = 2,    /* seed / shape / edge mismatch on merge or estimate    */
+    SK_EOVERFLOW = 3,    /* a counter or estimate bound would overflow; contraction unsupported    */
+    SK_ENOMEM = 4,       /* allocation failure                                                       */
+    SK_ECUDA = 5         /* CUDA runtime error / no device                                          */
+} sk_status;
+
+typedef struct sk_sketch sk_sketch;   /* opaque */
+
+/* ---------------------------------------------------------------------------
+ * Sketch descriptor.
+ *   d            rows (independent basic estimators), odd, 1 <= d <= 63
+ *                (PAPER.md:192 rows; median needs odd d).
+ *   ndim         1: Fast-AGMS vector  sk[r][j]
+ *                2: partitioned matrix M[r][i][j]
+ *   w[0..ndim)   buckets per dimension, powers of two in [2, 2^24]
+ *                (PAPER.md:395 uses 1023; powers of two enable folding).
+ *   master_seed  seed of the hash family (default 42).
+ *   edge_id[q]   canonical join-edge id of dimension q: the two "alias.column"
+ *                names sorted and joined by '|'.  Both sides of a
+ *                join use the same id and therefore the same xi/h family
+ *                (PAPER.md:148, 197); for ndim=2, strcmp(edge_id[0], edge_id[1]) < 0
+ *                (dimension 0 = canonically first edge).
+ * Hash family: x = key mod (2^61-1) after sign extension;
+ *   xi_r(x) = +1 iff ((a3 x + a2) x + a1) x + a0 mod p is odd, else -1;
+ *   h_r(x)  = ((b1 x + b0) mod p) mod w.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    uint32_t d;
+    uint32_t ndim;
+    uint32_t w[2];
+    uint64_t master_seed;
+    const char *edge_id[2];
+} sk_desc;
+
+/* Counter layout: int64, row-major, [d][w0] (ndim 1) or [d][w0][w1] (ndim 2). */
+
+/* Create a sketch on CUDA `device`.  counters_dev: caller-owned device buffer of
+ * d*w0(*w1) int64 (must already be zeroed if a fresh sketch is wanted), or NULL
+ * for a library-owned, zeroed buffer.  *out receives the handle. */
+SK_API sk_status sketch_create(const sk_desc *desc, int device, int64_t *counters_dev, sk_sketch **out);
+
+/* Destroy a handle (frees library-owned counters; never caller-owned ones).
+ * Synchronises the device first.  NULL is a no-op. */
+SK_API sk_status sketch_destroy(sk_sketch *sk);
+
+/* Device pointer and number of int64 counters of a sketch. */
+SK_API sk_status sketch_counters(const sk_sketch *sk, int64_t **counters_dev, uint64_t *n_counters);
+
+/* Zero all counters (async on stream). */
+SK_API sk_status sketch_zero(sk_sketch *sk, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * sketch_update_filtered — the fused scan ("sketch building is
+ * performed during the selection"; PAPER.md:99 one sketch per join attribute;
+ * SPEC.md:288-296).  One pass over n_rows tuples of a columnar table:
+ *   survive(i) = AND over preds of
+ *       POINT : v == lo
+ *       RANGE : lo <= v <= hi        (inclusive; use INT64_MIN / INT64_MAX for open ends)
+ *       SUBSET: v in set[0..set_size)  (set is a HOST array, copied by the call;
+ *                                       set_size == 0 means no value qualifies)
+ *   with v = cols[pred.col][i] sign-extended to int64.  n_preds == 0 keeps all rows.
+ *   For every surviving tuple and every target t, row r of t's sketch gets
+ *       ndim 1: sk[r][h_r(k0)]              += xi_r(k0)
+ *       ndim 2: M[r][h0_r(k0)][h1_r(k1)]     += xi0_r(k0) * xi1_r(k1)
+ *   with kq = cols[target.key_col[q]][i].
+ *   *survivors_dev (device int64, may be NULL) += number of surviving tuples
+ *   (the exact selection cardinality).
+ * cols: device pointers, each n_rows elements of int32 or int64, 16-byte aligned
+ *   recommended.  Counters are accumulated (+=), so calls over row shards add up
+ *   (linearity).
+ * Limits: n_cols <= 16, n_preds <= 8, n_targets <= 16, all targets on one device.
+ * ------------------------------------------------------------------------- */
+typedef enum { SK_INT32 = 0, SK_INT64 = 1 } sk_dtype;
+typedef struct {
+    const void *data;   /* device pointer */
+    uint32_t dtype;     /* sk_dtype */
+} sk_column;
+
+typedef enum { SK_PRED_POINT = 0, SK_PRED_RANGE = 1, SK_PRED_SUBSET = 2 } sk_pred_kind;
+typedef struct {
+    uint32_t col;        /* index into cols */
+    uint32_t kind;       /* sk_pred_kind */
+    int64_t lo, hi;      /* POINT uses lo; RANGE [lo, hi] */
+    const int64_t *set;  /* SUBSET: host array (any order, duplicates allowed) */
+    uint64_t set_size;
+} sk_pred;
+
+typedef struct {
+    sk_sketch *sketch;
+    uint32_t key_col[2]; /* key column per sketch dimension */
+} sk_target;
+
+SK_API sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_cols, uint64_t n_rows,
+                                 const sk_pred *preds, uint32_t n_preds,
+                                 const sk_target *targets, uint32_t n_targets,
+                                 int64_t *survivors_dev, void *stream);
+
+/* dst += src elementwise (PAPER.md:86 mergeability).  Requires an
+ * identical descriptor (d, ndim, w, master_seed, edge ids), else SK_EMISMATCH.
+ * Cross-GPU merge: all-reduce (SUM, int64) the counter buffers with NCCL. */
+SK_API sk_status sketch_merge(sk_sketch *dst, const sk_sketch *src, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Join graph of one query: tables are vertices carrying their
+ * exact post-selection cardinality; edge e joins tables edge_u[e] and edge_v[e]
+ * and carries one 1-D sketch per side (vec_u[e] built on table edge_u[e]'s join
+ * column, vec_v[e] on edge_v[e]'s), both with the edge's id and seed.  Optional
+ * partitioned matrices: mat[m] is table mat_table[m]'s 2-D sketch over edges
+ * (mat_e0[m], mat_e1[m]) (dimension 0 = mat_e0, the canonically first edge).
+ * All arrays are host arrays; sketches live on one device.  n_tables <= 64.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    uint32_t n_tables;
+    const int64_t *survivors;          /* [n_tables] */
+    uint32_t n_edges;
+    const uint32_t *edge_u, *edge_v;   /* [n_edges] */
+    sk_sketch *const *vec_u;           /* [n_edges] */
+    sk_sketch *const *vec_v;           /* [n_edges] */
+    uint32_t n_mats;
+    const uint32_t *mat_table;         /* [n_mats] */
+    const uint32_t *mat_e0, *mat_e1;   /* [n_mats] */
+    sk_sketch *const *mat;             /* [n_mats] */
+} sk_graph;
+
+/* ---------------------------------------------------------------------------
+ * estimate_join — cardinality estimate of the connected sub-plan whose tables
+ * are the set bits of vertex_mask:
+ *   |C| = 1: the exact survivors of that table.
+ *   |C| >= 2: per row r, E_r = sum over bucket assignments to every edge induced
+ *     by C of the product of the tables' tensors, where a table contributes its
+ *     1-D sketch (one incident edge in C), its matrix (if one is built over exactly
+ *     its incident edges), or the min-abs merged view of its 1-D
+ *     sketches in canonical edge order.  Vectors are folded to
+ *     the narrowest width on each edge.
+ *     Two-way: E_r = sum_j A[r][j] B[r][j].  Est = median_r E_r
+ *     (PAPER.md:201), computed exactly (integer arithmetic), rounded once to fp64.
+ * est: host double.  row_est: host double[d] or NULL (per-row E_r, rounded).
+ * Supported: induced graphs with at most one independent cycle and tables with
+ * at most 3 incident edges (SK_EOVERFLOW otherwise).  Synchronises `stream`.
+ * ------------------------------------------------------------------------- */
+SK_API sk_status estimate_join(const sk_graph *g, uint64_t vertex_mask, double *est, double *row_est, void *stream);
+
+/* Same, but writes each row's exact E_r as a decimal string into
+ * buf[r*stride .. r*stride+stride) (NUL-terminated); stride >= 160 recommended. */
+SK_API sk_status estimate_join_exact(const sk_graph *g, uint64_t vertex_mask, char *buf, uint32_t stride, void *stream);
+
+/* Batched estimates of n sub-plans: est[i] for masks[i]. */
+SK_API sk_status estimate_subplans(const sk_graph *g, const uint64_t *masks, uint32_t n, double *est, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * plan_greedy — greedy left-deep join order ("greedy", default in
+ * the experiments PAPER.md:395):
+ *   card(S) = survivors for |S| = 1, max(Est(S), 0) otherwise;
+ *   start pair = edge (u, v) with least card, ties by (min index, max index);
+ *   source = its endpoint with fewer survivors (ties: lower index);
+ *   repeatedly append the neighbour v of C minimising card(C + v) (ties: lower
+ *   index); cost = sum of card over all prefixes (Alg. 1 lines 14-15,
+ *   PAPER.md:325-326).
+ * order: host uint32[n_tables]; prefix_card: host double[n_tables]; cost: host.
+ * Table index order must match the alias order used for ties.  Synchronises.
+ * ------------------------------------------------------------------------- */
+SK_API sk_status plan_greedy(const sk_graph *g, uint32_t *order, double *prefix_card, double *cost, void *stream);
+
+/* Thread-local description of the last error (never NULL). */
+SK_API const char *sk_last_error(void);
+
+/* Number of CUDA kernels this library has launched since it was loaded
+ * (diagnostic; lets a caller count the library's launches in a timed region). */
+SK_API uint64_t sk_kernel_launches(void);
+
+/* Library build / device information, e.g. "compass_b200 sm_100a". */
+SK_API const char *sk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COMPASS_B200_H */

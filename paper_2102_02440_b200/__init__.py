@@ -1,0 +1,281 @@
+"""B200-native COMPASS hot path (arXiv 2102.02440): thin ctypes binding of
+``libcompass_b200.so`` (C-ABI in ``include/compass_b200.h``).
+
+This module only marshals arguments: every step of the hot path (filter, hash,
+sketch update, flush, merge, composition estimates) runs in the library's CUDA
+kernels; the greedy enumerator runs in the library's host code.  PyTorch is used
+for device memory and streams only.  There is no CPU fallback: if the compiled
+library is missing, importing works but every call raises ``RuntimeError``.
+
+Names follow the paper / SURVEY.md §8(b): ``sketch_create``, ``sketch_update_filtered``,
+``sketch_merge``, ``estimate_join``, ``plan_greedy``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libcompass_b200.so")
+
+SK_OK, SK_EINVAL, SK_EMISMATCH, SK_EOVERFLOW, SK_ENOMEM, SK_ECUDA = range(6)
+SK_INT32, SK_INT64 = 0, 1
+POINT, RANGE, SUBSET = 0, 1, 2
+INT64_MIN = -(1 << 63)
+INT64_MAX = (1 << 63) - 1
+
+_STATUS = {0: "SK_OK", 1: "SK_EINVAL", 2: "SK_EMISMATCH", 3: "SK_EOVERFLOW", 4: "SK_ENOMEM", 5: "SK_ECUDA"}
+
+
+class SkError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class sk_desc(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_uint32), ("ndim", ctypes.c_uint32), ("w", ctypes.c_uint32 * 2),
+                ("master_seed", ctypes.c_uint64), ("edge_id", ctypes.c_char_p * 2)]
+
+
+class sk_column(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("dtype", ctypes.c_uint32)]
+
+
+class sk_pred(ctypes.Structure):
+    _fields_ = [("col", ctypes.c_uint32), ("kind", ctypes.c_uint32), ("lo", ctypes.c_int64), ("hi", ctypes.c_int64),
+                ("set", ctypes.POINTER(ctypes.c_int64)), ("set_size", ctypes.c_uint64)]
+
+
+class sk_target(ctypes.Structure):
+    _fields_ = [("sketch", ctypes.c_void_p), ("key_col", ctypes.c_uint32 * 2)]
+
+
+class sk_graph(ctypes.Structure):
+    _fields_ = [("n_tables", ctypes.c_uint32), ("survivors", ctypes.POINTER(ctypes.c_int64)),
+                ("n_edges", ctypes.c_uint32), ("edge_u", ctypes.POINTER(ctypes.c_uint32)),
+                ("edge_v", ctypes.POINTER(ctypes.c_uint32)), ("vec_u", ctypes.POINTER(ctypes.c_void_p)),
+                ("vec_v", ctypes.POINTER(ctypes.c_void_p)), ("n_mats", ctypes.c_uint32),
+                ("mat_table", ctypes.POINTER(ctypes.c_uint32)), ("mat_e0", ctypes.POINTER(ctypes.c_uint32)),
+                ("mat_e1", ctypes.POINTER(ctypes.c_uint32)), ("mat", ctypes.POINTER(ctypes.c_void_p))]
+
+
+# every symbol include/compass_b200.h declares (checked by tests/test_abi.py)
+EXPORTS = ["sketch_create", "sketch_destroy", "sketch_counters", "sketch_zero", "sketch_update_filtered",
+           "sketch_merge", "estimate_join", "estimate_join_exact", "estimate_subplans", "plan_greedy",
+           "sk_last_error", "sk_version", "sk_kernel_launches"]
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the compiled C-ABI library.  Raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: build it with __graft_entry__.build() "
+                               "(the CUDA path has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        st, vp, u32, u64, i64 = ctypes.c_int, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int64
+        L.sketch_create.restype = st
+        L.sketch_create.argtypes = [ctypes.POINTER(sk_desc), ctypes.c_int, vp, ctypes.POINTER(vp)]
+        L.sketch_destroy.restype = st
+        L.sketch_destroy.argtypes = [vp]
+        L.sketch_counters.restype = st
+        L.sketch_counters.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(u64)]
+        L.sketch_zero.restype = st
+        L.sketch_zero.argtypes = [vp, vp]
+        L.sketch_update_filtered.restype = st
+        L.sketch_update_filtered.argtypes = [ctypes.POINTER(sk_column), u32, u64, ctypes.POINTER(sk_pred), u32,
+                                             ctypes.POINTER(sk_target), u32, vp, vp]
+        L.sketch_merge.restype = st
+        L.sketch_merge.argtypes = [vp, vp, vp]
+        L.estimate_join.restype = st
+        L.estimate_join.argtypes = [ctypes.POINTER(sk_graph), u64, ctypes.POINTER(ctypes.c_double),
+                                    ctypes.POINTER(ctypes.c_double), vp]
+        L.estimate_join_exact.restype = st
+        L.estimate_join_exact.argtypes = [ctypes.POINTER(sk_graph), u64, ctypes.c_char_p, u32, vp]
+        L.estimate_subplans.restype = st
+        L.estimate_subplans.argtypes = [ctypes.POINTER(sk_graph), ctypes.POINTER(u64), u32,
+                                        ctypes.POINTER(ctypes.c_double), vp]
+        L.plan_greedy.restype = st
+        L.plan_greedy.argtypes = [ctypes.POINTER(sk_graph), ctypes.POINTER(u32), ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_double), vp]
+        L.sk_last_error.restype = ctypes.c_char_p
+        L.sk_last_error.argtypes = []
+        L.sk_kernel_launches.restype = ctypes.c_uint64
+        L.sk_kernel_launches.argtypes = []
+        L.sk_version.restype = ctypes.c_char_p
+        L.sk_version.argtypes = []
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != SK_OK:
+        raise SkError(status, lib().sk_last_error().decode())
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class Sketch:
+    """A Fast-AGMS vector (ndim 1) or partitioned matrix (ndim 2) sketch whose
+    int64 counters are a caller-owned torch tensor (``self.counters``)."""
+
+    def __init__(self, d: int, w, edge_ids, master_seed: int = 42, device=None, counters: torch.Tensor | None = None):
+        w = list(w)
+        edge_ids = list(edge_ids)
+        assert len(w) == len(edge_ids) and len(w) in (1, 2)
+        self.d, self.w, self.edge_ids, self.master_seed = d, w, edge_ids, master_seed
+        device = torch.device(device if device is not None else "cuda")
+        if device.index is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        shape = (d, *w)
+        if counters is None:
+            counters = torch.zeros(shape, dtype=torch.int64, device=device)
+        assert counters.dtype == torch.int64 and counters.is_contiguous() and tuple(counters.shape) == shape
+        self.counters = counters
+        desc = sk_desc()
+        desc.d, desc.ndim = d, len(w)
+        for q in range(len(w)):
+            desc.w[q] = w[q]
+            desc.edge_id[q] = edge_ids[q].encode()
+        desc.master_seed = master_seed
+        h = ctypes.c_void_p()
+        _check(lib().sketch_create(ctypes.byref(desc), counters.device.index, ctypes.c_void_p(counters.data_ptr()),
+                                   ctypes.byref(h)))
+        self.handle = h
+
+    @property
+    def ndim(self) -> int:
+        return len(self.w)
+
+    def zero_(self, stream=None):
+        _check(lib().sketch_zero(self.handle, ctypes.c_void_p(_stream_ptr(stream))))
+        return self
+
+    def close(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            lib().sketch_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def sketch_update_filtered(columns, n_rows: int, preds, targets, survivors: torch.Tensor | None = None, stream=None):
+    """One fused scan.  columns: list of int32/int64 CUDA tensors; preds: list of
+    (col_index, kind, lo, hi, set_values); targets: list of (Sketch, [key col indices])."""
+    ncol = len(columns)
+    cols = (sk_column * max(1, ncol))()
+    for i, c in enumerate(columns):
+        assert c.is_cuda and c.dtype in (torch.int32, torch.int64) and c.is_contiguous()
+        cols[i].data = c.data_ptr()
+        cols[i].dtype = SK_INT64 if c.dtype == torch.int64 else SK_INT32
+    keep = []
+    pr = (sk_pred * max(1, len(preds)))()
+    for i, p in enumerate(preds):
+        p = tuple(p) + (None,) * (5 - len(p))
+        pr[i].col, pr[i].kind, pr[i].lo, pr[i].hi = p[0], p[1], p[2], p[3]
+        if p[1] == SUBSET:
+            vals = list(p[4] or [])
+            arr = (ctypes.c_int64 * max(1, len(vals)))(*vals)
+            keep.append(arr)
+            pr[i].set = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int64))
+            pr[i].set_size = len(vals)
+    tg = (sk_target * max(1, len(targets)))()
+    for i, (sk, keys) in enumerate(targets):
+        tg[i].sketch = sk.handle
+        for q, k in enumerate(keys):
+            tg[i].key_col[q] = k
+    sp = ctypes.c_void_p(survivors.data_ptr()) if survivors is not None else None
+    _check(lib().sketch_update_filtered(cols, ncol, n_rows, pr, len(preds), tg, len(targets), sp,
+                                        ctypes.c_void_p(_stream_ptr(stream))))
+
+
+def sketch_merge(dst: Sketch, src: Sketch, stream=None):
+    _check(lib().sketch_merge(dst.handle, src.handle, ctypes.c_void_p(_stream_ptr(stream))))
+
+
+class JoinGraph:
+    """sk_graph wrapper.  tables: list of aliases (index order = tie order);
+    survivors: list of ints; edges: list of (u, v, Sketch_u, Sketch_v);
+    mats: list of (table, e0, e1, Sketch)."""
+
+    def __init__(self, tables, survivors, edges, mats=()):
+        self.tables = list(tables)
+        n, E, M = len(self.tables), len(edges), len(mats)
+        self._surv = (ctypes.c_int64 * max(1, n))(*[int(s) for s in survivors])
+        self._eu = (ctypes.c_uint32 * max(1, E))(*[e[0] for e in edges])
+        self._ev = (ctypes.c_uint32 * max(1, E))(*[e[1] for e in edges])
+        self._vu = (ctypes.c_void_p * max(1, E))(*[e[2].handle.value for e in edges])
+        self._vv = (ctypes.c_void_p * max(1, E))(*[e[3].handle.value for e in edges])
+        self._mt = (ctypes.c_uint32 * max(1, M))(*[m[0] for m in mats])
+        self._m0 = (ctypes.c_uint32 * max(1, M))(*[m[1] for m in mats])
+        self._m1 = (ctypes.c_uint32 * max(1, M))(*[m[2] for m in mats])
+        self._mp = (ctypes.c_void_p * max(1, M))(*[m[3].handle.value for m in mats])
+        self._keep = (edges, mats)
+        g = sk_graph()
+        g.n_tables, g.survivors = n, self._surv
+        g.n_edges, g.edge_u, g.edge_v = E, self._eu, self._ev
+        g.vec_u = ctypes.cast(self._vu, ctypes.POINTER(ctypes.c_void_p))
+        g.vec_v = ctypes.cast(self._vv, ctypes.POINTER(ctypes.c_void_p))
+        g.n_mats, g.mat_table, g.mat_e0, g.mat_e1 = M, self._mt, self._m0, self._m1
+        g.mat = ctypes.cast(self._mp, ctypes.POINTER(ctypes.c_void_p))
+        self.g = g
+        self.d = edges[0][2].d if edges else 1
+
+    def mask(self, subset) -> int:
+        m = 0
+        for t in subset:
+            m |= 1 << self.tables.index(t)
+        return m
+
+    def estimate_join(self, subset, stream=None):
+        """(Est as fp64, per-row fp64 list)."""
+        est = ctypes.c_double()
+        rows = (ctypes.c_double * self.d)()
+        _check(lib().estimate_join(ctypes.byref(self.g), self.mask(subset), ctypes.byref(est), rows,
+                                   ctypes.c_void_p(_stream_ptr(stream))))
+        return est.value, list(rows)
+
+    def estimate_join_exact(self, subset, stream=None) -> list[int]:
+        stride = 192
+        buf = ctypes.create_string_buffer(stride * self.d)
+        _check(lib().estimate_join_exact(ctypes.byref(self.g), self.mask(subset), buf, stride,
+                                         ctypes.c_void_p(_stream_ptr(stream))))
+        raw = buf.raw
+        return [int(raw[r * stride:(r + 1) * stride].split(b"\0", 1)[0].decode()) for r in range(self.d)]
+
+    def estimate_subplans(self, subsets, stream=None) -> list[float]:
+        n = len(subsets)
+        masks = (ctypes.c_uint64 * max(1, n))(*[self.mask(s) for s in subsets])
+        est = (ctypes.c_double * max(1, n))()
+        _check(lib().estimate_subplans(ctypes.byref(self.g), masks, n, est, ctypes.c_void_p(_stream_ptr(stream))))
+        return list(est)[:n]
+
+    def plan_greedy(self, stream=None):
+        n = len(self.tables)
+        order = (ctypes.c_uint32 * n)()
+        pre = (ctypes.c_double * n)()
+        cost = ctypes.c_double()
+        _check(lib().plan_greedy(ctypes.byref(self.g), order, pre, ctypes.byref(cost),
+                                 ctypes.c_void_p(_stream_ptr(stream))))
+        return [self.tables[i] for i in order], list(pre), cost.value
+
+
+def kernel_launches() -> int:
+    return int(lib().sk_kernel_launches())
+
+
+def version() -> str:
+    return lib().sk_version().decode()

@@ -1,0 +1,1017 @@
+// estimate.cu — sketch composition: two-way and multi-way join estimates
+// (PAPER.md:197-201 two-way; PAPER.md:221-225 partitioned; PAPER.md:234-240
+// merging) and the greedy enumerator.
+//
+// Exactness.  E_r is an integer (a sum of products of integer counters).  The
+// GPU evaluates it modulo K pairwise-coprime Mersenne numbers m_k = 2^{a_k} - 1
+// (a_k in {61,59,57,55,53,49,47,43,41,37}; gcd(2^a-1, 2^b-1) = 2^gcd(a,b)-1 = 1),
+// where reduction is two shift-and-add folds.  K is chosen from a rigorous bound
+// |E_r| <= prod_t ||T_t||_1 (L1 norms measured on the device), and the host
+// reconstructs E_r exactly by Garner's mixed-radix CRT, takes the median over
+// rows, and rounds once to fp64 (round-to-nearest-even).
+//
+// Contraction.  The sub-plan's tensor network is contracted by message passing
+// over a spanning tree rooted at the lowest-index table; a single cycle is
+// handled by conditioning one cycle edge on each of its buckets (batched).
+// Node kinds: 1-D sketch, built matrix, min-abs merged view (<= 3 legs).  A
+// merged node contracts its first child leg with the identity of SURVEY.md O9:
+// with |c| sorted ascending and prefix sums P1 = sum x, P2 = sum x*c,
+//   sum_i x_i fold(L, c_i, R) = m(L,R) * sum_{|c_i|>=|L|} x_i
+//                             + sum_{|c_i|<|L|, |c_i|<=|R|} x_i c_i
+//                             + R * sum_{|R|<|c_i|<|L|} x_i.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+using namespace skb;
+
+namespace {
+
+constexpr int kMaxMod = 10;
+const int kModBits[kMaxMod] = {61, 59, 57, 55, 53, 49, 47, 43, 41, 37};
+enum { KV = 0, KM = 1, KG = 2 };          // vector, matrix, merged
+enum { RCHILD = 0, RPARENT = 1, RFIXED = 2 };
+
+struct Mods {
+    int K;
+    int a[kMaxMod];
+    uint64_t m[kMaxMod];
+};
+
+// ---------------------------------------------------------------- device modular arithmetic
+__device__ __forceinline__ uint64_t mm_mul(uint64_t x, uint64_t y, int a, uint64_t m) {
+    const uint64_t lo = x * y, hi = __umul64hi(x, y);
+    uint64_t r = (hi << (64 - a)) + (lo & m) + (lo >> a);
+    r = (r & m) + (r >> a);
+    return r >= m ? r - m : r;
+}
+__device__ __forceinline__ uint64_t mm_add(uint64_t x, uint64_t y, uint64_t m) {
+    const uint64_t s = x + y;
+    return s >= m ? s - m : s;
+}
+__device__ __forceinline__ uint64_t mm_sub(uint64_t x, uint64_t y, uint64_t m) {
+    return x >= y ? x - y : x + (m - y);
+}
+__device__ __forceinline__ uint64_t mm_u64(uint64_t u, int a, uint64_t m) {
+    u = (u & m) + (u >> a);
+    u = (u & m) + (u >> a);
+    return u >= m ? u - m : u;
+}
+__device__ __forceinline__ uint64_t mm_i64(int64_t v, int a, uint64_t m) {
+    if (v >= 0) return mm_u64((uint64_t)v, a, m);
+    const uint64_t r = mm_u64((uint64_t)(-(v + 1)) + 1ULL, a, m);
+    return r ? m - r : 0;
+}
+__device__ __forceinline__ uint64_t uabs(int64_t v) { return v < 0 ? (uint64_t)(-(v + 1)) + 1ULL : (uint64_t)v; }
+
+// ---------------------------------------------------------------- small kernels
+// per (item, row): sum |v| over `cells` counters
+struct L1Item { const int64_t *p; uint32_t d; uint32_t cells; };
+__global__ void k_l1(const L1Item *items, unsigned long long *out, int maxd) {
+    const L1Item it = items[blockIdx.x];
+    const uint32_t r = blockIdx.y;
+    if (r >= it.d) return;
+    unsigned long long s = 0;
+    for (uint32_t i = threadIdx.x; i < it.cells; i += blockDim.x) s += uabs(it.p[uint64_t(r) * it.cells + i]);
+    __shared__ unsigned long long red[32];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+        out[blockIdx.x * maxd + r] = t;
+    }
+}
+
+// fold [d][wn0][wn1] -> [d][w0][w1]: out[r][i][j] = sum_{s,t} in[r][i + s w0][j + t w1]  (O5)
+__global__ void k_fold(const int64_t *in, int64_t *out, uint32_t d, uint32_t wn0, uint32_t wn1, uint32_t w0, uint32_t w1) {
+    const uint64_t total = uint64_t(d) * w0 * w1;
+    for (uint64_t o = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; o < total; o += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t j = (uint32_t)(o % w1);
+        const uint32_t i = (uint32_t)((o / w1) % w0);
+        const uint32_t r = (uint32_t)(o / (uint64_t(w0) * w1));
+        int64_t s = 0;
+        for (uint32_t a = i; a < wn0; a += w0)
+            for (uint32_t b = j; b < wn1; b += w1) s += in[(uint64_t(r) * wn0 + a) * wn1 + b];
+        out[o] = s;
+    }
+}
+
+// per row: sort indices by |c| ascending (bitonic, w a power of two, w <= 8192)
+__global__ void k_sort_abs(const int64_t *c, uint32_t w, int32_t *ord, uint64_t *sabs) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    uint64_t *key = reinterpret_cast<uint64_t *>(sm);
+    uint32_t *idx = reinterpret_cast<uint32_t *>(key + w);
+    const uint32_t r = blockIdx.x;
+    for (uint32_t i = threadIdx.x; i < w; i += blockDim.x) {
+        key[i] = uabs(c[uint64_t(r) * w + i]);
+        idx[i] = i;
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= w; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < w; i += blockDim.x) {
+                const uint32_t l = i ^ j;
+                if (l > i) {
+                    const bool up = (i & k) == 0;
+                    const bool gt = key[i] > key[l] || (key[i] == key[l] && idx[i] > idx[l]);
+                    if (gt == up) {
+                        uint64_t tk = key[i]; key[i] = key[l]; key[l] = tk;
+                        uint32_t ti = idx[i]; idx[i] = idx[l]; idx[l] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < w; i += blockDim.x) {
+        ord[uint64_t(r) * w + i] = (int32_t)idx[i];
+        sabs[uint64_t(r) * w + i] = key[i];
+    }
+}
+
+// ---------------------------------------------------------------- node kernels
+struct Node {
+    int kind, nl;
+    int role[3];
+    int w[3];
+    const int64_t *data[3];     // folded; VEC [d][w0]; MAT [d][w0][w1]; MERGED data[q] = [d][w_q]
+    const uint64_t *msg[3];     // child messages, layout [K][d][bm][w]
+    int bm[3];
+    int qc;                     // merged: contracted child leg
+    const int32_t *ord;         // merged: [d][w_qc]
+    const uint64_t *sabs;       // merged: [d][w_qc]
+    uint64_t *out;              // parent message [K][d][out_bm][w_p], or root partials [K][d][B][tiles]
+    int out_bm;
+    int B, tiles, d;
+    int64_t b0;
+};
+
+__device__ __forceinline__ const uint64_t *msg_row(const Node &n, int q, int k, int r, int bb, int Kd_unused) {
+    const int bm = n.bm[q];
+    return n.msg[q] + ((uint64_t(k) * n.d + r) * bm + (bm > 1 ? bb : 0)) * (uint64_t)n.w[q];
+}
+
+__device__ __forceinline__ uint64_t block_sum_mod(uint64_t v, uint64_t m, uint64_t *red) {
+    // warp
+    for (int o = 16; o > 0; o >>= 1) v = mm_add(v, __shfl_xor_sync(0xffffffffu, v, o), m);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    uint64_t t = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = mm_add(t, red[i], m);
+    return t;
+}
+
+// value of a node's tensor at per-leg indices (merged: left fold of the min-abs rule)
+__device__ __forceinline__ int64_t tensor_val(const Node &n, int r, const int64_t *idx) {
+    if (n.kind == KV) return n.data[0][uint64_t(r) * n.w[0] + idx[0]];
+    if (n.kind == KM) return n.data[0][(uint64_t(r) * n.w[0] + idx[0]) * n.w[1] + idx[1]];
+    int64_t acc = n.data[0][uint64_t(r) * n.w[0] + idx[0]];
+    for (int q = 1; q < n.nl; ++q) {
+        const int64_t v = n.data[q][uint64_t(r) * n.w[q] + idx[q]];
+        if (!(uabs(acc) <= uabs(v))) acc = v;
+    }
+    return acc;
+}
+
+// VEC / MAT node, or a merged leaf.  blockIdx.x = (k*d + r)*B + bb, blockIdx.y = tile of the outer index.
+__global__ void k_node_dense(const __grid_constant__ Node n, const __grid_constant__ Mods md) {
+    __shared__ uint64_t red[32];
+    const int B = n.B;
+    const int bb = blockIdx.x % B;
+    const int r = (blockIdx.x / B) % n.d;
+    const int k = blockIdx.x / (B * n.d);
+    const int a = md.a[k];
+    const uint64_t m = md.m[k];
+    const int64_t b = n.b0 + bb;
+    int qp = -1, qf = -1, qc0 = -1, qc1 = -1;
+    for (int q = 0; q < n.nl; ++q) {
+        if (n.role[q] == RPARENT) qp = q;
+        else if (n.role[q] == RFIXED) qf = q;
+        else if (qc0 < 0) qc0 = q;
+        else qc1 = q;
+    }
+    // outer leg: parent if any, else first child; inner leg: the (other) child if any
+    const int qo = qp >= 0 ? qp : qc0;
+    const int qi = qp >= 0 ? qc0 : qc1;
+    const int wo = qo >= 0 ? n.w[qo] : 1;
+    const int wi = qi >= 0 ? n.w[qi] : 1;
+    const uint64_t *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row(n, qo, k, r, bb, 0) : nullptr;
+    const uint64_t *xi = (qi >= 0) ? msg_row(n, qi, k, r, bb, 0) : nullptr;
+    uint64_t acc = 0;
+    const int per_tile = (wo + n.tiles - 1) / n.tiles;
+    const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
+    for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
+        uint64_t s = 0;
+        for (int i = 0; i < wi; ++i) {
+            int64_t idx[3] = {0, 0, 0};
+            if (qo >= 0) idx[qo] = o;
+            if (qi >= 0) idx[qi] = i;
+            if (qf >= 0) idx[qf] = b;
+            uint64_t term = mm_i64(tensor_val(n, r, idx), a, m);
+            if (xi) term = mm_mul(term, xi[i], a, m);
+            s = mm_add(s, term, m);
+        }
+        if (qp >= 0) {
+            n.out[((uint64_t(k) * n.d + r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + o] = s;
+        } else {
+            if (xo) s = mm_mul(s, xo[o], a, m);
+            acc = mm_add(acc, s, m);
+        }
+    }
+    if (qp < 0) {
+        const uint64_t t = block_sum_mod(acc, m, red);
+        if (threadIdx.x == 0) n.out[((uint64_t(k) * n.d + r) * B + bb) * n.tiles + blockIdx.y] = t;
+    }
+}
+
+// merged node (min-abs view over <= 3 constituents), first child leg contracted by O9.
+__global__ void k_node_merged(const __grid_constant__ Node n, const __grid_constant__ Mods md) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ uint64_t red[32];
+    __shared__ uint64_t tot1[1024], tot2[1024];
+    const int B = n.B;
+    const int bb = blockIdx.x % B;
+    const int r = (blockIdx.x / B) % n.d;
+    const int k = blockIdx.x / (B * n.d);
+    const int a = md.a[k];
+    const uint64_t m = md.m[k];
+    const int64_t b = n.b0 + bb;
+    const int qc = n.qc;
+    const int wq = n.w[qc];
+    uint64_t *P1 = reinterpret_cast<uint64_t *>(sm);
+    uint64_t *P2 = P1 + (wq + 1);
+    uint64_t *S = P2 + (wq + 1);
+    const uint64_t *x = msg_row(n, qc, k, r, bb, 0);
+    const int64_t *cq = n.data[qc] + uint64_t(r) * wq;
+    const int32_t *ord = n.ord + uint64_t(r) * wq;
+    // --- prefix sums over the |c|-sorted order (block scan, contiguous chunks per thread)
+    const int nt = blockDim.x;
+    const int chunk = (wq + nt - 1) / nt;
+    const int s0 = threadIdx.x * chunk, s1 = min(wq, s0 + chunk);
+    uint64_t l1 = 0, l2 = 0;
+    for (int s = s0; s < s1; ++s) {
+        const int i = ord[s];
+        const uint64_t xv = x[i];
+        l1 = mm_add(l1, xv, m);
+        l2 = mm_add(l2, mm_mul(xv, mm_i64(cq[i], a, m), a, m), m);
+        S[s] = n.sabs[uint64_t(r) * wq + s];
+    }
+    tot1[threadIdx.x] = l1;
+    tot2[threadIdx.x] = l2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t c1 = 0, c2 = 0;
+        for (int t = 0; t < nt; ++t) {
+            const uint64_t v1 = tot1[t], v2 = tot2[t];
+            tot1[t] = c1; tot2[t] = c2;
+            c1 = mm_add(c1, v1, m); c2 = mm_add(c2, v2, m);
+        }
+        P1[wq] = c1; P2[wq] = c2;
+    }
+    __syncthreads();
+    {
+        uint64_t c1 = tot1[threadIdx.x], c2 = tot2[threadIdx.x];
+        for (int s = s0; s < s1; ++s) {
+            P1[s] = c1; P2[s] = c2;
+            const int i = ord[s];
+            const uint64_t xv = x[i];
+            c1 = mm_add(c1, xv, m);
+            c2 = mm_add(c2, mm_mul(xv, mm_i64(cq[i], a, m), a, m), m);
+        }
+    }
+    __syncthreads();
+    // --- enumerate the other legs
+    int qp = -1, qf = -1, qo2 = -1;
+    for (int q = 0; q < n.nl; ++q) {
+        if (q == qc) continue;
+        if (n.role[q] == RPARENT) qp = q;
+        else if (n.role[q] == RFIXED) qf = q;
+        else qo2 = q;  // another child leg
+    }
+    const int qo = qp >= 0 ? qp : qo2;       // outer
+    const int qi = qp >= 0 ? qo2 : -1;       // inner (other child, when a parent exists)
+    const int wo = qo >= 0 ? n.w[qo] : 1;
+    const int wi = qi >= 0 ? n.w[qi] : 1;
+    const uint64_t *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row(n, qo, k, r, bb, 0) : nullptr;
+    const uint64_t *xi2 = qi >= 0 ? msg_row(n, qi, k, r, bb, 0) : nullptr;
+    const int per_tile = (wo + n.tiles - 1) / n.tiles;
+    const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
+    uint64_t acc = 0;
+    for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
+        uint64_t s = 0;
+        for (int i = 0; i < wi; ++i) {
+            // constituent values of the non-contracted legs
+            int64_t val[3] = {0, 0, 0};
+            for (int q = 0; q < n.nl; ++q) {
+                if (q == qc) continue;
+                int64_t ix = (q == qf) ? b : (q == qo ? o : i);
+                val[q] = n.data[q][uint64_t(r) * n.w[q] + ix];
+            }
+            bool hasL = false, hasR = false;
+            int64_t L = 0, R = 0;
+            for (int q = 0; q < n.nl; ++q) {
+                if (q == qc) continue;
+                if (q < qc) { if (!hasL || !(uabs(L) <= uabs(val[q]))) L = val[q]; hasL = true; }
+                else { if (!hasR || !(uabs(R) <= uabs(val[q]))) R = val[q]; hasR = true; }
+            }
+            uint64_t V;
+            if (hasL) {
+                const uint64_t aL = uabs(L);
+                int lo = 0, hi = wq;                                 // #{|c| < |L|}
+                while (lo < hi) { int mid = (lo + hi) >> 1; if (S[mid] < aL) lo = mid + 1; else hi = mid; }
+                const int nless = lo;
+                const int64_t win = (hasR && !(aL <= uabs(R))) ? R : L;
+                V = mm_mul(mm_i64(win, a, m), mm_sub(P1[wq], P1[nless], m), a, m);
+                int endB = nless;
+                if (hasR) {
+                    const uint64_t aR = uabs(R);
+                    lo = 0; hi = wq;                                 // #{|c| <= |R|}
+                    while (lo < hi) { int mid = (lo + hi) >> 1; if (S[mid] <= aR) lo = mid + 1; else hi = mid; }
+                    if (lo < endB) {
+                        V = mm_add(V, mm_mul(mm_i64(R, a, m), mm_sub(P1[endB], P1[lo], m), a, m), m);
+                        endB = lo;
+                    }
+                }
+                V = mm_add(V, P2[endB], m);
+            } else {
+                const uint64_t aR = uabs(R);
+                int lo = 0, hi = wq;
+                while (lo < hi) { int mid = (lo + hi) >> 1; if (S[mid] <= aR) lo = mid + 1; else hi = mid; }
+                V = mm_add(mm_mul(mm_i64(R, a, m), mm_sub(P1[wq], P1[lo], m), a, m), P2[lo], m);
+            }
+            if (xi2) V = mm_mul(V, xi2[i], a, m);
+            s = mm_add(s, V, m);
+        }
+        if (qp >= 0) {
+            n.out[((uint64_t(k) * n.d + r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + o] = s;
+        } else {
+            if (xo) s = mm_mul(s, xo[o], a, m);
+            acc = mm_add(acc, s, m);
+        }
+    }
+    if (qp < 0) {
+        const uint64_t t = block_sum_mod(acc, m, red);
+        if (threadIdx.x == 0) n.out[((uint64_t(k) * n.d + r) * B + bb) * n.tiles + blockIdx.y] = t;
+    }
+}
+
+// acc[k][r] += sum over slots of part[k][r][slot]
+__global__ void k_root_reduce(const uint64_t *part, uint64_t *acc, int slots, int d, const __grid_constant__ Mods md) {
+    __shared__ uint64_t red[32];
+    const int k = blockIdx.x / d, r = blockIdx.x % d;
+    const uint64_t m = md.m[k];
+    uint64_t s = 0;
+    for (int i = threadIdx.x; i < slots; i += blockDim.x) s = mm_add(s, part[uint64_t(blockIdx.x) * slots + i], m);
+    const uint64_t t = block_sum_mod(s, m, red);
+    if (threadIdx.x == 0) acc[blockIdx.x] = mm_add(acc[blockIdx.x], t, m);
+}
+
+// ---------------------------------------------------------------- host big integers (Garner)
+struct UBig {
+    std::vector<uint64_t> l;  // little-endian limbs
+    void norm() { while (!l.empty() && l.back() == 0) l.pop_back(); }
+    bool zero() const { return l.empty(); }
+    void mul_small(uint64_t v) {
+        unsigned __int128 carry = 0;
+        for (auto &x : l) {
+            unsigned __int128 t = (unsigned __int128)x * v + carry;
+            x = (uint64_t)t;
+            carry = t >> 64;
+        }
+        if (carry) l.push_back((uint64_t)carry);
+        norm();
+    }
+    void add_small(uint64_t v) {
+        unsigned __int128 carry = v;
+        for (size_t i = 0; i < l.size() && carry; ++i) {
+            unsigned __int128 t = (unsigned __int128)l[i] + carry;
+            l[i] = (uint64_t)t;
+            carry = t >> 64;
+        }
+        if (carry) l.push_back((uint64_t)carry);
+    }
+    static int cmp(const UBig &x, const UBig &y) {
+        if (x.l.size() != y.l.size()) return x.l.size() < y.l.size() ? -1 : 1;
+        for (size_t i = x.l.size(); i-- > 0;)
+            if (x.l[i] != y.l[i]) return x.l[i] < y.l[i] ? -1 : 1;
+        return 0;
+    }
+    static UBig sub(const UBig &x, const UBig &y) {  // x >= y
+        UBig r;
+        r.l.resize(x.l.size());
+        unsigned __int128 borrow = 0;
+        for (size_t i = 0; i < x.l.size(); ++i) {
+            unsigned __int128 yi = (i < y.l.size() ? y.l[i] : 0) + borrow;
+            unsigned __int128 xi = x.l[i];
+            if (xi >= yi) { r.l[i] = (uint64_t)(xi - yi); borrow = 0; }
+            else { r.l[i] = (uint64_t)(((unsigned __int128)1 << 64) + xi - yi); borrow = 1; }
+        }
+        r.norm();
+        return r;
+    }
+    int bits() const {
+        if (l.empty()) return 0;
+        return int(l.size() - 1) * 64 + (64 - __builtin_clzll(l.back()));
+    }
+    bool bit(int i) const { return (size_t)(i / 64) < l.size() && ((l[i / 64] >> (i % 64)) & 1ULL); }
+    double to_double() const {  // round to nearest, ties to even
+        const int nb = bits();
+        if (nb == 0) return 0.0;
+        if (nb <= 53) return (double)l[0];
+        uint64_t top = 0;  // bits [nb-54, nb): 53 kept + 1 round bit
+        for (int i = 0; i < 54; ++i)
+            if (bit(nb - 54 + i)) top |= 1ULL << i;
+        bool sticky = false;
+        for (int i = 0; i < nb - 54 && !sticky; ++i) sticky = bit(i);
+        uint64_t keep = top >> 1;
+        const bool rbit = top & 1ULL;
+        if (rbit && (sticky || (keep & 1ULL))) ++keep;
+        return ldexp((double)keep, nb - 53);
+    }
+    std::string to_dec() const {
+        if (l.empty()) return "0";
+        UBig t = *this;
+        std::string s;
+        while (!t.zero()) {
+            unsigned __int128 rem = 0;
+            for (size_t i = t.l.size(); i-- > 0;) {
+                unsigned __int128 cur = (rem << 64) | t.l[i];
+                t.l[i] = (uint64_t)(cur / 10000000000000000000ULL);
+                rem = cur % 10000000000000000000ULL;
+            }
+            t.norm();
+            uint64_t r = (uint64_t)rem;
+            for (int j = 0; j < 19; ++j) { s.push_back(char('0' + r % 10)); r /= 10; }
+        }
+        while (s.size() > 1 && s.back() == '0') s.pop_back();
+        std::reverse(s.begin(), s.end());
+        return s;
+    }
+};
+
+struct SBig {
+    bool neg = false;
+    UBig mag;
+    static int cmp(const SBig &x, const SBig &y) {
+        const bool xz = x.mag.zero(), yz = y.mag.zero();
+        const bool xn = x.neg && !xz, yn = y.neg && !yz;
+        if (xn != yn) return xn ? -1 : 1;
+        const int c = UBig::cmp(x.mag, y.mag);
+        return xn ? -c : c;
+    }
+    double to_double() const { const double v = mag.to_double(); return neg ? -v : v; }
+    std::string to_dec() const { return (neg && !mag.zero() ? "-" : "") + mag.to_dec(); }
+};
+
+static uint64_t host_mulmod(uint64_t x, uint64_t y, uint64_t m) { return (uint64_t)((unsigned __int128)x * y % m); }
+static uint64_t host_powmod(uint64_t b, uint64_t e, uint64_t m) {
+    uint64_t r = 1 % m;
+    b %= m;
+    while (e) { if (e & 1) r = host_mulmod(r, b, m); b = host_mulmod(b, b, m); e >>= 1; }
+    return r;
+}
+static uint64_t host_inv(uint64_t v, uint64_t m) {  // m coprime to v; extended Euclid
+    __int128 t = 0, nt = 1, r = m, nr = v % m;
+    while (nr) { __int128 q = r / nr; __int128 tmp = t - q * nt; t = nt; nt = tmp; tmp = r - q * nr; r = nr; nr = tmp; }
+    if (t < 0) t += m;
+    (void)host_powmod;
+    return (uint64_t)t;
+}
+
+// Garner: residues[k] mod m_k  ->  signed integer in (-M/2, M/2]
+static SBig crt_signed(const uint64_t *res, const Mods &md) {
+    const int K = md.K;
+    std::vector<uint64_t> v(K);
+    for (int k = 0; k < K; ++k) {
+        const uint64_t mk = md.m[k];
+        // value of x_{<k} mod m_k and prod_{j<k} m_j mod m_k
+        uint64_t xk = 0, pk = 1 % mk;
+        for (int j = 0; j < k; ++j) {
+            xk = (xk + host_mulmod(v[j] % mk, pk, mk)) % mk;
+            pk = host_mulmod(pk, md.m[j] % mk, mk);
+        }
+        const uint64_t diff = (res[k] % mk + mk - xk) % mk;
+        v[k] = host_mulmod(diff, host_inv(pk, mk), mk);
+    }
+    UBig x;
+    for (int k = K - 1; k >= 0; --k) {
+        x.mul_small(md.m[k]);
+        x.add_small(v[k]);
+    }
+    UBig M;
+    M.l.push_back(1);
+    for (int k = 0; k < K; ++k) M.mul_small(md.m[k]);
+    UBig x2 = x;
+    x2.mul_small(2);
+    SBig out;
+    if (UBig::cmp(x2, M) > 0) { out.neg = true; out.mag = UBig::sub(M, x); }
+    else out.mag = x;
+    return out;
+}
+
+// ---------------------------------------------------------------- sub-plan model (host)
+struct TabT {
+    int t;                       // table index in the graph
+    int kind;                    // KV/KM/KG
+    std::vector<int> legs;       // local edge indices, canonical order
+    std::vector<const sk_sketch *> sk;   // VEC/MAT: 1 sketch; MERGED: one per leg
+};
+
+struct Plan {
+    std::vector<int> tabs;               // graph table indices in C (ascending)
+    std::vector<int> edges;              // graph edge indices in canonical (edge-id) order
+    std::vector<std::string> eid;
+    std::vector<int> width;              // per local edge
+    std::vector<TabT> T;
+    std::vector<std::pair<int, int>> ends;   // per local edge: local table positions
+    int cond = -1;
+    int d = 0, device = 0;
+};
+
+static sk_status build_plan(const sk_graph *g, uint64_t mask, Plan &P) {
+    if (!g) return fail(SK_EINVAL, "estimate: NULL graph");
+    if (g->n_tables == 0 || g->n_tables > 64) return fail(SK_EINVAL, "estimate: n_tables must be in [1,64]");
+    for (uint32_t t = 0; t < g->n_tables; ++t)
+        if ((mask >> t) & 1ULL) P.tabs.push_back((int)t);
+    if (P.tabs.size() < 2) return fail(SK_EINVAL, "estimate: need >= 2 tables");
+    if (g->n_tables < 64 && (mask >> g->n_tables)) return fail(SK_EINVAL, "estimate: mask has bits beyond n_tables");
+    std::vector<std::pair<std::string, int>> es;
+    for (uint32_t e = 0; e < g->n_edges; ++e) {
+        const uint32_t u = g->edge_u[e], v = g->edge_v[e];
+        if (u >= g->n_tables || v >= g->n_tables || u == v) return fail(SK_EINVAL, "estimate: bad edge %u", e);
+        if (((mask >> u) & 1ULL) && ((mask >> v) & 1ULL)) {
+            const sk_sketch *a = g->vec_u[e], *b = g->vec_v[e];
+            if (!a || !b) return fail(SK_EINVAL, "estimate: edge %u lacks a 1-D sketch", e);
+            if (a->ndim != 1 || b->ndim != 1) return fail(SK_EINVAL, "estimate: edge %u sketches must be 1-D", e);
+            if (a->edge[0] != b->edge[0] || a->master != b->master || a->d != b->d)
+                return fail(SK_EMISMATCH, "estimate: edge %u sides disagree on id/seed/d", e);
+            es.push_back({a->edge[0], (int)e});
+        }
+    }
+    std::sort(es.begin(), es.end());
+    for (size_t i = 1; i < es.size(); ++i)
+        if (es[i].first == es[i - 1].first) return fail(SK_EINVAL, "estimate: duplicate edge id %s", es[i].first.c_str());
+    for (auto &p : es) { P.edges.push_back(p.second); P.eid.push_back(p.first); }
+    const int E = (int)P.edges.size();
+    P.width.assign(E, 1 << 30);
+    P.ends.assign(E, {-1, -1});
+    const sk_sketch *ref = g->vec_u[P.edges.empty() ? 0 : P.edges[0]];
+    if (E == 0) return fail(SK_EINVAL, "estimate: sub-plan is not connected");
+    P.d = ref->d;
+    P.device = ref->device;
+    for (size_t i = 0; i < P.tabs.size(); ++i) {
+        const int t = P.tabs[i];
+        TabT tt;
+        tt.t = t;
+        for (int le = 0; le < E; ++le) {
+            const int e = P.edges[le];
+            if ((int)g->edge_u[e] == t || (int)g->edge_v[e] == t) {
+                tt.legs.push_back(le);
+                auto &en = P.ends[le];
+                (en.first < 0 ? en.first : en.second) = (int)i;
+            }
+        }
+        if (tt.legs.empty()) return fail(SK_EINVAL, "estimate: sub-plan is not connected");
+        if (tt.legs.size() > 3) return fail(SK_EOVERFLOW, "estimate: table with >3 join edges in a sub-plan is unsupported");
+        auto side = [&](int le) -> const sk_sketch * {
+            const int e = P.edges[le];
+            return (int)g->edge_u[e] == t ? g->vec_u[e] : g->vec_v[e];
+        };
+        if (tt.legs.size() == 1) {
+            tt.kind = KV;
+            tt.sk.push_back(side(tt.legs[0]));
+        } else {
+            const sk_sketch *mat = nullptr;
+            if (tt.legs.size() == 2)
+                for (uint32_t mi = 0; mi < g->n_mats; ++mi) {
+                    if ((int)g->mat_table[mi] != t || !g->mat[mi]) continue;
+                    const sk_sketch *ms = g->mat[mi];
+                    if (ms->ndim == 2 && ms->edge[0] == P.eid[tt.legs[0]] && ms->edge[1] == P.eid[tt.legs[1]]) mat = ms;
+                }
+            if (mat) { tt.kind = KM; tt.sk.push_back(mat); }
+            else { tt.kind = KG; for (int le : tt.legs) tt.sk.push_back(side(le)); }
+        }
+        for (const sk_sketch *s : tt.sk) {
+            if (s->d != P.d) return fail(SK_EMISMATCH, "estimate: sketches disagree on d");
+            if (s->device != P.device) return fail(SK_EMISMATCH, "estimate: sketches on different devices");
+            if (s->master != ref->master) return fail(SK_EMISMATCH, "estimate: sketches disagree on master seed");
+        }
+        for (size_t q = 0; q < tt.legs.size(); ++q) {
+            const int wn = tt.kind == KM ? (int)tt.sk[0]->w[q] : (int)tt.sk[tt.kind == KV ? 0 : q]->w[0];
+            P.width[tt.legs[q]] = std::min(P.width[tt.legs[q]], wn);
+        }
+        P.T.push_back(tt);
+    }
+    // connectivity
+    {
+        std::vector<int> seen(P.tabs.size(), 0), st{0};
+        seen[0] = 1;
+        while (!st.empty()) {
+            const int i = st.back(); st.pop_back();
+            for (int le : P.T[i].legs) {
+                const int j = P.ends[le].first == i ? P.ends[le].second : P.ends[le].first;
+                if (!seen[j]) { seen[j] = 1; st.push_back(j); }
+            }
+        }
+        for (int s : seen) if (!s) return fail(SK_EINVAL, "estimate: sub-plan is not connected");
+    }
+    const int cyc = E - (int)P.tabs.size() + 1;
+    if (cyc > 1) return fail(SK_EOVERFLOW, "estimate: sub-plans with more than one independent cycle are unsupported");
+    if (cyc == 1) {
+        // condition on the cycle edge whose endpoints have the most legs (ties: canonical order)
+        int best = -1, bestdeg = -1;
+        for (int le = 0; le < E; ++le) {
+            std::vector<int> seen(P.tabs.size(), 0), st{0};
+            seen[0] = 1;
+            while (!st.empty()) {
+                const int i = st.back(); st.pop_back();
+                for (int f : P.T[i].legs) {
+                    if (f == le) continue;
+                    const int j = P.ends[f].first == i ? P.ends[f].second : P.ends[f].first;
+                    if (!seen[j]) { seen[j] = 1; st.push_back(j); }
+                }
+            }
+            bool on = true;
+            for (int s : seen) if (!s) on = false;
+            if (!on) continue;
+            const int dg = (int)P.T[P.ends[le].first].legs.size() + (int)P.T[P.ends[le].second].legs.size();
+            if (dg > bestdeg) { bestdeg = dg; best = le; }
+        }
+        P.cond = best;
+    }
+    return SK_OK;
+}
+
+struct DevBuf {
+    void *p = nullptr;
+    cudaStream_t s = nullptr;
+    ~DevBuf() { if (p) cudaFreeAsync(p, s); }
+};
+
+static sk_status dalloc(std::vector<DevBuf> &pool, size_t bytes, cudaStream_t s, void **out) {
+    pool.emplace_back();
+    pool.back().s = s;
+    cudaError_t e = cudaMallocAsync(&pool.back().p, std::max<size_t>(bytes, 16), s);
+    if (e != cudaSuccess) { pool.back().p = nullptr; return cuda_fail(e, "cudaMallocAsync(estimate)"); }
+    *out = pool.back().p;
+    return SK_OK;
+}
+
+static sk_status run_plan(const Plan &P, std::vector<SBig> &rows, cudaStream_t stream) {
+    const int E = (int)P.edges.size();
+    const int NT = (int)P.T.size();
+    const int d = P.d;
+    std::vector<DevBuf> pool;
+    pool.reserve(256);
+    // ---- L1 bound -> number of moduli
+    std::vector<const sk_sketch *> uniq;
+    for (auto &t : P.T) for (auto *s : t.sk) if (std::find(uniq.begin(), uniq.end(), s) == uniq.end()) uniq.push_back(s);
+    std::vector<L1Item> items;
+    for (auto *s : uniq) items.push_back({s->counters, s->d, (uint32_t)(s->n_counters / s->d)});
+    void *d_items, *d_l1;
+    sk_status st;
+    if ((st = dalloc(pool, items.size() * sizeof(L1Item), stream, &d_items))) return st;
+    if ((st = dalloc(pool, items.size() * d * sizeof(unsigned long long), stream, &d_l1))) return st;
+    SKB_CUDA(cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(L1Item), cudaMemcpyHostToDevice, stream));
+    k_l1<<<dim3((unsigned)items.size(), d), 256, 0, stream>>>((const L1Item *)d_items, (unsigned long long *)d_l1, d); count_launch();
+    SKB_CUDA(cudaGetLastError());
+    std::vector<unsigned long long> l1(items.size() * d);
+    SKB_CUDA(cudaMemcpyAsync(l1.data(), d_l1, l1.size() * 8, cudaMemcpyDeviceToHost, stream));
+    SKB_CUDA(cudaStreamSynchronize(stream));
+    auto l1max = [&](const sk_sketch *s) {
+        const size_t i = std::find(uniq.begin(), uniq.end(), s) - uniq.begin();
+        unsigned long long mx = 0;
+        for (int r = 0; r < d; ++r) mx = std::max(mx, l1[i * d + r]);
+        return (double)std::max<unsigned long long>(mx, 1ULL);
+    };
+    double logB = 0;
+    for (auto &t : P.T) {
+        if (t.kind != KG) { logB += log2(l1max(t.sk[0])); continue; }
+        double best = 1e300;
+        for (size_t q = 0; q < t.legs.size(); ++q) {
+            double v = log2(l1max(t.sk[q]));
+            for (size_t q2 = 0; q2 < t.legs.size(); ++q2) if (q2 != q) v += log2((double)P.width[t.legs[q2]]);
+            best = std::min(best, v);
+        }
+        logB += best;
+    }
+    Mods md;
+    md.K = 0;
+    double have = 0;
+    while (md.K < kMaxMod && have < logB * (1 + 1e-9) + 3.0) {
+        md.a[md.K] = kModBits[md.K];
+        md.m[md.K] = (1ULL << kModBits[md.K]) - 1;
+        have += kModBits[md.K] - 1e-9;
+        ++md.K;
+    }
+    if (have < logB + 3.0) return fail(SK_EOVERFLOW, "estimate: bound 2^%.1f exceeds the exact range", logB);
+    const int K = md.K;
+    // ---- folded copies of every tensor leg
+    std::vector<std::vector<const int64_t *>> data(NT);
+    for (int i = 0; i < NT; ++i) {
+        const TabT &t = P.T[i];
+        if (t.kind == KM) {
+            const sk_sketch *s = t.sk[0];
+            const int w0 = P.width[t.legs[0]], w1 = P.width[t.legs[1]];
+            if ((int)s->w[0] == w0 && (int)s->w[1] == w1) { data[i].push_back(s->counters); continue; }
+            void *f;
+            if ((st = dalloc(pool, size_t(d) * w0 * w1 * 8, stream, &f))) return st;
+            k_fold<<<1184, 256, 0, stream>>>(s->counters, (int64_t *)f, d, s->w[0], s->w[1], w0, w1); count_launch();
+            data[i].push_back((const int64_t *)f);
+        } else {
+            for (size_t q = 0; q < t.sk.size(); ++q) {
+                const sk_sketch *s = t.sk[q];
+                const int w = P.width[t.legs[q]];
+                if ((int)s->w[0] == w) { data[i].push_back(s->counters); continue; }
+                void *f;
+                if ((st = dalloc(pool, size_t(d) * w * 8, stream, &f))) return st;
+                k_fold<<<592, 256, 0, stream>>>(s->counters, (int64_t *)f, d, 1, s->w[0], 1, w); count_launch();
+                data[i].push_back((const int64_t *)f);
+            }
+        }
+    }
+    SKB_CUDA(cudaGetLastError());
+    // ---- spanning tree rooted at local table 0 (DFS), post-order
+    std::vector<int> parent_edge(NT, -2), order;
+    {
+        std::vector<std::pair<int, int>> st2{{0, -1}};
+        std::vector<int> vis(NT, 0);
+        // iterative DFS producing pre-order; reverse gives a valid post-order for message passing
+        std::vector<int> pre;
+        while (!st2.empty()) {
+            auto [i, pe] = st2.back(); st2.pop_back();
+            if (vis[i]) continue;
+            vis[i] = 1;
+            parent_edge[i] = pe;
+            pre.push_back(i);
+            for (int le : P.T[i].legs) {
+                if (le == pe || le == P.cond) continue;
+                const int j = P.ends[le].first == i ? P.ends[le].second : P.ends[le].first;
+                if (!vis[j]) st2.push_back({j, le});
+            }
+        }
+        order.assign(pre.rbegin(), pre.rend());
+    }
+    // does the subtree of node i contain an endpoint of the conditioned edge?
+    std::vector<int> depb(NT, 0);
+    for (int i : order) {
+        if (P.cond >= 0 && (P.ends[P.cond].first == i || P.ends[P.cond].second == i)) depb[i] = 1;
+        for (int le : P.T[i].legs) {
+            if (le == parent_edge[i] || le == P.cond) continue;
+            const int j = P.ends[le].first == i ? P.ends[le].second : P.ends[le].first;
+            if (depb[j]) depb[i] = 1;
+        }
+    }
+    // ---- sorted orders for merged nodes' contracted legs
+    std::vector<int> qc_of(NT, -1);
+    std::vector<const int32_t *> ord_of(NT, nullptr);
+    std::vector<const uint64_t *> sabs_of(NT, nullptr);
+    for (int i = 0; i < NT; ++i) {
+        const TabT &t = P.T[i];
+        if (t.kind != KG) continue;
+        int qc = -1;
+        for (size_t q = 0; q < t.legs.size(); ++q) {
+            const int le = t.legs[q];
+            if (le == parent_edge[i] || le == P.cond) continue;
+            qc = (int)q;
+            break;
+        }
+        if (qc < 0) continue;   // merged leaf: evaluated densely
+        const int w = P.width[t.legs[qc]];
+        if (w > 8192) return fail(SK_EOVERFLOW, "estimate: merged contraction supports widths <= 8192");
+        void *o, *sa;
+        if ((st = dalloc(pool, size_t(d) * w * 4, stream, &o))) return st;
+        if ((st = dalloc(pool, size_t(d) * w * 8, stream, &sa))) return st;
+        const size_t sm = size_t(w) * 12;
+        SKB_CUDA(cudaFuncSetAttribute(k_sort_abs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_sort_abs<<<d, 512, sm, stream>>>(data[i][qc], w, (int32_t *)o, (uint64_t *)sa); count_launch();
+        SKB_CUDA(cudaGetLastError());
+        qc_of[i] = qc;
+        ord_of[i] = (const int32_t *)o;
+        sabs_of[i] = (const uint64_t *)sa;
+    }
+    // ---- chunking of the conditioned bucket
+    const int64_t Btot = P.cond >= 0 ? P.width[P.cond] : 1;
+    size_t per_b = 0;
+    for (int le = 0; le < E; ++le) per_b += size_t(K) * d * P.width[le] * 8;
+    int64_t Bc = Btot;
+    while (Bc > 1 && per_b * Bc > (size_t(768) << 20)) Bc = (Bc + 1) / 2;
+    // message buffers per local edge
+    std::vector<uint64_t *> msg(E, nullptr);
+    std::vector<int> msg_bm(E, 1);
+    for (int i : order) {
+        const int pe = parent_edge[i];
+        if (pe < 0) continue;
+        msg_bm[pe] = depb[i] ? (int)Bc : 1;
+        void *mb;
+        if ((st = dalloc(pool, size_t(K) * d * msg_bm[pe] * P.width[pe] * 8, stream, &mb))) return st;
+        msg[pe] = (uint64_t *)mb;
+    }
+    const int tiles_root = 1;
+    void *part, *acc;
+    if ((st = dalloc(pool, size_t(K) * d * Bc * tiles_root * 8, stream, &part))) return st;
+    if ((st = dalloc(pool, size_t(K) * d * 8, stream, &acc))) return st;
+    SKB_CUDA(cudaMemsetAsync(acc, 0, size_t(K) * d * 8, stream));
+    for (int64_t b0 = 0; b0 < Btot; b0 += Bc) {
+        const int B = (int)std::min<int64_t>(Bc, Btot - b0);
+        for (int i : order) {
+            const TabT &t = P.T[i];
+            const int pe = parent_edge[i];
+            Node n;
+            memset(&n, 0, sizeof(n));
+            n.kind = t.kind;
+            n.nl = (int)t.legs.size();
+            n.d = d;
+            n.B = B;
+            n.b0 = b0;
+            for (int q = 0; q < n.nl; ++q) {
+                const int le = t.legs[q];
+                n.w[q] = P.width[le];
+                n.role[q] = (le == P.cond) ? RFIXED : (le == pe ? RPARENT : RCHILD);
+                if (n.role[q] == RCHILD) { n.msg[q] = msg[le]; n.bm[q] = msg_bm[le]; }
+                n.data[q] = (t.kind == KG) ? data[i][q] : data[i][0];
+            }
+            // nodes whose message does not depend on b are computed once (first chunk)
+            if (pe >= 0 && msg_bm[pe] == 1 && b0 > 0) continue;
+            const int nB = (pe >= 0 && msg_bm[pe] == 1) ? 1 : B;
+            n.B = nB;
+            int tiles = 1;
+            const int blocks_xy = K * d * nB;
+            if (pe >= 0) {
+                n.out = msg[pe];
+                n.out_bm = msg_bm[pe];
+                const int wo = P.width[pe];
+                while (blocks_xy * tiles < 592 && tiles * 256 < wo) tiles *= 2;
+            } else {
+                n.out = (uint64_t *)part;
+            }
+            n.tiles = tiles;
+            if (t.kind == KG && qc_of[i] >= 0) {
+                n.qc = qc_of[i];
+                n.ord = ord_of[i];
+                n.sabs = sabs_of[i];
+                const size_t sm = (size_t(2) * (n.w[n.qc] + 1) + n.w[n.qc]) * 8;
+                SKB_CUDA(cudaFuncSetAttribute(k_node_merged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                k_node_merged<<<dim3(blocks_xy, tiles), 256, sm, stream>>>(n, md); count_launch();
+            } else {
+                k_node_dense<<<dim3(blocks_xy, tiles), 256, 0, stream>>>(n, md); count_launch();
+            }
+            SKB_CUDA(cudaGetLastError());
+        }
+        k_root_reduce<<<K * d, 256, 0, stream>>>((const uint64_t *)part, (uint64_t *)acc, B * tiles_root, d, md); count_launch();
+        SKB_CUDA(cudaGetLastError());
+    }
+    std::vector<uint64_t> res(size_t(K) * d);
+    SKB_CUDA(cudaMemcpyAsync(res.data(), acc, res.size() * 8, cudaMemcpyDeviceToHost, stream));
+    SKB_CUDA(cudaStreamSynchronize(stream));
+    rows.clear();
+    for (int r = 0; r < d; ++r) {
+        uint64_t rr[kMaxMod];
+        for (int k = 0; k < K; ++k) rr[k] = res[size_t(k) * d + r];
+        rows.push_back(crt_signed(rr, md));
+    }
+    return SK_OK;
+}
+
+}  // namespace
+
+namespace skb {
+
+sk_status estimate_mask(const sk_graph *g, uint64_t mask, double *est, double *row_est,
+                        std::vector<std::string> *rows_exact, cudaStream_t stream) {
+    if (!g) return fail(SK_EINVAL, "estimate: NULL graph");
+    const int pc = __builtin_popcountll(mask);
+    if (pc == 0) return fail(SK_EINVAL, "estimate: empty vertex mask");
+    if (pc == 1) {
+        const int t = __builtin_ctzll(mask);
+        if ((uint32_t)t >= g->n_tables || !g->survivors) return fail(SK_EINVAL, "estimate: bad singleton");
+        if (est) *est = (double)g->survivors[t];
+        return SK_OK;
+    }
+    Plan P;
+    sk_status st = build_plan(g, mask, P);
+    if (st) return st;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    SKB_CUDA(cudaSetDevice(P.device));
+    std::vector<SBig> rows;
+    st = run_plan(P, rows, stream);
+    cudaSetDevice(prev);
+    if (st) return st;
+    std::vector<int> idx(rows.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
+    std::sort(idx.begin(), idx.end(), [&](int x, int y) { return SBig::cmp(rows[x], rows[y]) < 0; });
+    if (est) *est = rows[idx[(rows.size() - 1) / 2]].to_double();
+    if (row_est) for (size_t r = 0; r < rows.size(); ++r) row_est[r] = rows[r].to_double();
+    if (rows_exact) { rows_exact->clear(); for (auto &v : rows) rows_exact->push_back(v.to_dec()); }
+    return SK_OK;
+}
+
+}  // namespace skb
+
+extern "C" sk_status estimate_join(const sk_graph *g, uint64_t vertex_mask, double *est, double *row_est, void *stream) {
+    return estimate_mask(g, vertex_mask, est, row_est, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" sk_status estimate_join_exact(const sk_graph *g, uint64_t vertex_mask, char *buf, uint32_t stride, void *stream) {
+    if (!buf || stride < 2) return fail(SK_EINVAL, "estimate_join_exact: bad buffer");
+    std::vector<std::string> rows;
+    double est;
+    sk_status st = estimate_mask(g, vertex_mask, &est, nullptr, &rows, (cudaStream_t)stream);
+    if (st) return st;
+    if (__builtin_popcountll(vertex_mask) == 1) {
+        snprintf(buf, stride, "%lld", (long long)est);
+        return SK_OK;
+    }
+    for (size_t r = 0; r < rows.size(); ++r) {
+        if (rows[r].size() + 1 > stride) return fail(SK_EINVAL, "estimate_join_exact: stride too small");
+        memcpy(buf + r * stride, rows[r].c_str(), rows[r].size() + 1);
+    }
+    return SK_OK;
+}
+
+extern "C" sk_status estimate_subplans(const sk_graph *g, const uint64_t *masks, uint32_t n, double *est, void *stream) {
+    if (n && (!masks || !est)) return fail(SK_EINVAL, "estimate_subplans: NULL array");
+    for (uint32_t i = 0; i < n; ++i) {
+        sk_status st = estimate_mask(g, masks[i], &est[i], nullptr, nullptr, (cudaStream_t)stream);
+        if (st) return st;
+    }
+    return SK_OK;
+}
+
+extern "C" sk_status plan_greedy(const sk_graph *g, uint32_t *order, double *prefix_card, double *cost, void *stream) {
+    if (!g || !order) return fail(SK_EINVAL, "plan_greedy: NULL argument");
+    const uint32_t n = g->n_tables;
+    if (n == 0 || n > 64) return fail(SK_EINVAL, "plan_greedy: n_tables must be in [1,64]");
+    std::map<uint64_t, double> cache;
+    sk_status err = SK_OK;
+    auto card = [&](uint64_t m) -> double {
+        auto it = cache.find(m);
+        if (it != cache.end()) return it->second;
+        double e = 0;
+        sk_status st = estimate_mask(g, m, &e, nullptr, nullptr, (cudaStream_t)stream);
+        if (st && !err) err = st;
+        const double c = std::max(e, 0.0);
+        cache[m] = c;
+        return c;
+    };
+    std::vector<uint32_t> C;
+    double total = 0;
+    std::vector<double> pre;
+    if (n == 1) {
+        C.push_back(0);
+        pre.push_back(card(1ULL));
+    } else {
+        // start pair: least card over adjacent pairs; ties by (min index, max index)
+        int bu = -1, bv = -1;
+        double bc = 0;
+        for (uint32_t e = 0; e < g->n_edges; ++e) {
+            int u = (int)std::min(g->edge_u[e], g->edge_v[e]), v = (int)std::max(g->edge_u[e], g->edge_v[e]);
+            const double c = card((1ULL << u) | (1ULL << v));
+            if (err) return err;
+            if (bu < 0 || c < bc || (c == bc && (u < bu || (u == bu && v < bv)))) { bu = u; bv = v; bc = c; }
+        }
+        if (bu < 0) return fail(SK_EINVAL, "plan_greedy: graph has no edges");
+        const int src = (g->survivors[bv] < g->survivors[bu]) ? bv : bu;
+        C.push_back((uint32_t)src);
+        uint64_t m = 1ULL << src;
+        pre.push_back(card(m));
+        while (C.size() < n) {
+            int best = -1;
+            double bcard = 0;
+            for (uint32_t e = 0; e < g->n_edges; ++e) {
+                const uint32_t u = g->edge_u[e], v = g->edge_v[e];
+                int cand = -1;
+                if (((m >> u) & 1ULL) && !((m >> v) & 1ULL)) cand = (int)v;
+                if (((m >> v) & 1ULL) && !((m >> u) & 1ULL)) cand = (int)u;
+                if (cand < 0) continue;
+                const double c = card(m | (1ULL << cand));
+                if (err) return err;
+                if (best < 0 || c < bcard || (c == bcard && cand < best)) { best = cand; bcard = c; }
+            }
+            if (best < 0) return fail(SK_EINVAL, "plan_greedy: join graph is not connected");
+            C.push_back((uint32_t)best);
+            m |= 1ULL << best;
+            pre.push_back(bcard);
+        }
+    }
+    if (err) return err;
+    for (size_t i = 0; i < C.size(); ++i) {
+        order[i] = C[i];
+        if (prefix_card) prefix_card[i] = pre[i];
+        total += pre[i];
+    }
+    if (cost) *cost = total;
+    return SK_OK;
+}

@@ -1,0 +1,53 @@
+// internal.cuh — private declarations of libcompass_b200 (not part of the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "compass_b200.h"
+
+// Mersenne prime of the hash family, p = 2^61 - 1.
+#define SKP_MERSENNE61 0x1FFFFFFFFFFFFFFFULL
+
+struct sk_sketch {
+    uint32_t d = 0, ndim = 0, w[2] = {0, 0};
+    uint64_t master = 0;
+    std::string edge[2];
+    int device = 0;
+    int64_t *counters = nullptr;
+    bool owned = false;
+    uint64_t n_counters = 0;
+    // per dimension q, per row r: {a0, a1, a2, a3, b0, b1} (H2), on device and host
+    uint64_t *seeds_dev = nullptr;
+    std::vector<uint64_t> seeds_host;
+};
+
+namespace skb {
+
+sk_status fail(sk_status st, const char *fmt, ...);
+sk_status cuda_fail(cudaError_t e, const char *what);
+void clear_error();
+
+// host seed derivation (H2): coefficient c(master, edge, row, role, idx) mod p
+uint64_t seed_coef(uint64_t master, const std::string &edge, uint32_t row, uint32_t role, uint32_t idx);
+
+bool same_desc(const sk_sketch *a, const sk_sketch *b);
+
+// count one kernel launch issued by the library (sk_kernel_launches)
+void count_launch(uint64_t n = 1);
+
+// estimate engine entry used by estimate_join / estimate_subplans / plan_greedy.
+// rows_exact (optional): per-row exact decimal strings.
+sk_status estimate_mask(const sk_graph *g, uint64_t mask, double *est, double *row_est,
+                        std::vector<std::string> *rows_exact, cudaStream_t stream);
+
+}  // namespace skb
+
+#define SKB_CUDA(call)                                           \
+    do {                                                         \
+        cudaError_t e_ = (call);                                 \
+        if (e_ != cudaSuccess) return skb::cuda_fail(e_, #call); \
+    } while (0)

@@ -1,0 +1,293 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): counters and survivor counts bit-exact (int64);
+estimates exact per row (both sides compute E_r exactly; the median is rounded
+once to fp64, so fp64 values are compared with ==, which is stricter than the
+north-star tolerance rel 1e-12); greedy join order identical.
+"""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+import paper_2102_02440_b200 as pb
+from paper_2102_02440_b200.query import QueryRun
+
+pytestmark = pytest.mark.gpu
+
+I64MIN, I64MAX = -(1 << 63), (1 << 63) - 1
+
+
+def _dev():
+    return torch.device("cuda", 0)
+
+
+def _rand_cols(n, seed):
+    rng = np.random.default_rng(seed)
+    k32 = rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+    k64 = rng.integers(I64MIN, I64MAX, n, dtype=np.int64, endpoint=True)
+    if n > 10:
+        k32[:4] = [-2**31, 2**31 - 1, 0, -1]
+        k64[:6] = [I64MIN, I64MAX, 0, -1, (1 << 61) - 1, 1 << 61]
+    zk = rng.zipf(1.3, n).astype(np.int64) % 5000          # skewed key
+    p = rng.integers(0, 100, n).astype(np.int32)
+    s = rng.integers(0, 50, n).astype(np.int64)
+    return {"k32": k32, "k64": k64, "zk": zk, "p": p, "s": s}
+
+
+def _to_dev(cols):
+    return {k: torch.from_numpy(v).to(_dev()) for k, v in cols.items()}
+
+
+TARGETS = [  # (key cols, d, w, edge ids)
+    (["k32"], 5, [1024], ["A.k32|B.x"]),
+    (["k64"], 3, [64], ["A.k64|C.y"]),
+    (["zk"], 7, [4096], ["A.zk|D.z"]),
+    (["k32", "k64"], 3, [32, 16], ["A.k32|B.x", "A.k64|C.y"]),
+    (["zk", "k32"], 5, [64, 128], ["A.k32|B.x", "A.zk|D.z"]),
+]
+
+
+def _gpu_build(cols, preds, targets, master=42, calls=1):
+    names = list(cols)
+    dcols = _to_dev(cols)
+    sks = [pb.Sketch(d, w, e, master, _dev()) for (_, d, w, e) in targets]
+    surv = torch.zeros(1, dtype=torch.int64, device=_dev())
+    n = len(cols[names[0]])
+    cuts = np.linspace(0, n, calls + 1).astype(int)
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        sub = [dcols[c][a:b].contiguous() for c in names]
+        pr = [(names.index(p[0]),) + tuple(p[1:]) for p in preds]
+        tg = [(sk, [names.index(k) for k in t[0]]) for sk, t in zip(sks, targets)]
+        pb.sketch_update_filtered(sub, int(b - a), pr, tg, survivors=surv)
+    torch.cuda.synchronize()
+    return [sk.counters.cpu().numpy() for sk in sks], int(surv.item())
+
+
+def _oracle_build(cols, preds, targets, master=42):
+    mask, cnt = oracle.filter_mask(cols, preds)
+    outs = []
+    for keys, d, w, e in targets:
+        outs.append(oracle.build([cols[k] for k in keys], mask, d, w, e, master=master))
+    return outs, cnt
+
+
+PRED_SETS = [
+    [],
+    [("p", pb.RANGE, 10, 69)],
+    [("p", pb.RANGE, 10, 69), ("s", pb.SUBSET, 0, 0, [1, 3, 5, 7, 11, 13, 49, 1000])],
+    [("s", pb.POINT, 7, 7)],
+    [("k64", pb.RANGE, I64MIN, 0), ("p", pb.RANGE, 0, I64MAX)],
+    [("s", pb.SUBSET, 0, 0, [])],                       # nothing qualifies
+    [("p", pb.POINT, 1000, 1000)],                      # nothing qualifies
+]
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 4097, 100_003])
+@pytest.mark.parametrize("pi", range(len(PRED_SETS)))
+def test_build_parity(n, pi):
+    cols = _rand_cols(n, 1000 + n + pi)
+    preds = PRED_SETS[pi]
+    g, gs = _gpu_build(cols, preds, TARGETS)
+    o, os_ = _oracle_build(cols, preds, TARGETS)
+    assert gs == os_
+    for a, b in zip(g, o):
+        assert np.array_equal(a, b)
+
+
+def test_build_parity_global_atomic_path_and_skew():
+    """A sketch too large for shared memory (C4 shape d=9, w=16384) next to a privatised one."""
+    cols = _rand_cols(300_001, 77)
+    tg = [(["zk"], 9, [16384], ["F.key1|D1.key"]), (["k64"], 9, [16384], ["F.key2|D2.key"]), (["k32"], 5, [1024], ["x|y"])]
+    preds = [("p", pb.RANGE, I64MIN, 36)]
+    g, gs = _gpu_build(cols, preds, tg)
+    o, os_ = _oracle_build(cols, preds, tg)
+    assert gs == os_ and all(np.array_equal(a, b) for a, b in zip(g, o))
+
+
+def test_sharded_calls_accumulate_and_merge_is_exact():
+    cols = _rand_cols(200_000, 5)
+    preds = PRED_SETS[2]
+    one, s1 = _gpu_build(cols, preds, TARGETS, calls=1)
+    many, s8 = _gpu_build(cols, preds, TARGETS, calls=8)
+    assert s1 == s8 and all(np.array_equal(a, b) for a, b in zip(one, many))
+    # sketch_merge of two independently built halves
+    names = list(cols)
+    dcols = _to_dev(cols)
+    half = 100_000
+    sks = []
+    for a, b in ((0, half), (half, 200_000)):
+        sk = pb.Sketch(5, [1024], ["A.k32|B.x"], 42, _dev())
+        pb.sketch_update_filtered([dcols[c][a:b].contiguous() for c in names], b - a,
+                                  [(names.index("p"), pb.RANGE, 10, 69)], [(sk, [names.index("k32")])])
+        sks.append(sk)
+    pb.sketch_merge(sks[0], sks[1])
+    full = oracle.build([cols["k32"]], oracle.filter_mask(cols, [("p", pb.RANGE, 10, 69)])[0], 5, [1024], ["A.k32|B.x"])
+    assert np.array_equal(sks[0].counters.cpu().numpy(), full)
+    other = pb.Sketch(5, [1024], ["A.k32|B.y"], 42, _dev())
+    with pytest.raises(pb.SkError) as ei:
+        pb.sketch_merge(sks[0], other)
+    assert ei.value.status == pb.SK_EMISMATCH
+
+
+def test_invalid_arguments_fail_loudly():
+    with pytest.raises(pb.SkError) as ei:
+        pb.Sketch(4, [1024], ["a|b"], 42, _dev())
+    assert ei.value.status == pb.SK_EINVAL
+    with pytest.raises(pb.SkError):
+        pb.Sketch(5, [1000], ["a|b"], 42, _dev())
+    with pytest.raises(pb.SkError):
+        pb.Sketch(5, [64, 64], ["z|z", "a|a"], 42, _dev())   # dims not in canonical order
+
+
+# ------------------------------------------------------------------ estimates on random networks
+def _random_graph(rng, topo, w, d, vmax, mat_prob=0.5):
+    T = 1 + max(max(e) for e in topo)
+    names = [f"t{i}" for i in range(T)]
+    eids = [f"{names[u]}.c{i}|{names[v]}.c{i}" for i, (u, v) in enumerate(topo)]
+    widths = {e: int(w * 2 ** rng.integers(0, 2)) for e in eids}
+    vec_np, mat_np = {}, {}
+    for i, (u, v) in enumerate(topo):
+        for t in (u, v):
+            vec_np[(names[t], eids[i])] = rng.integers(-vmax, vmax + 1, (d, widths[eids[i]])).astype(np.int64)
+    for t in range(T):
+        inc = sorted(eids[i] for i, e in enumerate(topo) if t in e)
+        if len(inc) == 2 and rng.random() < mat_prob:
+            mat_np[(names[t], tuple(inc))] = rng.integers(-vmax, vmax + 1, (d, w, w)).astype(np.int64)
+    og = oracle.Graph({n: int(rng.integers(1, 1000)) for n in names}, [(eids[i], names[u], names[v]) for i, (u, v) in enumerate(topo)],
+                      vec_np, mat_np)
+    sk = {}
+    for key, arr in vec_np.items():
+        s = pb.Sketch(d, [arr.shape[1]], [key[1]], 42, _dev())
+        s.counters.copy_(torch.from_numpy(arr))
+        sk[key] = s
+    mats = []
+    for (t, inc), arr in mat_np.items():
+        s = pb.Sketch(d, [w, w], list(inc), 42, _dev())
+        s.counters.copy_(torch.from_numpy(arr))
+        mats.append((names.index(t), eids.index(inc[0]), eids.index(inc[1]), s))
+    edges = [(u, v, sk[(names[u], eids[i])], sk[(names[v], eids[i])]) for i, (u, v) in enumerate(topo)]
+    jg = pb.JoinGraph(names, [og.tables[n] for n in names], edges, mats)
+    return og, jg, (sk, mats)
+
+
+TOPOS = [
+    [(0, 1)], [(0, 1), (1, 2)], [(0, 1), (1, 2), (2, 3), (3, 4)], [(0, 1), (1, 2), (0, 2)],
+    [(1, 0), (0, 2), (1, 2), (2, 3), (1, 4)], [(0, 1), (0, 2), (0, 3)], [(0, 1), (1, 2), (2, 3), (3, 0)],
+    [(2, 1), (0, 1), (3, 1), (2, 0)], [(0, 1), (1, 2), (2, 3), (3, 4), (4, 0)],
+]
+
+
+@pytest.mark.parametrize("ti", range(len(TOPOS)))
+def test_estimates_equal_oracle_on_random_networks(ti):
+    rng = np.random.default_rng(300 + ti)
+    for trial in range(3):
+        og, jg, keep = _random_graph(rng, TOPOS[ti], w=8, d=3, vmax=[3, 1000, 2**40][trial])
+        for s in oracle.connected_subplans(og):
+            want = oracle.estimate_rows(og, s)
+            got = jg.estimate_join_exact(s)
+            assert got == want, (ti, trial, s)
+            est, rows = jg.estimate_join(s)
+            assert est == float(oracle.median_odd(want)) and rows == [float(v) for v in want]
+        assert tuple(jg.plan_greedy()) == tuple(oracle.plan_greedy(og))
+
+
+# ------------------------------------------------------------------ workloads C1-C5
+def _run_workload(ws, device=None):
+    device = device or _dev()
+    run = QueryRun(ws, device)
+    data_d, data_h, preds = {}, {}, {}
+    for t in ws.tables:
+        data_d[t.name] = datagen.generate_table(ws, t.name, device)
+        data_h[t.name] = {k: v.cpu().numpy() for k, v in data_d[t.name].items()}
+        preds[t.name] = datagen.resolve_preds(ws, t.name)
+    run.build(data_d, preds)
+    torch.cuda.synchronize()
+    return run, data_h, preds
+
+
+def _oracle_workload(ws, data_h, preds):
+    vec, mat, surv = {}, {}, {}
+    for t in ws.tables:
+        mask, cnt = oracle.filter_mask(data_h[t.name], preds[t.name])
+        surv[t.name] = cnt
+        for s in ws.sketches_of(t.name):
+            arr = oracle.build([data_h[t.name][k] for k in s.key_cols], mask, s.d, s.w, s.edge_ids, master=ws.master_seed)
+            if len(s.w) == 1:
+                vec[(t.name, s.edge_ids[0])] = arr
+            else:
+                mat[(t.name, tuple(s.edge_ids))] = arr
+    return oracle.Graph(surv, ws.edges, vec, mat), surv
+
+
+def _check_counters(ws, run, og, surv):
+    assert run.survivors.tolist() == [surv[t.name] for t in ws.tables]
+    for s, sk in zip(ws.sketches, run.sketches):
+        want = og.vec[(s.table, s.edge_ids[0])] if len(s.w) == 1 else og.mat[(s.table, tuple(s.edge_ids))]
+        assert np.array_equal(sk.counters.cpu().numpy(), want), (s.table, s.edge_ids)
+
+
+def test_c1_end_to_end():
+    ws = datagen.c1()
+    run, data_h, preds = _run_workload(ws)
+    og, surv = _oracle_workload(ws, data_h, preds)
+    _check_counters(ws, run, og, surv)
+    jg = run.graph()
+    assert jg.estimate_join_exact(("R", "S")) == oracle.estimate_rows(og, ("R", "S"))
+    est, _ = jg.estimate_join(("R", "S"))
+    assert est == oracle.estimate(og, ("R", "S"))[0]
+    assert list(jg.plan_greedy()[0]) == oracle.plan_greedy(og)[0]
+
+
+def _all_subplans_match(ws, run, og, rows=None):
+    jg = run.graph()
+    for s in oracle.connected_subplans(og):
+        want = oracle.estimate_rows(og, s, rows=rows)
+        got = jg.estimate_join_exact(s)
+        if rows is not None:
+            got = [got[r] for r in rows]
+        assert got == want, s
+    return jg
+
+
+def test_c2_scaled_chain_parity():
+    ws = datagen.c2(scale=0.01)
+    run, data_h, preds = _run_workload(ws)
+    og, surv = _oracle_workload(ws, data_h, preds)
+    _check_counters(ws, run, og, surv)
+    jg = _all_subplans_match(ws, run, og)
+    order, pre, cost = jg.plan_greedy()
+    o_order, o_pre, o_cost = oracle.plan_greedy(og)
+    assert order == o_order and pre == o_pre and cost == o_cost
+
+
+def test_c3_scaled_parity_all_14_subplans_and_plan():
+    ws = datagen.c3(scale=0.005, w=256)
+    run, data_h, preds = _run_workload(ws)
+    og, surv = _oracle_workload(ws, data_h, preds)
+    _check_counters(ws, run, og, surv)
+    jg = _all_subplans_match(ws, run, og)
+    assert tuple(jg.plan_greedy()) == tuple(oracle.plan_greedy(og))
+
+
+@pytest.mark.parametrize("cycle", [False, True])
+def test_c5_scaled_parity_all_subplans_and_plan(cycle):
+    ws = datagen.c5(scale=2e-4, cycle=cycle, w=128, wm=64)
+    run, data_h, preds = _run_workload(ws)
+    og, surv = _oracle_workload(ws, data_h, preds)
+    _check_counters(ws, run, og, surv)
+    jg = _all_subplans_match(ws, run, og)
+    assert tuple(jg.plan_greedy()) == tuple(oracle.plan_greedy(og))
+
+
+def test_c3_full_width_triangle_sampled_row():
+    """C3 at its full sketch shape (d=7, w=4096), rows scaled: the triangle and the
+    5-table sub-plan, row 0 only (the oracle's cost is O(w^2 log w) big-int ops)."""
+    ws = datagen.c3(scale=0.01)
+    run, data_h, preds = _run_workload(ws)
+    og, surv = _oracle_workload(ws, data_h, preds)
+    _check_counters(ws, run, og, surv)
+    jg = run.graph()
+    for s in [("CI", "MK", "T"), ("CI", "K", "MK", "N", "T")]:
+        assert jg.estimate_join_exact(s)[0] == oracle.estimate_rows(og, s, rows=[0])[0]
