@@ -292,15 +292,16 @@ __global__ void k_node_merged(const __grid_constant__ Node n, const __grid_const
     }
     __syncthreads();
     // --- enumerate the other legs
-    int qp = -1, qf = -1, qo2 = -1;
+    int qp = -1, qf = -1, oc[2] = {-1, -1}, noc = 0;
     for (int q = 0; q < n.nl; ++q) {
         if (q == qc) continue;
         if (n.role[q] == RPARENT) qp = q;
         else if (n.role[q] == RFIXED) qf = q;
-        else qo2 = q;  // another child leg
+        else oc[noc++] = q;  // other child legs
     }
-    const int qo = qp >= 0 ? qp : qo2;       // outer
-    const int qi = qp >= 0 ? qo2 : -1;       // inner (other child, when a parent exists)
+    // outer leg: the parent if any, else the first other child; inner: the remaining other child
+    const int qo = qp >= 0 ? qp : oc[0];
+    const int qi = qp >= 0 ? oc[0] : oc[1];
     const int wo = qo >= 0 ? n.w[qo] : 1;
     const int wi = qi >= 0 ? n.w[qi] : 1;
     const uint64_t *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row(n, qo, k, r, bb, 0) : nullptr;

@@ -1,0 +1,649 @@
+// scan.cu — the optimised fused scan of sketch_update_filtered.
+//
+// Persistent kernel, one CTA per SM, 16 consumer warps + 1 producer warp.
+//   A1  The producer streams 2048-row tiles of the staged columns (predicate
+//       columns; key columns too when the table has no predicate) HBM -> smem
+//       with cp.async.bulk (TMA bulk copies, UBLKCP) into a 3-stage ring
+//       guarded by mbarriers (full: tx-count; empty: consumer release).
+//   A2  Consumers read 4 rows per lane with 128-bit shared loads and evaluate
+//       the conjunction of point / range / subset predicates.
+//   A3  Survivors are compacted per warp (popc prefix) into a per-tile list; the
+//       key columns of survivors only are gathered with cp.async (LDGSTS,
+//       sector-granular HBM traffic) one tile ahead of their use.
+//   A4  Hashes mod 2^61-1 on the integer pipe (hash.cuh).
+//   A5  Keys are aggregated per warp with __match_any_sync (leader adds
+//       count * xi, exact by linearity).  1-D sketches that fit
+//       are privatised as int32 in smem; others get a per-CTA heavy-hitter
+//       table (canonical key -> count) flushed once, misses go to L2 atomics.
+//   A6  Matrix sketches: per-survivor cell update, smem or L2.
+//   A7  CTA flush: int32 smem counters and heavy-hitter counts -> int64 HBM
+//       sketch with red.global.add (order-independent, bit-exact).
+#include <stdint.h>
+
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+#include "hash.cuh"
+#include "internal.cuh"
+#include "scan.cuh"
+
+using namespace skb;
+
+namespace {
+
+constexpr int kTile = 2048;
+constexpr int kWarps = 16;
+constexpr int kConsumers = kWarps * 32;
+constexpr int kThreads = kConsumers + 32;
+constexpr int kStages = 4;
+constexpr int kMaxSCols = 8, kMaxSPreds = 8, kMaxKeys = 4, kMaxSTargets = 16;
+constexpr uint64_t kEmpty = ~0ULL;   // canonical keys are < 2^61: never equal
+
+struct SCol {
+    const void *p;
+    uint32_t bytes;       // 4 or 8
+    int32_t soff;         // byte offset inside a stage, -1 = not staged
+};
+enum { PR_R32 = 0, PR_R64 = 1, PR_SET = 2, PR_NONE = 3 };
+struct SPred {
+    uint32_t col, kind;   // PR_R32: (uint32)(v - lo32) <= span32; PR_R64: (uint64)(v - lo) <= span; PR_NONE: no row
+    int64_t lo;           // POINT c is RANGE [c, c]
+    uint64_t span;
+    const int64_t *set;
+    uint32_t n;
+};
+struct SKey {
+    uint32_t col;
+    int32_t hh_off;       // byte offset of this key's heavy-hitter table, -1 = none
+    uint32_t has1d;       // some 1-D target hashes this key
+    uint32_t hasglob;     // some non-privatised 1-D target hashes this key
+};
+struct STarget {
+    int64_t *counters;
+    uint32_t ndim, d, wmask0, wmask1, lw1;
+    uint32_t k0, k1;      // indices into keys[]
+    int32_t smem_off;     // int32 offset of privatised copy, -1 = global
+    uint32_t cells;
+    uint32_t seed_off;
+};
+struct SParams {
+    SCol col[kMaxSCols];
+    SPred pred[kMaxSPreds];
+    SKey key[kMaxKeys];
+    STarget tgt[kMaxSTargets];
+    const uint64_t *seeds[kMaxSTargets];
+    uint32_t n_cols, n_preds, n_keys, n_targets;
+    uint64_t n_rows, n_tiles;
+    uint32_t stage_bytes;
+    uint32_t gather;      // 1: survivors' keys gathered, 0: keys staged (no predicate)
+    uint32_t cap;         // entries of each warp's survivor-key ring (power of two)
+    uint32_t kb_bytes;    // bytes of one warp's ring
+    uint32_t hh_log2;     // heavy-hitter slots per key = 1 << hh_log2
+    // smem layout (byte offsets)
+    uint32_t off_ring, off_kbuf, off_hh, off_sc, off_seed;
+    uint32_t smem_counters, seed_words;
+    unsigned long long *survivors;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all_but1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
+__device__ __forceinline__ void red_add_s64(int64_t *p, int64_t v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ------------------------------------------------------------------ column access
+__device__ __forceinline__ int64_t gval(const SCol &c, uint64_t row) {
+    if (c.bytes == 8) return __ldg(reinterpret_cast<const long long *>(c.p) + row);
+    return (int64_t)__ldg(reinterpret_cast<const int *>(c.p) + row);
+}
+
+__device__ __forceinline__ bool in_set(const int64_t *s, uint32_t n, int64_t v) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(reinterpret_cast<const long long *>(s) + mid) < v) lo = mid + 1; else hi = mid;
+    }
+    return lo < n && __ldg(reinterpret_cast<const long long *>(s) + lo) == v;
+}
+
+// conjunction of the predicates over this lane's 4 rows -> bit mask (A2)
+__device__ __forceinline__ uint32_t eval_preds(const SParams &P, const unsigned char *stage, bool staged,
+                                               uint64_t row0, int r0, int valid) {
+    uint32_t bits = (1u << valid) - 1u;
+    for (uint32_t q = 0; q < P.n_preds; ++q) {
+        const SPred &pr = P.pred[q];
+        const SCol &c = P.col[pr.col];
+        if (pr.kind == PR_R32) {
+            int4 v;
+            if (staged) v = *reinterpret_cast<const int4 *>(stage + c.soff + r0 * 4);
+            else {
+                const int *g = reinterpret_cast<const int *>(c.p) + row0 + r0;
+                v.x = valid > 0 ? __ldg(g) : 0; v.y = valid > 1 ? __ldg(g + 1) : 0;
+                v.z = valid > 2 ? __ldg(g + 2) : 0; v.w = valid > 3 ? __ldg(g + 3) : 0;
+            }
+            const uint32_t lo = (uint32_t)pr.lo, sp = (uint32_t)pr.span;
+            const uint32_t m = ((uint32_t)v.x - lo <= sp) | (((uint32_t)v.y - lo <= sp) << 1) |
+                               (((uint32_t)v.z - lo <= sp) << 2) | (((uint32_t)v.w - lo <= sp) << 3);
+            bits &= m;
+        } else if (pr.kind == PR_R64) {
+            int64_t v[4];
+            if (staged) {
+                const longlong2 a = *reinterpret_cast<const longlong2 *>(stage + c.soff + r0 * 8);
+                const longlong2 b = *reinterpret_cast<const longlong2 *>(stage + c.soff + r0 * 8 + 16);
+                v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = j < valid ? gval(c, row0 + r0 + j) : 0;
+            }
+            uint32_t m = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) m |= (uint32_t)((uint64_t)v[j] - (uint64_t)pr.lo <= pr.span) << j;
+            bits &= m;
+        } else if (pr.kind == PR_SET) {
+            uint32_t b = bits;
+            while (b) {
+                const int j = __ffs(b) - 1;
+                b &= b - 1;
+                const int64_t v = staged ? (c.bytes == 8 ? *reinterpret_cast<const int64_t *>(stage + c.soff + (r0 + j) * 8)
+                                                         : (int64_t) * reinterpret_cast<const int *>(stage + c.soff + (r0 + j) * 4))
+                                         : gval(c, row0 + r0 + j);
+                if (!in_set(pr.set, pr.n, v)) bits &= ~(1u << j);
+            }
+        } else {
+            bits = 0;
+        }
+    }
+    return bits;
+}
+
+// values of rows [r0, r0+4) of column c within the tile (staged: 128-bit smem reads)
+__device__ __forceinline__ void load4(const SParams &P, const SCol &c, const unsigned char *stage, bool staged,
+                                      uint64_t tile_row0, int r0, int valid, int64_t v[4]) {
+    if (staged && c.soff >= 0) {
+        if (c.bytes == 4) {
+            const int4 q = *reinterpret_cast<const int4 *>(stage + c.soff + r0 * 4);
+            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        } else {
+            const longlong2 a = *reinterpret_cast<const longlong2 *>(stage + c.soff + r0 * 8);
+            const longlong2 b = *reinterpret_cast<const longlong2 *>(stage + c.soff + r0 * 8 + 16);
+            v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = (j < valid) ? gval(c, tile_row0 + r0 + j) : 0;
+    }
+}
+
+// ------------------------------------------------------------------ heavy-hitter table
+__device__ __forceinline__ bool hh_add(unsigned char *tab, uint32_t log2s, uint64_t x, int cnt) {
+    uint64_t *keys = reinterpret_cast<uint64_t *>(tab);
+    int *cnts = reinterpret_cast<int *>(tab + (8u << log2s));
+    const uint32_t mask = (1u << log2s) - 1;
+    const uint32_t h = (uint32_t)((x * 0x9E3779B97F4A7C15ULL) >> (64 - log2s));
+#pragma unroll 1
+    for (uint32_t probe = 0; probe < 8; ++probe) {
+        const uint32_t s = (h + probe) & mask;
+        const uint64_t k = *reinterpret_cast<volatile uint64_t *>(&keys[s]);
+        if (k == x) { atomicAdd(&cnts[s], cnt); return true; }
+        if (k == kEmpty) {
+            const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long *>(&keys[s]), kEmpty, x);
+            if (prev == kEmpty || prev == x) { atomicAdd(&cnts[s], cnt); return true; }
+        }
+    }
+    return false;
+}
+
+// ------------------------------------------------------------------ sketch updates
+// 1-D target t: row r gets cnt * xi_r(x) at bucket h_r(x)
+__device__ __forceinline__ void update_1d(const SParams &P, const STarget &tg, const uint64_t *seed, int32_t *sc,
+                                          uint64_t x, int cnt) {
+    for (uint32_t r = 0; r < tg.d; ++r) {
+        const uint64_t *a = seed + r * 6;
+        const uint32_t cell = (uint32_t)(hash_g61(a[4], a[5], x) & tg.wmask0);
+        const int v = xi_sign61(a, x) * cnt;
+        if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
+        else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
+    }
+}
+
+__device__ __forceinline__ void update_2d(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, uint64_t y) {
+    const uint64_t *s1 = seed + tg.d * 6;
+    for (uint32_t r = 0; r < tg.d; ++r) {
+        const uint64_t *a = seed + r * 6, *b = s1 + r * 6;
+        const uint32_t cell = ((uint32_t)(hash_g61(a[4], a[5], x) & tg.wmask0) << tg.lw1) |
+                              (uint32_t)(hash_g61(b[4], b[5], y) & tg.wmask1);
+        const int v = xi_sign61(a, x) * xi_sign61(b, y);
+        if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
+        else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
+    }
+}
+
+// one warp-wide batch: lanes with `valid` hold one surviving tuple each, keys x[k]
+__device__ __forceinline__ void process_batch(const SParams &P, unsigned char *smem, bool valid, const uint64_t *x) {
+    const uint32_t act = __ballot_sync(0xffffffffu, valid);
+    if (!act) return;
+    int32_t *sc = reinterpret_cast<int32_t *>(smem + P.off_sc);
+    const uint64_t *seeds = reinterpret_cast<const uint64_t *>(smem + P.off_seed);
+    const int lane = threadIdx.x & 31;
+    // 1-D targets: aggregate equal keys of the warp (match_any), leader updates with the count
+    for (uint32_t k = 0; k < P.n_keys; ++k) {
+        if (!P.key[k].has1d) continue;
+        bool leader = false, miss = false;
+        int cnt = 0;
+        if (valid) {
+            const uint32_t grp = __match_any_sync(act, x[k]);
+            leader = lane == __ffs(grp) - 1;
+            cnt = __popc(grp);
+        }
+        if (leader) {
+            bool done = false;
+            if (P.key[k].hh_off >= 0) done = hh_add(smem + P.key[k].hh_off, P.hh_log2, x[k], cnt);
+            miss = !done;
+            for (uint32_t t = 0; t < P.n_targets; ++t) {
+                const STarget &tg = P.tgt[t];
+                if (tg.ndim != 1 || tg.k0 != k || tg.smem_off < 0) continue;
+                update_1d(P, tg, seeds + tg.seed_off, sc, x[k], cnt);   // privatised: always direct
+            }
+        }
+        if (P.key[k].hasglob) {
+            // keys that did not get a heavy-hitter slot: warp-cooperative L2 updates,
+            // lane r handles sketch row r (SIMT-efficient instead of one lane doing d rows)
+            uint32_t mb = __ballot_sync(0xffffffffu, miss);
+            while (mb) {
+                const int src = __ffs(mb) - 1;
+                mb &= mb - 1;
+                const uint64_t xv = __shfl_sync(0xffffffffu, x[k], src);
+                const int cv = __shfl_sync(0xffffffffu, cnt, src);
+                for (uint32_t t = 0; t < P.n_targets; ++t) {
+                    const STarget &tg = P.tgt[t];
+                    if (tg.ndim != 1 || tg.k0 != k || tg.smem_off >= 0) continue;
+                    for (uint32_t r = lane; r < tg.d; r += 32) {
+                        const uint64_t *a = seeds + tg.seed_off + r * 6;
+                        const uint32_t cell = (uint32_t)(hash_g61(a[4], a[5], xv) & tg.wmask0);
+                        red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)(xi_sign61(a, xv) * cv));
+                    }
+                }
+            }
+        }
+    }
+    // matrix targets: one cell per surviving tuple and row
+    if (valid) {
+        for (uint32_t t = 0; t < P.n_targets; ++t) {
+            const STarget &tg = P.tgt[t];
+            if (tg.ndim != 2) continue;
+            update_2d(tg, seeds + tg.seed_off, sc, x[tg.k0], x[tg.k1]);
+        }
+    }
+}
+
+// raw key of queue slot `slot` for key k (int32 keys use the low 4 bytes of an 8-byte slot)
+__device__ __forceinline__ uint64_t queue_key(const SParams &P, const unsigned char *q, uint32_t slot, uint32_t k) {
+    const unsigned char *p = q + (slot * P.n_keys + k) * 8;
+    return canon61(P.col[P.key[k].col].bytes == 8 ? *reinterpret_cast<const int64_t *>(p)
+                                                  : (int64_t) * reinterpret_cast<const int32_t *>(p));
+}
+
+// process queue entries [head, head + n) (n <= 32) as one batch
+__device__ __forceinline__ void drain_batch(const SParams &P, unsigned char *smem, const unsigned char *q, uint32_t head, uint32_t n) {
+    const int lane = threadIdx.x & 31;
+    const bool valid = (uint32_t)lane < n;
+    uint64_t xk[kMaxKeys] = {0, 0, 0, 0};
+    if (valid)
+        for (uint32_t k = 0; k < P.n_keys; ++k) xk[k] = queue_key(P, q, (head + lane) & (P.cap - 1), k);
+    process_batch(P, smem, valid, xk);
+}
+
+template <int NK>
+__global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SParams P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+    uint64_t *empty = full + kStages;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    // ---- setup: barriers, smem counters, heavy-hitter tables, seeds
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kWarps); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    {
+        int32_t *sc = reinterpret_cast<int32_t *>(smem + P.off_sc);
+        for (uint32_t i = tid; i < P.smem_counters; i += kThreads) sc[i] = 0;
+        for (uint32_t k = 0; k < P.n_keys; ++k) {
+            if (P.key[k].hh_off < 0) continue;
+            uint64_t *keys = reinterpret_cast<uint64_t *>(smem + P.key[k].hh_off);
+            int *cnts = reinterpret_cast<int *>(smem + P.key[k].hh_off + (8u << P.hh_log2));
+            for (uint32_t i = tid; i < (1u << P.hh_log2); i += kThreads) { keys[i] = kEmpty; cnts[i] = 0; }
+        }
+        uint64_t *sseed = reinterpret_cast<uint64_t *>(smem + P.off_seed);
+        for (uint32_t t = 0; t < P.n_targets; ++t) {
+            const uint32_t words = P.tgt[t].ndim * P.tgt[t].d * 6;
+            for (uint32_t i = tid; i < words; i += kThreads) sseed[P.tgt[t].seed_off + i] = P.seeds[t][i];
+        }
+    }
+    __syncthreads();
+
+    if (warp == kWarps) {
+        // ================= producer warp: TMA bulk copies of staged columns
+        if (lane == 0) {
+            uint32_t i = 0;
+            for (uint64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x, ++i) {
+                const uint32_t s = i % kStages;
+                if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
+                const uint64_t row0 = t * kTile;
+                const bool fulltile = row0 + kTile <= P.n_rows;
+                if (fulltile && P.stage_bytes) {
+                    mbar_arrive_tx(&full[s], P.stage_bytes);
+                    unsigned char *stage = smem + P.off_ring + s * P.stage_bytes;
+                    for (uint32_t c = 0; c < P.n_cols; ++c) {
+                        if (P.col[c].soff < 0) continue;
+                        const uint32_t b = P.col[c].bytes;
+                        bulk_g2s(stage + P.col[c].soff, reinterpret_cast<const unsigned char *>(P.col[c].p) + row0 * b,
+                                 kTile * b, &full[s]);
+                    }
+                } else {
+                    mbar_arrive(&full[s]);
+                }
+            }
+        }
+        return;
+    }
+
+    // ================= consumer warps: independent pipelines, no CTA-wide barrier in the loop
+    uint32_t my_surv = 0;
+    const int r0 = warp * 128 + lane * 4;   // this lane's 4 rows inside a tile
+    unsigned char *q = smem + P.off_kbuf + warp * P.kb_bytes;   // this warp's survivor-key ring
+    uint32_t head = 0, tail = 0;             // ring positions (monotone)
+    uint32_t i = 0;
+    for (uint64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x, ++i) {
+        const uint64_t row0 = t * kTile;
+        const uint32_t s = i % kStages;
+        mbar_wait(&full[s], (i / kStages) & 1);
+        const unsigned char *stage = smem + P.off_ring + s * P.stage_bytes;
+        const bool staged = (row0 + kTile <= P.n_rows) && P.stage_bytes;
+        const int64_t rem = (int64_t)P.n_rows - (int64_t)(row0 + r0);
+        const int valid = rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem);
+        const uint32_t bits = eval_preds(P, stage, staged, row0, r0, valid);
+        const int cnt = __popc(bits);
+        my_surv += cnt;
+        if (P.gather) {
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int n = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += n;
+            }
+            const uint32_t wtot = (uint32_t)__shfl_sync(0xffffffffu, incl, 31);
+            if (tail - head + wtot > P.cap) {
+                // ring would overflow: finish outstanding gathers and drain every full batch
+                cp_wait_all();
+                __syncwarp();
+                while (tail - head >= 32) { drain_batch(P, smem, q, head, 32); head += 32; }
+            }
+            // survivors' keys: sector-granular gathers into the ring
+            uint32_t pos = tail + (uint32_t)(incl - cnt);
+            uint32_t b = bits;
+            while (b) {
+                const int j = __ffs(b) - 1;
+                b &= b - 1;
+                const uint64_t row = row0 + r0 + j;
+                unsigned char *dst = q + (pos & (P.cap - 1)) * (NK * 8);
+#pragma unroll
+                for (int k = 0; k < NK; ++k) {
+                    const SCol &c = P.col[P.key[k].col];
+                    if (c.bytes == 8) cp_async8(dst + k * 8, reinterpret_cast<const long long *>(c.p) + row);
+                    else cp_async4(dst + k * 8, reinterpret_cast<const int *>(c.p) + row);
+                }
+                ++pos;
+            }
+            cp_commit();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);          // this warp is done with stage s
+            const uint32_t ready_end = tail;                 // entries of earlier tiles
+            tail += wtot;
+            cp_wait_all_but1();
+            __syncwarp();
+            while (ready_end - head >= 32) { drain_batch(P, smem, q, head, 32); head += 32; }
+        } else {
+            // keys are staged (no predicate): aggregate and update straight from the stage
+            uint64_t xs[4][kMaxKeys];
+            for (uint32_t k = 0; k < P.n_keys; ++k) {
+                int64_t v[4];
+                load4(P, P.col[P.key[k].col], stage, staged, row0, r0, valid, v);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) xs[j][k] = canon61(v[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) process_batch(P, smem, (bits >> j) & 1u, xs[j]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+    }
+    if (P.gather) {
+        cp_wait_all();
+        __syncwarp();
+        while (tail - head > 0) {
+            const uint32_t n = min(32u, tail - head);
+            drain_batch(P, smem, q, head, n);
+            head += n;
+        }
+    }
+
+    // ---- exact survivor count
+    const uint32_t ws = __reduce_add_sync(0xffffffffu, my_surv);
+    if (lane == 0 && ws && P.survivors) atomicAdd(P.survivors, (unsigned long long)ws);
+    consumer_sync();
+    // ---- flush heavy-hitter tables (one hash evaluation per distinct key per CTA)
+    int32_t *sc = reinterpret_cast<int32_t *>(smem + P.off_sc);
+    const uint64_t *seeds = reinterpret_cast<const uint64_t *>(smem + P.off_seed);
+    for (uint32_t k = 0; k < P.n_keys; ++k) {
+        if (P.key[k].hh_off < 0) continue;
+        const uint64_t *keys = reinterpret_cast<const uint64_t *>(smem + P.key[k].hh_off);
+        const int *cnts = reinterpret_cast<const int *>(smem + P.key[k].hh_off + (8u << P.hh_log2));
+        for (uint32_t s = tid; s < (1u << P.hh_log2); s += kConsumers) {
+            const uint64_t x = keys[s];
+            const int c = cnts[s];
+            if (x == kEmpty || c == 0) continue;
+            for (uint32_t tt = 0; tt < P.n_targets; ++tt) {
+                const STarget &tg = P.tgt[tt];
+                if (tg.ndim != 1 || tg.k0 != k || tg.smem_off >= 0) continue;
+                update_1d(P, tg, seeds + tg.seed_off, sc, x, c);
+            }
+        }
+    }
+    // ---- flush privatised int32 counters into the int64 sketches
+    for (uint32_t tt = 0; tt < P.n_targets; ++tt) {
+        const STarget &tg = P.tgt[tt];
+        if (tg.smem_off < 0) continue;
+        const uint32_t n = tg.d * tg.cells;
+        for (uint32_t qq = tid; qq < n; qq += kConsumers) {
+            const int32_t v = sc[tg.smem_off + qq];
+            if (v) red_add_s64(tg.counters + qq, (int64_t)v);
+        }
+    }
+}
+
+}  // namespace
+
+namespace skb {
+
+// Returns SK_OK and sets *launched if the optimised scan handled the call; leaves
+// *launched false (and returns SK_OK) when the call is outside its envelope.
+sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
+    *launched = false;
+    if (c.n_cols > kMaxSCols || c.n_preds > kMaxSPreds || c.n_targets > kMaxSTargets || c.n_rows == 0) return SK_OK;
+    SParams P;
+    memset(&P, 0, sizeof(P));
+    P.n_cols = c.n_cols;
+    P.n_rows = c.n_rows;
+    P.n_tiles = (c.n_rows + kTile - 1) / kTile;
+    for (uint32_t i = 0; i < c.n_cols; ++i) {
+        P.col[i].p = c.col_ptr[i];
+        P.col[i].bytes = c.col_bytes[i];
+        P.col[i].soff = -1;
+        if (((uintptr_t)c.col_ptr[i]) & 15) return SK_OK;   // bulk copies need 16-byte alignment
+    }
+    // distinct key columns
+    std::vector<uint32_t> keys;
+    for (uint32_t t = 0; t < c.n_targets; ++t)
+        for (uint32_t q = 0; q < c.tgt_ndim[t]; ++q)
+            if (std::find(keys.begin(), keys.end(), c.tgt_key[t][q]) == keys.end()) keys.push_back(c.tgt_key[t][q]);
+    if (keys.size() > (size_t)kMaxKeys) return SK_OK;
+    P.n_keys = (uint32_t)keys.size();
+    P.n_preds = c.n_preds;
+    for (uint32_t q = 0; q < c.n_preds; ++q) {
+        SPred &pr = P.pred[q];
+        pr.col = c.pred_col[q];
+        pr.set = c.pred_set[q];
+        pr.n = c.pred_n[q];
+        int64_t lo = c.pred_lo[q], hi = c.pred_kind[q] == SK_PRED_POINT ? c.pred_lo[q] : c.pred_hi[q];
+        if (c.pred_kind[q] == SK_PRED_SUBSET) { pr.kind = pr.n ? PR_SET : PR_NONE; continue; }
+        if (c.col_bytes[pr.col] == 4) {
+            lo = std::max<int64_t>(lo, INT32_MIN);
+            hi = std::min<int64_t>(hi, INT32_MAX);
+            if (lo > hi) { pr.kind = PR_NONE; continue; }
+            pr.kind = PR_R32;
+            pr.lo = (int64_t)(uint32_t)(int32_t)lo;
+            pr.span = (uint32_t)((int32_t)hi - (int32_t)lo);
+        } else {
+            if (lo > hi) { pr.kind = PR_NONE; continue; }
+            pr.kind = PR_R64;
+            pr.lo = lo;
+            pr.span = (uint64_t)hi - (uint64_t)lo;
+        }
+    }
+    P.gather = c.n_preds > 0 ? 1u : 0u;
+    // staged columns: predicate columns, plus key columns when there is no predicate
+    uint32_t soff = 0;
+    auto stage_col = [&](uint32_t col) {
+        if (P.col[col].soff >= 0) return;
+        P.col[col].soff = (int32_t)soff;
+        soff += kTile * P.col[col].bytes;
+    };
+    for (uint32_t q = 0; q < c.n_preds; ++q) stage_col(c.pred_col[q]);
+    if (!P.gather) for (uint32_t k : keys) stage_col(k);
+    P.stage_bytes = soff;
+    // smem budget
+    const uint32_t kBudget = 227 * 1024;
+    uint32_t off = 128;                                  // barriers
+    P.off_ring = off;
+    off += kStages * P.stage_bytes;
+    off = (off + 15) & ~15u;
+    uint32_t seed_words = 0;
+    for (uint32_t t = 0; t < c.n_targets; ++t) seed_words += c.tgt_ndim[t] * c.tgt_d[t] * 6;
+    P.seed_words = seed_words;
+    const uint32_t fixed_tail = seed_words * 8 + 64;
+    if (off + fixed_tail > kBudget) return SK_OK;
+    for (uint32_t k = 0; k < P.n_keys; ++k) P.key[k].col = keys[k];
+    // per-warp survivor-key rings (gather mode): cap entries x n_keys x 8 bytes
+    P.cap = 0;
+    if (P.gather) {
+        for (uint32_t cap = 512; cap >= 256; cap /= 2)
+            if (off + kWarps * cap * P.n_keys * 8 + fixed_tail <= kBudget - 24 * 1024) { P.cap = cap; break; }
+        if (P.cap == 0) return SK_OK;                   // cap must exceed 128 + 31 (one tile + a partial batch)
+        P.kb_bytes = P.cap * P.n_keys * 8;
+        P.off_kbuf = off;
+        off += kWarps * P.kb_bytes;
+    }
+    uint32_t avail = kBudget - off - fixed_tail;
+    // privatise targets in declaration order while they fit (leave room for heavy hitters)
+    P.n_targets = c.n_targets;
+    uint32_t sc_count = 0, seed_off = 0;
+    bool key_needs_hh[kMaxKeys] = {false, false, false, false};
+    for (uint32_t t = 0; t < c.n_targets; ++t) {
+        STarget &tg = P.tgt[t];
+        tg.counters = c.tgt_counters[t];
+        tg.ndim = c.tgt_ndim[t];
+        tg.d = c.tgt_d[t];
+        tg.wmask0 = c.tgt_w[t][0] - 1;
+        tg.wmask1 = tg.ndim == 2 ? c.tgt_w[t][1] - 1 : 0;
+        tg.lw1 = tg.ndim == 2 ? (uint32_t)__builtin_ctz(c.tgt_w[t][1]) : 0;
+        tg.k0 = (uint32_t)(std::find(keys.begin(), keys.end(), c.tgt_key[t][0]) - keys.begin());
+        tg.k1 = tg.ndim == 2 ? (uint32_t)(std::find(keys.begin(), keys.end(), c.tgt_key[t][1]) - keys.begin()) : 0;
+        tg.cells = tg.ndim == 2 ? c.tgt_w[t][0] * c.tgt_w[t][1] : c.tgt_w[t][0];
+        tg.seed_off = seed_off;
+        seed_off += tg.ndim * tg.d * 6;
+        P.seeds[t] = c.tgt_seeds[t];
+        const uint64_t need = uint64_t(tg.d) * tg.cells * 4;
+        if (sc_count * 4 + need <= avail) {
+            tg.smem_off = (int32_t)sc_count;
+            sc_count += (uint32_t)(need / 4);
+        } else {
+            tg.smem_off = -1;
+        }
+        if (tg.ndim == 1) {
+            P.key[tg.k0].has1d = 1;
+            if (tg.smem_off < 0) { P.key[tg.k0].hasglob = 1; key_needs_hh[tg.k0] = true; }
+        }
+    }
+    P.smem_counters = sc_count;
+    P.off_sc = off;
+    off += ((sc_count * 4 + 15) & ~15u);
+    avail = kBudget - off - fixed_tail;
+    // heavy-hitter tables for key columns feeding non-privatised 1-D sketches
+    uint32_t nhh = 0;
+    for (uint32_t k = 0; k < P.n_keys; ++k) nhh += key_needs_hh[k];
+    P.hh_log2 = 0;
+    for (uint32_t l = 13; l >= 8 && nhh; --l)
+        if (nhh * (12u << l) <= avail) { P.hh_log2 = l; break; }
+    for (uint32_t k = 0; k < P.n_keys; ++k) {
+        P.key[k].hh_off = -1;
+        if (key_needs_hh[k] && P.hh_log2) {
+            P.key[k].hh_off = (int32_t)off;
+            off += 12u << P.hh_log2;
+        }
+    }
+    P.off_seed = (off + 15) & ~15u;
+    off = P.off_seed + seed_words * 8;
+    if (off > kBudget) return SK_OK;
+    P.survivors = c.survivors;
+
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    uint64_t grid = std::min<uint64_t>((uint64_t)sms, P.n_tiles);
+    // int32 privatised counts stay exact: rows per CTA < 2^31
+    if ((P.n_tiles + grid - 1) / grid * kTile >= (1ULL << 31)) return SK_OK;
+    void (*kern)(const SParams) = P.n_keys == 1 ? k_scan<1> : P.n_keys == 2 ? k_scan<2> : P.n_keys == 3 ? k_scan<3> : k_scan<4>;
+    SKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)off));
+    kern<<<(unsigned)grid, kThreads, off, stream>>>(P);
+    SKB_CUDA(cudaGetLastError());
+    count_launch();
+    *launched = true;
+    return SK_OK;
+}
+
+}  // namespace skb

@@ -1,0 +1,30 @@
+// scan.cuh — host-side description of one fused-scan call (shared by update.cu and scan.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "compass_b200.h"
+
+namespace skb {
+
+struct ScanCall {
+    uint32_t n_cols = 0;
+    const void *col_ptr[16];
+    uint32_t col_bytes[16];
+    uint64_t n_rows = 0;
+    uint32_t n_preds = 0;
+    uint32_t pred_col[8], pred_kind[8];
+    int64_t pred_lo[8], pred_hi[8];
+    const int64_t *pred_set[8];
+    uint32_t pred_n[8];
+    uint32_t n_targets = 0;
+    int64_t *tgt_counters[16];
+    uint32_t tgt_ndim[16], tgt_d[16], tgt_w[16][2], tgt_key[16][2];
+    const uint64_t *tgt_seeds[16];
+    unsigned long long *survivors = nullptr;
+};
+
+// Launch the optimised persistent scan if the call fits its envelope (sets *launched).
+sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched);
+
+}  // namespace skb

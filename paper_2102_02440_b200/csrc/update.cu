@@ -11,8 +11,12 @@
 #include <algorithm>
 #include <vector>
 
+#include <stdlib.h>
+#include <string.h>
+
 #include "hash.cuh"
 #include "internal.cuh"
+#include "scan.cuh"
 
 using namespace skb;
 
@@ -238,6 +242,45 @@ extern "C" sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_co
     p.survivors = reinterpret_cast<unsigned long long *>(survivors_dev);
 
     if (n_rows == 0) { release(); return SK_OK; }
+    // optimised persistent scan (scan.cu) unless disabled or outside its envelope
+    const char *mode = getenv("COMPASS_SCAN");
+    if (!(mode && strcmp(mode, "generic") == 0)) {
+        ScanCall sc;
+        sc.n_cols = n_cols;
+        for (uint32_t c = 0; c < n_cols; ++c) {
+            sc.col_ptr[c] = cols[c].data;
+            sc.col_bytes[c] = cols[c].dtype == SK_INT64 ? 8 : 4;
+        }
+        sc.n_rows = n_rows;
+        sc.n_preds = n_preds;
+        for (uint32_t q = 0; q < n_preds; ++q) {
+            sc.pred_col[q] = p.pred[q].col;
+            sc.pred_kind[q] = p.pred[q].kind;
+            sc.pred_lo[q] = p.pred[q].lo;
+            sc.pred_hi[q] = p.pred[q].hi;
+            sc.pred_set[q] = p.pred[q].set;
+            sc.pred_n[q] = p.pred[q].n;
+        }
+        sc.n_targets = n_targets;
+        for (uint32_t t = 0; t < n_targets; ++t) {
+            const sk_sketch *sk = targets[t].sketch;
+            sc.tgt_counters[t] = sk->counters;
+            sc.tgt_ndim[t] = sk->ndim;
+            sc.tgt_d[t] = sk->d;
+            sc.tgt_w[t][0] = sk->w[0];
+            sc.tgt_w[t][1] = sk->ndim == 2 ? sk->w[1] : 1;
+            sc.tgt_key[t][0] = targets[t].key_col[0];
+            sc.tgt_key[t][1] = sk->ndim == 2 ? targets[t].key_col[1] : 0;
+            sc.tgt_seeds[t] = sk->seeds_dev;
+        }
+        sc.survivors = p.survivors;
+        bool launched = false;
+        sk_status st = scan_launch(sc, stream, &launched);
+        if (st != SK_OK || launched) {
+            release();
+            return st;
+        }
+    }
     const int block = 512;
     cudaError_t e = cudaFuncSetAttribute(k_update_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) { release(); return cuda_fail(e, "cudaFuncSetAttribute"); }

@@ -84,9 +84,19 @@ PRED_SETS = [
 ]
 
 
-@pytest.mark.parametrize("n", [0, 1, 31, 4097, 100_003])
+@pytest.fixture(params=["optimised", "generic"])
+def scan_mode(request, monkeypatch):
+    """Run build tests through both kernels: the persistent TMA scan and the generic one."""
+    if request.param == "generic":
+        monkeypatch.setenv("COMPASS_SCAN", "generic")
+    else:
+        monkeypatch.delenv("COMPASS_SCAN", raising=False)
+    return request.param
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 4097, 100_003, 1_000_000])
 @pytest.mark.parametrize("pi", range(len(PRED_SETS)))
-def test_build_parity(n, pi):
+def test_build_parity(n, pi, scan_mode):
     cols = _rand_cols(n, 1000 + n + pi)
     preds = PRED_SETS[pi]
     g, gs = _gpu_build(cols, preds, TARGETS)
@@ -96,9 +106,9 @@ def test_build_parity(n, pi):
         assert np.array_equal(a, b)
 
 
-def test_build_parity_global_atomic_path_and_skew():
+def test_build_parity_global_atomic_path_and_skew(scan_mode):
     """A sketch too large for shared memory (C4 shape d=9, w=16384) next to a privatised one."""
-    cols = _rand_cols(300_001, 77)
+    cols = _rand_cols(3_000_001, 77)
     tg = [(["zk"], 9, [16384], ["F.key1|D1.key"]), (["k64"], 9, [16384], ["F.key2|D2.key"]), (["k32"], 5, [1024], ["x|y"])]
     preds = [("p", pb.RANGE, I64MIN, 36)]
     g, gs = _gpu_build(cols, preds, tg)
@@ -106,7 +116,7 @@ def test_build_parity_global_atomic_path_and_skew():
     assert gs == os_ and all(np.array_equal(a, b) for a, b in zip(g, o))
 
 
-def test_sharded_calls_accumulate_and_merge_is_exact():
+def test_sharded_calls_accumulate_and_merge_is_exact(scan_mode):
     cols = _rand_cols(200_000, 5)
     preds = PRED_SETS[2]
     one, s1 = _gpu_build(cols, preds, TARGETS, calls=1)
