@@ -83,6 +83,7 @@ struct SParams {
     // smem layout (byte offsets)
     uint32_t off_ring, off_kbuf, off_hh, off_sc, off_seed;
     uint32_t smem_counters, seed_words;
+    uint32_t has2d;       // some target is a matrix
     unsigned long long *survivors;
 };
 
@@ -140,74 +141,6 @@ __device__ __forceinline__ bool in_set(const int64_t *s, uint32_t n, int64_t v) 
     return lo < n && __ldg(reinterpret_cast<const long long *>(s) + lo) == v;
 }
 
-// conjunction of the predicates over this lane's 4 rows -> bit mask (A2)
-__device__ __forceinline__ uint32_t eval_preds(const SParams &P, const unsigned char *stage, bool staged,
-                                               uint64_t row0, int r0, int valid) {
-    uint32_t bits = (1u << valid) - 1u;
-    for (uint32_t q = 0; q < P.n_preds; ++q) {
-        const SPred &pr = P.pred[q];
-        const SCol &c = P.col[pr.col];
-        if (pr.kind == PR_R32) {
-            int4 v;
-            if (staged) v = *reinterpret_cast<const int4 *>(stage + c.soff + r0 * 4);
-            else {
-                const int *g = reinterpret_cast<const int *>(c.p) + row0 + r0;
-                v.x = valid > 0 ? __ldg(g) : 0; v.y = valid > 1 ? __ldg(g + 1) : 0;
-                v.z = valid > 2 ? __ldg(g + 2) : 0; v.w = valid > 3 ? __ldg(g + 3) : 0;
-            }
-            const uint32_t lo = (uint32_t)pr.lo, sp = (uint32_t)pr.span;
-            const uint32_t m = ((uint32_t)v.x - lo <= sp) | (((uint32_t)v.y - lo <= sp) << 1) |
-                               (((uint32_t)v.z - lo <= sp) << 2) | (((uint32_t)v.w - lo <= sp) << 3);
-            bits &= m;
-        } else if (pr.kind == PR_R64) {
-            int64_t v[4];
-            if (staged) {
-                const longlong2 a = *reinterpret_cast<const longlong2 *>(stage + c.soff + r0 * 8);
-                const longlong2 b = *reinterpret_cast<const longlong2 *>(stage + c.soff + r0 * 8 + 16);
-                v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-            } else {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) v[j] = j < valid ? gval(c, row0 + r0 + j) : 0;
-            }
-            uint32_t m = 0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) m |= (uint32_t)((uint64_t)v[j] - (uint64_t)pr.lo <= pr.span) << j;
-            bits &= m;
-        } else if (pr.kind == PR_SET) {
-            uint32_t b = bits;
-            while (b) {
-                const int j = __ffs(b) - 1;
-                b &= b - 1;
-                const int64_t v = staged ? (c.bytes == 8 ? *reinterpret_cast<const int64_t *>(stage + c.soff + (r0 + j) * 8)
-                                                         : (int64_t) * reinterpret_cast<const int *>(stage + c.soff + (r0 + j) * 4))
-                                         : gval(c, row0 + r0 + j);
-                if (!in_set(pr.set, pr.n, v)) bits &= ~(1u << j);
-            }
-        } else {
-            bits = 0;
-        }
-    }
-    return bits;
-}
-
-// values of rows [r0, r0+4) of column c within the tile (staged: 128-bit smem reads)
-__device__ __forceinline__ void load4(const SParams &P, const SCol &c, const unsigned char *stage, bool staged,
-                                      uint64_t tile_row0, int r0, int valid, int64_t v[4]) {
-    if (staged && c.soff >= 0) {
-        if (c.bytes == 4) {
-            const int4 q = *reinterpret_cast<const int4 *>(stage + c.soff + r0 * 4);
-            v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-        } else {
-            const longlong2 a = *reinterpret_cast<const longlong2 *>(stage + c.soff + r0 * 8);
-            const longlong2 b = *reinterpret_cast<const longlong2 *>(stage + c.soff + r0 * 8 + 16);
-            v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = (j < valid) ? gval(c, tile_row0 + r0 + j) : 0;
-    }
-}
-
 // ------------------------------------------------------------------ heavy-hitter table
 __device__ __forceinline__ bool hh_add(unsigned char *tab, uint32_t log2s, uint64_t x, int cnt) {
     uint64_t *keys = reinterpret_cast<uint64_t *>(tab);
@@ -229,8 +162,7 @@ __device__ __forceinline__ bool hh_add(unsigned char *tab, uint32_t log2s, uint6
 
 // ------------------------------------------------------------------ sketch updates
 // 1-D target t: row r gets cnt * xi_r(x) at bucket h_r(x)
-__device__ __forceinline__ void update_1d(const SParams &P, const STarget &tg, const uint64_t *seed, int32_t *sc,
-                                          uint64_t x, int cnt) {
+__device__ __forceinline__ void update_1d(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, int cnt) {
     for (uint32_t r = 0; r < tg.d; ++r) {
         const uint64_t *a = seed + r * 6;
         const uint32_t cell = (uint32_t)(hash_g61(a[4], a[5], x) & tg.wmask0);
@@ -252,16 +184,28 @@ __device__ __forceinline__ void update_2d(const STarget &tg, const uint64_t *see
     }
 }
 
-// one warp-wide batch: lanes with `valid` hold one surviving tuple each, keys x[k]
-__device__ __forceinline__ void process_batch(const SParams &P, unsigned char *smem, bool valid, const uint64_t *x) {
+// x[idx] with compile-time indexing only (keeps the key array in registers)
+template <int NK>
+__device__ __forceinline__ uint64_t pick(const uint64_t (&x)[NK], uint32_t idx) {
+    uint64_t v = x[0];
+#pragma unroll
+    for (int k = 1; k < NK; ++k)
+        if (idx == (uint32_t)k) v = x[k];
+    return v;
+}
+
+// one warp-wide batch: lanes with `valid` hold one surviving tuple each, canonical keys x[k]
+template <int NK>
+__device__ __forceinline__ void process_batch(const SParams &P, unsigned char *smem, bool valid, const uint64_t (&x)[NK]) {
     const uint32_t act = __ballot_sync(0xffffffffu, valid);
     if (!act) return;
     int32_t *sc = reinterpret_cast<int32_t *>(smem + P.off_sc);
     const uint64_t *seeds = reinterpret_cast<const uint64_t *>(smem + P.off_seed);
     const int lane = threadIdx.x & 31;
-    // 1-D targets: aggregate equal keys of the warp (match_any), leader updates with the count
-    for (uint32_t k = 0; k < P.n_keys; ++k) {
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
         if (!P.key[k].has1d) continue;
+        // aggregate equal keys of the warp (match_any); the leader updates with the count
         bool leader = false, miss = false;
         int cnt = 0;
         if (valid) {
@@ -270,18 +214,16 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
             cnt = __popc(grp);
         }
         if (leader) {
-            bool done = false;
-            if (P.key[k].hh_off >= 0) done = hh_add(smem + P.key[k].hh_off, P.hh_log2, x[k], cnt);
-            miss = !done;
+            if (P.key[k].hh_off >= 0) miss = !hh_add(smem + P.key[k].hh_off, P.hh_log2, x[k], cnt);
+            else miss = P.key[k].hasglob;
             for (uint32_t t = 0; t < P.n_targets; ++t) {
                 const STarget &tg = P.tgt[t];
-                if (tg.ndim != 1 || tg.k0 != k || tg.smem_off < 0) continue;
-                update_1d(P, tg, seeds + tg.seed_off, sc, x[k], cnt);   // privatised: always direct
+                if (tg.ndim != 1 || tg.k0 != (uint32_t)k || tg.smem_off < 0) continue;
+                update_1d(tg, seeds + tg.seed_off, sc, x[k], cnt);   // privatised: always direct
             }
         }
         if (P.key[k].hasglob) {
-            // keys that did not get a heavy-hitter slot: warp-cooperative L2 updates,
-            // lane r handles sketch row r (SIMT-efficient instead of one lane doing d rows)
+            // keys without a heavy-hitter slot: warp-cooperative L2 updates, lane r = sketch row r
             uint32_t mb = __ballot_sync(0xffffffffu, miss);
             while (mb) {
                 const int src = __ffs(mb) - 1;
@@ -290,7 +232,7 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
                 const int cv = __shfl_sync(0xffffffffu, cnt, src);
                 for (uint32_t t = 0; t < P.n_targets; ++t) {
                     const STarget &tg = P.tgt[t];
-                    if (tg.ndim != 1 || tg.k0 != k || tg.smem_off >= 0) continue;
+                    if (tg.ndim != 1 || tg.k0 != (uint32_t)k || tg.smem_off >= 0) continue;
                     for (uint32_t r = lane; r < tg.d; r += 32) {
                         const uint64_t *a = seeds + tg.seed_off + r * 6;
                         const uint32_t cell = (uint32_t)(hash_g61(a[4], a[5], xv) & tg.wmask0);
@@ -301,33 +243,93 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
         }
     }
     // matrix targets: one cell per surviving tuple and row
-    if (valid) {
+    if (valid && P.has2d) {
         for (uint32_t t = 0; t < P.n_targets; ++t) {
             const STarget &tg = P.tgt[t];
             if (tg.ndim != 2) continue;
-            update_2d(tg, seeds + tg.seed_off, sc, x[tg.k0], x[tg.k1]);
+            update_2d(tg, seeds + tg.seed_off, sc, pick<NK>(x, tg.k0), pick<NK>(x, tg.k1));
         }
     }
 }
 
-// raw key of queue slot `slot` for key k (int32 keys use the low 4 bytes of an 8-byte slot)
-__device__ __forceinline__ uint64_t queue_key(const SParams &P, const unsigned char *q, uint32_t slot, uint32_t k) {
-    const unsigned char *p = q + (slot * P.n_keys + k) * 8;
-    return canon61(P.col[P.key[k].col].bytes == 8 ? *reinterpret_cast<const int64_t *>(p)
-                                                  : (int64_t) * reinterpret_cast<const int32_t *>(p));
-}
+// register copy of one predicate (A2)
+struct PR {
+    uint32_t kind, bytes, n;
+    int32_t soff;
+    int64_t lo;
+    uint64_t span;
+    const void *p;
+    const int64_t *set;
+};
 
-// process queue entries [head, head + n) (n <= 32) as one batch
-__device__ __forceinline__ void drain_batch(const SParams &P, unsigned char *smem, const unsigned char *q, uint32_t head, uint32_t n) {
-    const int lane = threadIdx.x & 31;
-    const bool valid = (uint32_t)lane < n;
-    uint64_t xk[kMaxKeys] = {0, 0, 0, 0};
-    if (valid)
-        for (uint32_t k = 0; k < P.n_keys; ++k) xk[k] = queue_key(P, q, (head + lane) & (P.cap - 1), k);
-    process_batch(P, smem, valid, xk);
+// conjunction of the predicates over this lane's 4 rows -> bit mask (branch-free per kind)
+template <int NP>
+__device__ __forceinline__ uint32_t eval_preds(const PR (&pr)[NP], const unsigned char *stage, bool staged,
+                                               uint64_t row0, int r0, int valid) {
+    uint32_t bits = (1u << valid) - 1u;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        if (pr[q].kind == PR_R32) {
+            int4 v;
+            if (staged) v = *reinterpret_cast<const int4 *>(stage + pr[q].soff + r0 * 4);
+            else {
+                const int *g = reinterpret_cast<const int *>(pr[q].p) + row0 + r0;
+                v.x = valid > 0 ? __ldg(g) : 0; v.y = valid > 1 ? __ldg(g + 1) : 0;
+                v.z = valid > 2 ? __ldg(g + 2) : 0; v.w = valid > 3 ? __ldg(g + 3) : 0;
+            }
+            const uint32_t lo = (uint32_t)pr[q].lo, sp = (uint32_t)pr[q].span;
+            bits &= ((uint32_t)v.x - lo <= sp) | (((uint32_t)v.y - lo <= sp) << 1) |
+                    (((uint32_t)v.z - lo <= sp) << 2) | (((uint32_t)v.w - lo <= sp) << 3);
+        } else if (pr[q].kind == PR_R64) {
+            int64_t v[4];
+            if (staged) {
+                const longlong2 a = *reinterpret_cast<const longlong2 *>(stage + pr[q].soff + r0 * 8);
+                const longlong2 b = *reinterpret_cast<const longlong2 *>(stage + pr[q].soff + r0 * 8 + 16);
+                v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+            } else {
+                const long long *g = reinterpret_cast<const long long *>(pr[q].p) + row0 + r0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = j < valid ? __ldg(g + j) : 0;
+            }
+            uint32_t m = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) m |= (uint32_t)((uint64_t)v[j] - (uint64_t)pr[q].lo <= pr[q].span) << j;
+            bits &= m;
+        } else if (pr[q].kind == PR_SET) {
+            uint32_t b = bits;
+            while (b) {
+                const int j = __ffs(b) - 1;
+                b &= b - 1;
+                int64_t v;
+                if (staged) v = pr[q].bytes == 8 ? *reinterpret_cast<const int64_t *>(stage + pr[q].soff + (r0 + j) * 8)
+                                                 : (int64_t) * reinterpret_cast<const int *>(stage + pr[q].soff + (r0 + j) * 4);
+                else v = pr[q].bytes == 8 ? __ldg(reinterpret_cast<const long long *>(pr[q].p) + row0 + r0 + j)
+                                          : (int64_t)__ldg(reinterpret_cast<const int *>(pr[q].p) + row0 + r0 + j);
+                if (!in_set(pr[q].set, pr[q].n, v)) bits &= ~(1u << j);
+            }
+        } else {
+            bits = 0;
+        }
+    }
+    return bits;
 }
 
 template <int NK>
+__device__ __forceinline__ void drain_batch(const SParams &P, unsigned char *smem, const unsigned char *q,
+                                            const uint32_t (&kbytes)[NK], uint32_t head, uint32_t n) {
+    const int lane = threadIdx.x & 31;
+    const bool valid = (uint32_t)lane < n;
+    uint64_t xk[NK];
+    const unsigned char *e = q + ((head + lane) & (P.cap - 1)) * (NK * 8);
+#pragma unroll
+    for (int k = 0; k < NK; ++k)
+        xk[k] = valid ? canon61(kbytes[k] == 8 ? *reinterpret_cast<const int64_t *>(e + k * 8)
+                                               : (int64_t) * reinterpret_cast<const int32_t *>(e + k * 8))
+                      : 0;
+    process_batch<NK>(P, smem, valid, xk);
+}
+
+template <int NK, int NP>
 __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -383,6 +385,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
     }
 
     // ================= consumer warps: independent pipelines, no CTA-wide barrier in the loop
+    PR pr[(NP > 0) ? NP : 1];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        const SPred &sp = P.pred[q];
+        const SCol &c = P.col[sp.col];
+        pr[q] = PR{sp.kind, c.bytes, sp.n, c.soff, sp.lo, sp.span, c.p, sp.set};
+    }
+    const void *kptr[NK];
+    uint32_t kbytes[NK];
+    int32_t ksoff[NK];
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+        const SCol &c = P.col[P.key[k].col];
+        kptr[k] = c.p;
+        kbytes[k] = c.bytes;
+        ksoff[k] = c.soff;
+    }
+    const uint32_t cap = P.cap;
     uint32_t my_surv = 0;
     const int r0 = warp * 128 + lane * 4;   // this lane's 4 rows inside a tile
     unsigned char *q = smem + P.off_kbuf + warp * P.kb_bytes;   // this warp's survivor-key ring
@@ -396,10 +416,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
         const bool staged = (row0 + kTile <= P.n_rows) && P.stage_bytes;
         const int64_t rem = (int64_t)P.n_rows - (int64_t)(row0 + r0);
         const int valid = rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem);
-        const uint32_t bits = eval_preds(P, stage, staged, row0, r0, valid);
+        constexpr int NPX = (NP > 0) ? NP : 1;
+        const uint32_t bits = (NP > 0) ? eval_preds<NPX>(pr, stage, staged, row0, r0, valid) : (1u << valid) - 1u;
         const int cnt = __popc(bits);
         my_surv += cnt;
-        if (P.gather) {
+        if (NP > 0) {
             int incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -407,25 +428,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                 if (lane >= o) incl += n;
             }
             const uint32_t wtot = (uint32_t)__shfl_sync(0xffffffffu, incl, 31);
-            if (tail - head + wtot > P.cap) {
+            if (tail - head + wtot > cap) {
                 // ring would overflow: finish outstanding gathers and drain every full batch
                 cp_wait_all();
                 __syncwarp();
-                while (tail - head >= 32) { drain_batch(P, smem, q, head, 32); head += 32; }
+                while (tail - head >= 32) { drain_batch<NK>(P, smem, q, kbytes, head, 32); head += 32; }
             }
-            // survivors' keys: sector-granular gathers into the ring
+            // survivors' keys: sector-granular gathers into the ring (A3)
             uint32_t pos = tail + (uint32_t)(incl - cnt);
             uint32_t b = bits;
             while (b) {
                 const int j = __ffs(b) - 1;
                 b &= b - 1;
                 const uint64_t row = row0 + r0 + j;
-                unsigned char *dst = q + (pos & (P.cap - 1)) * (NK * 8);
+                unsigned char *dst = q + (pos & (cap - 1)) * (NK * 8);
 #pragma unroll
                 for (int k = 0; k < NK; ++k) {
-                    const SCol &c = P.col[P.key[k].col];
-                    if (c.bytes == 8) cp_async8(dst + k * 8, reinterpret_cast<const long long *>(c.p) + row);
-                    else cp_async4(dst + k * 8, reinterpret_cast<const int *>(c.p) + row);
+                    if (kbytes[k] == 8) cp_async8(dst + k * 8, reinterpret_cast<const long long *>(kptr[k]) + row);
+                    else cp_async4(dst + k * 8, reinterpret_cast<const int *>(kptr[k]) + row);
                 }
                 ++pos;
             }
@@ -436,28 +456,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             tail += wtot;
             cp_wait_all_but1();
             __syncwarp();
-            while (ready_end - head >= 32) { drain_batch(P, smem, q, head, 32); head += 32; }
+            while (ready_end - head >= 32) { drain_batch<NK>(P, smem, q, kbytes, head, 32); head += 32; }
         } else {
             // keys are staged (no predicate): aggregate and update straight from the stage
-            uint64_t xs[4][kMaxKeys];
-            for (uint32_t k = 0; k < P.n_keys; ++k) {
-                int64_t v[4];
-                load4(P, P.col[P.key[k].col], stage, staged, row0, r0, valid, v);
+            uint64_t xs[4][NK];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) xs[j][k] = canon61(v[j]);
+            for (int k = 0; k < NK; ++k) {
+                if (kbytes[k] == 4) {
+                    int4 v;
+                    if (staged) v = *reinterpret_cast<const int4 *>(stage + ksoff[k] + r0 * 4);
+                    else {
+                        const int *g = reinterpret_cast<const int *>(kptr[k]) + row0 + r0;
+                        v.x = valid > 0 ? __ldg(g) : 0; v.y = valid > 1 ? __ldg(g + 1) : 0;
+                        v.z = valid > 2 ? __ldg(g + 2) : 0; v.w = valid > 3 ? __ldg(g + 3) : 0;
+                    }
+                    xs[0][k] = canon61(v.x); xs[1][k] = canon61(v.y); xs[2][k] = canon61(v.z); xs[3][k] = canon61(v.w);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        int64_t v = 0;
+                        if (staged) v = *reinterpret_cast<const int64_t *>(stage + ksoff[k] + (r0 + j) * 8);
+                        else if (j < valid) v = __ldg(reinterpret_cast<const long long *>(kptr[k]) + row0 + r0 + j);
+                        xs[j][k] = canon61(v);
+                    }
+                }
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) process_batch(P, smem, (bits >> j) & 1u, xs[j]);
+            for (int j = 0; j < 4; ++j) process_batch<NK>(P, smem, (bits >> j) & 1u, xs[j]);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
         }
     }
-    if (P.gather) {
+    if (NP > 0) {
         cp_wait_all();
         __syncwarp();
         while (tail - head > 0) {
             const uint32_t n = min(32u, tail - head);
-            drain_batch(P, smem, q, head, n);
+            drain_batch<NK>(P, smem, q, kbytes, head, n);
             head += n;
         }
     }
@@ -480,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             for (uint32_t tt = 0; tt < P.n_targets; ++tt) {
                 const STarget &tg = P.tgt[tt];
                 if (tg.ndim != 1 || tg.k0 != k || tg.smem_off >= 0) continue;
-                update_1d(P, tg, seeds + tg.seed_off, sc, x, c);
+                update_1d(tg, seeds + tg.seed_off, sc, x, c);
             }
         }
     }
@@ -496,6 +531,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
     }
 }
 
+typedef void (*ScanKernel)(const SParams);
+
+template <int NK>
+static ScanKernel pick_np(uint32_t np) {
+    switch (np) {
+        case 0: return k_scan<NK, 0>;
+        case 1: return k_scan<NK, 1>;
+        case 2: return k_scan<NK, 2>;
+        case 3: return k_scan<NK, 3>;
+        default: return k_scan<NK, 4>;
+    }
+}
+
+static ScanKernel pick_kernel(uint32_t nk, uint32_t np) {
+    switch (nk) {
+        case 1: return pick_np<1>(np);
+        case 2: return pick_np<2>(np);
+        case 3: return pick_np<3>(np);
+        default: return pick_np<4>(np);
+    }
+}
+
 }  // namespace
 
 namespace skb {
@@ -504,7 +561,7 @@ namespace skb {
 // *launched false (and returns SK_OK) when the call is outside its envelope.
 sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     *launched = false;
-    if (c.n_cols > kMaxSCols || c.n_preds > kMaxSPreds || c.n_targets > kMaxSTargets || c.n_rows == 0) return SK_OK;
+    if (c.n_cols > kMaxSCols || c.n_preds > 4 || c.n_targets > kMaxSTargets || c.n_rows == 0) return SK_OK;
     SParams P;
     memset(&P, 0, sizeof(P));
     P.n_cols = c.n_cols;
@@ -604,6 +661,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         } else {
             tg.smem_off = -1;
         }
+        if (tg.ndim == 2) P.has2d = 1;
         if (tg.ndim == 1) {
             P.key[tg.k0].has1d = 1;
             if (tg.smem_off < 0) { P.key[tg.k0].hasglob = 1; key_needs_hh[tg.k0] = true; }
@@ -637,7 +695,8 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     uint64_t grid = std::min<uint64_t>((uint64_t)sms, P.n_tiles);
     // int32 privatised counts stay exact: rows per CTA < 2^31
     if ((P.n_tiles + grid - 1) / grid * kTile >= (1ULL << 31)) return SK_OK;
-    void (*kern)(const SParams) = P.n_keys == 1 ? k_scan<1> : P.n_keys == 2 ? k_scan<2> : P.n_keys == 3 ? k_scan<3> : k_scan<4>;
+    if (P.n_keys == 0) return SK_OK;
+    ScanKernel kern = pick_kernel(P.n_keys, P.n_preds);
     SKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)off));
     kern<<<(unsigned)grid, kThreads, off, stream>>>(P);
     SKB_CUDA(cudaGetLastError());

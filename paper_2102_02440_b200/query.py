@@ -17,6 +17,30 @@ import torch.distributed as dist
 from . import JoinGraph, Sketch, sketch_update_filtered
 
 
+def packed_layout(q):
+    """Layout of the packed int64 buffer of one query: survivors[n_tables] first, then
+    every sketch's counters (row-major [d][w0](w1)), each starting 16-byte aligned.
+    Returns (total_len, [(offset, count) per sketch])."""
+    off = len(q.tables)
+    off += off & 1
+    out = []
+    for s in q.sketches:
+        n = s.d
+        for w in s.w:
+            n *= w
+        out.append((off, n))
+        off += n + (n & 1)
+    return off, out
+
+
+def allreduce_packed(buffer: torch.Tensor, group=None):
+    """Cross-rank merge of partial sketches + survivor counts: one int64 SUM all-reduce
+    (exact: integer addition is associative)."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(buffer, op=dist.ReduceOp.SUM, group=group)
+    return buffer
+
+
 class QueryRun:
     def __init__(self, q, device="cuda"):
         self.q = q
@@ -24,20 +48,10 @@ class QueryRun:
         if self.device.index is None:
             self.device = torch.device("cuda", torch.cuda.current_device())
         self.tnames = [t.name for t in q.tables]
-        # packed layout: survivors[n_tables] | sketch 0 | sketch 1 | ... (each 16-byte aligned)
-        sizes = []
-        for s in q.sketches:
-            n = s.d
-            for w in s.w:
-                n *= w
-            sizes.append(n)
-        off = len(self.tnames)
-        off += off & 1
-        offs = []
-        for n in sizes:
-            offs.append(off)
-            off += n + (n & 1)
-        self.buffer = torch.zeros(off, dtype=torch.int64, device=self.device)
+        total, lay = packed_layout(q)
+        offs = [o for o, _ in lay]
+        sizes = [n for _, n in lay]
+        self.buffer = torch.zeros(total, dtype=torch.int64, device=self.device)
         self.survivors = self.buffer[:len(self.tnames)]
         self.sketches = []
         for s, o, n in zip(q.sketches, offs, sizes):
@@ -65,9 +79,8 @@ class QueryRun:
             self.build_table(name, data[name], preds[name], stream=stream)
 
     def allreduce(self, group=None):
-        """Cross-GPU merge of all partial sketches and survivor counts: one int64 SUM."""
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-            dist.all_reduce(self.buffer, op=dist.ReduceOp.SUM, group=group)
+        """Cross-GPU merge of all partial sketches and survivor counts: one int64 SUM (NCCL)."""
+        allreduce_packed(self.buffer, group)
 
     def sketch_of(self, table: str, edge_ids) -> Sketch:
         for s, sk in zip(self.q.sketches, self.sketches):

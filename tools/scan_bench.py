@@ -24,7 +24,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="C4")
     ap.add_argument("--table", default=None)
-    ap.add_argument("--scale", type=float, default=0.1)
+    ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--generic", action="store_true")
