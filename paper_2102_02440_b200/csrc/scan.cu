@@ -19,6 +19,7 @@
 //   A7  CTA flush: int32 smem counters and heavy-hitter counts -> int64 HBM
 //       sketch with red.global.add (order-independent, bit-exact).
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <climits>
@@ -36,7 +37,7 @@ constexpr int kTile = 2048;
 constexpr int kWarps = 16;
 constexpr int kConsumers = kWarps * 32;
 constexpr int kThreads = kConsumers + 32;
-constexpr int kStages = 4;
+constexpr int kMaxStages = 8;
 constexpr int kMaxSCols = 8, kMaxSPreds = 8, kMaxKeys = 4, kMaxSTargets = 16;
 constexpr uint64_t kEmpty = ~0ULL;   // canonical keys are < 2^61: never equal
 
@@ -76,6 +77,7 @@ struct SParams {
     uint32_t n_cols, n_preds, n_keys, n_targets;
     uint64_t n_rows, n_tiles;
     uint32_t stage_bytes;
+    uint32_t stages;      // ring depth (<= kMaxStages)
     uint32_t gather;      // 1: survivors' keys gathered, 0: keys staged (no predicate)
     uint32_t cap;         // entries of each warp's survivor-key ring (power of two)
     uint32_t kb_bytes;    // bytes of one warp's ring
@@ -84,6 +86,7 @@ struct SParams {
     uint32_t off_ring, off_kbuf, off_hh, off_sc, off_seed;
     uint32_t smem_counters, seed_words;
     uint32_t has2d;       // some target is a matrix
+    uint32_t off_miss, off_missn;   // per-warp miss buffers (x, count) and fill counts
     unsigned long long *survivors;
 };
 
@@ -113,10 +116,10 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 __device__ __forceinline__ void cp_async4(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+    asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+    asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all_but1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
@@ -142,20 +145,32 @@ __device__ __forceinline__ bool in_set(const int64_t *s, uint32_t n, int64_t v) 
 }
 
 // ------------------------------------------------------------------ heavy-hitter table
+// Bucketised table: 8 slots per bucket, the bucket's 8 keys read with four 128-bit
+// shared loads (one latency) instead of a dependent probe chain.  Two warps may insert
+// the same key into two slots of one bucket; both counts are flushed, which is exact
+// by linearity.
 __device__ __forceinline__ bool hh_add(unsigned char *tab, uint32_t log2s, uint64_t x, int cnt) {
     uint64_t *keys = reinterpret_cast<uint64_t *>(tab);
     int *cnts = reinterpret_cast<int *>(tab + (8u << log2s));
-    const uint32_t mask = (1u << log2s) - 1;
-    const uint32_t h = (uint32_t)((x * 0x9E3779B97F4A7C15ULL) >> (64 - log2s));
+    const uint32_t b = (uint32_t)((x * 0x9E3779B97F4A7C15ULL) >> (64 - (log2s - 3))) * 8u;
 #pragma unroll 1
-    for (uint32_t probe = 0; probe < 8; ++probe) {
-        const uint32_t s = (h + probe) & mask;
-        const uint64_t k = *reinterpret_cast<volatile uint64_t *>(&keys[s]);
-        if (k == x) { atomicAdd(&cnts[s], cnt); return true; }
-        if (k == kEmpty) {
-            const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long *>(&keys[s]), kEmpty, x);
-            if (prev == kEmpty || prev == x) { atomicAdd(&cnts[s], cnt); return true; }
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        uint64_t k[8];
+        const uint32_t a = smem_u32(keys + b);
+        asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(k[0]), "=l"(k[1]) : "r"(a));
+        asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(k[2]), "=l"(k[3]) : "r"(a + 16));
+        asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(k[4]), "=l"(k[5]) : "r"(a + 32));
+        asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(k[6]), "=l"(k[7]) : "r"(a + 48));
+        int hit = -1, emp = -1;
+#pragma unroll
+        for (int j = 7; j >= 0; --j) {
+            if (k[j] == x) hit = j;
+            if (k[j] == kEmpty) emp = j;
         }
+        if (hit >= 0) { atomicAdd(&cnts[b + hit], cnt); return true; }
+        if (emp < 0) return false;
+        const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long *>(&keys[b + emp]), kEmpty, x);
+        if (prev == kEmpty || prev == x) { atomicAdd(&cnts[b + emp], cnt); return true; }
     }
     return false;
 }
@@ -194,6 +209,23 @@ __device__ __forceinline__ uint64_t pick(const uint64_t (&x)[NK], uint32_t idx) 
     return v;
 }
 
+// all lanes: lane i < n applies buffered miss i (key x, count c) to every non-privatised
+// 1-D sketch hashed on key column k
+__device__ __forceinline__ void flush_misses(const SParams &P, const uint64_t *seeds, const uint64_t *mx, const int *mc,
+                                             uint32_t n, uint32_t k) {
+    const int lane = threadIdx.x & 31;
+    if ((uint32_t)lane < n) {
+        const uint64_t xv = mx[lane];
+        const int cv = mc[lane];
+        for (uint32_t t = 0; t < P.n_targets; ++t) {
+            const STarget &tg = P.tgt[t];
+            if (tg.ndim != 1 || tg.k0 != k || tg.smem_off >= 0) continue;
+            update_1d(tg, seeds + tg.seed_off, nullptr, xv, cv);
+        }
+    }
+    __syncwarp();
+}
+
 // one warp-wide batch: lanes with `valid` hold one surviving tuple each, canonical keys x[k]
 template <int NK>
 __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *smem, bool valid, const uint64_t (&x)[NK]) {
@@ -223,22 +255,29 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
             }
         }
         if (P.key[k].hasglob) {
-            // keys without a heavy-hitter slot: warp-cooperative L2 updates, lane r = sketch row r
-            uint32_t mb = __ballot_sync(0xffffffffu, miss);
-            while (mb) {
-                const int src = __ffs(mb) - 1;
-                mb &= mb - 1;
-                const uint64_t xv = __shfl_sync(0xffffffffu, x[k], src);
-                const int cv = __shfl_sync(0xffffffffu, cnt, src);
-                for (uint32_t t = 0; t < P.n_targets; ++t) {
-                    const STarget &tg = P.tgt[t];
-                    if (tg.ndim != 1 || tg.k0 != (uint32_t)k || tg.smem_off >= 0) continue;
-                    for (uint32_t r = lane; r < tg.d; r += 32) {
-                        const uint64_t *a = seeds + tg.seed_off + r * 6;
-                        const uint32_t cell = (uint32_t)(hash_g61(a[4], a[5], xv) & tg.wmask0);
-                        red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)(xi_sign61(a, xv) * cv));
-                    }
+            // keys without a heavy-hitter slot go to this warp's miss buffer; 32 buffered
+            // misses are flushed together so every lane hashes (SIMT-efficient L2 updates)
+            const uint32_t mb = __ballot_sync(0xffffffffu, miss);
+            if (mb) {
+                const uint32_t mi = (threadIdx.x >> 5) * P.n_keys + k;
+                uint64_t *mx = reinterpret_cast<uint64_t *>(smem + P.off_miss) + mi * 32;
+                int *mc = reinterpret_cast<int *>(smem + P.off_miss + kWarps * P.n_keys * 32 * 8) + mi * 32;
+                uint32_t *nm = reinterpret_cast<uint32_t *>(smem + P.off_missn) + mi;
+                uint32_t fill = *nm;
+                const uint32_t nnew = __popc(mb);
+                if (fill + nnew > 32) {
+                    __syncwarp();
+                    flush_misses(P, seeds, mx, mc, fill, (uint32_t)k);
+                    fill = 0;
                 }
+                if (miss) {
+                    const uint32_t pos = fill + __popc(mb & ((1u << lane) - 1u));
+                    mx[pos] = x[k];
+                    mc[pos] = cnt;
+                }
+                __syncwarp();
+                if (lane == 0) *nm = fill + nnew;
+                __syncwarp();
             }
         }
     }
@@ -333,12 +372,13 @@ template <int NK, int NP>
 __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-    uint64_t *empty = full + kStages;
+    uint64_t *empty = full + kMaxStages;
+    const uint32_t kStages = P.stages;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     // ---- setup: barriers, smem counters, heavy-hitter tables, seeds
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kWarps); }
+        for (uint32_t s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kWarps); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     {
@@ -355,6 +395,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             const uint32_t words = P.tgt[t].ndim * P.tgt[t].d * 6;
             for (uint32_t i = tid; i < words; i += kThreads) sseed[P.tgt[t].seed_off + i] = P.seeds[t][i];
         }
+        uint32_t *nm = reinterpret_cast<uint32_t *>(smem + P.off_missn);
+        for (uint32_t i = tid; i < kWarps * P.n_keys; i += kThreads) nm[i] = 0;
     }
     __syncthreads();
 
@@ -429,10 +471,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             }
             const uint32_t wtot = (uint32_t)__shfl_sync(0xffffffffu, incl, 31);
             if (tail - head + wtot > cap) {
-                // ring would overflow: finish outstanding gathers and drain every full batch
+                // ring would overflow: finish outstanding gathers and drain it completely
                 cp_wait_all();
                 __syncwarp();
-                while (tail - head >= 32) { drain_batch<NK>(P, smem, q, kbytes, head, 32); head += 32; }
+                while (tail != head) {
+                    const uint32_t n = min(32u, tail - head);
+                    drain_batch<NK>(P, smem, q, kbytes, head, n);
+                    head += n;
+                }
             }
             // survivors' keys: sector-granular gathers into the ring (A3)
             uint32_t pos = tail + (uint32_t)(incl - cnt);
@@ -497,6 +543,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
         }
     }
 
+    // ---- this warp's buffered heavy-hitter misses
+    {
+        const uint64_t *seeds = reinterpret_cast<const uint64_t *>(smem + P.off_seed);
+        __syncwarp();
+        for (uint32_t k = 0; k < P.n_keys; ++k) {
+            if (!P.key[k].hasglob) continue;
+            const uint32_t mi = warp * P.n_keys + k;
+            const uint32_t n = reinterpret_cast<volatile uint32_t *>(smem + P.off_missn)[mi];
+            if (n) flush_misses(P, seeds, reinterpret_cast<const uint64_t *>(smem + P.off_miss) + mi * 32,
+                                reinterpret_cast<const int *>(smem + P.off_miss + kWarps * P.n_keys * 32 * 8) + mi * 32, n, k);
+        }
+    }
     // ---- exact survivor count
     const uint32_t ws = __reduce_add_sync(0xffffffffu, my_surv);
     if (lane == 0 && ws && P.survivors) atomicAdd(P.survivors, (unsigned long long)ws);
@@ -613,30 +671,30 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     for (uint32_t q = 0; q < c.n_preds; ++q) stage_col(c.pred_col[q]);
     if (!P.gather) for (uint32_t k : keys) stage_col(k);
     P.stage_bytes = soff;
-    // smem budget
+    // ---- shared-memory plan (227 KB): barriers | TMA ring (stages x stage) | per-warp key
+    //      rings | privatised counters | heavy-hitter tables | seeds.  Tunables via env
+    //      (COMPASS_STAGES, COMPASS_HH_LOG2) for experiments only.
     const uint32_t kBudget = 227 * 1024;
-    uint32_t off = 128;                                  // barriers
-    P.off_ring = off;
-    off += kStages * P.stage_bytes;
-    off = (off + 15) & ~15u;
+    const char *env_st = getenv("COMPASS_STAGES"), *env_hh = getenv("COMPASS_HH_LOG2");
+    const uint32_t want_stages = env_st ? (uint32_t)atoi(env_st) : 6;
+    const uint32_t max_hh = env_hh ? (uint32_t)atoi(env_hh) : 12;
     uint32_t seed_words = 0;
     for (uint32_t t = 0; t < c.n_targets; ++t) seed_words += c.tgt_ndim[t] * c.tgt_d[t] * 6;
     P.seed_words = seed_words;
-    const uint32_t fixed_tail = seed_words * 8 + 64;
-    if (off + fixed_tail > kBudget) return SK_OK;
+    const uint32_t seed_bytes = (seed_words * 8 + 15) & ~15u;
     for (uint32_t k = 0; k < P.n_keys; ++k) P.key[k].col = keys[k];
-    // per-warp survivor-key rings (gather mode): cap entries x n_keys x 8 bytes
     P.cap = 0;
+    P.kb_bytes = 0;
     if (P.gather) {
-        for (uint32_t cap = 512; cap >= 256; cap /= 2)
-            if (off + kWarps * cap * P.n_keys * 8 + fixed_tail <= kBudget - 24 * 1024) { P.cap = cap; break; }
-        if (P.cap == 0) return SK_OK;                   // cap must exceed 128 + 31 (one tile + a partial batch)
+        P.cap = P.n_keys == 1 ? 256 : 128;              // >= one tile-slice of survivors (128); overflow drains
         P.kb_bytes = P.cap * P.n_keys * 8;
-        P.off_kbuf = off;
-        off += kWarps * P.kb_bytes;
     }
-    uint32_t avail = kBudget - off - fixed_tail;
-    // privatise targets in declaration order while they fit (leave room for heavy hitters)
+    const uint32_t min_stages = 3;
+    const uint32_t miss_bytes = kWarps * P.n_keys * 32 * 12 + ((kWarps * P.n_keys * 4 + 15) & ~15u);
+    const uint32_t fixed = 128 + min_stages * P.stage_bytes + kWarps * P.kb_bytes + seed_bytes + miss_bytes + 256;
+    if (fixed > kBudget) return SK_OK;
+    uint32_t avail = kBudget - fixed;
+    // privatise targets in declaration order while they fit
     P.n_targets = c.n_targets;
     uint32_t sc_count = 0, seed_off = 0;
     bool key_needs_hh[kMaxKeys] = {false, false, false, false};
@@ -668,15 +726,26 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         }
     }
     P.smem_counters = sc_count;
-    P.off_sc = off;
-    off += ((sc_count * 4 + 15) & ~15u);
-    avail = kBudget - off - fixed_tail;
-    // heavy-hitter tables for key columns feeding non-privatised 1-D sketches
+    avail -= (sc_count * 4 + 15) & ~15u;
+    // ring depth first (up to want_stages), then heavy-hitter tables, then any extra stages
+    uint32_t stages = min_stages;
+    while (stages < want_stages && stages < kMaxStages && avail >= P.stage_bytes) { ++stages; avail -= P.stage_bytes; }
     uint32_t nhh = 0;
     for (uint32_t k = 0; k < P.n_keys; ++k) nhh += key_needs_hh[k];
     P.hh_log2 = 0;
-    for (uint32_t l = 13; l >= 8 && nhh; --l)
+    for (uint32_t l = max_hh; l >= 8 && nhh; --l)
         if (nhh * (12u << l) <= avail) { P.hh_log2 = l; break; }
+    if (P.hh_log2) avail -= nhh * (12u << P.hh_log2);
+    while (stages < kMaxStages && !env_st && avail >= P.stage_bytes && nhh == 0) { ++stages; avail -= P.stage_bytes; }
+    P.stages = stages;
+    uint32_t off = 128;                                  // 2 x kMaxStages mbarriers
+    P.off_ring = off;
+    off += stages * P.stage_bytes;
+    off = (off + 127) & ~127u;
+    P.off_kbuf = off;
+    off += kWarps * P.kb_bytes;
+    P.off_sc = off;
+    off += (sc_count * 4 + 15) & ~15u;
     for (uint32_t k = 0; k < P.n_keys; ++k) {
         P.key[k].hh_off = -1;
         if (key_needs_hh[k] && P.hh_log2) {
@@ -684,8 +753,12 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
             off += 12u << P.hh_log2;
         }
     }
+    P.off_miss = (off + 15) & ~15u;
+    off = P.off_miss + kWarps * P.n_keys * 32 * 12;
+    P.off_missn = (off + 15) & ~15u;
+    off = P.off_missn + kWarps * P.n_keys * 4;
     P.off_seed = (off + 15) & ~15u;
-    off = P.off_seed + seed_words * 8;
+    off = P.off_seed + seed_bytes;
     if (off > kBudget) return SK_OK;
     P.survivors = c.survivors;
 
