@@ -87,6 +87,7 @@ struct SParams {
     uint32_t smem_counters, seed_words;
     uint32_t has2d;       // some target is a matrix
     uint32_t off_miss, off_missn;   // per-warp miss buffers (x, count) and fill counts
+    uint32_t off_rows;              // per-warp survivor row-offset list (128 x uint16)
     unsigned long long *survivors;
 };
 
@@ -106,8 +107,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity), "r"(0x989680u) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(bar), "r"(parity), "r"(0x989680u) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile(
@@ -302,8 +313,8 @@ struct PR {
 };
 
 // conjunction of the predicates over this lane's 4 rows -> bit mask (branch-free per kind)
-template <int NP>
-__device__ __forceinline__ uint32_t eval_preds(const PR (&pr)[NP], const unsigned char *stage, bool staged,
+template <int NP, bool staged>
+__device__ __forceinline__ uint32_t eval_preds(const PR (&pr)[NP], const unsigned char *stage,
                                                uint64_t row0, int r0, int valid) {
     uint32_t bits = (1u << valid) - 1u;
 #pragma unroll
@@ -403,10 +414,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
     if (warp == kWarps) {
         // ================= producer warp: TMA bulk copies of staged columns
         if (lane == 0) {
-            uint32_t i = 0;
-            for (uint64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x, ++i) {
-                const uint32_t s = i % kStages;
-                if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
+            uint32_t s = 0, ph = 0;
+            bool wrapped = false;
+            for (uint64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+                if (wrapped) mbar_wait(&empty[s], ph ^ 1);
                 const uint64_t row0 = t * kTile;
                 const bool fulltile = row0 + kTile <= P.n_rows;
                 if (fulltile && P.stage_bytes) {
@@ -421,6 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                 } else {
                     mbar_arrive(&full[s]);
                 }
+                if (++s == kStages) { s = 0; ph ^= 1; wrapped = true; }
             }
         }
         return;
@@ -449,60 +461,82 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
     const int r0 = warp * 128 + lane * 4;   // this lane's 4 rows inside a tile
     unsigned char *q = smem + P.off_kbuf + warp * P.kb_bytes;   // this warp's survivor-key ring
     uint32_t head = 0, tail = 0;             // ring positions (monotone)
-    uint32_t i = 0;
-    for (uint64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x, ++i) {
+    bool pending = false;                    // a cp.async group of this warp may be in flight
+    const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
+    uint32_t s = 0, ph = 0;
+    for (uint64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x, s = (s + 1 == kStages) ? 0u : s + 1, ph ^= (s == 0)) {
         const uint64_t row0 = t * kTile;
-        const uint32_t s = i % kStages;
-        mbar_wait(&full[s], (i / kStages) & 1);
+        mbar_wait_a(full_a + s * 8, ph);
         const unsigned char *stage = smem + P.off_ring + s * P.stage_bytes;
         const bool staged = (row0 + kTile <= P.n_rows) && P.stage_bytes;
         const int64_t rem = (int64_t)P.n_rows - (int64_t)(row0 + r0);
         const int valid = rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem);
         constexpr int NPX = (NP > 0) ? NP : 1;
-        const uint32_t bits = (NP > 0) ? eval_preds<NPX>(pr, stage, staged, row0, r0, valid) : (1u << valid) - 1u;
+        uint32_t bits = (1u << valid) - 1u;
+        if (NP > 0) bits = staged ? eval_preds<NPX, true>(pr, stage, row0, r0, valid)
+                                  : eval_preds<NPX, false>(pr, stage, row0, r0, valid);
         const int cnt = __popc(bits);
         my_surv += cnt;
         if (NP > 0) {
-            int incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int n = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += n;
+            // survivor prefix from 4 ballots (one per row slot): no dependent shuffle chain
+            const uint32_t lt = (1u << lane) - 1u;
+            const uint32_t B0 = __ballot_sync(0xffffffffu, bits & 1u), B1 = __ballot_sync(0xffffffffu, bits & 2u);
+            const uint32_t B2 = __ballot_sync(0xffffffffu, bits & 4u), B3 = __ballot_sync(0xffffffffu, bits & 8u);
+            const uint32_t wtot = __popc(B0) + __popc(B1) + __popc(B2) + __popc(B3);
+            if (wtot == 0) {
+                // nothing to gather: release the stage, drain only what earlier tiles made ready
+                __syncwarp();
+                if (lane == 0) mbar_arrive_a(empty_a + s * 8);
+                if (tail - head >= 32) {
+                    if (pending) { cp_wait_all(); __syncwarp(); pending = false; }
+                    while (tail - head >= 32) { drain_batch<NK>(P, smem, q, kbytes, head, 32); head += 32; }
+                }
+                continue;
             }
-            const uint32_t wtot = (uint32_t)__shfl_sync(0xffffffffu, incl, 31);
+            const uint32_t excl = __popc(B0 & lt) + __popc(B1 & lt) + __popc(B2 & lt) + __popc(B3 & lt);
             if (tail - head + wtot > cap) {
                 // ring would overflow: finish outstanding gathers and drain it completely
                 cp_wait_all();
                 __syncwarp();
+                pending = false;
                 while (tail != head) {
                     const uint32_t n = min(32u, tail - head);
                     drain_batch<NK>(P, smem, q, kbytes, head, n);
                     head += n;
                 }
             }
-            // survivors' keys: sector-granular gathers into the ring (A3)
-            uint32_t pos = tail + (uint32_t)(incl - cnt);
-            uint32_t b = bits;
-            while (b) {
-                const int j = __ffs(b) - 1;
-                b &= b - 1;
-                const uint64_t row = row0 + r0 + j;
-                unsigned char *dst = q + (pos & (cap - 1)) * (NK * 8);
-#pragma unroll
-                for (int k = 0; k < NK; ++k) {
-                    if (kbytes[k] == 8) cp_async8(dst + k * 8, reinterpret_cast<const long long *>(kptr[k]) + row);
-                    else cp_async4(dst + k * 8, reinterpret_cast<const int *>(kptr[k]) + row);
+            // survivors' keys: sector-granular gathers into the ring (A3).  Row offsets go to a
+            // per-warp list first so the cp.async loop runs converged over all 32 lanes.
+            {
+                uint16_t *rl = reinterpret_cast<uint16_t *>(smem + P.off_rows) + warp * 128;
+                uint32_t pos = excl;
+                uint32_t b = bits;
+                while (b) {
+                    const int j = __ffs(b) - 1;
+                    b &= b - 1;
+                    rl[pos++] = (uint16_t)(r0 + j);
                 }
-                ++pos;
+                __syncwarp();
+                if (lane == 0) mbar_arrive_a(empty_a + s * 8);          // this warp is done with stage s
+                for (uint32_t e = lane; e < wtot; e += 32) {
+                    const uint64_t row = row0 + rl[e];
+                    unsigned char *dst = q + ((tail + e) & (cap - 1)) * (NK * 8);
+#pragma unroll
+                    for (int k = 0; k < NK; ++k) {
+                        if (kbytes[k] == 8) cp_async8(dst + k * 8, reinterpret_cast<const long long *>(kptr[k]) + row);
+                        else cp_async4(dst + k * 8, reinterpret_cast<const int *>(kptr[k]) + row);
+                    }
+                }
             }
             cp_commit();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);          // this warp is done with stage s
             const uint32_t ready_end = tail;                 // entries of earlier tiles
             tail += wtot;
-            cp_wait_all_but1();
-            __syncwarp();
-            while (ready_end - head >= 32) { drain_batch<NK>(P, smem, q, kbytes, head, 32); head += 32; }
+            if (ready_end - head >= 32) {
+                if (pending) cp_wait_all_but1();             // the group committed before this one
+                __syncwarp();
+                while (ready_end - head >= 32) { drain_batch<NK>(P, smem, q, kbytes, head, 32); head += 32; }
+            }
+            pending = true;
         } else {
             // keys are staged (no predicate): aggregate and update straight from the stage
             uint64_t xs[4][NK];
@@ -530,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
 #pragma unroll
             for (int j = 0; j < 4; ++j) process_batch<NK>(P, smem, (bits >> j) & 1u, xs[j]);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+            if (lane == 0) mbar_arrive_a(empty_a + s * 8);
         }
     }
     if (NP > 0) {
@@ -691,7 +725,8 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     }
     const uint32_t min_stages = 3;
     const uint32_t miss_bytes = kWarps * P.n_keys * 32 * 12 + ((kWarps * P.n_keys * 4 + 15) & ~15u);
-    const uint32_t fixed = 128 + min_stages * P.stage_bytes + kWarps * P.kb_bytes + seed_bytes + miss_bytes + 256;
+    const uint32_t fixed = 128 + min_stages * P.stage_bytes + kWarps * P.kb_bytes + seed_bytes + miss_bytes +
+                           kWarps * 128 * 2 + 256;
     if (fixed > kBudget) return SK_OK;
     uint32_t avail = kBudget - fixed;
     // privatise targets in declaration order while they fit
@@ -753,6 +788,8 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
             off += 12u << P.hh_log2;
         }
     }
+    P.off_rows = (off + 15) & ~15u;
+    off = P.off_rows + kWarps * 128 * 2;
     P.off_miss = (off + 15) & ~15u;
     off = P.off_miss + kWarps * P.n_keys * 32 * 12;
     P.off_missn = (off + 15) & ~15u;
