@@ -23,6 +23,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <deque>
 #include <map>
 #include <string>
 #include <vector>
@@ -71,14 +72,18 @@ __device__ __forceinline__ uint64_t mm_i64(int64_t v, int a, uint64_t m) {
 __device__ __forceinline__ uint64_t uabs(int64_t v) { return v < 0 ? (uint64_t)(-(v + 1)) + 1ULL : (uint64_t)v; }
 
 // ---------------------------------------------------------------- small kernels
-// per (item, row): sum |v| over `cells` counters
+// per (item, row): sum |v| over `cells` counters (blockIdx.z = chunk; atomically accumulated)
 struct L1Item { const int64_t *p; uint32_t d; uint32_t cells; };
-__global__ void k_l1(const L1Item *items, unsigned long long *out, int maxd) {
-    const L1Item it = items[blockIdx.x];
+constexpr int kMaxL1Items = 48;
+struct L1Items { L1Item it[kMaxL1Items]; int n; };
+__global__ void k_l1(const __grid_constant__ L1Items items, unsigned long long *out, int maxd) {
+    const L1Item it = items.it[blockIdx.x];
     const uint32_t r = blockIdx.y;
     if (r >= it.d) return;
+    const uint32_t chunk = (it.cells + gridDim.z - 1) / gridDim.z;
+    const uint32_t c0 = blockIdx.z * chunk, c1 = min(it.cells, c0 + chunk);
     unsigned long long s = 0;
-    for (uint32_t i = threadIdx.x; i < it.cells; i += blockDim.x) s += uabs(it.p[uint64_t(r) * it.cells + i]);
+    for (uint32_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) s += uabs(it.p[uint64_t(r) * it.cells + i]);
     __shared__ unsigned long long red[32];
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
@@ -86,7 +91,7 @@ __global__ void k_l1(const L1Item *items, unsigned long long *out, int maxd) {
     if (threadIdx.x == 0) {
         unsigned long long t = 0;
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
-        out[blockIdx.x * maxd + r] = t;
+        if (t) atomicAdd(&out[blockIdx.x * maxd + r], t);
     }
 }
 
@@ -654,13 +659,19 @@ static sk_status build_plan(const sk_graph *g, uint64_t mask, Plan &P) {
     return SK_OK;
 }
 
+// stream-ordered device temporary; non-copyable (kept in a std::deque so growth never
+// relocates, and therefore never frees, a live buffer)
 struct DevBuf {
     void *p = nullptr;
     cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
     ~DevBuf() { if (p) cudaFreeAsync(p, s); }
 };
+using DevPool = std::deque<DevBuf>;
 
-static sk_status dalloc(std::vector<DevBuf> &pool, size_t bytes, cudaStream_t s, void **out) {
+static sk_status dalloc(DevPool &pool, size_t bytes, cudaStream_t s, void **out) {
     pool.emplace_back();
     pool.back().s = s;
     cudaError_t e = cudaMallocAsync(&pool.back().p, std::max<size_t>(bytes, 16), s);
@@ -669,55 +680,66 @@ static sk_status dalloc(std::vector<DevBuf> &pool, size_t bytes, cudaStream_t s,
     return SK_OK;
 }
 
-static sk_status run_plan(const Plan &P, std::vector<SBig> &rows, cudaStream_t stream) {
-    const int E = (int)P.edges.size();
-    const int NT = (int)P.T.size();
-    const int d = P.d;
-    std::vector<DevBuf> pool;
-    pool.reserve(256);
-    // ---- L1 bound -> number of moduli
-    std::vector<const sk_sketch *> uniq;
-    for (auto &t : P.T) for (auto *s : t.sk) if (std::find(uniq.begin(), uniq.end(), s) == uniq.end()) uniq.push_back(s);
-    std::vector<L1Item> items;
-    for (auto *s : uniq) items.push_back({s->counters, s->d, (uint32_t)(s->n_counters / s->d)});
-    void *d_items, *d_l1;
-    sk_status st;
-    if ((st = dalloc(pool, items.size() * sizeof(L1Item), stream, &d_items))) return st;
-    if ((st = dalloc(pool, items.size() * d * sizeof(unsigned long long), stream, &d_l1))) return st;
-    SKB_CUDA(cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(L1Item), cudaMemcpyHostToDevice, stream));
-    k_l1<<<dim3((unsigned)items.size(), d), 256, 0, stream>>>((const L1Item *)d_items, (unsigned long long *)d_l1, d); count_launch();
-    SKB_CUDA(cudaGetLastError());
-    std::vector<unsigned long long> l1(items.size() * d);
-    SKB_CUDA(cudaMemcpyAsync(l1.data(), d_l1, l1.size() * 8, cudaMemcpyDeviceToHost, stream));
-    SKB_CUDA(cudaStreamSynchronize(stream));
-    auto l1max = [&](const sk_sketch *s) {
-        const size_t i = std::find(uniq.begin(), uniq.end(), s) - uniq.begin();
-        unsigned long long mx = 0;
-        for (int r = 0; r < d; ++r) mx = std::max(mx, l1[i * d + r]);
-        return (double)std::max<unsigned long long>(mx, 1ULL);
-    };
-    double logB = 0;
-    for (auto &t : P.T) {
-        if (t.kind != KG) { logB += log2(l1max(t.sk[0])); continue; }
-        double best = 1e300;
-        for (size_t q = 0; q < t.legs.size(); ++q) {
-            double v = log2(l1max(t.sk[q]));
-            for (size_t q2 = 0; q2 < t.legs.size(); ++q2) if (q2 != q) v += log2((double)P.width[t.legs[q2]]);
-            best = std::min(best, v);
-        }
-        logB += best;
-    }
+static Mods mods_for(double logB, int K_min) {
     Mods md;
     md.K = 0;
     double have = 0;
-    while (md.K < kMaxMod && have < logB * (1 + 1e-9) + 3.0) {
+    while (md.K < kMaxMod && (have < logB * (1 + 1e-9) + 3.0 || md.K < K_min)) {
         md.a[md.K] = kModBits[md.K];
         md.m[md.K] = (1ULL << kModBits[md.K]) - 1;
         have += kModBits[md.K] - 1e-9;
         ++md.K;
     }
-    if (have < logB + 3.0) return fail(SK_EOVERFLOW, "estimate: bound 2^%.1f exceeds the exact range", logB);
+    return md;
+}
+
+static double mods_capacity(const Mods &md) {
+    double have = 0;
+    for (int k = 0; k < md.K; ++k) have += md.a[k] - 1e-9;
+    return have;
+}
+
+// log2 of the bound prod_t ||T_t||_1 from per-sketch L1 values (merged views: the best
+// constituent times the widths of the other legs)
+template <typename F>
+static double log_bound(const Plan &P, F l1of) {
+    double logB = 0;
+    for (auto &t : P.T) {
+        if (t.kind != KG) { logB += log2(std::max(1.0, l1of(t.sk[0]))); continue; }
+        double best = 1e300;
+        for (size_t q = 0; q < t.legs.size(); ++q) {
+            double v = log2(std::max(1.0, l1of(t.sk[q])));
+            for (size_t q2 = 0; q2 < t.legs.size(); ++q2) if (q2 != q) v += log2((double)P.width[t.legs[q2]]);
+            best = std::min(best, v);
+        }
+        logB += best;
+    }
+    return logB;
+}
+
+// Enqueue every kernel of one sub-plan on `stream` (no host synchronisation): per-row
+// residues -> acc[K][d] (zeroed by the caller), per-sketch-row L1 norms -> l1[n_uniq][d].
+static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const sk_sketch *> &uniq,
+                              DevPool &pool, uint64_t *acc, unsigned long long *l1, cudaStream_t stream) {
+    const int E = (int)P.edges.size();
+    const int NT = (int)P.T.size();
+    const int d = P.d;
     const int K = md.K;
+    sk_status st;
+    // ---- L1 norms of every sketch involved (checked against the moduli after the batch)
+    for (size_t b0 = 0; b0 < uniq.size(); b0 += kMaxL1Items) {
+        L1Items items;
+        items.n = (int)std::min<size_t>(kMaxL1Items, uniq.size() - b0);
+        uint32_t maxcells = 1;
+        for (int i = 0; i < items.n; ++i) {
+            const sk_sketch *s = uniq[b0 + i];
+            items.it[i] = {s->counters, s->d, (uint32_t)(s->n_counters / s->d)};
+            maxcells = std::max(maxcells, items.it[i].cells);
+        }
+        const unsigned chunks = std::min<unsigned>(64, (maxcells + 8191) / 8192);
+        k_l1<<<dim3(items.n, d, chunks), 256, 0, stream>>>(items, l1 + b0 * d, d); count_launch();
+        SKB_CUDA_CHECK("estimate launch 1");
+    }
     // ---- folded copies of every tensor leg
     std::vector<std::vector<const int64_t *>> data(NT);
     for (int i = 0; i < NT; ++i) {
@@ -742,7 +764,7 @@ static sk_status run_plan(const Plan &P, std::vector<SBig> &rows, cudaStream_t s
             }
         }
     }
-    SKB_CUDA(cudaGetLastError());
+    SKB_CUDA_CHECK("estimate launch 2");
     // ---- spanning tree rooted at local table 0 (DFS), post-order
     std::vector<int> parent_edge(NT, -2), order;
     {
@@ -797,7 +819,7 @@ static sk_status run_plan(const Plan &P, std::vector<SBig> &rows, cudaStream_t s
         const size_t sm = size_t(w) * 12;
         SKB_CUDA(cudaFuncSetAttribute(k_sort_abs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k_sort_abs<<<d, 512, sm, stream>>>(data[i][qc], w, (int32_t *)o, (uint64_t *)sa); count_launch();
-        SKB_CUDA(cudaGetLastError());
+        SKB_CUDA_CHECK("estimate launch 3");
         qc_of[i] = qc;
         ord_of[i] = (const int32_t *)o;
         sabs_of[i] = (const uint64_t *)sa;
@@ -820,10 +842,8 @@ static sk_status run_plan(const Plan &P, std::vector<SBig> &rows, cudaStream_t s
         msg[pe] = (uint64_t *)mb;
     }
     const int tiles_root = 1;
-    void *part, *acc;
+    void *part;
     if ((st = dalloc(pool, size_t(K) * d * Bc * tiles_root * 8, stream, &part))) return st;
-    if ((st = dalloc(pool, size_t(K) * d * 8, stream, &acc))) return st;
-    SKB_CUDA(cudaMemsetAsync(acc, 0, size_t(K) * d * 8, stream));
     for (int64_t b0 = 0; b0 < Btot; b0 += Bc) {
         const int B = (int)std::min<int64_t>(Bc, Btot - b0);
         for (int i : order) {
@@ -868,19 +888,89 @@ static sk_status run_plan(const Plan &P, std::vector<SBig> &rows, cudaStream_t s
             } else {
                 k_node_dense<<<dim3(blocks_xy, tiles), 256, 0, stream>>>(n, md); count_launch();
             }
-            SKB_CUDA(cudaGetLastError());
+            SKB_CUDA_CHECK("estimate launch 4");
         }
-        k_root_reduce<<<K * d, 256, 0, stream>>>((const uint64_t *)part, (uint64_t *)acc, B * tiles_root, d, md); count_launch();
-        SKB_CUDA(cudaGetLastError());
+        k_root_reduce<<<K * d, 256, 0, stream>>>((const uint64_t *)part, acc, B * tiles_root, d, md); count_launch();
+        SKB_CUDA_CHECK("estimate launch 5");
     }
-    std::vector<uint64_t> res(size_t(K) * d);
-    SKB_CUDA(cudaMemcpyAsync(res.data(), acc, res.size() * 8, cudaMemcpyDeviceToHost, stream));
+    return SK_OK;
+}
+
+// Evaluate a batch of sub-plans: all kernels enqueued, one device->host copy, one sync.
+// The moduli come from the survivor bound (a sketch row built from N tuples has
+// ||row||_1 <= N); the device-measured L1 norms verify it, else the plan is redone.
+static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vector<std::vector<SBig>> &rows,
+                           cudaStream_t stream) {
+    const size_t n = plans.size();
+    rows.assign(n, {});
+    if (!n) return SK_OK;
+    std::vector<Mods> mds(n);
+    std::vector<std::vector<const sk_sketch *>> uniqs(n);
+    std::vector<size_t> off_acc(n), off_l1(n);
+    size_t words = 0;
+    for (size_t i = 0; i < n; ++i) {
+        Plan &P = plans[i];
+        for (auto &t : P.T)
+            for (auto *s : t.sk)
+                if (std::find(uniqs[i].begin(), uniqs[i].end(), s) == uniqs[i].end()) uniqs[i].push_back(s);
+        const double logB = log_bound(P, [&](const sk_sketch *) { return 0.0; }) +
+                            [&] { double v = 0; for (int t : P.tabs) v += log2(std::max<double>(1.0, (double)g->survivors[t])); return v; }();
+        mds[i] = mods_for(logB, 1);
+        off_acc[i] = words;
+        words += size_t(mds[i].K) * P.d;
+        off_l1[i] = words;
+        words += uniqs[i].size() * P.d;
+    }
+    DevPool pool;
+    void *dres;
+    sk_status st;
+    if ((st = dalloc(pool, words * 8, stream, &dres))) return st;
+    SKB_CUDA(cudaMemsetAsync(dres, 0, words * 8, stream));
+    uint64_t *res = (uint64_t *)dres;
+    for (size_t i = 0; i < n; ++i)
+        if ((st = enqueue_plan(plans[i], mds[i], uniqs[i], pool, res + off_acc[i], (unsigned long long *)(res + off_l1[i]),
+                               stream)))
+            return st;
+    std::vector<uint64_t> host(words);
+    SKB_CUDA(cudaMemcpyAsync(host.data(), res, words * 8, cudaMemcpyDeviceToHost, stream));
     SKB_CUDA(cudaStreamSynchronize(stream));
-    rows.clear();
-    for (int r = 0; r < d; ++r) {
-        uint64_t rr[kMaxMod];
-        for (int k = 0; k < K; ++k) rr[k] = res[size_t(k) * d + r];
-        rows.push_back(crt_signed(rr, md));
+    for (size_t i = 0; i < n; ++i) {
+        const Plan &P = plans[i];
+        const int d = P.d;
+        auto l1of = [&](const sk_sketch *s) {
+            const size_t u = std::find(uniqs[i].begin(), uniqs[i].end(), s) - uniqs[i].begin();
+            uint64_t mx = 0;
+            for (int r = 0; r < d; ++r) mx = std::max<uint64_t>(mx, host[off_l1[i] + u * d + r]);
+            return (double)mx;
+        };
+        const double logB = log_bound(P, l1of);
+        if (logB + 3.0 > mods_capacity(mds[i])) {
+            // the survivor bound did not hold for these sketches: redo with the measured bound
+            Mods md = mods_for(logB, 1);
+            if (mods_capacity(md) < logB + 3.0)
+                return fail(SK_EOVERFLOW, "estimate: bound 2^%.1f exceeds the exact range", logB);
+            DevPool pool2;
+            void *d2;
+            const size_t w2 = size_t(md.K) * d + uniqs[i].size() * d;
+            if ((st = dalloc(pool2, w2 * 8, stream, &d2))) return st;
+            SKB_CUDA(cudaMemsetAsync(d2, 0, w2 * 8, stream));
+            if ((st = enqueue_plan(P, md, uniqs[i], pool2, (uint64_t *)d2, (unsigned long long *)d2 + size_t(md.K) * d, stream)))
+                return st;
+            std::vector<uint64_t> h2(w2);
+            SKB_CUDA(cudaMemcpyAsync(h2.data(), d2, w2 * 8, cudaMemcpyDeviceToHost, stream));
+            SKB_CUDA(cudaStreamSynchronize(stream));
+            for (int r = 0; r < d; ++r) {
+                uint64_t rr[kMaxMod];
+                for (int k = 0; k < md.K; ++k) rr[k] = h2[size_t(k) * d + r];
+                rows[i].push_back(crt_signed(rr, md));
+            }
+            continue;
+        }
+        for (int r = 0; r < d; ++r) {
+            uint64_t rr[kMaxMod];
+            for (int k = 0; k < mds[i].K; ++k) rr[k] = host[off_acc[i] + size_t(k) * d + r];
+            rows[i].push_back(crt_signed(rr, mds[i]));
+        }
     }
     return SK_OK;
 }
@@ -889,33 +979,58 @@ static sk_status run_plan(const Plan &P, std::vector<SBig> &rows, cudaStream_t s
 
 namespace skb {
 
-sk_status estimate_mask(const sk_graph *g, uint64_t mask, double *est, double *row_est,
-                        std::vector<std::string> *rows_exact, cudaStream_t stream) {
+// Batched evaluation: masks[i] -> est[i] (median, fp64), optional per-row values.
+sk_status estimate_batch(const sk_graph *g, const uint64_t *masks, uint32_t n, double *est,
+                         std::vector<std::vector<SBig>> *rows_out, cudaStream_t stream) {
     if (!g) return fail(SK_EINVAL, "estimate: NULL graph");
-    const int pc = __builtin_popcountll(mask);
-    if (pc == 0) return fail(SK_EINVAL, "estimate: empty vertex mask");
-    if (pc == 1) {
-        const int t = __builtin_ctzll(mask);
-        if ((uint32_t)t >= g->n_tables || !g->survivors) return fail(SK_EINVAL, "estimate: bad singleton");
-        if (est) *est = (double)g->survivors[t];
-        return SK_OK;
+    std::vector<Plan> plans;
+    std::vector<uint32_t> which;
+    for (uint32_t i = 0; i < n; ++i) {
+        const uint64_t mask = masks[i];
+        const int pc = __builtin_popcountll(mask);
+        if (pc == 0) return fail(SK_EINVAL, "estimate: empty vertex mask");
+        if (pc == 1) {
+            const int t = __builtin_ctzll(mask);
+            if ((uint32_t)t >= g->n_tables || !g->survivors) return fail(SK_EINVAL, "estimate: bad singleton");
+            if (est) est[i] = (double)g->survivors[t];
+            continue;
+        }
+        if (!g->survivors) return fail(SK_EINVAL, "estimate: graph survivors missing");
+        Plan P;
+        sk_status st = build_plan(g, mask, P);
+        if (st) return st;
+        plans.push_back(std::move(P));
+        which.push_back(i);
     }
-    Plan P;
-    sk_status st = build_plan(g, mask, P);
-    if (st) return st;
+    if (rows_out) rows_out->assign(n, {});
+    if (plans.empty()) return SK_OK;
     int prev = 0;
     cudaGetDevice(&prev);
-    SKB_CUDA(cudaSetDevice(P.device));
-    std::vector<SBig> rows;
-    st = run_plan(P, rows, stream);
+    SKB_CUDA(cudaSetDevice(plans[0].device));
+    std::vector<std::vector<SBig>> rows;
+    sk_status st = run_batch(g, plans, rows, stream);
     cudaSetDevice(prev);
     if (st) return st;
-    std::vector<int> idx(rows.size());
-    for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
-    std::sort(idx.begin(), idx.end(), [&](int x, int y) { return SBig::cmp(rows[x], rows[y]) < 0; });
-    if (est) *est = rows[idx[(rows.size() - 1) / 2]].to_double();
-    if (row_est) for (size_t r = 0; r < rows.size(); ++r) row_est[r] = rows[r].to_double();
-    if (rows_exact) { rows_exact->clear(); for (auto &v : rows) rows_exact->push_back(v.to_dec()); }
+    for (size_t j = 0; j < plans.size(); ++j) {
+        const uint32_t i = which[j];
+        std::vector<int> idx(rows[j].size());
+        for (size_t r = 0; r < idx.size(); ++r) idx[r] = (int)r;
+        std::sort(idx.begin(), idx.end(), [&](int x, int y) { return SBig::cmp(rows[j][x], rows[j][y]) < 0; });
+        if (est) est[i] = rows[j][idx[(rows[j].size() - 1) / 2]].to_double();
+        if (rows_out) (*rows_out)[i] = std::move(rows[j]);
+    }
+    return SK_OK;
+}
+
+sk_status estimate_mask(const sk_graph *g, uint64_t mask, double *est, double *row_est,
+                        std::vector<std::string> *rows_exact, cudaStream_t stream) {
+    std::vector<std::vector<SBig>> rows;
+    double e = 0;
+    sk_status st = estimate_batch(g, &mask, 1, &e, &rows, stream);
+    if (st) return st;
+    if (est) *est = e;
+    if (row_est) for (size_t r = 0; r < rows[0].size(); ++r) row_est[r] = rows[0][r].to_double();
+    if (rows_exact) { rows_exact->clear(); for (auto &v : rows[0]) rows_exact->push_back(v.to_dec()); }
     return SK_OK;
 }
 
@@ -944,11 +1059,7 @@ extern "C" sk_status estimate_join_exact(const sk_graph *g, uint64_t vertex_mask
 
 extern "C" sk_status estimate_subplans(const sk_graph *g, const uint64_t *masks, uint32_t n, double *est, void *stream) {
     if (n && (!masks || !est)) return fail(SK_EINVAL, "estimate_subplans: NULL array");
-    for (uint32_t i = 0; i < n; ++i) {
-        sk_status st = estimate_mask(g, masks[i], &est[i], nullptr, nullptr, (cudaStream_t)stream);
-        if (st) return st;
-    }
-    return SK_OK;
+    return estimate_batch(g, masks, n, est, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" sk_status plan_greedy(const sk_graph *g, uint32_t *order, double *prefix_card, double *cost, void *stream) {
@@ -957,6 +1068,34 @@ extern "C" sk_status plan_greedy(const sk_graph *g, uint32_t *order, double *pre
     if (n == 0 || n > 64) return fail(SK_EINVAL, "plan_greedy: n_tables must be in [1,64]");
     std::map<uint64_t, double> cache;
     sk_status err = SK_OK;
+    // A11: evaluate every connected sub-plan in one batch when there are few of them
+    if (n <= 16) {
+        std::vector<uint64_t> adj(n, 0);
+        for (uint32_t e = 0; e < g->n_edges; ++e) {
+            if (g->edge_u[e] >= n || g->edge_v[e] >= n) return fail(SK_EINVAL, "plan_greedy: bad edge");
+            adj[g->edge_u[e]] |= 1ULL << g->edge_v[e];
+            adj[g->edge_v[e]] |= 1ULL << g->edge_u[e];
+        }
+        std::vector<uint64_t> masks;
+        for (uint64_t m = 1; m < (1ULL << n) && masks.size() <= 512; ++m) {
+            if (__builtin_popcountll(m) < 2) continue;
+            uint64_t seen = m & (~m + 1), frontier = seen;
+            while (frontier) {
+                uint64_t nxt = 0;
+                for (uint64_t f = frontier; f; f &= f - 1) nxt |= adj[__builtin_ctzll(f)];
+                nxt &= m & ~seen;
+                seen |= nxt;
+                frontier = nxt;
+            }
+            if (seen == m) masks.push_back(m);
+        }
+        if (masks.size() <= 512) {
+            std::vector<double> est(masks.size());
+            sk_status st = estimate_batch(g, masks.data(), (uint32_t)masks.size(), est.data(), nullptr, (cudaStream_t)stream);
+            if (st) return st;
+            for (size_t i = 0; i < masks.size(); ++i) cache[masks[i]] = std::max(est[i], 0.0);
+        }
+    }
     auto card = [&](uint64_t m) -> double {
         auto it = cache.find(m);
         if (it != cache.end()) return it->second;

@@ -51,3 +51,9 @@ sk_status estimate_mask(const sk_graph *g, uint64_t mask, double *est, double *r
         cudaError_t e_ = (call);                                 \
         if (e_ != cudaSuccess) return skb::cuda_fail(e_, #call); \
     } while (0)
+
+#define SKB_CUDA_CHECK(what)                                     \
+    do {                                                         \
+        cudaError_t e_ = cudaGetLastError();                     \
+        if (e_ != cudaSuccess) return skb::cuda_fail(e_, what);  \
+    } while (0)
