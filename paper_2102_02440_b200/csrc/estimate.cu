@@ -34,23 +34,33 @@ using namespace skb;
 
 namespace {
 
-constexpr int kMaxMod = 10;
-const int kModBits[kMaxMod] = {61, 59, 57, 55, 53, 49, 47, 43, 41, 37};
+constexpr int kMaxMod = 28;
+// the 28 largest primes below 2^26 (pinned by tests/test_abi.py): residue products fit in
+// 52 bits, so up to 4096 of them accumulate exactly in one 64-bit register
+const uint32_t kPrimes[kMaxMod] = {67108859, 67108837, 67108819, 67108777, 67108763, 67108757, 67108753,
+                                   67108747, 67108739, 67108729, 67108721, 67108709, 67108693, 67108669,
+                                   67108667, 67108661, 67108649, 67108633, 67108597, 67108579, 67108529,
+                                   67108511, 67108507, 67108493, 67108471, 67108463, 67108453, 67108439};
 enum { KV = 0, KM = 1, KG = 2 };          // vector, matrix, merged
 enum { RCHILD = 0, RPARENT = 1, RFIXED = 2 };
 
 struct Mods {
     int K;
-    int a[kMaxMod];
-    uint64_t m[kMaxMod];
+    uint64_t m[kMaxMod];    // primes < 2^26
+    uint64_t mu[kMaxMod];   // floor(2^64 / m) (Barrett)
 };
 
 // ---------------------------------------------------------------- device modular arithmetic
-__device__ __forceinline__ uint64_t mm_mul(uint64_t x, uint64_t y, int a, uint64_t m) {
-    const uint64_t lo = x * y, hi = __umul64hi(x, y);
-    uint64_t r = (hi << (64 - a)) + (lo & m) + (lo >> a);
-    r = (r & m) + (r >> a);
-    return r >= m ? r - m : r;
+// t < 2^64 -> t mod m (Barrett: q >= t/m - 2, so at most two corrections)
+__device__ __forceinline__ uint64_t mm_red(uint64_t t, uint64_t m, uint64_t mu) {
+    const uint64_t q = __umul64hi(t, mu);
+    uint64_t r = t - q * m;
+    if (r >= m) r -= m;
+    if (r >= m) r -= m;
+    return r;
+}
+__device__ __forceinline__ uint64_t mm_mul(uint64_t x, uint64_t y, uint64_t m, uint64_t mu) {
+    return mm_red(x * y, m, mu);
 }
 __device__ __forceinline__ uint64_t mm_add(uint64_t x, uint64_t y, uint64_t m) {
     const uint64_t s = x + y;
@@ -59,17 +69,11 @@ __device__ __forceinline__ uint64_t mm_add(uint64_t x, uint64_t y, uint64_t m) {
 __device__ __forceinline__ uint64_t mm_sub(uint64_t x, uint64_t y, uint64_t m) {
     return x >= y ? x - y : x + (m - y);
 }
-__device__ __forceinline__ uint64_t mm_u64(uint64_t u, int a, uint64_t m) {
-    u = (u & m) + (u >> a);
-    u = (u & m) + (u >> a);
-    return u >= m ? u - m : u;
-}
-__device__ __forceinline__ uint64_t mm_i64(int64_t v, int a, uint64_t m) {
-    if (v >= 0) return mm_u64((uint64_t)v, a, m);
-    const uint64_t r = mm_u64((uint64_t)(-(v + 1)) + 1ULL, a, m);
-    return r ? m - r : 0;
-}
 __device__ __forceinline__ uint64_t uabs(int64_t v) { return v < 0 ? (uint64_t)(-(v + 1)) + 1ULL : (uint64_t)v; }
+__device__ __forceinline__ uint64_t mm_i64(int64_t v, uint64_t m, uint64_t mu) {
+    const uint64_t r = mm_red(uabs(v), m, mu);
+    return (v < 0 && r) ? m - r : r;
+}
 
 // ---------------------------------------------------------------- small kernels
 // per (item, row): sum |v| over `cells` counters (blockIdx.z = chunk; atomically accumulated)
@@ -110,7 +114,7 @@ __global__ void k_fold(const int64_t *in, int64_t *out, uint32_t d, uint32_t wn0
 }
 
 // per row: sort indices by |c| ascending (bitonic, w a power of two, w <= 8192)
-__global__ void k_sort_abs(const int64_t *c, uint32_t w, int32_t *ord, uint64_t *sabs) {
+__global__ void k_sort_abs(const int64_t *c, uint32_t w, int32_t *ord, uint64_t *sabs, int32_t *rank, int64_t *csorted) {
     extern __shared__ __align__(16) unsigned char sm[];
     uint64_t *key = reinterpret_cast<uint64_t *>(sm);
     uint32_t *idx = reinterpret_cast<uint32_t *>(key + w);
@@ -139,6 +143,8 @@ __global__ void k_sort_abs(const int64_t *c, uint32_t w, int32_t *ord, uint64_t 
     for (uint32_t i = threadIdx.x; i < w; i += blockDim.x) {
         ord[uint64_t(r) * w + i] = (int32_t)idx[i];
         sabs[uint64_t(r) * w + i] = key[i];
+        rank[uint64_t(r) * w + idx[i]] = (int32_t)i;
+        csorted[uint64_t(r) * w + i] = c[uint64_t(r) * w + idx[i]];
     }
 }
 
@@ -153,6 +159,8 @@ struct Node {
     int qc;                     // merged: contracted child leg
     const int32_t *ord;         // merged: [d][w_qc]
     const uint64_t *sabs;       // merged: [d][w_qc]
+    const int64_t *csorted;     // merged: constituent qc in |c|-sorted order [d][w_qc]
+    const int32_t *out_perm;    // parent message written at out_perm[r][o] (the parent's sorted order), or null
     uint64_t *out;              // parent message [K][d][out_bm][w_p], or root partials [K][d][B][tiles]
     int out_bm;
     int B, tiles, d;
@@ -196,7 +204,7 @@ __global__ void k_node_dense(const __grid_constant__ Node n, const __grid_consta
     const int bb = blockIdx.x % B;
     const int r = (blockIdx.x / B) % n.d;
     const int k = blockIdx.x / (B * n.d);
-    const int a = md.a[k];
+    const uint64_t mu = md.mu[k];
     const uint64_t m = md.m[k];
     const int64_t b = n.b0 + bb;
     int qp = -1, qf = -1, qc0 = -1, qc1 = -1;
@@ -223,14 +231,15 @@ __global__ void k_node_dense(const __grid_constant__ Node n, const __grid_consta
             if (qo >= 0) idx[qo] = o;
             if (qi >= 0) idx[qi] = i;
             if (qf >= 0) idx[qf] = b;
-            uint64_t term = mm_i64(tensor_val(n, r, idx), a, m);
-            if (xi) term = mm_mul(term, xi[i], a, m);
+            uint64_t term = mm_i64(tensor_val(n, r, idx), m, mu);
+            if (xi) term = mm_mul(term, xi[i], m, mu);
             s = mm_add(s, term, m);
         }
         if (qp >= 0) {
-            n.out[((uint64_t(k) * n.d + r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + o] = s;
+            const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
+            n.out[((uint64_t(k) * n.d + r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = s;
         } else {
-            if (xo) s = mm_mul(s, xo[o], a, m);
+            if (xo) s = mm_mul(s, xo[o], m, mu);
             acc = mm_add(acc, s, m);
         }
     }
@@ -241,62 +250,69 @@ __global__ void k_node_dense(const __grid_constant__ Node n, const __grid_consta
 }
 
 // merged node (min-abs view over <= 3 constituents), first child leg contracted by O9.
+// One CTA per (row r, conditioned bucket bb, tile of the outer leg) handles all K moduli:
+// the |c|-threshold positions of each outer index (binary searches, independent of the
+// modulus) are computed once into shared memory, then per modulus only the prefix sums
+// of the message and one O(1) combination per output remain.
+__device__ __forceinline__ void merged_LR(const Node &n, int r, int qc, int qf, int qo, int qi, int64_t b, int o, int i,
+                                          bool &hasL, int64_t &L, bool &hasR, int64_t &R) {
+    hasL = hasR = false;
+    L = R = 0;
+    for (int q = 0; q < n.nl; ++q) {
+        if (q == qc) continue;
+        const int64_t ix = (q == qf) ? b : (q == qo ? o : i);
+        const int64_t v = n.data[q][uint64_t(r) * n.w[q] + ix];
+        if (q < qc) { if (!hasL || !(uabs(L) <= uabs(v))) L = v; hasL = true; }
+        else { if (!hasR || !(uabs(R) <= uabs(v))) R = v; hasR = true; }
+    }
+}
+
+// #{s : S[s] < t} and #{s : S[s] <= t} over the ascending array S[0..w)
+__device__ __forceinline__ int count_lt(const uint64_t *S, int w, uint64_t t) {
+    int lo = 0, hi = w;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (S[mid] < t) lo = mid + 1; else hi = mid; }
+    return lo;
+}
+__device__ __forceinline__ int count_le(const uint64_t *S, int w, uint64_t t) {
+    int lo = 0, hi = w;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (S[mid] <= t) lo = mid + 1; else hi = mid; }
+    return lo;
+}
+
+// sum_i x_i fold(L, c_i, R) mod m from the prefix sums P1 (x) and P2 (x*c)
+__device__ __forceinline__ uint64_t o9_value(const uint64_t *P1, const uint64_t *P2, int wq, bool hasL, int64_t L,
+                                             bool hasR, int64_t R, int nless, int nle, uint64_t m, uint64_t mu) {
+    uint64_t V;
+    if (hasL) {
+        const int64_t win = (hasR && !(uabs(L) <= uabs(R))) ? R : L;
+        V = mm_mul(mm_i64(win, m, mu), mm_sub(P1[wq], P1[nless], m), m, mu);
+        int endB = nless;
+        if (hasR && nle < endB) {
+            V = mm_add(V, mm_mul(mm_i64(R, m, mu), mm_sub(P1[endB], P1[nle], m), m, mu), m);
+            endB = nle;
+        }
+        V = mm_add(V, P2[endB], m);
+    } else {
+        V = mm_add(mm_mul(mm_i64(R, m, mu), mm_sub(P1[wq], P1[nle], m), m, mu), P2[nle], m);
+    }
+    return V;
+}
+
 __global__ void k_node_merged(const __grid_constant__ Node n, const __grid_constant__ Mods md) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ uint64_t red[32];
-    __shared__ uint64_t tot1[1024], tot2[1024];
+    __shared__ uint64_t tot1[256], tot2[256];
     const int B = n.B;
     const int bb = blockIdx.x % B;
-    const int r = (blockIdx.x / B) % n.d;
-    const int k = blockIdx.x / (B * n.d);
-    const int a = md.a[k];
-    const uint64_t m = md.m[k];
+    const int r = blockIdx.x / B;
     const int64_t b = n.b0 + bb;
     const int qc = n.qc;
     const int wq = n.w[qc];
     uint64_t *P1 = reinterpret_cast<uint64_t *>(sm);
     uint64_t *P2 = P1 + (wq + 1);
     uint64_t *S = P2 + (wq + 1);
-    const uint64_t *x = msg_row(n, qc, k, r, bb, 0);
-    const int64_t *cq = n.data[qc] + uint64_t(r) * wq;
-    const int32_t *ord = n.ord + uint64_t(r) * wq;
-    // --- prefix sums over the |c|-sorted order (block scan, contiguous chunks per thread)
-    const int nt = blockDim.x;
-    const int chunk = (wq + nt - 1) / nt;
-    const int s0 = threadIdx.x * chunk, s1 = min(wq, s0 + chunk);
-    uint64_t l1 = 0, l2 = 0;
-    for (int s = s0; s < s1; ++s) {
-        const int i = ord[s];
-        const uint64_t xv = x[i];
-        l1 = mm_add(l1, xv, m);
-        l2 = mm_add(l2, mm_mul(xv, mm_i64(cq[i], a, m), a, m), m);
-        S[s] = n.sabs[uint64_t(r) * wq + s];
-    }
-    tot1[threadIdx.x] = l1;
-    tot2[threadIdx.x] = l2;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t c1 = 0, c2 = 0;
-        for (int t = 0; t < nt; ++t) {
-            const uint64_t v1 = tot1[t], v2 = tot2[t];
-            tot1[t] = c1; tot2[t] = c2;
-            c1 = mm_add(c1, v1, m); c2 = mm_add(c2, v2, m);
-        }
-        P1[wq] = c1; P2[wq] = c2;
-    }
-    __syncthreads();
-    {
-        uint64_t c1 = tot1[threadIdx.x], c2 = tot2[threadIdx.x];
-        for (int s = s0; s < s1; ++s) {
-            P1[s] = c1; P2[s] = c2;
-            const int i = ord[s];
-            const uint64_t xv = x[i];
-            c1 = mm_add(c1, xv, m);
-            c2 = mm_add(c2, mm_mul(xv, mm_i64(cq[i], a, m), a, m), m);
-        }
-    }
-    __syncthreads();
-    // --- enumerate the other legs
+    uint32_t *pos = reinterpret_cast<uint32_t *>(S + wq);     // per outer index: nless | nle << 16
+    const int64_t *cs = n.csorted + uint64_t(r) * wq;
     int qp = -1, qf = -1, oc[2] = {-1, -1}, noc = 0;
     for (int q = 0; q < n.nl; ++q) {
         if (q == qc) continue;
@@ -309,66 +325,160 @@ __global__ void k_node_merged(const __grid_constant__ Node n, const __grid_const
     const int qi = qp >= 0 ? oc[0] : oc[1];
     const int wo = qo >= 0 ? n.w[qo] : 1;
     const int wi = qi >= 0 ? n.w[qi] : 1;
-    const uint64_t *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row(n, qo, k, r, bb, 0) : nullptr;
-    const uint64_t *xi2 = qi >= 0 ? msg_row(n, qi, k, r, bb, 0) : nullptr;
     const int per_tile = (wo + n.tiles - 1) / n.tiles;
     const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
-    uint64_t acc = 0;
-    for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
-        uint64_t s = 0;
-        for (int i = 0; i < wi; ++i) {
-            // constituent values of the non-contracted legs
-            int64_t val[3] = {0, 0, 0};
-            for (int q = 0; q < n.nl; ++q) {
-                if (q == qc) continue;
-                int64_t ix = (q == qf) ? b : (q == qo ? o : i);
-                val[q] = n.data[q][uint64_t(r) * n.w[q] + ix];
-            }
-            bool hasL = false, hasR = false;
-            int64_t L = 0, R = 0;
-            for (int q = 0; q < n.nl; ++q) {
-                if (q == qc) continue;
-                if (q < qc) { if (!hasL || !(uabs(L) <= uabs(val[q]))) L = val[q]; hasL = true; }
-                else { if (!hasR || !(uabs(R) <= uabs(val[q]))) R = val[q]; hasR = true; }
-            }
-            uint64_t V;
-            if (hasL) {
-                const uint64_t aL = uabs(L);
-                int lo = 0, hi = wq;                                 // #{|c| < |L|}
-                while (lo < hi) { int mid = (lo + hi) >> 1; if (S[mid] < aL) lo = mid + 1; else hi = mid; }
-                const int nless = lo;
-                const int64_t win = (hasR && !(aL <= uabs(R))) ? R : L;
-                V = mm_mul(mm_i64(win, a, m), mm_sub(P1[wq], P1[nless], m), a, m);
-                int endB = nless;
-                if (hasR) {
-                    const uint64_t aR = uabs(R);
-                    lo = 0; hi = wq;                                 // #{|c| <= |R|}
-                    while (lo < hi) { int mid = (lo + hi) >> 1; if (S[mid] <= aR) lo = mid + 1; else hi = mid; }
-                    if (lo < endB) {
-                        V = mm_add(V, mm_mul(mm_i64(R, a, m), mm_sub(P1[endB], P1[lo], m), a, m), m);
-                        endB = lo;
-                    }
-                }
-                V = mm_add(V, P2[endB], m);
-            } else {
-                const uint64_t aR = uabs(R);
-                int lo = 0, hi = wq;
-                while (lo < hi) { int mid = (lo + hi) >> 1; if (S[mid] <= aR) lo = mid + 1; else hi = mid; }
-                V = mm_add(mm_mul(mm_i64(R, a, m), mm_sub(P1[wq], P1[lo], m), a, m), P2[lo], m);
-            }
-            if (xi2) V = mm_mul(V, xi2[i], a, m);
-            s = mm_add(s, V, m);
-        }
-        if (qp >= 0) {
-            n.out[((uint64_t(k) * n.d + r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + o] = s;
-        } else {
-            if (xo) s = mm_mul(s, xo[o], a, m);
-            acc = mm_add(acc, s, m);
+    for (int s = threadIdx.x; s < wq; s += blockDim.x) S[s] = n.sabs[uint64_t(r) * wq + s];
+    __syncthreads();
+    // --- threshold positions per outer index (modulus-independent), when there is no inner leg
+    const bool cache_pos = qi < 0;
+    if (cache_pos) {
+        for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
+            bool hasL, hasR;
+            int64_t L, R;
+            merged_LR(n, r, qc, qf, qo, qi, b, o, 0, hasL, L, hasR, R);
+            const int nless = hasL ? count_lt(S, wq, uabs(L)) : 0;
+            const int nle = hasR ? count_le(S, wq, uabs(R)) : 0;
+            pos[o - o_begin] = (uint32_t)nless | ((uint32_t)nle << 16);
         }
     }
-    if (qp < 0) {
-        const uint64_t t = block_sum_mod(acc, m, red);
-        if (threadIdx.x == 0) n.out[((uint64_t(k) * n.d + r) * B + bb) * n.tiles + blockIdx.y] = t;
+    const int nt = blockDim.x;
+    const int chunk = (wq + nt - 1) / nt;
+    const int s0 = threadIdx.x * chunk, s1 = min(wq, s0 + chunk);
+    for (int k = 0; k < md.K; ++k) {
+        const uint64_t mu = md.mu[k];
+        const uint64_t m = md.m[k];
+        const uint64_t *x = msg_row(n, qc, k, r, bb, 0);
+        // --- prefix sums over the |c|-sorted order (block scan, contiguous chunks per thread)
+        uint64_t l1 = 0, l2 = 0;
+        for (int s = s0; s < s1; ++s) {      // x arrives in the |c|-sorted order (out_perm of the child)
+            const uint64_t xv = x[s];
+            l1 = mm_add(l1, xv, m);
+            l2 = mm_add(l2, mm_mul(xv, mm_i64(cs[s], m, mu), m, mu), m);
+        }
+        __syncthreads();   // previous modulus finished reading P1/P2
+        tot1[threadIdx.x] = l1;
+        tot2[threadIdx.x] = l2;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t c1 = 0, c2 = 0;
+            for (int t = 0; t < nt; ++t) {
+                const uint64_t v1 = tot1[t], v2 = tot2[t];
+                tot1[t] = c1; tot2[t] = c2;
+                c1 = mm_add(c1, v1, m); c2 = mm_add(c2, v2, m);
+            }
+            P1[wq] = c1; P2[wq] = c2;
+        }
+        __syncthreads();
+        {
+            uint64_t c1 = tot1[threadIdx.x], c2 = tot2[threadIdx.x];
+            for (int s = s0; s < s1; ++s) {
+                P1[s] = c1; P2[s] = c2;
+                const uint64_t xv = x[s];
+                c1 = mm_add(c1, xv, m);
+                c2 = mm_add(c2, mm_mul(xv, mm_i64(cs[s], m, mu), m, mu), m);
+            }
+        }
+        __syncthreads();
+        // --- outputs
+        const uint64_t *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row(n, qo, k, r, bb, 0) : nullptr;
+        const uint64_t *xi2 = qi >= 0 ? msg_row(n, qi, k, r, bb, 0) : nullptr;
+        uint64_t acc = 0;
+        for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
+            uint64_t sacc = 0;
+            for (int i = 0; i < wi; ++i) {
+                bool hasL, hasR;
+                int64_t L, R;
+                merged_LR(n, r, qc, qf, qo, qi, b, o, i, hasL, L, hasR, R);
+                int nless, nle;
+                if (cache_pos) {
+                    const uint32_t pv = pos[o - o_begin];
+                    nless = (int)(pv & 0xffffu);
+                    nle = (int)(pv >> 16);
+                } else {
+                    nless = hasL ? count_lt(S, wq, uabs(L)) : 0;
+                    nle = hasR ? count_le(S, wq, uabs(R)) : 0;
+                }
+                uint64_t V = o9_value(P1, P2, wq, hasL, L, hasR, R, nless, nle, m, mu);
+                if (xi2) V = mm_mul(V, xi2[i], m, mu);
+                sacc = mm_add(sacc, V, m);
+            }
+            if (qp >= 0) {
+                const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
+                n.out[((uint64_t(k) * n.d + r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = sacc;
+            } else {
+                if (xo) sacc = mm_mul(sacc, xo[o], m, mu);
+                acc = mm_add(acc, sacc, m);
+            }
+        }
+        if (qp < 0) {
+            const uint64_t t = block_sum_mod(acc, m, red);
+            if (threadIdx.x == 0) n.out[((uint64_t(k) * n.d + r) * B + bb) * n.tiles + blockIdx.y] = t;
+        }
+    }
+}
+
+// Matrix node with one child leg and one parent leg, batched over the conditioned bucket:
+// out[b][j] = sum_i x[b][i] * M(i, j) mod m — a modular GEMM.  Residues are < 2^26, so
+// products (< 2^52) accumulate exactly in 64 bits (IMAD.WIDE.U32) for 4096 steps between
+// Barrett reductions.  Tile 32 b x 64 j x 32 i, 8 outputs per thread.
+constexpr int GBM = 32, GBN = 64, GBK = 32;
+__global__ void __launch_bounds__(256) k_node_mat_gemm(const __grid_constant__ Node n, const __grid_constant__ Mods md, int qc) {
+    __shared__ uint32_t Xs[GBK][GBM + 1];
+    __shared__ uint32_t Ms[GBK][GBN + 4];
+    const int k = blockIdx.x / n.d, r = blockIdx.x % n.d;
+    const uint64_t m = md.m[k], mu = md.mu[k];
+    const int nbt = (n.B + GBM - 1) / GBM;
+    const int b0 = (blockIdx.y % nbt) * GBM, j0 = (blockIdx.y / nbt) * GBN;
+    const int qp = 1 - qc;
+    const int wi = n.w[qc], wj = n.w[qp];
+    const int64_t *T = n.data[0] + uint64_t(r) * n.w[0] * n.w[1];
+    const int tid = threadIdx.x;
+    const int tb = (tid >> 4) * 2, tj = (tid & 15) * 4;
+    uint64_t acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+    int since = 0;
+    for (int i0 = 0; i0 < wi; i0 += GBK) {
+        for (int e = tid; e < GBK * GBM; e += 256) {
+            const int ii = e % GBK, bl = e / GBK;
+            const int b = b0 + bl, i = i0 + ii;
+            Xs[ii][bl] = (b < n.B && i < wi) ? (uint32_t)msg_row(n, qc, k, r, b, 0)[i] : 0u;
+        }
+        for (int e = tid; e < GBK * GBN; e += 256) {
+            int ii, jj;
+            if (qc == 0) { jj = e % GBN; ii = e / GBN; } else { ii = e % GBK; jj = e / GBK; }
+            const int i = i0 + ii, j = j0 + jj;
+            uint32_t v = 0;
+            if (i < wi && j < wj) v = (uint32_t)mm_i64(qc == 0 ? T[uint64_t(i) * wj + j] : T[uint64_t(j) * wi + i], m, mu);
+            Ms[ii][jj] = v;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int ii = 0; ii < GBK; ++ii) {
+            const uint64_t x0 = Xs[ii][tb], x1 = Xs[ii][tb + 1];
+            const uint64_t m0 = Ms[ii][tj], m1 = Ms[ii][tj + 1], m2 = Ms[ii][tj + 2], m3 = Ms[ii][tj + 3];
+            acc[0][0] += x0 * m0; acc[0][1] += x0 * m1; acc[0][2] += x0 * m2; acc[0][3] += x0 * m3;
+            acc[1][0] += x1 * m0; acc[1][1] += x1 * m1; acc[1][2] += x1 * m2; acc[1][3] += x1 * m3;
+        }
+        __syncthreads();
+        since += GBK;
+        if (since >= 4096) {
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[a][c] = mm_red(acc[a][c], m, mu);
+            since = 0;
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        const int b = b0 + tb + a;
+        if (b >= n.B) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int j = j0 + tj + c;
+            if (j >= wj) continue;
+            const int jo = n.out_perm ? n.out_perm[uint64_t(r) * wj + j] : j;
+            n.out[((uint64_t(k) * n.d + r) * n.out_bm + (n.out_bm > 1 ? b : 0)) * wj + jo] = mm_red(acc[a][c], m, mu);
+        }
     }
 }
 
@@ -685,9 +795,9 @@ static Mods mods_for(double logB, int K_min) {
     md.K = 0;
     double have = 0;
     while (md.K < kMaxMod && (have < logB * (1 + 1e-9) + 3.0 || md.K < K_min)) {
-        md.a[md.K] = kModBits[md.K];
-        md.m[md.K] = (1ULL << kModBits[md.K]) - 1;
-        have += kModBits[md.K] - 1e-9;
+        md.m[md.K] = kPrimes[md.K];
+        md.mu[md.K] = (uint64_t)(((unsigned __int128)1 << 64) / kPrimes[md.K]);
+        have += log2((double)kPrimes[md.K]) - 1e-9;
         ++md.K;
     }
     return md;
@@ -695,7 +805,7 @@ static Mods mods_for(double logB, int K_min) {
 
 static double mods_capacity(const Mods &md) {
     double have = 0;
-    for (int k = 0; k < md.K; ++k) have += md.a[k] - 1e-9;
+    for (int k = 0; k < md.K; ++k) have += log2((double)md.m[k]) - 1e-9;
     return have;
 }
 
@@ -800,6 +910,8 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
     std::vector<int> qc_of(NT, -1);
     std::vector<const int32_t *> ord_of(NT, nullptr);
     std::vector<const uint64_t *> sabs_of(NT, nullptr);
+    std::vector<const int64_t *> csorted_of(NT, nullptr);
+    std::vector<const int32_t *> perm_of_edge(E, nullptr);   // messages delivered in the parent's sorted order
     for (int i = 0; i < NT; ++i) {
         const TabT &t = P.T[i];
         if (t.kind != KG) continue;
@@ -813,12 +925,16 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
         if (qc < 0) continue;   // merged leaf: evaluated densely
         const int w = P.width[t.legs[qc]];
         if (w > 8192) return fail(SK_EOVERFLOW, "estimate: merged contraction supports widths <= 8192");
-        void *o, *sa;
+        void *o, *sa, *rk, *csd;
         if ((st = dalloc(pool, size_t(d) * w * 4, stream, &o))) return st;
         if ((st = dalloc(pool, size_t(d) * w * 8, stream, &sa))) return st;
+        if ((st = dalloc(pool, size_t(d) * w * 4, stream, &rk))) return st;
+        if ((st = dalloc(pool, size_t(d) * w * 8, stream, &csd))) return st;
         const size_t sm = size_t(w) * 12;
         SKB_CUDA(cudaFuncSetAttribute(k_sort_abs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k_sort_abs<<<d, 512, sm, stream>>>(data[i][qc], w, (int32_t *)o, (uint64_t *)sa); count_launch();
+        k_sort_abs<<<d, 512, sm, stream>>>(data[i][qc], w, (int32_t *)o, (uint64_t *)sa, (int32_t *)rk, (int64_t *)csd); count_launch();
+        perm_of_edge[t.legs[qc]] = (const int32_t *)rk;
+        csorted_of[i] = (const int64_t *)csd;
         SKB_CUDA_CHECK("estimate launch 3");
         qc_of[i] = qc;
         ord_of[i] = (const int32_t *)o;
@@ -826,10 +942,11 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
     }
     // ---- chunking of the conditioned bucket
     const int64_t Btot = P.cond >= 0 ? P.width[P.cond] : 1;
-    size_t per_b = 0;
-    for (int le = 0; le < E; ++le) per_b += size_t(K) * d * P.width[le] * 8;
+    size_t per_b = size_t(K) * d * 8;                      // root partials
+    for (int i : order)
+        if (parent_edge[i] >= 0 && depb[i]) per_b += size_t(K) * d * P.width[parent_edge[i]] * 8;
     int64_t Bc = Btot;
-    while (Bc > 1 && per_b * Bc > (size_t(768) << 20)) Bc = (Bc + 1) / 2;
+    while (Bc > 1 && per_b * Bc > (size_t(3) << 30)) Bc = (Bc + 1) / 2;
     // message buffers per local edge
     std::vector<uint64_t *> msg(E, nullptr);
     std::vector<int> msg_bm(E, 1);
@@ -872,19 +989,37 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
             if (pe >= 0) {
                 n.out = msg[pe];
                 n.out_bm = msg_bm[pe];
+                n.out_perm = perm_of_edge[pe];
                 const int wo = P.width[pe];
                 while (blocks_xy * tiles < 592 && tiles * 256 < wo) tiles *= 2;
             } else {
                 n.out = (uint64_t *)part;
             }
             n.tiles = tiles;
-            if (t.kind == KG && qc_of[i] >= 0) {
+            int nchild = 0, qchild = -1;
+            bool hasfixed = false;
+            for (int q = 0; q < n.nl; ++q) {
+                if (n.role[q] == RCHILD) { ++nchild; qchild = q; }
+                if (n.role[q] == RFIXED) hasfixed = true;
+            }
+            if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB >= 16) {
+                const int nbt = (nB + GBM - 1) / GBM;
+                const int njt = (P.width[pe] + GBN - 1) / GBN;
+                k_node_mat_gemm<<<dim3(K * d, nbt * njt), 256, 0, stream>>>(n, md, qchild); count_launch();
+            } else if (t.kind == KG && qc_of[i] >= 0) {
                 n.qc = qc_of[i];
                 n.ord = ord_of[i];
                 n.sabs = sabs_of[i];
-                const size_t sm = (size_t(2) * (n.w[n.qc] + 1) + n.w[n.qc]) * 8;
+                n.csorted = csorted_of[i];
+                int wo_max = 1;
+                for (int q = 0; q < n.nl; ++q) if (q != n.qc && n.role[q] != RFIXED) wo_max = std::max(wo_max, n.w[q]);
+                int mtiles = 1;
+                while (d * nB * mtiles < 296 && mtiles * 256 < wo_max) mtiles *= 2;
+                n.tiles = (pe >= 0) ? mtiles : 1;
+                const size_t sm = (size_t(2) * (n.w[n.qc] + 1) + n.w[n.qc]) * 8 + size_t(wo_max) * 4 + 16;
+                if (sm > 227 * 1024) return fail(SK_EOVERFLOW, "estimate: merged contraction too wide");
                 SKB_CUDA(cudaFuncSetAttribute(k_node_merged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-                k_node_merged<<<dim3(blocks_xy, tiles), 256, sm, stream>>>(n, md); count_launch();
+                k_node_merged<<<dim3(d * nB, n.tiles), 256, sm, stream>>>(n, md); count_launch();
             } else {
                 k_node_dense<<<dim3(blocks_xy, tiles), 256, 0, stream>>>(n, md); count_launch();
             }

@@ -105,3 +105,38 @@ def test_workload_shapes_match_baseline_configs():
     # C3 canonical edge order quoted in SURVEY.md O11: e4 < e3 < e5 < e1 < e2
     ids = [e[0] for e in c3.edges]
     assert sorted(ids) == ["CI.mid|MK.mid", "CI.mid|T.id", "CI.pid|N.id", "K.id|MK.kid", "MK.mid|T.id"]
+
+
+def test_crt_moduli_are_distinct_primes_below_2_26():
+    """The exact-estimate engine's CRT moduli (csrc/estimate.cu kPrimes): distinct primes
+    < 2^26 (so residue products accumulate exactly in 64 bits), >= 700 bits in total."""
+    import math
+    src = open(os.path.join(ROOT, "paper_2102_02440_b200", "csrc", "estimate.cu")).read()
+    body = src[src.index("kPrimes[kMaxMod] = {") + len("kPrimes[kMaxMod] = {"):]
+    primes = [int(x) for x in body[:body.index("}")].replace("\n", " ").split(",")]
+
+    def is_prime(n):
+        if n < 2:
+            return False
+        for p in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+            if n % p == 0:
+                return n == p
+        d, s = n - 1, 0
+        while d % 2 == 0:
+            d //= 2
+            s += 1
+        for a in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+            x = pow(a, d, n)
+            if x in (1, n - 1):
+                continue
+            for _ in range(s - 1):
+                x = x * x % n
+                if x == n - 1:
+                    break
+            else:
+                return False
+        return True
+
+    assert len(set(primes)) == len(primes) == 28
+    assert all(is_prime(p) and p < (1 << 26) for p in primes)
+    assert sum(math.log2(p) for p in primes) > 700
