@@ -84,6 +84,8 @@ class Col:
     name: str
     dtype: str                 # "int32" | "int64"
     dist: tuple                # ("uniform", lo, hi) | ("zipf", s, N) | ("rowid",)
+    domain: int = 0            # values lie in [0, domain) (0 = not stated); filled by Table
+
 
 
 @dataclass
@@ -102,6 +104,16 @@ class Table:
     n_rows: int
     cols: list
     preds: list = field(default_factory=list)
+
+    def __post_init__(self):
+        # value-domain statement of each generated column (a property of the generator)
+        for c in self.cols:
+            if c.dist[0] == "rowid":
+                c.domain = self.n_rows
+            elif c.dist[0] == "uniform" and c.dist[1] >= 0:
+                c.domain = int(c.dist[2])
+            elif c.dist[0] == "zipf":
+                c.domain = int(c.dist[2])
 
 
 @dataclass

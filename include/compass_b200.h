@@ -116,6 +116,11 @@ typedef enum { SK_INT32 = 0, SK_INT64 = 1 } sk_dtype;
 typedef struct {
     const void *data;   /* device pointer */
     uint32_t dtype;     /* sk_dtype */
+    uint64_t domain;    /* optional hint: key values lie in [0, domain); 0 = unknown.  With a
+                           hint <= 2^22 the 1-D sketches of this key column are built by
+                           histogram-then-sketch (one L2 atomic per surviving tuple, hashing once
+                           per distinct key; exact by linearity).  Values outside
+                           the hinted domain are still counted exactly (direct path). */
 } sk_column;
 
 typedef enum { SK_PRED_POINT = 0, SK_PRED_RANGE = 1, SK_PRED_SUBSET = 2 } sk_pred_kind;

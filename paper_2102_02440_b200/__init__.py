@@ -41,7 +41,7 @@ class sk_desc(ctypes.Structure):
 
 
 class sk_column(ctypes.Structure):
-    _fields_ = [("data", ctypes.c_void_p), ("dtype", ctypes.c_uint32)]
+    _fields_ = [("data", ctypes.c_void_p), ("dtype", ctypes.c_uint32), ("domain", ctypes.c_uint64)]
 
 
 class sk_pred(ctypes.Structure):
@@ -172,15 +172,18 @@ class Sketch:
             pass
 
 
-def sketch_update_filtered(columns, n_rows: int, preds, targets, survivors: torch.Tensor | None = None, stream=None):
+def sketch_update_filtered(columns, n_rows: int, preds, targets, survivors: torch.Tensor | None = None, stream=None,
+                           domains=None):
     """One fused scan.  columns: list of int32/int64 CUDA tensors; preds: list of
-    (col_index, kind, lo, hi, set_values); targets: list of (Sketch, [key col indices])."""
+    (col_index, kind, lo, hi, set_values); targets: list of (Sketch, [key col indices]);
+    domains: optional per-column key-domain hints (0 = unknown)."""
     ncol = len(columns)
     cols = (sk_column * max(1, ncol))()
     for i, c in enumerate(columns):
         assert c.is_cuda and c.dtype in (torch.int32, torch.int64) and c.is_contiguous()
         cols[i].data = c.data_ptr()
         cols[i].dtype = SK_INT64 if c.dtype == torch.int64 else SK_INT32
+        cols[i].domain = int(domains[i]) if domains else 0
     keep = []
     pr = (sk_pred * max(1, len(preds)))()
     for i, p in enumerate(preds):

@@ -58,6 +58,19 @@ uint64_t seed_coef(uint64_t master, const std::string &edge, uint32_t row, uint3
     return v % SKP_MERSENNE61;
 }
 
+// Stream-ordered temporaries (cudaMallocAsync) come from the device's default pool; keep
+// freed blocks in the pool instead of releasing them to the driver at every synchronisation.
+void ensure_pool(int device) {
+    static std::atomic<uint64_t> done{0};
+    if (device < 0 || device >= 64 || ((done.load() >> device) & 1ULL)) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = ~0ULL;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done.fetch_or(1ULL << device);
+}
+
 bool same_desc(const sk_sketch *a, const sk_sketch *b) {
     if (a->d != b->d || a->ndim != b->ndim || a->master != b->master) return false;
     for (uint32_t q = 0; q < a->ndim; ++q)
@@ -107,6 +120,7 @@ extern "C" sk_status sketch_create(const sk_desc *desc, int device, int64_t *cou
     }
     sk->device = device;
     sk->n_counters = cells * desc->d;
+    ensure_pool(device);
     sk->seeds_host.resize(size_t(sk->ndim) * sk->d * 6);
     for (uint32_t q = 0; q < sk->ndim; ++q)
         for (uint32_t r = 0; r < sk->d; ++r) {

@@ -36,6 +36,9 @@ uint64_t seed_coef(uint64_t master, const std::string &edge, uint32_t row, uint3
 
 bool same_desc(const sk_sketch *a, const sk_sketch *b);
 
+// keep the device's default memory pool from releasing memory at every sync
+void ensure_pool(int device);
+
 // count one kernel launch issued by the library (sk_kernel_launches)
 void count_launch(uint64_t n = 1);
 

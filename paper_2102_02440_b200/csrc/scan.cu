@@ -20,6 +20,7 @@
 //       sketch with red.global.add (order-independent, bit-exact).
 #include <stdint.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <climits>
@@ -59,6 +60,8 @@ struct SKey {
     int32_t hh_off;       // byte offset of this key's heavy-hitter table, -1 = none
     uint32_t has1d;       // some 1-D target hashes this key
     uint32_t hasglob;     // some non-privatised 1-D target hashes this key
+    uint32_t *hist;       // histogram mode: per-key counts over [0, domain), else null
+    uint64_t domain;
 };
 struct STarget {
     int64_t *counters;
@@ -136,6 +139,9 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 __device__ __forceinline__ void cp_wait_all_but1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
+__device__ __forceinline__ void red_add_u32(uint32_t *p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_add_s64(int64_t *p, int64_t v) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -198,13 +204,14 @@ __device__ __forceinline__ void update_1d(const STarget &tg, const uint64_t *see
     }
 }
 
-__device__ __forceinline__ void update_2d(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, uint64_t y) {
+__device__ __forceinline__ void update_2d(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, uint64_t y,
+                                          int cnt) {
     const uint64_t *s1 = seed + tg.d * 6;
     for (uint32_t r = 0; r < tg.d; ++r) {
         const uint64_t *a = seed + r * 6, *b = s1 + r * 6;
         const uint32_t cell = ((uint32_t)(hash_g61(a[4], a[5], x) & tg.wmask0) << tg.lw1) |
                               (uint32_t)(hash_g61(b[4], b[5], y) & tg.wmask1);
-        const int v = xi_sign61(a, x) * xi_sign61(b, y);
+        const int v = xi_sign61(a, x) * xi_sign61(b, y) * cnt;
         if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
         else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
     }
@@ -257,12 +264,27 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
             cnt = __popc(grp);
         }
         if (leader) {
-            if (P.key[k].hh_off >= 0) miss = !hh_add(smem + P.key[k].hh_off, P.hh_log2, x[k], cnt);
-            else miss = P.key[k].hasglob;
-            for (uint32_t t = 0; t < P.n_targets; ++t) {
-                const STarget &tg = P.tgt[t];
-                if (tg.ndim != 1 || tg.k0 != (uint32_t)k || tg.smem_off < 0) continue;
-                update_1d(tg, seeds + tg.seed_off, sc, x[k], cnt);   // privatised: always direct
+            if (P.key[k].hist) {
+                // histogram mode: count the key (heavy-hitter table first, then the L2 histogram);
+                // all 1-D sketches of this key are built from the counts after the scan
+                bool done = P.key[k].hh_off >= 0 && hh_add(smem + P.key[k].hh_off, P.hh_log2, x[k], cnt);
+                if (!done && x[k] < P.key[k].domain) { red_add_u32(P.key[k].hist + x[k], (uint32_t)cnt); done = true; }
+                if (!done) {   // outside the hinted domain: direct updates
+                    miss = P.key[k].hasglob;
+                    for (uint32_t t = 0; t < P.n_targets; ++t) {
+                        const STarget &tg = P.tgt[t];
+                        if (tg.ndim != 1 || tg.k0 != (uint32_t)k || tg.smem_off < 0) continue;
+                        update_1d(tg, seeds + tg.seed_off, sc, x[k], cnt);
+                    }
+                }
+            } else {
+                if (P.key[k].hh_off >= 0) miss = !hh_add(smem + P.key[k].hh_off, P.hh_log2, x[k], cnt);
+                else miss = P.key[k].hasglob;
+                for (uint32_t t = 0; t < P.n_targets; ++t) {
+                    const STarget &tg = P.tgt[t];
+                    if (tg.ndim != 1 || tg.k0 != (uint32_t)k || tg.smem_off < 0) continue;
+                    update_1d(tg, seeds + tg.seed_off, sc, x[k], cnt);   // privatised: always direct
+                }
             }
         }
         if (P.key[k].hasglob) {
@@ -292,12 +314,15 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
             }
         }
     }
-    // matrix targets: one cell per surviving tuple and row
+    // matrix targets: equal key pairs of the warp aggregated (two match_any), the leader
+    // updates one cell per row with count * xi * xi
     if (valid && P.has2d) {
         for (uint32_t t = 0; t < P.n_targets; ++t) {
             const STarget &tg = P.tgt[t];
             if (tg.ndim != 2) continue;
-            update_2d(tg, seeds + tg.seed_off, sc, pick<NK>(x, tg.k0), pick<NK>(x, tg.k1));
+            const uint64_t xa = pick<NK>(x, tg.k0), xb = pick<NK>(x, tg.k1);
+            const uint32_t grp = __match_any_sync(act, xa) & __match_any_sync(act, xb);
+            if (lane == __ffs(grp) - 1) update_2d(tg, seeds + tg.seed_off, sc, xa, xb, __popc(grp));
         }
     }
 }
@@ -604,6 +629,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             const uint64_t x = keys[s];
             const int c = cnts[s];
             if (x == kEmpty || c == 0) continue;
+            if (P.key[k].hist) {
+                if (x < P.key[k].domain) { red_add_u32(P.key[k].hist + x, (uint32_t)c); continue; }
+                for (uint32_t tt = 0; tt < P.n_targets; ++tt) {   // outside the domain: all targets directly
+                    const STarget &tg = P.tgt[tt];
+                    if (tg.ndim != 1 || tg.k0 != k) continue;
+                    update_1d(tg, seeds + tg.seed_off, sc, x, c);
+                }
+                continue;
+            }
             for (uint32_t tt = 0; tt < P.n_targets; ++tt) {
                 const STarget &tg = P.tgt[tt];
                 if (tg.ndim != 1 || tg.k0 != k || tg.smem_off >= 0) continue;
@@ -619,6 +653,54 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
         for (uint32_t qq = tid; qq < n; qq += kConsumers) {
             const int32_t v = sc[tg.smem_off + qq];
             if (v) red_add_s64(tg.counters + qq, (int64_t)v);
+        }
+    }
+}
+
+// Histogram-then-sketch epilogue (SURVEY.md §8(d) lever f): every key x with count c in
+// [0, domain) adds c * xi_r(x) at bucket h_r(x) of each 1-D sketch on that key column.
+// Exact by linearity: identical to adding +-1 once per surviving tuple.
+struct EpiTarget {
+    int64_t *counters;
+    const uint64_t *seeds;   // device [d][6]
+    uint32_t d, wmask, cells;
+    int32_t smem_off;        // int32 offset of the CTA-private copy, -1 = L2 atomics
+};
+constexpr int kMaxEpiTargets = 8;
+struct EpiParams {
+    const uint32_t *hist;
+    uint64_t domain;
+    uint32_t n_targets, smem_counters;
+    EpiTarget tgt[kMaxEpiTargets];
+};
+
+__global__ void __launch_bounds__(512) k_hist_epilogue(const __grid_constant__ EpiParams E) {
+    extern __shared__ __align__(16) int32_t esc[];
+    for (uint32_t i = threadIdx.x; i < E.smem_counters; i += blockDim.x) esc[i] = 0;
+    __syncthreads();
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < E.domain; x += stride) {
+        const uint32_t c = __ldg(E.hist + x);
+        if (!c) continue;
+        for (uint32_t t = 0; t < E.n_targets; ++t) {
+            const EpiTarget &tg = E.tgt[t];
+            for (uint32_t r = 0; r < tg.d; ++r) {
+                const uint64_t *a = tg.seeds + r * 6;
+                const uint32_t cell = (uint32_t)(hash_g61(__ldg(a + 4), __ldg(a + 5), x) & tg.wmask);
+                uint64_t sa[4] = {__ldg(a), __ldg(a + 1), __ldg(a + 2), __ldg(a + 3)};
+                const int64_t v = (int64_t)xi_sign61(sa, x) * (int64_t)c;
+                if (tg.smem_off >= 0) atomicAdd(&esc[tg.smem_off + r * tg.cells + cell], (int32_t)v);
+                else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, v);
+            }
+        }
+    }
+    __syncthreads();
+    for (uint32_t t = 0; t < E.n_targets; ++t) {
+        const EpiTarget &tg = E.tgt[t];
+        if (tg.smem_off < 0) continue;
+        for (uint32_t q = threadIdx.x; q < tg.d * tg.cells; q += blockDim.x) {
+            const int32_t v = esc[tg.smem_off + q];
+            if (v) red_add_s64(tg.counters + q, (int64_t)v);
         }
     }
 }
@@ -672,6 +754,16 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
             if (std::find(keys.begin(), keys.end(), c.tgt_key[t][q]) == keys.end()) keys.push_back(c.tgt_key[t][q]);
     if (keys.size() > (size_t)kMaxKeys) return SK_OK;
     P.n_keys = (uint32_t)keys.size();
+    // histogram mode for key columns with a small hinted domain feeding 1-D sketches
+    const char *env_hist = getenv("COMPASS_HIST");
+    const bool allow_hist = !(env_hist && strcmp(env_hist, "0") == 0) && c.n_rows < (1ULL << 31);
+    bool hist_key[kMaxKeys] = {false, false, false, false};
+    for (uint32_t k = 0; k < P.n_keys; ++k) {
+        bool one_d = false;
+        for (uint32_t t = 0; t < c.n_targets; ++t) one_d |= (c.tgt_ndim[t] == 1 && c.tgt_key[t][0] == keys[k]);
+        const uint64_t dom = c.col_domain[keys[k]];
+        hist_key[k] = allow_hist && one_d && dom > 0 && dom <= (1ULL << 22);
+    }
     P.n_preds = c.n_preds;
     for (uint32_t q = 0; q < c.n_preds; ++q) {
         SPred &pr = P.pred[q];
@@ -748,7 +840,8 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         seed_off += tg.ndim * tg.d * 6;
         P.seeds[t] = c.tgt_seeds[t];
         const uint64_t need = uint64_t(tg.d) * tg.cells * 4;
-        if (sc_count * 4 + need <= avail) {
+        const bool via_hist = tg.ndim == 1 && hist_key[tg.k0];
+        if (!via_hist && sc_count * 4 + need <= avail) {
             tg.smem_off = (int32_t)sc_count;
             sc_count += (uint32_t)(need / 4);
         } else {
@@ -758,6 +851,8 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         if (tg.ndim == 1) {
             P.key[tg.k0].has1d = 1;
             if (tg.smem_off < 0) { P.key[tg.k0].hasglob = 1; key_needs_hh[tg.k0] = true; }
+            if (hist_key[tg.k0] && !(getenv("COMPASS_HISTHH") && strcmp(getenv("COMPASS_HISTHH"), "0") == 0))
+                key_needs_hh[tg.k0] = true;
         }
     }
     P.smem_counters = sc_count;
@@ -806,11 +901,53 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     // int32 privatised counts stay exact: rows per CTA < 2^31
     if ((P.n_tiles + grid - 1) / grid * kTile >= (1ULL << 31)) return SK_OK;
     if (P.n_keys == 0) return SK_OK;
+    std::vector<void *> hists;
+    for (uint32_t k = 0; k < P.n_keys; ++k) {
+        P.key[k].hist = nullptr;
+        P.key[k].domain = 0;
+        if (!hist_key[k]) continue;
+        void *h = nullptr;
+        const uint64_t dom = c.col_domain[keys[k]];
+        SKB_CUDA(cudaMallocAsync(&h, dom * 4, stream));
+        SKB_CUDA(cudaMemsetAsync(h, 0, dom * 4, stream));
+        hists.push_back(h);
+        P.key[k].hist = (uint32_t *)h;
+        P.key[k].domain = dom;
+    }
     ScanKernel kern = pick_kernel(P.n_keys, P.n_preds);
     SKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)off));
     kern<<<(unsigned)grid, kThreads, off, stream>>>(P);
     SKB_CUDA(cudaGetLastError());
     count_launch();
+    // histogram -> sketches, then release the histograms (stream-ordered)
+    for (uint32_t k = 0; k < P.n_keys; ++k) {
+        if (!P.key[k].hist) continue;
+        EpiParams E;
+        memset(&E, 0, sizeof(E));
+        E.hist = P.key[k].hist;
+        E.domain = P.key[k].domain;
+        uint32_t sc2 = 0;
+        for (uint32_t t = 0; t < c.n_targets && E.n_targets < kMaxEpiTargets; ++t) {
+            if (c.tgt_ndim[t] != 1 || c.tgt_key[t][0] != keys[k]) continue;
+            EpiTarget &et = E.tgt[E.n_targets++];
+            et.counters = c.tgt_counters[t];
+            et.seeds = c.tgt_seeds[t];
+            et.d = c.tgt_d[t];
+            et.wmask = c.tgt_w[t][0] - 1;
+            et.cells = c.tgt_w[t][0];
+            const uint32_t need = et.d * et.cells;
+            if ((sc2 + need) * 4 <= 200 * 1024) { et.smem_off = (int32_t)sc2; sc2 += need; }
+            else et.smem_off = -1;
+        }
+        E.smem_counters = sc2;
+        const size_t esm = size_t(sc2) * 4;
+        SKB_CUDA(cudaFuncSetAttribute(k_hist_epilogue, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
+        const unsigned eg = (unsigned)std::min<uint64_t>(uint64_t(sms), (E.domain + 511) / 512);
+        k_hist_epilogue<<<std::max(1u, eg), 512, esm, stream>>>(E);
+        SKB_CUDA(cudaGetLastError());
+        count_launch();
+    }
+    for (void *h : hists) cudaFreeAsync(h, stream);
     *launched = true;
     return SK_OK;
 }

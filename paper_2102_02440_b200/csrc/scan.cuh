@@ -11,6 +11,7 @@ struct ScanCall {
     uint32_t n_cols = 0;
     const void *col_ptr[16];
     uint32_t col_bytes[16];
+    uint64_t col_domain[16];    // key-domain hints (0 = unknown)
     uint64_t n_rows = 0;
     uint32_t n_preds = 0;
     uint32_t pred_col[8], pred_kind[8];

@@ -250,6 +250,7 @@ extern "C" sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_co
         for (uint32_t c = 0; c < n_cols; ++c) {
             sc.col_ptr[c] = cols[c].data;
             sc.col_bytes[c] = cols[c].dtype == SK_INT64 ? 8 : 4;
+            sc.col_domain[c] = cols[c].domain;
         }
         sc.n_rows = n_rows;
         sc.n_preds = n_preds;

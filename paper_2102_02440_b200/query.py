@@ -42,8 +42,9 @@ def allreduce_packed(buffer: torch.Tensor, group=None):
 
 
 class QueryRun:
-    def __init__(self, q, device="cuda"):
+    def __init__(self, q, device="cuda", use_domains=True):
         self.q = q
+        self.use_domains = use_domains
         self.device = torch.device(device)
         if self.device.index is None:
             self.device = torch.device("cuda", torch.cuda.current_device())
@@ -72,7 +73,9 @@ class QueryRun:
         targets = [(sk, [cnames.index(k) for k in s.key_cols])
                    for s, sk in zip(self.q.sketches, self.sketches) if s.table == name]
         ti = self.tnames.index(name)
-        sketch_update_filtered(cols, n_rows, pr, targets, survivors=self.survivors[ti:ti + 1], stream=stream)
+        domains = [getattr(c, "domain", 0) or 0 for c in t.cols] if self.use_domains else None
+        sketch_update_filtered(cols, n_rows, pr, targets, survivors=self.survivors[ti:ti + 1], stream=stream,
+                               domains=domains)
 
     def build(self, data: dict, preds: dict, stream=None):
         for name in self.tnames:

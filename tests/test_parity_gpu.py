@@ -49,8 +49,9 @@ TARGETS = [  # (key cols, d, w, edge ids)
 ]
 
 
-def _gpu_build(cols, preds, targets, master=42, calls=1):
+def _gpu_build(cols, preds, targets, master=42, calls=1, domains=None):
     names = list(cols)
+    dom = [domains.get(c, 0) for c in names] if domains else None
     dcols = _to_dev(cols)
     sks = [pb.Sketch(d, w, e, master, _dev()) for (_, d, w, e) in targets]
     surv = torch.zeros(1, dtype=torch.int64, device=_dev())
@@ -60,7 +61,7 @@ def _gpu_build(cols, preds, targets, master=42, calls=1):
         sub = [dcols[c][a:b].contiguous() for c in names]
         pr = [(names.index(p[0]),) + tuple(p[1:]) for p in preds]
         tg = [(sk, [names.index(k) for k in t[0]]) for sk, t in zip(sks, targets)]
-        pb.sketch_update_filtered(sub, int(b - a), pr, tg, survivors=surv)
+        pb.sketch_update_filtered(sub, int(b - a), pr, tg, survivors=surv, domains=dom)
     torch.cuda.synchronize()
     return [sk.counters.cpu().numpy() for sk in sks], int(surv.item())
 
@@ -100,6 +101,24 @@ def test_build_parity(n, pi, scan_mode):
     cols = _rand_cols(n, 1000 + n + pi)
     preds = PRED_SETS[pi]
     g, gs = _gpu_build(cols, preds, TARGETS)
+    o, os_ = _oracle_build(cols, preds, TARGETS)
+    assert gs == os_
+    for a, b in zip(g, o):
+        assert np.array_equal(a, b)
+
+
+# key-domain hints: zk is in [0, 5000) (histogram mode), k32's hint 1000 is violated by most
+# rows (out-of-domain fallback), p/s hints on predicate-only columns are ignored
+DOMAINS = [None, {"zk": 5000, "k32": 1000, "p": 100, "s": 50}, {"zk": 4096}]
+
+
+@pytest.mark.parametrize("n", [1, 4097, 1_000_000])
+@pytest.mark.parametrize("di", range(1, len(DOMAINS)))
+@pytest.mark.parametrize("pi", [0, 1, 2, 5])
+def test_build_parity_domain_hints(n, di, pi):
+    cols = _rand_cols(n, 2000 + n + pi)
+    preds = PRED_SETS[pi]
+    g, gs = _gpu_build(cols, preds, TARGETS, domains=DOMAINS[di])
     o, os_ = _oracle_build(cols, preds, TARGETS)
     assert gs == os_
     for a, b in zip(g, o):
