@@ -18,7 +18,7 @@ import os
 import torch
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libcompass_b200.so")
+LIB_PATH = os.environ.get("COMPASS_LIB") or os.path.join(PKG, "libcompass_b200.so")
 
 SK_OK, SK_EINVAL, SK_EMISMATCH, SK_EOVERFLOW, SK_ENOMEM, SK_ECUDA = range(6)
 SK_INT32, SK_INT64 = 0, 1

@@ -36,7 +36,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for s in sources():
         o = os.path.join(objdir, os.path.basename(s) + ".o")
-        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", SRC, "-c", s, "-o", o]
+        extra = os.environ.get("COMPASS_NVCC_FLAGS", "").split()
+        cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", SRC, "-c", s, "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {s}:\n{r.stderr}")

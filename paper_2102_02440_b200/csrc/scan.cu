@@ -34,8 +34,12 @@ using namespace skb;
 
 namespace {
 
-constexpr int kTile = 2048;
-constexpr int kWarps = 16;
+#ifndef SCAN_WARPS
+#define SCAN_WARPS 20
+#endif
+constexpr int kWarps = SCAN_WARPS;
+constexpr int kTile = kWarps * 128;
+
 constexpr int kConsumers = kWarps * 32;
 constexpr int kThreads = kConsumers + 32;
 constexpr int kMaxStages = 8;
@@ -91,6 +95,7 @@ struct SParams {
     uint32_t has2d;       // some target is a matrix
     uint32_t off_miss, off_missn;   // per-warp miss buffers (x, count) and fill counts
     uint32_t off_rows;              // per-warp survivor row-offset list (128 x uint16)
+    uint32_t tile_rows;             // rows per ring stage
     unsigned long long *survivors;
 };
 
@@ -138,6 +143,7 @@ __device__ __forceinline__ void cp_async8(void *dst, const void *src) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all_but1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_lag() { asm volatile("cp.async.wait_group 3;" ::: "memory"); }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 __device__ __forceinline__ void red_add_u32(uint32_t *p, uint32_t v) {
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -443,8 +449,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             bool wrapped = false;
             for (uint64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
                 if (wrapped) mbar_wait(&empty[s], ph ^ 1);
-                const uint64_t row0 = t * kTile;
-                const bool fulltile = row0 + kTile <= P.n_rows;
+                const uint64_t row0 = t * P.tile_rows;
+                const bool fulltile = row0 + P.tile_rows <= P.n_rows;
                 if (fulltile && P.stage_bytes) {
                     mbar_arrive_tx(&full[s], P.stage_bytes);
                     unsigned char *stage = smem + P.off_ring + s * P.stage_bytes;
@@ -452,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                         if (P.col[c].soff < 0) continue;
                         const uint32_t b = P.col[c].bytes;
                         bulk_g2s(stage + P.col[c].soff, reinterpret_cast<const unsigned char *>(P.col[c].p) + row0 * b,
-                                 kTile * b, &full[s]);
+                                 P.tile_rows * b, &full[s]);
                     }
                 } else {
                     mbar_arrive(&full[s]);
@@ -486,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
     const int r0 = warp * 128 + lane * 4;   // this lane's 4 rows inside a tile
     unsigned char *q = smem + P.off_kbuf + warp * P.kb_bytes;   // this warp's survivor-key ring
     uint32_t head = 0, tail = 0;             // ring positions (monotone)
-    bool pending = false;                    // a cp.async group of this warp may be in flight
+    uint32_t t1 = 0, t2 = 0, t3 = 0;         // ring tail after the previous 1, 2, 3 tiles
     const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
     uint32_t s = 0, ph = 0;
     for (uint64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x, s = (s + 1 == kStages) ? 0u : s + 1, ph ^= (s == 0)) {
@@ -508,31 +514,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             const uint32_t B0 = __ballot_sync(0xffffffffu, bits & 1u), B1 = __ballot_sync(0xffffffffu, bits & 2u);
             const uint32_t B2 = __ballot_sync(0xffffffffu, bits & 4u), B3 = __ballot_sync(0xffffffffu, bits & 8u);
             const uint32_t wtot = __popc(B0) + __popc(B1) + __popc(B2) + __popc(B3);
-            if (wtot == 0) {
-                // nothing to gather: release the stage, drain only what earlier tiles made ready
-                __syncwarp();
-                if (lane == 0) mbar_arrive_a(empty_a + s * 8);
-                if (tail - head >= 32) {
-                    if (pending) { cp_wait_all(); __syncwarp(); pending = false; }
-                    while (tail - head >= 32) { drain_batch<NK>(P, smem, q, kbytes, head, 32); head += 32; }
+            if (wtot) {
+                const uint32_t excl = __popc(B0 & lt) + __popc(B1 & lt) + __popc(B2 & lt) + __popc(B3 & lt);
+                if (tail - head + wtot > cap) {
+                    // ring would overflow: finish outstanding gathers and drain it completely
+                    cp_wait_all();
+                    __syncwarp();
+                    while (tail != head) {
+                        const uint32_t n = min(32u, tail - head);
+                        drain_batch<NK>(P, smem, q, kbytes, head, n);
+                        head += n;
+                    }
+                    t1 = t2 = t3 = tail;
                 }
-                continue;
-            }
-            const uint32_t excl = __popc(B0 & lt) + __popc(B1 & lt) + __popc(B2 & lt) + __popc(B3 & lt);
-            if (tail - head + wtot > cap) {
-                // ring would overflow: finish outstanding gathers and drain it completely
-                cp_wait_all();
-                __syncwarp();
-                pending = false;
-                while (tail != head) {
-                    const uint32_t n = min(32u, tail - head);
-                    drain_batch<NK>(P, smem, q, kbytes, head, n);
-                    head += n;
-                }
-            }
-            // survivors' keys: sector-granular gathers into the ring (A3).  Row offsets go to a
-            // per-warp list first so the cp.async loop runs converged over all 32 lanes.
-            {
+                // survivors' keys: sector-granular gathers into the ring (A3).  Row offsets go to
+                // a per-warp list first so the cp.async loop runs converged over all 32 lanes.
                 uint16_t *rl = reinterpret_cast<uint16_t *>(smem + P.off_rows) + warp * 128;
                 uint32_t pos = excl;
                 uint32_t b = bits;
@@ -552,16 +548,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                         else cp_async4(dst + k * 8, reinterpret_cast<const int *>(kptr[k]) + row);
                     }
                 }
+                tail += wtot;
+            } else {
+                __syncwarp();
+                if (lane == 0) mbar_arrive_a(empty_a + s * 8);
             }
+            // one cp.async group per tile (possibly empty): wait_group kLag then guarantees the
+            // entries appended kLag tiles ago (t3) have landed; the latency hides behind 3 tiles
             cp_commit();
-            const uint32_t ready_end = tail;                 // entries of earlier tiles
-            tail += wtot;
+            const uint32_t ready_end = t3;
+            t3 = t2; t2 = t1; t1 = tail;
             if (ready_end - head >= 32) {
-                if (pending) cp_wait_all_but1();             // the group committed before this one
+                cp_wait_lag();
                 __syncwarp();
                 while (ready_end - head >= 32) { drain_batch<NK>(P, smem, q, kbytes, head, 32); head += 32; }
             }
-            pending = true;
         } else {
             // keys are staged (no predicate): aggregate and update straight from the stage
             uint64_t xs[4][NK];
@@ -645,6 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             }
         }
     }
+    consumer_sync();
     // ---- flush privatised int32 counters into the int64 sketches
     for (uint32_t tt = 0; tt < P.n_targets; ++tt) {
         const STarget &tg = P.tgt[tt];
@@ -740,7 +742,6 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     memset(&P, 0, sizeof(P));
     P.n_cols = c.n_cols;
     P.n_rows = c.n_rows;
-    P.n_tiles = (c.n_rows + kTile - 1) / kTile;
     for (uint32_t i = 0; i < c.n_cols; ++i) {
         P.col[i].p = c.col_ptr[i];
         P.col[i].bytes = c.col_bytes[i];
@@ -787,12 +788,14 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         }
     }
     P.gather = c.n_preds > 0 ? 1u : 0u;
+    P.tile_rows = kTile;
+    P.n_tiles = (c.n_rows + P.tile_rows - 1) / P.tile_rows;
     // staged columns: predicate columns, plus key columns when there is no predicate
     uint32_t soff = 0;
     auto stage_col = [&](uint32_t col) {
         if (P.col[col].soff >= 0) return;
         P.col[col].soff = (int32_t)soff;
-        soff += kTile * P.col[col].bytes;
+        soff += P.tile_rows * P.col[col].bytes;
     };
     for (uint32_t q = 0; q < c.n_preds; ++q) stage_col(c.pred_col[q]);
     if (!P.gather) for (uint32_t k : keys) stage_col(k);
@@ -811,13 +814,14 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     for (uint32_t k = 0; k < P.n_keys; ++k) P.key[k].col = keys[k];
     P.cap = 0;
     P.kb_bytes = 0;
+    const uint32_t ring_warps = kWarps;                 // warps owning a survivor-key ring
     if (P.gather) {
         P.cap = P.n_keys == 1 ? 256 : 128;              // >= one tile-slice of survivors (128); overflow drains
         P.kb_bytes = P.cap * P.n_keys * 8;
     }
     const uint32_t min_stages = 3;
     const uint32_t miss_bytes = kWarps * P.n_keys * 32 * 12 + ((kWarps * P.n_keys * 4 + 15) & ~15u);
-    const uint32_t fixed = 128 + min_stages * P.stage_bytes + kWarps * P.kb_bytes + seed_bytes + miss_bytes +
+    const uint32_t fixed = 128 + min_stages * P.stage_bytes + ring_warps * P.kb_bytes + seed_bytes + miss_bytes +
                            kWarps * 128 * 2 + 256;
     if (fixed > kBudget) return SK_OK;
     uint32_t avail = kBudget - fixed;
@@ -873,7 +877,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     off += stages * P.stage_bytes;
     off = (off + 127) & ~127u;
     P.off_kbuf = off;
-    off += kWarps * P.kb_bytes;
+    off += ring_warps * P.kb_bytes;
     P.off_sc = off;
     off += (sc_count * 4 + 15) & ~15u;
     for (uint32_t k = 0; k < P.n_keys; ++k) {
@@ -899,7 +903,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     uint64_t grid = std::min<uint64_t>((uint64_t)sms, P.n_tiles);
     // int32 privatised counts stay exact: rows per CTA < 2^31
-    if ((P.n_tiles + grid - 1) / grid * kTile >= (1ULL << 31)) return SK_OK;
+    if ((P.n_tiles + grid - 1) / grid * P.tile_rows >= (1ULL << 31)) return SK_OK;
     if (P.n_keys == 0) return SK_OK;
     std::vector<void *> hists;
     for (uint32_t k = 0; k < P.n_keys; ++k) {
@@ -915,8 +919,9 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         P.key[k].domain = dom;
     }
     ScanKernel kern = pick_kernel(P.n_keys, P.n_preds);
+    const int threads = kThreads;
     SKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)off));
-    kern<<<(unsigned)grid, kThreads, off, stream>>>(P);
+    kern<<<(unsigned)grid, threads, off, stream>>>(P);
     SKB_CUDA(cudaGetLastError());
     count_launch();
     // histogram -> sketches, then release the histograms (stream-ordered)
