@@ -337,7 +337,7 @@ def main():
         pass
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
-            "kernel": "k_update_generic (fused filter+hash+update+flush)",
+            "kernel": "k_scan (persistent TMA-ring fused filter+hash+update+flush)",
             "alg_bytes_per_step": ab["alg"], "kernel_ms_per_step": round(kms, 4),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "_fallback" not in peaks else "fallback 6.65 TB/s",
             "frac_of_nominal_8TBs": round(achieved / 8000.0, 4)}
