@@ -4,6 +4,7 @@ from __future__ import annotations
 import glob
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -33,17 +34,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for s in sources():
+    extra = os.environ.get("COMPASS_NVCC_FLAGS", "").split()
+
+    def compile_one(s):
         o = os.path.join(objdir, os.path.basename(s) + ".o")
-        extra = os.environ.get("COMPASS_NVCC_FLAGS", "").split()
         cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", SRC, "-c", s, "-o", o]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {s}:\n{r.stderr}")
-        if verbose:
-            print(r.stderr)
-        objs.append(o)
+        return s, o, subprocess.run(cmd, capture_output=True, text=True)
+
+    objs = []
+    with ThreadPoolExecutor(max_workers=len(sources()) or 1) as ex:   # one nvcc per source file
+        for s, o, r in ex.map(compile_one, sources()):
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed for {s}:\n{r.stderr}")
+            if verbose:
+                print(r.stderr)
+            objs.append(o)
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs, "-lcudart_static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -343,27 +343,33 @@ struct PR {
     const int64_t *set;
 };
 
-// conjunction of the predicates over this lane's 4 rows -> bit mask (branch-free per kind)
-template <int NP, bool staged>
-__device__ __forceinline__ uint32_t eval_preds(const PR (&pr)[NP], const unsigned char *stage,
-                                               uint64_t row0, int r0, int valid) {
-    uint32_t bits = (1u << valid) - 1u;
+// conjunction of the predicates over this lane's 4 rows r0..r0+3 -> m[j] (A2).  FULL: the
+// rows come from the staged tile (128-bit shared loads); otherwise from global memory,
+// rows past the end are false.  R32: every predicate is an int32 range (no kind branches):
+// one unsigned subtract-compare per row, ANDed into a predicate register.
+template <int NP, bool R32, bool FULL>
+__device__ __forceinline__ void eval_preds(const PR (&pr)[NP], const unsigned char *stage, uint64_t row0, int r0,
+                                           int valid, bool (&m)[4]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) m[j] = FULL || j < valid;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-        if (pr[q].kind == PR_R32) {
+        if (R32 || pr[q].kind == PR_R32) {
             int4 v;
-            if (staged) v = *reinterpret_cast<const int4 *>(stage + pr[q].soff + r0 * 4);
+            if (FULL) v = *reinterpret_cast<const int4 *>(stage + pr[q].soff + r0 * 4);
             else {
                 const int *g = reinterpret_cast<const int *>(pr[q].p) + row0 + r0;
                 v.x = valid > 0 ? __ldg(g) : 0; v.y = valid > 1 ? __ldg(g + 1) : 0;
                 v.z = valid > 2 ? __ldg(g + 2) : 0; v.w = valid > 3 ? __ldg(g + 3) : 0;
             }
             const uint32_t lo = (uint32_t)pr[q].lo, sp = (uint32_t)pr[q].span;
-            bits &= ((uint32_t)v.x - lo <= sp) | (((uint32_t)v.y - lo <= sp) << 1) |
-                    (((uint32_t)v.z - lo <= sp) << 2) | (((uint32_t)v.w - lo <= sp) << 3);
+            m[0] = m[0] & ((uint32_t)v.x - lo <= sp);
+            m[1] = m[1] & ((uint32_t)v.y - lo <= sp);
+            m[2] = m[2] & ((uint32_t)v.z - lo <= sp);
+            m[3] = m[3] & ((uint32_t)v.w - lo <= sp);
         } else if (pr[q].kind == PR_R64) {
             int64_t v[4];
-            if (staged) {
+            if (FULL) {
                 const longlong2 a = *reinterpret_cast<const longlong2 *>(stage + pr[q].soff + r0 * 8);
                 const longlong2 b = *reinterpret_cast<const longlong2 *>(stage + pr[q].soff + r0 * 8 + 16);
                 v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
@@ -372,27 +378,38 @@ __device__ __forceinline__ uint32_t eval_preds(const PR (&pr)[NP], const unsigne
 #pragma unroll
                 for (int j = 0; j < 4; ++j) v[j] = j < valid ? __ldg(g + j) : 0;
             }
-            uint32_t m = 0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) m |= (uint32_t)((uint64_t)v[j] - (uint64_t)pr[q].lo <= pr[q].span) << j;
-            bits &= m;
+            for (int j = 0; j < 4; ++j) m[j] = m[j] & ((uint64_t)v[j] - (uint64_t)pr[q].lo <= pr[q].span);
         } else if (pr[q].kind == PR_SET) {
-            uint32_t b = bits;
-            while (b) {
-                const int j = __ffs(b) - 1;
-                b &= b - 1;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (!m[j]) continue;
                 int64_t v;
-                if (staged) v = pr[q].bytes == 8 ? *reinterpret_cast<const int64_t *>(stage + pr[q].soff + (r0 + j) * 8)
-                                                 : (int64_t) * reinterpret_cast<const int *>(stage + pr[q].soff + (r0 + j) * 4);
+                if (FULL) v = pr[q].bytes == 8 ? *reinterpret_cast<const int64_t *>(stage + pr[q].soff + (r0 + j) * 8)
+                                               : (int64_t) * reinterpret_cast<const int *>(stage + pr[q].soff + (r0 + j) * 4);
                 else v = pr[q].bytes == 8 ? __ldg(reinterpret_cast<const long long *>(pr[q].p) + row0 + r0 + j)
                                           : (int64_t)__ldg(reinterpret_cast<const int *>(pr[q].p) + row0 + r0 + j);
-                if (!in_set(pr[q].set, pr[q].n, v)) bits &= ~(1u << j);
+                m[j] = in_set(pr[q].set, pr[q].n, v);
             }
         } else {
-            bits = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) m[j] = false;
         }
     }
-    return bits;
+}
+
+// A3: this lane's surviving row `row` (if m) gets ring entry `pos`; its key sectors are
+// gathered with cp.async straight into the warp's survivor-key ring
+template <int NK>
+__device__ __forceinline__ void gather_slot(bool m, uint32_t pos, uint64_t row, unsigned char *q, uint32_t cap,
+                                            const void *const (&kptr)[NK], const uint32_t (&kbytes)[NK]) {
+    if (!m) return;
+    unsigned char *dst = q + (pos & (cap - 1)) * (NK * 8);
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+        if (kbytes[k] == 8) cp_async8(dst + k * 8, reinterpret_cast<const long long *>(kptr[k]) + row);
+        else cp_async4(dst + k * 8, reinterpret_cast<const int *>(kptr[k]) + row);
+    }
 }
 
 template <int NK>
@@ -410,7 +427,7 @@ __device__ __forceinline__ void drain_batch(const SParams &P, unsigned char *sme
     process_batch<NK>(P, smem, valid, xk);
 }
 
-template <int NK, int NP>
+template <int NK, int NP, bool R32>
 __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -488,34 +505,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
         ksoff[k] = c.soff;
     }
     const uint32_t cap = P.cap;
-    uint32_t my_surv = 0;
+    uint32_t surv = 0;                       // warp-uniform exact survivor count
     const int r0 = warp * 128 + lane * 4;   // this lane's 4 rows inside a tile
     unsigned char *q = smem + P.off_kbuf + warp * P.kb_bytes;   // this warp's survivor-key ring
     uint32_t head = 0, tail = 0;             // ring positions (monotone)
     uint32_t t1 = 0, t2 = 0, t3 = 0;         // ring tail after the previous 1, 2, 3 tiles
     const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t n_tiles = (uint32_t)P.n_tiles;
+    constexpr int NPX = (NP > 0) ? NP : 1;
     uint32_t s = 0, ph = 0;
-    for (uint64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x, s = (s + 1 == kStages) ? 0u : s + 1, ph ^= (s == 0)) {
-        const uint64_t row0 = t * kTile;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const uint64_t row0 = uint64_t(t) * kTile;
         mbar_wait_a(full_a + s * 8, ph);
         const unsigned char *stage = smem + P.off_ring + s * P.stage_bytes;
-        const bool staged = (row0 + kTile <= P.n_rows) && P.stage_bytes;
-        const int64_t rem = (int64_t)P.n_rows - (int64_t)(row0 + r0);
-        const int valid = rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem);
-        constexpr int NPX = (NP > 0) ? NP : 1;
-        uint32_t bits = (1u << valid) - 1u;
-        if (NP > 0) bits = staged ? eval_preds<NPX, true>(pr, stage, row0, r0, valid)
-                                  : eval_preds<NPX, false>(pr, stage, row0, r0, valid);
-        const int cnt = __popc(bits);
-        my_surv += cnt;
+        const bool full_tile = row0 + kTile <= P.n_rows;   // staged by the producer
         if (NP > 0) {
-            // survivor prefix from 4 ballots (one per row slot): no dependent shuffle chain
-            const uint32_t lt = (1u << lane) - 1u;
-            const uint32_t B0 = __ballot_sync(0xffffffffu, bits & 1u), B1 = __ballot_sync(0xffffffffu, bits & 2u);
-            const uint32_t B2 = __ballot_sync(0xffffffffu, bits & 4u), B3 = __ballot_sync(0xffffffffu, bits & 8u);
-            const uint32_t wtot = __popc(B0) + __popc(B1) + __popc(B2) + __popc(B3);
+            bool m[4];
+            if (full_tile) eval_preds<NPX, R32, true>(pr, stage, row0, r0, 4, m);
+            else {
+                const int64_t rem = (int64_t)P.n_rows - (int64_t)(row0 + r0);
+                eval_preds<NPX, R32, false>(pr, stage, row0, r0, rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem), m);
+            }
+            // one ballot per row slot; the ballots also order every lane's shared reads of
+            // stage s before lane 0 releases it
+            const uint32_t B0 = __ballot_sync(0xffffffffu, m[0]), B1 = __ballot_sync(0xffffffffu, m[1]);
+            const uint32_t B2 = __ballot_sync(0xffffffffu, m[2]), B3 = __ballot_sync(0xffffffffu, m[3]);
+            if (lane == 0) mbar_arrive_a(empty_a + s * 8);
+            const uint32_t c0 = __popc(B0), c1 = __popc(B1), c2 = __popc(B2), c3 = __popc(B3);
+            const uint32_t wtot = c0 + c1 + c2 + c3;
+            surv += wtot;
             if (wtot) {
-                const uint32_t excl = __popc(B0 & lt) + __popc(B1 & lt) + __popc(B2 & lt) + __popc(B3 & lt);
                 if (tail - head + wtot > cap) {
                     // ring would overflow: finish outstanding gathers and drain it completely
                     cp_wait_all();
@@ -527,31 +547,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                     }
                     t1 = t2 = t3 = tail;
                 }
-                // survivors' keys: sector-granular gathers into the ring (A3).  Row offsets go to
-                // a per-warp list first so the cp.async loop runs converged over all 32 lanes.
-                uint16_t *rl = reinterpret_cast<uint16_t *>(smem + P.off_rows) + warp * 128;
-                uint32_t pos = excl;
-                uint32_t b = bits;
-                while (b) {
-                    const int j = __ffs(b) - 1;
-                    b &= b - 1;
-                    rl[pos++] = (uint16_t)(r0 + j);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive_a(empty_a + s * 8);          // this warp is done with stage s
-                for (uint32_t e = lane; e < wtot; e += 32) {
-                    const uint64_t row = row0 + rl[e];
-                    unsigned char *dst = q + ((tail + e) & (cap - 1)) * (NK * 8);
-#pragma unroll
-                    for (int k = 0; k < NK; ++k) {
-                        if (kbytes[k] == 8) cp_async8(dst + k * 8, reinterpret_cast<const long long *>(kptr[k]) + row);
-                        else cp_async4(dst + k * 8, reinterpret_cast<const int *>(kptr[k]) + row);
-                    }
-                }
+                // survivors in slot-major order (slot j of every lane, then slot j+1): the
+                // ring position is a popc of one ballot, no shuffle chain, no divergence
+                const uint64_t rb = row0 + r0;
+                gather_slot<NK>(m[0], tail + __popc(B0 & lt), rb, q, cap, kptr, kbytes);
+                gather_slot<NK>(m[1], tail + c0 + __popc(B1 & lt), rb + 1, q, cap, kptr, kbytes);
+                gather_slot<NK>(m[2], tail + c0 + c1 + __popc(B2 & lt), rb + 2, q, cap, kptr, kbytes);
+                gather_slot<NK>(m[3], tail + c0 + c1 + c2 + __popc(B3 & lt), rb + 3, q, cap, kptr, kbytes);
                 tail += wtot;
-            } else {
-                __syncwarp();
-                if (lane == 0) mbar_arrive_a(empty_a + s * 8);
             }
             // one cp.async group per tile (possibly empty): wait_group kLag then guarantees the
             // entries appended kLag tiles ago (t3) have landed; the latency hides behind 3 tiles
@@ -565,12 +568,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             }
         } else {
             // keys are staged (no predicate): aggregate and update straight from the stage
+            const int64_t rem = (int64_t)P.n_rows - (int64_t)(row0 + r0);
+            const int valid = rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem);
+            const uint32_t bits = (1u << valid) - 1u;
+            surv += __reduce_add_sync(0xffffffffu, (uint32_t)valid);
             uint64_t xs[4][NK];
 #pragma unroll
             for (int k = 0; k < NK; ++k) {
                 if (kbytes[k] == 4) {
                     int4 v;
-                    if (staged) v = *reinterpret_cast<const int4 *>(stage + ksoff[k] + r0 * 4);
+                    if (full_tile) v = *reinterpret_cast<const int4 *>(stage + ksoff[k] + r0 * 4);
                     else {
                         const int *g = reinterpret_cast<const int *>(kptr[k]) + row0 + r0;
                         v.x = valid > 0 ? __ldg(g) : 0; v.y = valid > 1 ? __ldg(g + 1) : 0;
@@ -581,7 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         int64_t v = 0;
-                        if (staged) v = *reinterpret_cast<const int64_t *>(stage + ksoff[k] + (r0 + j) * 8);
+                        if (full_tile) v = *reinterpret_cast<const int64_t *>(stage + ksoff[k] + (r0 + j) * 8);
                         else if (j < valid) v = __ldg(reinterpret_cast<const long long *>(kptr[k]) + row0 + r0 + j);
                         xs[j][k] = canon61(v);
                     }
@@ -592,6 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             __syncwarp();
             if (lane == 0) mbar_arrive_a(empty_a + s * 8);
         }
+        if (++s == kStages) { s = 0; ph ^= 1; }
     }
     if (NP > 0) {
         cp_wait_all();
@@ -616,8 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
         }
     }
     // ---- exact survivor count
-    const uint32_t ws = __reduce_add_sync(0xffffffffu, my_surv);
-    if (lane == 0 && ws && P.survivors) atomicAdd(P.survivors, (unsigned long long)ws);
+    if (lane == 0 && surv && P.survivors) atomicAdd(P.survivors, (unsigned long long)surv);
     consumer_sync();
     // ---- flush heavy-hitter tables (one hash evaluation per distinct key per CTA)
     int32_t *sc = reinterpret_cast<int32_t *>(smem + P.off_sc);
@@ -710,22 +717,22 @@ __global__ void __launch_bounds__(512) k_hist_epilogue(const __grid_constant__ E
 typedef void (*ScanKernel)(const SParams);
 
 template <int NK>
-static ScanKernel pick_np(uint32_t np) {
+static ScanKernel pick_np(uint32_t np, bool r32) {
     switch (np) {
-        case 0: return k_scan<NK, 0>;
-        case 1: return k_scan<NK, 1>;
-        case 2: return k_scan<NK, 2>;
-        case 3: return k_scan<NK, 3>;
-        default: return k_scan<NK, 4>;
+        case 0: return k_scan<NK, 0, false>;
+        case 1: return r32 ? k_scan<NK, 1, true> : k_scan<NK, 1, false>;
+        case 2: return r32 ? k_scan<NK, 2, true> : k_scan<NK, 2, false>;
+        case 3: return r32 ? k_scan<NK, 3, true> : k_scan<NK, 3, false>;
+        default: return r32 ? k_scan<NK, 4, true> : k_scan<NK, 4, false>;
     }
 }
 
-static ScanKernel pick_kernel(uint32_t nk, uint32_t np) {
+static ScanKernel pick_kernel(uint32_t nk, uint32_t np, bool r32) {
     switch (nk) {
-        case 1: return pick_np<1>(np);
-        case 2: return pick_np<2>(np);
-        case 3: return pick_np<3>(np);
-        default: return pick_np<4>(np);
+        case 1: return pick_np<1>(np, r32);
+        case 2: return pick_np<2>(np, r32);
+        case 3: return pick_np<3>(np, r32);
+        default: return pick_np<4>(np, r32);
     }
 }
 
@@ -918,7 +925,9 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         P.key[k].hist = (uint32_t *)h;
         P.key[k].domain = dom;
     }
-    ScanKernel kern = pick_kernel(P.n_keys, P.n_preds);
+    bool all_r32 = true;
+    for (uint32_t q = 0; q < P.n_preds; ++q) all_r32 &= P.pred[q].kind == PR_R32;
+    ScanKernel kern = pick_kernel(P.n_keys, P.n_preds, all_r32);
     const int threads = kThreads;
     SKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)off));
     kern<<<(unsigned)grid, threads, off, stream>>>(P);
