@@ -66,6 +66,8 @@ struct SKey {
     uint32_t hasglob;     // some non-privatised 1-D target hashes this key
     uint32_t *hist;       // histogram mode: per-key counts over [0, domain), else null
     uint64_t domain;
+    uint32_t priv1d;      // bit t: 1-D target t on this key, privatised in smem
+    uint32_t glob1d;      // bit t: 1-D target t on this key, updated in HBM/L2
 };
 struct STarget {
     int64_t *counters;
@@ -133,12 +135,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
-}
-__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
-    asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all_but1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
@@ -241,9 +237,8 @@ __device__ __forceinline__ void flush_misses(const SParams &P, const uint64_t *s
     if ((uint32_t)lane < n) {
         const uint64_t xv = mx[lane];
         const int cv = mc[lane];
-        for (uint32_t t = 0; t < P.n_targets; ++t) {
-            const STarget &tg = P.tgt[t];
-            if (tg.ndim != 1 || tg.k0 != k || tg.smem_off >= 0) continue;
+        for (uint32_t tm = P.key[k].glob1d; tm; tm &= tm - 1) {
+            const STarget &tg = P.tgt[__ffs(tm) - 1];
             update_1d(tg, seeds + tg.seed_off, nullptr, xv, cv);
         }
     }
@@ -277,19 +272,17 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
                 if (!done && x[k] < P.key[k].domain) { red_add_u32(P.key[k].hist + x[k], (uint32_t)cnt); done = true; }
                 if (!done) {   // outside the hinted domain: direct updates
                     miss = P.key[k].hasglob;
-                    for (uint32_t t = 0; t < P.n_targets; ++t) {
-                        const STarget &tg = P.tgt[t];
-                        if (tg.ndim != 1 || tg.k0 != (uint32_t)k || tg.smem_off < 0) continue;
+                    for (uint32_t tm = P.key[k].priv1d; tm; tm &= tm - 1) {
+                        const STarget &tg = P.tgt[__ffs(tm) - 1];
                         update_1d(tg, seeds + tg.seed_off, sc, x[k], cnt);
                     }
                 }
             } else {
                 if (P.key[k].hh_off >= 0) miss = !hh_add(smem + P.key[k].hh_off, P.hh_log2, x[k], cnt);
                 else miss = P.key[k].hasglob;
-                for (uint32_t t = 0; t < P.n_targets; ++t) {
-                    const STarget &tg = P.tgt[t];
-                    if (tg.ndim != 1 || tg.k0 != (uint32_t)k || tg.smem_off < 0) continue;
-                    update_1d(tg, seeds + tg.seed_off, sc, x[k], cnt);   // privatised: always direct
+                for (uint32_t tm = P.key[k].priv1d; tm; tm &= tm - 1) {   // privatised: always direct
+                    const STarget &tg = P.tgt[__ffs(tm) - 1];
+                    update_1d(tg, seeds + tg.seed_off, sc, x[k], cnt);
                 }
             }
         }
@@ -398,18 +391,22 @@ __device__ __forceinline__ void eval_preds(const PR (&pr)[NP], const unsigned ch
     }
 }
 
-// A3: this lane's surviving row `row` (if m) gets ring entry `pos`; its key sectors are
-// gathered with cp.async straight into the warp's survivor-key ring
-template <int NK>
-__device__ __forceinline__ void gather_slot(bool m, uint32_t pos, uint64_t row, unsigned char *q, uint32_t cap,
-                                            const void *const (&kptr)[NK], const uint32_t (&kbytes)[NK]) {
-    if (!m) return;
-    unsigned char *dst = q + (pos & (cap - 1)) * (NK * 8);
-#pragma unroll
-    for (int k = 0; k < NK; ++k) {
-        if (kbytes[k] == 8) cp_async8(dst + k * 8, reinterpret_cast<const long long *>(kptr[k]) + row);
-        else cp_async4(dst + k * 8, reinterpret_cast<const int *>(kptr[k]) + row);
-    }
+// A3: one sector-granular gather of a survivor's key into the ring; the copy size (4 or 8
+// bytes) is chosen by a predicate so one address computation serves both key widths
+__device__ __forceinline__ void cp_async_key(uint32_t dst, const void *src, uint32_t is8) {
+    asm volatile(
+        "{\n\t.reg .pred p8;\n\tsetp.ne.u32 p8, %2, 0;\n\t"
+        "@p8 cp.async.ca.shared.global.L2::64B [%0], [%1], 8;\n\t"
+        "@!p8 cp.async.ca.shared.global.L2::64B [%0], [%1], 4;\n}" ::"r"(dst), "l"(src), "r"(is8)
+        : "memory");
+}
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+    return v;
 }
 
 template <int NK>
@@ -508,6 +505,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
     uint32_t surv = 0;                       // warp-uniform exact survivor count
     const int r0 = warp * 128 + lane * 4;   // this lane's 4 rows inside a tile
     unsigned char *q = smem + P.off_kbuf + warp * P.kb_bytes;   // this warp's survivor-key ring
+    const uint32_t q_a = smem_u32(q);
+    const uint32_t rl_a = smem_u32(smem + P.off_rows) + warp * 256;   // this warp's survivor row list
     uint32_t head = 0, tail = 0;             // ring positions (monotone)
     uint32_t t1 = 0, t2 = 0, t3 = 0;         // ring tail after the previous 1, 2, 3 tiles
     const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
@@ -547,13 +546,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                     }
                     t1 = t2 = t3 = tail;
                 }
-                // survivors in slot-major order (slot j of every lane, then slot j+1): the
-                // ring position is a popc of one ballot, no shuffle chain, no divergence
-                const uint64_t rb = row0 + r0;
-                gather_slot<NK>(m[0], tail + __popc(B0 & lt), rb, q, cap, kptr, kbytes);
-                gather_slot<NK>(m[1], tail + c0 + __popc(B1 & lt), rb + 1, q, cap, kptr, kbytes);
-                gather_slot<NK>(m[2], tail + c0 + c1 + __popc(B2 & lt), rb + 2, q, cap, kptr, kbytes);
-                gather_slot<NK>(m[3], tail + c0 + c1 + c2 + __popc(B3 & lt), rb + 3, q, cap, kptr, kbytes);
+                // survivors in slot-major order (slot j of every lane, then slot j+1): each
+                // survivor's tile offset goes to the warp's row list at a popc of one ballot
+                // (no shuffle chain, no divergence), then the gathers run converged
+                if (m[0]) sts_u16(rl_a + 2 * __popc(B0 & lt), r0);
+                if (m[1]) sts_u16(rl_a + 2 * (c0 + __popc(B1 & lt)), r0 + 1);
+                if (m[2]) sts_u16(rl_a + 2 * (c0 + c1 + __popc(B2 & lt)), r0 + 2);
+                if (m[3]) sts_u16(rl_a + 2 * (c0 + c1 + c2 + __popc(B3 & lt)), r0 + 3);
+                __syncwarp();
+                for (uint32_t e = lane; e < wtot; e += 32) {
+                    const uint64_t row = row0 + lds_u16(rl_a + 2 * e);
+                    const uint32_t dst = q_a + ((tail + e) & (cap - 1)) * (NK * 8);
+#pragma unroll
+                    for (int k = 0; k < NK; ++k)
+                        cp_async_key(dst + k * 8, reinterpret_cast<const unsigned char *>(kptr[k]) + row * kbytes[k],
+                                     kbytes[k] == 8);
+                }
+                __syncwarp();
                 tail += wtot;
             }
             // one cp.async group per tile (possibly empty): wait_group kLag then guarantees the
@@ -861,6 +870,8 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         if (tg.ndim == 2) P.has2d = 1;
         if (tg.ndim == 1) {
             P.key[tg.k0].has1d = 1;
+            if (tg.smem_off >= 0) P.key[tg.k0].priv1d |= 1u << t;
+            else P.key[tg.k0].glob1d |= 1u << t;
             if (tg.smem_off < 0) { P.key[tg.k0].hasglob = 1; key_needs_hh[tg.k0] = true; }
             if (hist_key[tg.k0] && !(getenv("COMPASS_HISTHH") && strcmp(getenv("COMPASS_HISTHH"), "0") == 0))
                 key_needs_hh[tg.k0] = true;
