@@ -34,6 +34,12 @@ using namespace skb;
 
 namespace {
 
+#ifndef SCAN_WAIT_HINT
+#define SCAN_WAIT_HINT 1
+#endif
+#ifndef SCAN_CAP2
+#define SCAN_CAP2 64
+#endif
 #ifndef SCAN_WARPS
 #define SCAN_WARPS 20
 #endif
@@ -121,11 +127,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity), "r"(0x989680u) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
+#if SCAN_WAIT_HINT
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n}" ::"r"(bar), "r"(parity), "r"(0x989680u) : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
@@ -138,7 +152,10 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all_but1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+// every committed group has landed (cp.async issued since the last commit are not covered)
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+// commits the current (possibly partial) group too: every cp.async issued so far has landed
+__device__ __forceinline__ void cp_commit_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_lag() { asm volatile("cp.async.wait_group 3;" ::: "memory"); }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 __device__ __forceinline__ void red_add_u32(uint32_t *p, uint32_t v) {
@@ -164,32 +181,29 @@ __device__ __forceinline__ bool in_set(const int64_t *s, uint32_t n, int64_t v) 
 }
 
 // ------------------------------------------------------------------ heavy-hitter table
-// Bucketised table: 8 slots per bucket, the bucket's 8 keys read with four 128-bit
-// shared loads (one latency) instead of a dependent probe chain.  Two warps may insert
-// the same key into two slots of one bucket; both counts are flushed, which is exact
-// by linearity.
+// Two-choice table of 2^log2s slots (canonical key -> int32 count): a key lives in slot
+// s1(x) or s2(x); a probe is one 64-bit shared load and compare per choice, so a hit on
+// the first choice (every hot key: they arrive first) costs a handful of instructions.
+// Slots are never freed, so a key found in s2 cannot also sit in s1.  Two warps may
+// still insert one key twice in a race; both counts are flushed, which is exact by
+// linearity.
+__device__ __forceinline__ uint64_t lds_v64(uint32_t a) {
+    uint64_t v;
+    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ bool hh_add(unsigned char *tab, uint32_t log2s, uint64_t x, int cnt) {
     uint64_t *keys = reinterpret_cast<uint64_t *>(tab);
     int *cnts = reinterpret_cast<int *>(tab + (8u << log2s));
-    const uint32_t b = (uint32_t)((x * 0x9E3779B97F4A7C15ULL) >> (64 - (log2s - 3))) * 8u;
-#pragma unroll 1
-    for (int attempt = 0; attempt < 8; ++attempt) {
-        uint64_t k[8];
-        const uint32_t a = smem_u32(keys + b);
-        asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(k[0]), "=l"(k[1]) : "r"(a));
-        asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(k[2]), "=l"(k[3]) : "r"(a + 16));
-        asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(k[4]), "=l"(k[5]) : "r"(a + 32));
-        asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(k[6]), "=l"(k[7]) : "r"(a + 48));
-        int hit = -1, emp = -1;
+    const uint64_t h = x * 0x9E3779B97F4A7C15ULL;
+    const uint32_t mask = (1u << log2s) - 1u;
+    const uint32_t ka = smem_u32(keys);
 #pragma unroll
-        for (int j = 7; j >= 0; --j) {
-            if (k[j] == x) hit = j;
-            if (k[j] == kEmpty) emp = j;
-        }
-        if (hit >= 0) { atomicAdd(&cnts[b + hit], cnt); return true; }
-        if (emp < 0) return false;
-        const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long *>(&keys[b + emp]), kEmpty, x);
-        if (prev == kEmpty || prev == x) { atomicAdd(&cnts[b + emp], cnt); return true; }
+    for (int c = 0; c < 2; ++c) {
+        const uint32_t sl = (uint32_t)(h >> (c ? 24 : 44)) & mask;
+        uint64_t k = lds_v64(ka + sl * 8);
+        if (k == kEmpty) k = atomicCAS(reinterpret_cast<unsigned long long *>(&keys[sl]), kEmpty, x);
+        if (k == x || k == kEmpty) { atomicAdd(&cnts[sl], cnt); return true; }
     }
     return false;
 }
@@ -412,6 +426,9 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
 template <int NK>
 __device__ __forceinline__ void drain_batch(const SParams &P, unsigned char *smem, const unsigned char *q,
                                             const uint32_t (&kbytes)[NK], uint32_t head, uint32_t n) {
+#ifdef SCAN_NOHASH   // timing experiments only (tools/build_variant.sh): results are wrong
+    return;
+#endif
     const int lane = threadIdx.x & 31;
     const bool valid = (uint32_t)lane < n;
     uint64_t xk[NK];
@@ -535,17 +552,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             const uint32_t wtot = c0 + c1 + c2 + c3;
             surv += wtot;
             if (wtot) {
-                if (tail - head + wtot > cap) {
-                    // ring would overflow: finish outstanding gathers and drain it completely
-                    cp_wait_all();
-                    __syncwarp();
-                    while (tail != head) {
-                        const uint32_t n = min(32u, tail - head);
-                        drain_batch<NK>(P, smem, q, kbytes, head, n);
-                        head += n;
-                    }
-                    t1 = t2 = t3 = tail;
-                }
                 // survivors in slot-major order (slot j of every lane, then slot j+1): each
                 // survivor's tile offset goes to the warp's row list at a popc of one ballot
                 // (no shuffle chain, no divergence), then the gathers run converged
@@ -554,16 +560,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                 if (m[2]) sts_u16(rl_a + 2 * (c0 + c1 + __popc(B2 & lt)), r0 + 2);
                 if (m[3]) sts_u16(rl_a + 2 * (c0 + c1 + c2 + __popc(B3 & lt)), r0 + 3);
                 __syncwarp();
-                for (uint32_t e = lane; e < wtot; e += 32) {
-                    const uint64_t row = row0 + lds_u16(rl_a + 2 * e);
-                    const uint32_t dst = q_a + ((tail + e) & (cap - 1)) * (NK * 8);
+                for (uint32_t e0 = 0; e0 < wtot;) {
+                    if (tail - head == cap || (e0 == 0 && tail - head + wtot > cap)) {
+                        // ring would overflow: finish outstanding gathers and drain it completely
+                        // (mid-tile, the gathers just issued are not committed yet)
+                        if (e0 == 0) cp_wait_all();
+                        else cp_commit_wait_all();
+                        __syncwarp();
+                        while (tail != head) {
+                            const uint32_t n = min(32u, tail - head);
+                            drain_batch<NK>(P, smem, q, kbytes, head, n);
+                            head += n;
+                        }
+                        t1 = t2 = t3 = tail;
+                    }
+                    const uint32_t n = min(wtot - e0, cap - (tail - head));   // a tile may exceed cap
+                    for (uint32_t e = lane; e < n; e += 32) {
+                        const uint64_t row = row0 + lds_u16(rl_a + 2 * (e0 + e));
+                        const uint32_t dst = q_a + ((tail + e) & (cap - 1)) * (NK * 8);
+#ifndef SCAN_NOGATHER   // timing experiments only (tools/build_variant.sh): results are wrong
 #pragma unroll
-                    for (int k = 0; k < NK; ++k)
-                        cp_async_key(dst + k * 8, reinterpret_cast<const unsigned char *>(kptr[k]) + row * kbytes[k],
-                                     kbytes[k] == 8);
+                        for (int k = 0; k < NK; ++k)
+                            cp_async_key(dst + k * 8, reinterpret_cast<const unsigned char *>(kptr[k]) + row * kbytes[k],
+                                         kbytes[k] == 8);
+#endif
+                    }
+                    tail += n;
+                    e0 += n;
                 }
                 __syncwarp();
-                tail += wtot;
             }
             // one cp.async group per tile (possibly empty): wait_group kLag then guarantees the
             // entries appended kLag tiles ago (t3) have landed; the latency hides behind 3 tiles
@@ -822,7 +847,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     const uint32_t kBudget = 227 * 1024;
     const char *env_st = getenv("COMPASS_STAGES"), *env_hh = getenv("COMPASS_HH_LOG2");
     const uint32_t want_stages = env_st ? (uint32_t)atoi(env_st) : 6;
-    const uint32_t max_hh = env_hh ? (uint32_t)atoi(env_hh) : 12;
+    const uint32_t max_hh = env_hh ? (uint32_t)atoi(env_hh) : 11;
     uint32_t seed_words = 0;
     for (uint32_t t = 0; t < c.n_targets; ++t) seed_words += c.tgt_ndim[t] * c.tgt_d[t] * 6;
     P.seed_words = seed_words;
@@ -832,7 +857,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     P.kb_bytes = 0;
     const uint32_t ring_warps = kWarps;                 // warps owning a survivor-key ring
     if (P.gather) {
-        P.cap = P.n_keys == 1 ? 256 : 128;              // >= one tile-slice of survivors (128); overflow drains
+        P.cap = P.n_keys == 1 ? 256 : SCAN_CAP2;              // >= one tile-slice of survivors (128); overflow drains
         P.kb_bytes = P.cap * P.n_keys * 8;
     }
     const uint32_t min_stages = 3;
@@ -879,15 +904,17 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     }
     P.smem_counters = sc_count;
     avail -= (sc_count * 4 + 15) & ~15u;
-    // ring depth first (up to want_stages), then heavy-hitter tables, then any extra stages
+    // ring depth to 4 stages first, then heavy-hitter tables (up to 2^11 slots per key),
+    // then further stages up to want_stages
     uint32_t stages = min_stages;
-    while (stages < want_stages && stages < kMaxStages && avail >= P.stage_bytes) { ++stages; avail -= P.stage_bytes; }
+    while (stages < 4 && stages < want_stages && avail >= P.stage_bytes) { ++stages; avail -= P.stage_bytes; }
     uint32_t nhh = 0;
     for (uint32_t k = 0; k < P.n_keys; ++k) nhh += key_needs_hh[k];
     P.hh_log2 = 0;
     for (uint32_t l = max_hh; l >= 8 && nhh; --l)
         if (nhh * (12u << l) <= avail) { P.hh_log2 = l; break; }
     if (P.hh_log2) avail -= nhh * (12u << P.hh_log2);
+    while (stages < want_stages && stages < kMaxStages && avail >= P.stage_bytes) { ++stages; avail -= P.stage_bytes; }
     while (stages < kMaxStages && !env_st && avail >= P.stage_bytes && nhh == 0) { ++stages; avail -= P.stage_bytes; }
     P.stages = stages;
     uint32_t off = 128;                                  // 2 x kMaxStages mbarriers
