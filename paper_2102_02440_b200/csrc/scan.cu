@@ -43,11 +43,17 @@ namespace {
 #ifndef SCAN_WARPS
 #define SCAN_WARPS 20
 #endif
-constexpr int kWarps = SCAN_WARPS;
-constexpr int kTile = kWarps * 128;
+#ifndef SCAN_GROUPS
+#define SCAN_GROUPS 1
+#endif
+constexpr int kWarps = SCAN_WARPS;           // consumer warps per CTA
+constexpr int kGroups = SCAN_GROUPS;         // independent ring groups per CTA (one producer warp each)
+constexpr int kGW = kWarps / kGroups;        // consumer warps per group
+constexpr int kTile = kGW * 128;             // rows per group tile (one ring stage)
+static_assert(kWarps % kGroups == 0, "warps must split evenly into ring groups");
 
 constexpr int kConsumers = kWarps * 32;
-constexpr int kThreads = kConsumers + 32;
+constexpr int kThreads = kConsumers + 32 * kGroups;
 constexpr int kMaxStages = 8;
 constexpr int kMaxSCols = 8, kMaxSPreds = 8, kMaxKeys = 4, kMaxSTargets = 16;
 constexpr uint64_t kEmpty = ~0ULL;   // canonical keys are < 2^61: never equal
@@ -104,6 +110,7 @@ struct SParams {
     uint32_t off_miss, off_missn;   // per-warp miss buffers (x, count) and fill counts
     uint32_t off_rows;              // per-warp survivor row-offset list (128 x uint16)
     uint32_t tile_rows;             // rows per ring stage
+    uint32_t n_full_tiles;          // tiles with tile_rows rows (staged by TMA)
     unsigned long long *survivors;
 };
 
@@ -414,6 +421,11 @@ __device__ __forceinline__ void cp_async_key(uint32_t dst, const void *src, uint
         "@!p8 cp.async.ca.shared.global.L2::64B [%0], [%1], 4;\n}" ::"r"(dst), "l"(src), "r"(is8)
         : "memory");
 }
+template <int W>
+__device__ __forceinline__ void cp_async_fixed(uint32_t dst, const void *src) {
+    if (W == 8) asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+    else asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
@@ -441,17 +453,25 @@ __device__ __forceinline__ void drain_batch(const SParams &P, unsigned char *sme
     process_batch<NK>(P, smem, valid, xk);
 }
 
-template <int NK, int NP, bool R32>
+// KW = 0: generic (any predicate kinds, key widths read at run time); KW = 4 / 8: every
+// predicate is an int32 range and every key column is KW bytes wide (no kind or width
+// branches; survivors' keys are gathered straight from the ballots)
+template <int NK, int NP, int KW>
 __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SParams P) {
+    constexpr bool R32 = KW != 0;
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-    uint64_t *empty = full + kMaxStages;
+    uint64_t *full_all = reinterpret_cast<uint64_t *>(smem);   // [kGroups][kMaxStages]
+    uint64_t *empty_all = full_all + kGroups * kMaxStages;     // [kGroups][kMaxStages]
     const uint32_t kStages = P.stages;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // ring group of this warp (producers are warps kWarps .. kWarps + kGroups - 1)
+    const int grp = warp < kWarps ? warp / kGW : warp - kWarps;
+    uint64_t *full = full_all + grp * kMaxStages, *empty = empty_all + grp * kMaxStages;
+    const uint32_t G = gridDim.x * kGroups, gid = blockIdx.x * kGroups + grp;   // this group's tiles: gid + k*G
 
     // ---- setup: barriers, smem counters, heavy-hitter tables, seeds
     if (tid == 0) {
-        for (uint32_t s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kWarps); }
+        for (uint32_t s = 0; s < kGroups * kMaxStages; ++s) { mbar_init(&full_all[s], 1); mbar_init(&empty_all[s], kGW); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     {
@@ -473,18 +493,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
     }
     __syncthreads();
 
-    if (warp == kWarps) {
-        // ================= producer warp: TMA bulk copies of staged columns
+    if (warp >= kWarps) {
+        // ================= producer warp of ring group grp: TMA bulk copies of staged columns
         if (lane == 0) {
             uint32_t s = 0, ph = 0;
             bool wrapped = false;
-            for (uint64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+            for (uint64_t t = gid; t < P.n_tiles; t += G) {
                 if (wrapped) mbar_wait(&empty[s], ph ^ 1);
                 const uint64_t row0 = t * P.tile_rows;
                 const bool fulltile = row0 + P.tile_rows <= P.n_rows;
                 if (fulltile && P.stage_bytes) {
                     mbar_arrive_tx(&full[s], P.stage_bytes);
-                    unsigned char *stage = smem + P.off_ring + s * P.stage_bytes;
+                    unsigned char *stage = smem + P.off_ring + (grp * kStages + s) * P.stage_bytes;
                     for (uint32_t c = 0; c < P.n_cols; ++c) {
                         if (P.col[c].soff < 0) continue;
                         const uint32_t b = P.col[c].bytes;
@@ -520,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
     }
     const uint32_t cap = P.cap;
     uint32_t surv = 0;                       // warp-uniform exact survivor count
-    const int r0 = warp * 128 + lane * 4;   // this lane's 4 rows inside a tile
+    const int r0 = (warp % kGW) * 128 + lane * 4;   // this lane's 4 rows inside its group's tile
     unsigned char *q = smem + P.off_kbuf + warp * P.kb_bytes;   // this warp's survivor-key ring
     const uint32_t q_a = smem_u32(q);
     const uint32_t rl_a = smem_u32(smem + P.off_rows) + warp * 256;   // this warp's survivor row list
@@ -531,11 +551,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
     const uint32_t n_tiles = (uint32_t)P.n_tiles;
     constexpr int NPX = (NP > 0) ? NP : 1;
     uint32_t s = 0, ph = 0;
-    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (uint32_t t = gid; t < n_tiles; t += G) {
         const uint64_t row0 = uint64_t(t) * kTile;
         mbar_wait_a(full_a + s * 8, ph);
-        const unsigned char *stage = smem + P.off_ring + s * P.stage_bytes;
-        const bool full_tile = row0 + kTile <= P.n_rows;   // staged by the producer
+        const unsigned char *stage = smem + P.off_ring + (grp * kStages + s) * P.stage_bytes;
+        const bool full_tile = t < P.n_full_tiles;   // staged by the producer
         if (NP > 0) {
             bool m[4];
             if (full_tile) eval_preds<NPX, R32, true>(pr, stage, row0, r0, 4, m);
@@ -552,43 +572,62 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             const uint32_t wtot = c0 + c1 + c2 + c3;
             surv += wtot;
             if (wtot) {
-                // survivors in slot-major order (slot j of every lane, then slot j+1): each
-                // survivor's tile offset goes to the warp's row list at a popc of one ballot
-                // (no shuffle chain, no divergence), then the gathers run converged
-                if (m[0]) sts_u16(rl_a + 2 * __popc(B0 & lt), r0);
-                if (m[1]) sts_u16(rl_a + 2 * (c0 + __popc(B1 & lt)), r0 + 1);
-                if (m[2]) sts_u16(rl_a + 2 * (c0 + c1 + __popc(B2 & lt)), r0 + 2);
-                if (m[3]) sts_u16(rl_a + 2 * (c0 + c1 + c2 + __popc(B3 & lt)), r0 + 3);
-                __syncwarp();
-                for (uint32_t e0 = 0; e0 < wtot;) {
-                    if (tail - head == cap || (e0 == 0 && tail - head + wtot > cap)) {
-                        // ring would overflow: finish outstanding gathers and drain it completely
-                        // (mid-tile, the gathers just issued are not committed yet)
-                        if (e0 == 0) cp_wait_all();
-                        else cp_commit_wait_all();
-                        __syncwarp();
-                        while (tail != head) {
-                            const uint32_t n = min(32u, tail - head);
-                            drain_batch<NK>(P, smem, q, kbytes, head, n);
-                            head += n;
-                        }
-                        t1 = t2 = t3 = tail;
+                if (KW != 0 && tail - head + wtot <= cap) {
+                    // survivors in slot-major order (slot j of every lane, then slot j+1): ring
+                    // position = popc of one ballot, gathered straight from the owning lane
+                    const uint32_t pb[4] = {tail, tail + c0, tail + c0 + c1, tail + c0 + c1 + c2};
+                    const uint32_t bj[4] = {B0, B1, B2, B3};
+                    const unsigned char *kb[NK];
+#pragma unroll
+                    for (int k = 0; k < NK; ++k)
+                        kb[k] = reinterpret_cast<const unsigned char *>(kptr[k]) + (row0 + r0) * (uint64_t)(KW ? KW : 8);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (!m[j]) continue;
+                        const uint32_t dst = q_a + ((pb[j] + __popc(bj[j] & lt)) & (cap - 1)) * (NK * 8);
+#pragma unroll
+                        for (int k = 0; k < NK; ++k) cp_async_fixed<KW ? KW : 8>(dst + k * 8, kb[k] + j * (KW ? KW : 8));
                     }
-                    const uint32_t n = min(wtot - e0, cap - (tail - head));   // a tile may exceed cap
-                    for (uint32_t e = lane; e < n; e += 32) {
-                        const uint64_t row = row0 + lds_u16(rl_a + 2 * (e0 + e));
-                        const uint32_t dst = q_a + ((tail + e) & (cap - 1)) * (NK * 8);
+                    tail += wtot;
+                } else {
+                    // generic / ring-full path: each survivor's tile offset goes to the warp's
+                    // row list (same slot-major order), then the gathers run converged over the
+                    // list, in rounds that fit the ring (a tile may hold more survivors than it)
+                    if (m[0]) sts_u16(rl_a + 2 * __popc(B0 & lt), r0);
+                    if (m[1]) sts_u16(rl_a + 2 * (c0 + __popc(B1 & lt)), r0 + 1);
+                    if (m[2]) sts_u16(rl_a + 2 * (c0 + c1 + __popc(B2 & lt)), r0 + 2);
+                    if (m[3]) sts_u16(rl_a + 2 * (c0 + c1 + c2 + __popc(B3 & lt)), r0 + 3);
+                    __syncwarp();
+                    for (uint32_t e0 = 0; e0 < wtot;) {
+                        if (tail - head == cap || (e0 == 0 && tail - head + wtot > cap)) {
+                            // ring would overflow: finish outstanding gathers and drain it completely
+                            // (mid-tile, the gathers just issued are not committed yet)
+                            if (e0 == 0) cp_wait_all();
+                            else cp_commit_wait_all();
+                            __syncwarp();
+                            while (tail != head) {
+                                const uint32_t n = min(32u, tail - head);
+                                drain_batch<NK>(P, smem, q, kbytes, head, n);
+                                head += n;
+                            }
+                            t1 = t2 = t3 = tail;
+                        }
+                        const uint32_t n = min(wtot - e0, cap - (tail - head));   // a tile may exceed cap
+                        for (uint32_t e = lane; e < n; e += 32) {
+                            const uint64_t row = row0 + lds_u16(rl_a + 2 * (e0 + e));
+                            const uint32_t dst = q_a + ((tail + e) & (cap - 1)) * (NK * 8);
 #ifndef SCAN_NOGATHER   // timing experiments only (tools/build_variant.sh): results are wrong
 #pragma unroll
-                        for (int k = 0; k < NK; ++k)
-                            cp_async_key(dst + k * 8, reinterpret_cast<const unsigned char *>(kptr[k]) + row * kbytes[k],
-                                         kbytes[k] == 8);
+                            for (int k = 0; k < NK; ++k)
+                                cp_async_key(dst + k * 8, reinterpret_cast<const unsigned char *>(kptr[k]) + row * kbytes[k],
+                                             kbytes[k] == 8);
 #endif
+                        }
+                        tail += n;
+                        e0 += n;
                     }
-                    tail += n;
-                    e0 += n;
+                    __syncwarp();
                 }
-                __syncwarp();
             }
             // one cp.async group per tile (possibly empty): wait_group kLag then guarantees the
             // entries appended kLag tiles ago (t3) have landed; the latency hides behind 3 tiles
@@ -750,23 +789,29 @@ __global__ void __launch_bounds__(512) k_hist_epilogue(const __grid_constant__ E
 
 typedef void (*ScanKernel)(const SParams);
 
+template <int NK, int NP>
+static ScanKernel pick_kw(int kw) {
+    if (NP == 0) return k_scan<NK, NP, 0>;
+    return kw == 4 ? k_scan<NK, NP, 4> : kw == 8 ? k_scan<NK, NP, 8> : k_scan<NK, NP, 0>;
+}
+
 template <int NK>
-static ScanKernel pick_np(uint32_t np, bool r32) {
+static ScanKernel pick_np(uint32_t np, int kw) {
     switch (np) {
-        case 0: return k_scan<NK, 0, false>;
-        case 1: return r32 ? k_scan<NK, 1, true> : k_scan<NK, 1, false>;
-        case 2: return r32 ? k_scan<NK, 2, true> : k_scan<NK, 2, false>;
-        case 3: return r32 ? k_scan<NK, 3, true> : k_scan<NK, 3, false>;
-        default: return r32 ? k_scan<NK, 4, true> : k_scan<NK, 4, false>;
+        case 0: return pick_kw<NK, 0>(kw);
+        case 1: return pick_kw<NK, 1>(kw);
+        case 2: return pick_kw<NK, 2>(kw);
+        case 3: return pick_kw<NK, 3>(kw);
+        default: return pick_kw<NK, 4>(kw);
     }
 }
 
-static ScanKernel pick_kernel(uint32_t nk, uint32_t np, bool r32) {
+static ScanKernel pick_kernel(uint32_t nk, uint32_t np, int kw) {
     switch (nk) {
-        case 1: return pick_np<1>(np, r32);
-        case 2: return pick_np<2>(np, r32);
-        case 3: return pick_np<3>(np, r32);
-        default: return pick_np<4>(np, r32);
+        case 1: return pick_np<1>(np, kw);
+        case 2: return pick_np<2>(np, kw);
+        case 3: return pick_np<3>(np, kw);
+        default: return pick_np<4>(np, kw);
     }
 }
 
@@ -831,6 +876,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     P.gather = c.n_preds > 0 ? 1u : 0u;
     P.tile_rows = kTile;
     P.n_tiles = (c.n_rows + P.tile_rows - 1) / P.tile_rows;
+    P.n_full_tiles = (uint32_t)(c.n_rows / P.tile_rows);
     // staged columns: predicate columns, plus key columns when there is no predicate
     uint32_t soff = 0;
     auto stage_col = [&](uint32_t col) {
@@ -862,7 +908,9 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     }
     const uint32_t min_stages = 3;
     const uint32_t miss_bytes = kWarps * P.n_keys * 32 * 12 + ((kWarps * P.n_keys * 4 + 15) & ~15u);
-    const uint32_t fixed = 128 + min_stages * P.stage_bytes + ring_warps * P.kb_bytes + seed_bytes + miss_bytes +
+    const uint32_t kBarBytes = 2 * kGroups * kMaxStages * 8;
+    const uint32_t ring_stage = kGroups * P.stage_bytes;   // one stage of every group's ring
+    const uint32_t fixed = kBarBytes + min_stages * ring_stage + ring_warps * P.kb_bytes + seed_bytes + miss_bytes +
                            kWarps * 128 * 2 + 256;
     if (fixed > kBudget) return SK_OK;
     uint32_t avail = kBudget - fixed;
@@ -907,19 +955,19 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     // ring depth to 4 stages first, then heavy-hitter tables (up to 2^11 slots per key),
     // then further stages up to want_stages
     uint32_t stages = min_stages;
-    while (stages < 4 && stages < want_stages && avail >= P.stage_bytes) { ++stages; avail -= P.stage_bytes; }
+    while (stages < 4 && stages < want_stages && avail >= ring_stage) { ++stages; avail -= ring_stage; }
     uint32_t nhh = 0;
     for (uint32_t k = 0; k < P.n_keys; ++k) nhh += key_needs_hh[k];
     P.hh_log2 = 0;
     for (uint32_t l = max_hh; l >= 8 && nhh; --l)
         if (nhh * (12u << l) <= avail) { P.hh_log2 = l; break; }
     if (P.hh_log2) avail -= nhh * (12u << P.hh_log2);
-    while (stages < want_stages && stages < kMaxStages && avail >= P.stage_bytes) { ++stages; avail -= P.stage_bytes; }
-    while (stages < kMaxStages && !env_st && avail >= P.stage_bytes && nhh == 0) { ++stages; avail -= P.stage_bytes; }
+    while (stages < want_stages && stages < kMaxStages && avail >= ring_stage) { ++stages; avail -= ring_stage; }
+    while (stages < kMaxStages && !env_st && avail >= ring_stage && nhh == 0) { ++stages; avail -= ring_stage; }
     P.stages = stages;
-    uint32_t off = 128;                                  // 2 x kMaxStages mbarriers
+    uint32_t off = (kBarBytes + 127) & ~127u;            // full + empty mbarriers per group
     P.off_ring = off;
-    off += stages * P.stage_bytes;
+    off += stages * ring_stage;
     off = (off + 127) & ~127u;
     P.off_kbuf = off;
     off += ring_warps * P.kb_bytes;
@@ -946,9 +994,9 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    uint64_t grid = std::min<uint64_t>((uint64_t)sms, P.n_tiles);
+    uint64_t grid = std::min<uint64_t>((uint64_t)sms, (P.n_tiles + kGroups - 1) / kGroups);
     // int32 privatised counts stay exact: rows per CTA < 2^31
-    if ((P.n_tiles + grid - 1) / grid * P.tile_rows >= (1ULL << 31)) return SK_OK;
+    if ((P.n_tiles + grid * kGroups - 1) / (grid * kGroups) * P.tile_rows * kGroups >= (1ULL << 31)) return SK_OK;
     if (P.n_keys == 0) return SK_OK;
     std::vector<void *> hists;
     for (uint32_t k = 0; k < P.n_keys; ++k) {
@@ -963,9 +1011,14 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         P.key[k].hist = (uint32_t *)h;
         P.key[k].domain = dom;
     }
-    bool all_r32 = true;
-    for (uint32_t q = 0; q < P.n_preds; ++q) all_r32 &= P.pred[q].kind == PR_R32;
-    ScanKernel kern = pick_kernel(P.n_keys, P.n_preds, all_r32);
+    // specialisation: all predicates int32 ranges and one key width -> KW, else generic
+    int kw = (int)P.col[P.key[0].col].bytes;
+    for (uint32_t k = 1; k < P.n_keys; ++k)
+        if ((int)P.col[P.key[k].col].bytes != kw) kw = 0;
+    for (uint32_t q = 0; q < P.n_preds; ++q)
+        if (P.pred[q].kind != PR_R32) kw = 0;
+    if (getenv("COMPASS_SCAN_KW0")) kw = 0;   // experiments / parity of the generic variant
+    ScanKernel kern = pick_kernel(P.n_keys, P.n_preds, kw);
     const int threads = kThreads;
     SKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)off));
     kern<<<(unsigned)grid, threads, off, stream>>>(P);

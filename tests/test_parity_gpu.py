@@ -125,6 +125,37 @@ def test_build_parity_domain_hints(n, di, pi):
         assert np.array_equal(a, b)
 
 
+# single-width key targets under int32 range predicates select the specialised scan
+# (KW = 4 or 8: survivors gathered straight from the ballots); the same inputs through the
+# generic variant (COMPASS_SCAN_KW0) and the grid-stride kernel must give the same counters.
+# Selectivities 1% .. 100% cover the ring-full rounds (a 128-row slice with > 64 survivors).
+KW_TARGETS = {
+    4: [(["k32"], 5, [1024], ["A.k32|B.x"]), (["p2"], 3, [64], ["A.p2|C.y"]),
+        (["k32", "p2"], 3, [32, 16], ["A.k32|B.x", "A.p2|C.y"])],
+    8: [(["k64"], 3, [64], ["A.k64|C.y"]), (["zk"], 9, [16384], ["A.zk|D.z"]),
+        (["zk", "k64"], 5, [64, 128], ["A.k64|C.y", "A.zk|D.z"])],
+}
+
+
+@pytest.mark.parametrize("kw", [4, 8])
+@pytest.mark.parametrize("hi", [0, 36, 49, 99])
+@pytest.mark.parametrize("variant", ["kw", "kw0", "generic"])
+@pytest.mark.parametrize("n", [31, 100_003, 1_000_000])
+def test_build_parity_specialised_scan(kw, hi, variant, n, monkeypatch):
+    if variant == "kw0":
+        monkeypatch.setenv("COMPASS_SCAN_KW0", "1")
+    elif variant == "generic":
+        monkeypatch.setenv("COMPASS_SCAN", "generic")
+    cols = _rand_cols(n, 3000 + n + hi)
+    cols["p2"] = np.random.default_rng(n).integers(-50, 50, n).astype(np.int32)
+    preds = [("p", pb.RANGE, 0, hi), ("p2", pb.RANGE, -50, 49)]
+    g, gs = _gpu_build(cols, preds, KW_TARGETS[kw])
+    o, os_ = _oracle_build(cols, preds, KW_TARGETS[kw])
+    assert gs == os_
+    for a, b in zip(g, o):
+        assert np.array_equal(a, b)
+
+
 def test_build_parity_global_atomic_path_and_skew(scan_mode):
     """A sketch too large for shared memory (C4 shape d=9, w=16384) next to a privatised one."""
     cols = _rand_cols(3_000_001, 77)
