@@ -107,6 +107,11 @@ struct SParams {
     uint32_t off_ring, off_kbuf, off_hh, off_sc, off_seed;
     uint32_t smem_counters, seed_words;
     uint32_t has2d;       // some target is a matrix
+    // trio: a matrix M on key columns (ka, kb) whose two hash families equal those of the
+    // privatised 1-D sketches A on ka and B on kb (same edges, same d).  One row loop hashes
+    // each survivor's two keys once and updates A, B and M (the matrix reuses the 1-D hash
+    // values).
+    uint32_t trio_on, trio_ka, trio_kb, trio_a, trio_b, trio_m;
     uint32_t off_miss, off_missn;   // per-warp miss buffers (x, count) and fill counts
     uint32_t off_rows;              // per-warp survivor row-offset list (128 x uint16)
     uint32_t tile_rows;             // rows per ring stage
@@ -274,6 +279,8 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
     int32_t *sc = reinterpret_cast<int32_t *>(smem + P.off_sc);
     const uint64_t *seeds = reinterpret_cast<const uint64_t *>(smem + P.off_seed);
     const int lane = threadIdx.x & 31;
+    bool la = false, lb = false;   // trio keys: this lane leads its key group (size ca / cb)
+    int ca = 0, cb = 0;
 #pragma unroll
     for (int k = 0; k < NK; ++k) {
         if (!P.key[k].has1d) continue;
@@ -284,6 +291,10 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
             const uint32_t grp = __match_any_sync(act, x[k]);
             leader = lane == __ffs(grp) - 1;
             cnt = __popc(grp);
+        }
+        if (P.trio_on) {
+            if ((uint32_t)k == P.trio_ka) { la = leader; ca = cnt; }
+            if ((uint32_t)k == P.trio_kb) { lb = leader; cb = cnt; }
         }
         if (leader) {
             if (P.key[k].hist) {
@@ -339,10 +350,33 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
     if (valid && P.has2d) {
         for (uint32_t t = 0; t < P.n_targets; ++t) {
             const STarget &tg = P.tgt[t];
-            if (tg.ndim != 2) continue;
+            if (tg.ndim != 2 || (P.trio_on && t == P.trio_m)) continue;
             const uint64_t xa = pick<NK>(x, tg.k0), xb = pick<NK>(x, tg.k1);
             const uint32_t grp = __match_any_sync(act, xa) & __match_any_sync(act, xb);
             if (lane == __ffs(grp) - 1) update_2d(tg, seeds + tg.seed_off, sc, xa, xb, __popc(grp));
+        }
+    }
+    if (valid && P.trio_on) {
+        const uint64_t xa = pick<NK>(x, P.trio_ka), xb = pick<NK>(x, P.trio_kb);
+        const uint32_t grp = __match_any_sync(act, xa) & __match_any_sync(act, xb);
+        const bool lm = lane == __ffs(grp) - 1;
+        const int cm = __popc(grp);
+        if (la || lb || lm) {
+            const STarget &A = P.tgt[P.trio_a], &B = P.tgt[P.trio_b], &M = P.tgt[P.trio_m];
+            const uint64_t *sa = seeds + A.seed_off, *sb = seeds + B.seed_off;
+            for (uint32_t r = 0; r < M.d; ++r) {
+                const uint64_t *a = sa + r * 6, *b = sb + r * 6;
+                const uint32_t ga = (uint32_t)hash_g61(a[4], a[5], xa), gb = (uint32_t)hash_g61(b[4], b[5], xb);
+                const int xia = xi_sign61(a, xa), xib = xi_sign61(b, xb);
+                if (la) atomicAdd(&sc[A.smem_off + r * A.cells + (ga & A.wmask0)], xia * ca);
+                if (lb) atomicAdd(&sc[B.smem_off + r * B.cells + (gb & B.wmask0)], xib * cb);
+                if (lm) {
+                    const uint32_t cell = ((ga & M.wmask0) << M.lw1) | (gb & M.wmask1);
+                    const int v = xia * xib * cm;
+                    if (M.smem_off >= 0) atomicAdd(&sc[M.smem_off + r * M.cells + cell], v);
+                    else red_add_s64(M.counters + uint64_t(r) * M.cells + cell, (int64_t)v);
+                }
+            }
         }
     }
 }
@@ -952,6 +986,33 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     }
     P.smem_counters = sc_count;
     avail -= (sc_count * 4 + 15) & ~15u;
+    // trio detection: matrix M whose dimension-q hash rows equal those of a privatised 1-D
+    // sketch on the same key (exact comparison of the coefficient rows; same d)
+    P.trio_on = 0;
+    for (uint32_t m = 0; m < c.n_targets && !P.trio_on; ++m) {
+        const STarget &M = P.tgt[m];
+        if (M.ndim != 2 || M.k0 == M.k1) continue;
+        int ab[2] = {-1, -1};
+        for (uint32_t q = 0; q < 2; ++q) {
+            const uint32_t k = q ? M.k1 : M.k0;
+            const uint64_t *rows = c.tgt_seeds_host[m] + size_t(q) * M.d * 6;
+            for (uint32_t t = 0; t < c.n_targets && ab[q] < 0; ++t) {
+                const STarget &T = P.tgt[t];
+                if (T.ndim == 1 && T.k0 == k && T.smem_off >= 0 && T.d == M.d &&
+                    memcmp(c.tgt_seeds_host[t], rows, size_t(M.d) * 6 * 8) == 0)
+                    ab[q] = (int)t;
+            }
+        }
+        if (ab[0] < 0 || ab[1] < 0) continue;
+        P.trio_on = 1;
+        P.trio_ka = M.k0;
+        P.trio_kb = M.k1;
+        P.trio_a = (uint32_t)ab[0];
+        P.trio_b = (uint32_t)ab[1];
+        P.trio_m = m;
+        P.key[M.k0].priv1d &= ~(1u << ab[0]);   // updated in the trio loop, not per key
+        P.key[M.k1].priv1d &= ~(1u << ab[1]);
+    }
     // ring depth to 4 stages first, then heavy-hitter tables (up to 2^11 slots per key),
     // then further stages up to want_stages
     uint32_t stages = min_stages;

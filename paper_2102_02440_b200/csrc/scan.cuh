@@ -22,6 +22,7 @@ struct ScanCall {
     int64_t *tgt_counters[16];
     uint32_t tgt_ndim[16], tgt_d[16], tgt_w[16][2], tgt_key[16][2];
     const uint64_t *tgt_seeds[16];
+    const uint64_t *tgt_seeds_host[16];   // host copies [ndim][d][6] (hash-unit sharing)
     unsigned long long *survivors = nullptr;
 };
 
