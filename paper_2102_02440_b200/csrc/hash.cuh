@@ -27,8 +27,32 @@ __device__ __forceinline__ uint64_t mulmod61(uint64_t a, uint64_t b) {
     return red61(r);
 }
 
+// Lazily reduced v*x mod p for a key x < 2^32 (every int32 key >= 0 and most dense key
+// domains): two 32x32->64 products instead of a 64x64->128 one.  v < 2^64; the result is
+// congruent to v*x mod p and < 2^62 + 2^35 + 8 (not fully reduced).
+//   v*x = p1 + p2*2^32, p1 = vlo*x, p2 = vhi*x;  p1 = (p1 & p) + (p1 >> 61) (mod p);
+//   p2*2^32 = (p2 >> 29)*2^61 + (p2 & (2^29-1))*2^32 == (p2 >> 29) + ((p2 & (2^29-1)) << 32).
+__device__ __forceinline__ uint64_t mulmod61_x32(uint64_t v, uint32_t x) {
+    const uint64_t p1 = (uint64_t)(uint32_t)v * x;
+    const uint64_t p2 = (uint64_t)(uint32_t)(v >> 32) * x;
+    return (p1 & SKH_P) + (p1 >> 61) + (p2 >> 29) + ((p2 & 0x1FFFFFFFULL) << 32);
+}
+
+// any v < 2^63  ->  v mod p
+__device__ __forceinline__ uint64_t full61(uint64_t v) {
+    v = (v & SKH_P) + (v >> 61);   // < 2^61 + 4 < 2p
+    return v >= SKH_P ? v - SKH_P : v;
+}
+
 // H3: xi(x) = +1 iff ((a3 x + a2) x + a1) x + a0 mod p is odd.  s = {a0,a1,a2,a3,...}
 __device__ __forceinline__ int xi_sign61(const uint64_t *s, uint64_t x) {
+    if (x < (1ULL << 32)) {
+        // lazy Horner: each step stays < 2^62 + 2^35 + 8 + 2^61 < 2^63, reduced once at the end
+        uint64_t v = mulmod61_x32(s[3], (uint32_t)x) + s[2];
+        v = mulmod61_x32(v, (uint32_t)x) + s[1];
+        v = mulmod61_x32(v, (uint32_t)x) + s[0];
+        return (full61(v) & 1ULL) ? 1 : -1;
+    }
     uint64_t v = s[3];
     v = red61(mulmod61(v, x) + s[2]);
     v = red61(mulmod61(v, x) + s[1]);
@@ -38,5 +62,6 @@ __device__ __forceinline__ int xi_sign61(const uint64_t *s, uint64_t x) {
 
 // H4: g(x) = (b1 x + b0) mod p; the bucket is g mod w = g & (w-1).
 __device__ __forceinline__ uint64_t hash_g61(uint64_t b0, uint64_t b1, uint64_t x) {
+    if (x < (1ULL << 32)) return full61(mulmod61_x32(b1, (uint32_t)x) + b0);
     return red61(mulmod61(b1, x) + b0);
 }
