@@ -45,9 +45,12 @@ __device__ __forceinline__ uint64_t full61(uint64_t v) {
 }
 
 // H3: xi(x) = +1 iff ((a3 x + a2) x + a1) x + a0 mod p is odd.  s = {a0,a1,a2,a3,...}
-__device__ __forceinline__ int xi_sign61(const uint64_t *s, uint64_t x) {
-    if (x < (1ULL << 32)) {
-        // lazy Horner: each step stays < 2^62 + 2^35 + 8 + 2^61 < 2^63, reduced once at the end
+// NARROW = true requires x < 2^32 (lazy 64x32 Horner, one final reduction); callers pick
+// the variant once per loop, so the two paths are never if-converted into one.
+template <bool NARROW>
+__device__ __forceinline__ int xi_sign61_t(const uint64_t *s, uint64_t x) {
+    if (NARROW) {
+        // each step stays < 2^62 + 2^35 + 8 + 2^61 < 2^63
         uint64_t v = mulmod61_x32(s[3], (uint32_t)x) + s[2];
         v = mulmod61_x32(v, (uint32_t)x) + s[1];
         v = mulmod61_x32(v, (uint32_t)x) + s[0];
@@ -61,7 +64,16 @@ __device__ __forceinline__ int xi_sign61(const uint64_t *s, uint64_t x) {
 }
 
 // H4: g(x) = (b1 x + b0) mod p; the bucket is g mod w = g & (w-1).
-__device__ __forceinline__ uint64_t hash_g61(uint64_t b0, uint64_t b1, uint64_t x) {
-    if (x < (1ULL << 32)) return full61(mulmod61_x32(b1, (uint32_t)x) + b0);
+template <bool NARROW>
+__device__ __forceinline__ uint64_t hash_g61_t(uint64_t b0, uint64_t b1, uint64_t x) {
+    if (NARROW) return full61(mulmod61_x32(b1, (uint32_t)x) + b0);
     return red61(mulmod61(b1, x) + b0);
+}
+
+// any key
+__device__ __forceinline__ int xi_sign61(const uint64_t *s, uint64_t x) {
+    return x < (1ULL << 32) ? xi_sign61_t<true>(s, x) : xi_sign61_t<false>(s, x);
+}
+__device__ __forceinline__ uint64_t hash_g61(uint64_t b0, uint64_t b1, uint64_t x) {
+    return x < (1ULL << 32) ? hash_g61_t<true>(b0, b1, x) : hash_g61_t<false>(b0, b1, x);
 }

@@ -222,27 +222,38 @@ __device__ __forceinline__ bool hh_add(unsigned char *tab, uint32_t log2s, uint6
 
 // ------------------------------------------------------------------ sketch updates
 // 1-D target t: row r gets cnt * xi_r(x) at bucket h_r(x)
-__device__ __forceinline__ void update_1d(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, int cnt) {
+template <bool N>
+__device__ __forceinline__ void update_1d_t(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, int cnt) {
     for (uint32_t r = 0; r < tg.d; ++r) {
         const uint64_t *a = seed + r * 6;
-        const uint32_t cell = (uint32_t)(hash_g61(a[4], a[5], x) & tg.wmask0);
-        const int v = xi_sign61(a, x) * cnt;
+        const uint32_t cell = (uint32_t)(hash_g61_t<N>(a[4], a[5], x) & tg.wmask0);
+        const int v = xi_sign61_t<N>(a, x) * cnt;
         if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
         else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
     }
 }
+__device__ __forceinline__ void update_1d(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, int cnt) {
+    if (x < (1ULL << 32)) update_1d_t<true>(tg, seed, sc, x, cnt);
+    else update_1d_t<false>(tg, seed, sc, x, cnt);
+}
 
-__device__ __forceinline__ void update_2d(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, uint64_t y,
-                                          int cnt) {
+template <bool N>
+__device__ __forceinline__ void update_2d_t(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, uint64_t y,
+                                            int cnt) {
     const uint64_t *s1 = seed + tg.d * 6;
     for (uint32_t r = 0; r < tg.d; ++r) {
         const uint64_t *a = seed + r * 6, *b = s1 + r * 6;
-        const uint32_t cell = ((uint32_t)(hash_g61(a[4], a[5], x) & tg.wmask0) << tg.lw1) |
-                              (uint32_t)(hash_g61(b[4], b[5], y) & tg.wmask1);
-        const int v = xi_sign61(a, x) * xi_sign61(b, y) * cnt;
+        const uint32_t cell = ((uint32_t)(hash_g61_t<N>(a[4], a[5], x) & tg.wmask0) << tg.lw1) |
+                              (uint32_t)(hash_g61_t<N>(b[4], b[5], y) & tg.wmask1);
+        const int v = xi_sign61_t<N>(a, x) * xi_sign61_t<N>(b, y) * cnt;
         if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
         else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
     }
+}
+__device__ __forceinline__ void update_2d(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, uint64_t y,
+                                          int cnt) {
+    if ((x | y) < (1ULL << 32)) update_2d_t<true>(tg, seed, sc, x, y, cnt);
+    else update_2d_t<false>(tg, seed, sc, x, y, cnt);
 }
 
 // x[idx] with compile-time indexing only (keeps the key array in registers)
@@ -364,10 +375,22 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
         if (la || lb || lm) {
             const STarget &A = P.tgt[P.trio_a], &B = P.tgt[P.trio_b], &M = P.tgt[P.trio_m];
             const uint64_t *sa = seeds + A.seed_off, *sb = seeds + B.seed_off;
+            const bool narrow = (xa | xb) < (1ULL << 32);
             for (uint32_t r = 0; r < M.d; ++r) {
                 const uint64_t *a = sa + r * 6, *b = sb + r * 6;
-                const uint32_t ga = (uint32_t)hash_g61(a[4], a[5], xa), gb = (uint32_t)hash_g61(b[4], b[5], xb);
-                const int xia = xi_sign61(a, xa), xib = xi_sign61(b, xb);
+                uint32_t ga, gb;
+                int xia, xib;
+                if (narrow) {
+                    ga = (uint32_t)hash_g61_t<true>(a[4], a[5], xa);
+                    gb = (uint32_t)hash_g61_t<true>(b[4], b[5], xb);
+                    xia = xi_sign61_t<true>(a, xa);
+                    xib = xi_sign61_t<true>(b, xb);
+                } else {
+                    ga = (uint32_t)hash_g61_t<false>(a[4], a[5], xa);
+                    gb = (uint32_t)hash_g61_t<false>(b[4], b[5], xb);
+                    xia = xi_sign61_t<false>(a, xa);
+                    xib = xi_sign61_t<false>(b, xb);
+                }
                 if (la) atomicAdd(&sc[A.smem_off + r * A.cells + (ga & A.wmask0)], xia * ca);
                 if (lb) atomicAdd(&sc[B.smem_off + r * B.cells + (gb & B.wmask0)], xib * cb);
                 if (lm) {
@@ -802,9 +825,10 @@ __global__ void __launch_bounds__(512) k_hist_epilogue(const __grid_constant__ E
             const EpiTarget &tg = E.tgt[t];
             for (uint32_t r = 0; r < tg.d; ++r) {
                 const uint64_t *a = tg.seeds + r * 6;
-                const uint32_t cell = (uint32_t)(hash_g61(__ldg(a + 4), __ldg(a + 5), x) & tg.wmask);
+                // x < domain <= 2^22: the narrow (64x32) hash path
+                const uint32_t cell = (uint32_t)(hash_g61_t<true>(__ldg(a + 4), __ldg(a + 5), x) & tg.wmask);
                 uint64_t sa[4] = {__ldg(a), __ldg(a + 1), __ldg(a + 2), __ldg(a + 3)};
-                const int64_t v = (int64_t)xi_sign61(sa, x) * (int64_t)c;
+                const int64_t v = (int64_t)xi_sign61_t<true>(sa, x) * (int64_t)c;
                 if (tg.smem_off >= 0) atomicAdd(&esc[tg.smem_off + r * tg.cells + cell], (int32_t)v);
                 else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, v);
             }
