@@ -20,6 +20,7 @@
 //                             + sum_{|c_i|<|L|, |c_i|<=|R|} x_i c_i
 //                             + R * sum_{|R|<|c_i|<|L|} x_i.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -493,6 +494,53 @@ __global__ void k_root_reduce(const uint64_t *part, uint64_t *acc, int slots, in
     if (threadIdx.x == 0) acc[blockIdx.x] = mm_add(acc[blockIdx.x], t, m);
 }
 
+// ---------------------------------------------------------------- two-way estimate (A9)
+// E_r = sum_j A[r][j] * B[r][j] in exact int128:
+// |A[r][j] B[r][j]| <= N_A N_B < 2^126 for any pair of sketches built from < 2^63 tuples,
+// so the sum over a row never leaves int128 — no moduli, no bound check.  Both legs are
+// folded to the common width w inline (O5): A'[j] = sum_s A[j + s w].
+struct DotItem {
+    const int64_t *a, *b;
+    uint32_t wa, wb, w;
+};
+constexpr int kMaxDot = 64;
+struct DotItems { DotItem it[kMaxDot]; int n, d; };
+
+__device__ __forceinline__ void add128(uint64_t &lo, uint64_t &hi, uint64_t l2, uint64_t h2) {
+    const uint64_t t = lo + l2;
+    hi += h2 + (t < lo);
+    lo = t;
+}
+
+// one CTA per (item, row): out[(item*d + r)*2 + {0,1}] = {lo, hi} of the two's-complement sum
+__global__ void __launch_bounds__(512) k_dot128(const __grid_constant__ DotItems items, uint64_t *out) {
+    const int item = blockIdx.x / items.d, r = blockIdx.x % items.d;
+    const DotItem it = items.it[item];
+    const int64_t *A = it.a + uint64_t(r) * it.wa, *B = it.b + uint64_t(r) * it.wb;
+    uint64_t lo = 0, hi = 0;
+    for (uint32_t j = threadIdx.x; j < it.w; j += blockDim.x) {
+        int64_t x = 0, y = 0;
+        for (uint32_t s = j; s < it.wa; s += it.w) x += __ldg(reinterpret_cast<const long long *>(A) + s);
+        for (uint32_t s = j; s < it.wb; s += it.w) y += __ldg(reinterpret_cast<const long long *>(B) + s);
+        const __int128 p = (__int128)x * (__int128)y;
+        add128(lo, hi, (uint64_t)p, (uint64_t)((unsigned __int128)p >> 64));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+        add128(lo, hi, l2, h2);
+    }
+    __shared__ uint64_t slo[16], shi[16];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) { slo[wid] = lo; shi[wid] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t L = 0, H = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) add128(L, H, slo[i], shi[i]);
+        out[uint64_t(blockIdx.x) * 2] = L;
+        out[uint64_t(blockIdx.x) * 2 + 1] = H;
+    }
+}
+
 // ---------------------------------------------------------------- host big integers (Garner)
 struct UBig {
     std::vector<uint64_t> l;  // little-endian limbs
@@ -589,6 +637,15 @@ struct SBig {
     double to_double() const { const double v = mag.to_double(); return neg ? -v : v; }
     std::string to_dec() const { return (neg && !mag.zero() ? "-" : "") + mag.to_dec(); }
 };
+
+static SBig sbig_from_i128(uint64_t lo, uint64_t hi) {
+    SBig v;
+    unsigned __int128 u = ((unsigned __int128)hi << 64) | lo;
+    if ((int64_t)hi < 0) { v.neg = true; u = ~u + 1; }
+    v.mag.l = {(uint64_t)u, (uint64_t)(u >> 64)};
+    v.mag.norm();
+    return v;
+}
 
 static uint64_t host_mulmod(uint64_t x, uint64_t y, uint64_t m) { return (uint64_t)((unsigned __int128)x * y % m); }
 static uint64_t host_powmod(uint64_t b, uint64_t e, uint64_t m) {
@@ -1034,11 +1091,82 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
 // Evaluate a batch of sub-plans: all kernels enqueued, one device->host copy, one sync.
 // The moduli come from the survivor bound (a sketch row built from N tuples has
 // ||row||_1 <= N); the device-measured L1 norms verify it, else the plan is redone.
+static bool is_two_way(const Plan &P) { return P.T.size() == 2 && P.T[0].kind == KV && P.T[1].kind == KV; }
+
+// all two-way plans of a batch: one k_dot128 launch per kMaxDot plans, one copy, one sync
+static sk_status run_two_way(std::vector<Plan> &plans, const std::vector<size_t> &idx,
+                             std::vector<std::vector<SBig>> &rows, cudaStream_t stream) {
+    if (idx.empty()) return SK_OK;
+    int d = plans[idx[0]].d;
+    for (size_t i : idx) d = std::max(d, plans[i].d);
+    DevPool pool;
+    void *dout;
+    sk_status st;
+    if ((st = dalloc(pool, idx.size() * d * 16, stream, &dout))) return st;
+    uint64_t *out = (uint64_t *)dout;
+    for (size_t b0 = 0; b0 < idx.size();) {
+        // one launch per run of plans with equal d (grid = items x d)
+        DotItems items;
+        items.n = 0;
+        items.d = plans[idx[b0]].d;
+        size_t b1 = b0;
+        while (b1 < idx.size() && items.n < kMaxDot && plans[idx[b1]].d == items.d) {
+            const Plan &P = plans[idx[b1]];
+            const sk_sketch *a = P.T[0].sk[0], *b = P.T[1].sk[0];
+            items.it[items.n++] = {a->counters, b->counters, a->w[0], b->w[0], (uint32_t)P.width[0]};
+            ++b1;
+        }
+        k_dot128<<<items.n * items.d, 512, 0, stream>>>(items, out + b0 * d * 2); count_launch();
+        SKB_CUDA_CHECK("k_dot128 launch");
+        b0 = b1;
+    }
+    std::vector<uint64_t> host(idx.size() * d * 2);
+    SKB_CUDA(cudaMemcpyAsync(host.data(), out, host.size() * 8, cudaMemcpyDeviceToHost, stream));
+    SKB_CUDA(cudaStreamSynchronize(stream));
+    // items of one launch are laid out [item][d_launch][2] from the launch's base b0 * d * 2
+    for (size_t b0 = 0; b0 < idx.size();) {
+        const int dl = plans[idx[b0]].d;
+        size_t b1 = b0;
+        while (b1 < idx.size() && b1 - b0 < (size_t)kMaxDot && plans[idx[b1]].d == dl) ++b1;
+        for (size_t j = b0; j < b1; ++j) {
+            auto &rr = rows[idx[j]];
+            rr.clear();
+            const uint64_t *h = host.data() + b0 * d * 2 + (j - b0) * dl * 2;
+            for (int r = 0; r < dl; ++r) rr.push_back(sbig_from_i128(h[2 * r], h[2 * r + 1]));
+        }
+        b0 = b1;
+    }
+    return SK_OK;
+}
+
 static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vector<std::vector<SBig>> &rows,
                            cudaStream_t stream) {
     const size_t n = plans.size();
     rows.assign(n, {});
     if (!n) return SK_OK;
+    // two-way sub-plans: exact int128 dot products; everything else: the CRT engine below
+    {
+        std::vector<size_t> tw;
+        std::vector<Plan> rest;
+        std::vector<size_t> rest_idx;
+        for (size_t i = 0; i < n; ++i) {
+            if (is_two_way(plans[i]) && !getenv("COMPASS_EST_CRT_ONLY")) tw.push_back(i);
+            else rest_idx.push_back(i);
+        }
+        if (!tw.empty()) {
+            sk_status st = run_two_way(plans, tw, rows, stream);
+            if (st) return st;
+            if (rest_idx.empty()) return SK_OK;
+            for (size_t i : rest_idx) rest.push_back(std::move(plans[i]));
+            std::vector<std::vector<SBig>> rrows;
+            st = run_batch(g, rest, rrows, stream);
+            for (size_t j = 0; j < rest_idx.size(); ++j) {
+                plans[rest_idx[j]] = std::move(rest[j]);
+                rows[rest_idx[j]] = std::move(rrows[j]);
+            }
+            return st;
+        }
+    }
     std::vector<Mods> mds(n);
     std::vector<std::vector<const sk_sketch *>> uniqs(n);
     std::vector<size_t> off_acc(n), off_l1(n);
