@@ -483,6 +483,57 @@ __global__ void __launch_bounds__(256) k_node_mat_gemm(const __grid_constant__ N
     }
 }
 
+// Matrix node with one child leg and one parent leg, one conditioned bucket (chains, PAPER.md
+// :222-225): out[k][r][o] = sum_i x[k][r][i] * M(i, o) mod m_k for every modulus k in one pass
+// over the matrix (each element is reduced once per modulus; the int64 matrix is read once per
+// group of 8 moduli).  Block = 32 outputs (lanes) x 8 slices of the child index (warps); the
+// slices' partial sums are combined in shared memory.  Residues < 2^26: products < 2^52, so up
+// to 4096 of them accumulate exactly in 64 bits between reductions.
+constexpr int MV_OUT = 32, MV_SL = 8, MV_G = 8;
+__global__ void __launch_bounds__(256) k_node_matvec(const __grid_constant__ Node n, const __grid_constant__ Mods md, int qc) {
+    __shared__ uint64_t part[MV_SL][MV_G][MV_OUT];
+    const int r = blockIdx.x;
+    const int qp = 1 - qc;
+    const int wi = n.w[qc], wo = n.w[qp];
+    const int lane = threadIdx.x & 31, sl = threadIdx.x >> 5;
+    const int o = blockIdx.y * MV_OUT + lane;
+    const int64_t *T = n.data[0] + uint64_t(r) * n.w[0] * n.w[1];
+    const int chunk = (wi + MV_SL - 1) / MV_SL;
+    const int i0 = sl * chunk, i1 = min(wi, i0 + chunk);
+    for (int g0 = 0; g0 < md.K; g0 += MV_G) {
+        const int ng = min(MV_G, md.K - g0);
+        uint64_t acc[MV_G];
+#pragma unroll
+        for (int g = 0; g < MV_G; ++g) acc[g] = 0;
+        if (o < wo) {
+            for (int i = i0; i < i1; ++i) {
+                const int64_t v = qc == 0 ? T[uint64_t(i) * wo + o] : T[uint64_t(o) * wi + i];
+                const uint64_t av = uabs(v);
+#pragma unroll
+                for (int g = 0; g < MV_G; ++g) {
+                    if (g >= ng) break;
+                    const int k = g0 + g;
+                    uint64_t rv = mm_red(av, md.m[k], md.mu[k]);
+                    if (v < 0 && rv) rv = md.m[k] - rv;
+                    acc[g] += rv * __ldg(reinterpret_cast<const unsigned long long *>(msg_row(n, qc, k, r, 0, 0)) + i);
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < MV_G; ++g) part[sl][g][lane] = g < ng ? mm_red(acc[g], md.m[g0 + g], md.mu[g0 + g]) : 0;
+        __syncthreads();
+        // warp sl finishes modulus g = sl of this group for the block's 32 outputs
+        if (sl < ng && o < wo) {
+            const int k = g0 + sl;
+            uint64_t t = 0;
+            for (int s2 = 0; s2 < MV_SL; ++s2) t = mm_add(t, part[s2][sl][lane], md.m[k]);
+            const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
+            n.out[(uint64_t(k) * n.d + r) * n.out_bm * wo + oo] = t;
+        }
+        __syncthreads();
+    }
+}
+
 // acc[k][r] += sum over slots of part[k][r][slot]
 __global__ void k_root_reduce(const uint64_t *part, uint64_t *acc, int slots, int d, const __grid_constant__ Mods md) {
     __shared__ uint64_t red[32];
@@ -1059,7 +1110,9 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                 if (n.role[q] == RCHILD) { ++nchild; qchild = q; }
                 if (n.role[q] == RFIXED) hasfixed = true;
             }
-            if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB >= 16) {
+            if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB == 1 && !getenv("COMPASS_EST_NO_MATVEC")) {
+                k_node_matvec<<<dim3(d, (P.width[pe] + MV_OUT - 1) / MV_OUT), 256, 0, stream>>>(n, md, qchild); count_launch();
+            } else if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB >= 16) {
                 const int nbt = (nB + GBM - 1) / GBM;
                 const int njt = (P.width[pe] + GBN - 1) / GBN;
                 k_node_mat_gemm<<<dim3(K * d, nbt * njt), 256, 0, stream>>>(n, md, qchild); count_launch();
