@@ -299,125 +299,6 @@ __device__ __forceinline__ uint64_t o9_value(const uint64_t *P1, const uint64_t 
     return V;
 }
 
-__global__ void k_node_merged(const __grid_constant__ Node n, const __grid_constant__ Mods md) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    __shared__ uint64_t red[32];
-    __shared__ uint64_t tot1[256], tot2[256];
-    const int B = n.B;
-    const int bb = blockIdx.x % B;
-    const int r = blockIdx.x / B;
-    const int64_t b = n.b0 + bb;
-    const int qc = n.qc;
-    const int wq = n.w[qc];
-    uint64_t *P1 = reinterpret_cast<uint64_t *>(sm);
-    uint64_t *P2 = P1 + (wq + 1);
-    uint64_t *S = P2 + (wq + 1);
-    uint32_t *pos = reinterpret_cast<uint32_t *>(S + wq);     // per outer index: nless | nle << 16
-    const int64_t *cs = n.csorted + uint64_t(r) * wq;
-    int qp = -1, qf = -1, oc[2] = {-1, -1}, noc = 0;
-    for (int q = 0; q < n.nl; ++q) {
-        if (q == qc) continue;
-        if (n.role[q] == RPARENT) qp = q;
-        else if (n.role[q] == RFIXED) qf = q;
-        else oc[noc++] = q;  // other child legs
-    }
-    // outer leg: the parent if any, else the first other child; inner: the remaining other child
-    const int qo = qp >= 0 ? qp : oc[0];
-    const int qi = qp >= 0 ? oc[0] : oc[1];
-    const int wo = qo >= 0 ? n.w[qo] : 1;
-    const int wi = qi >= 0 ? n.w[qi] : 1;
-    const int per_tile = (wo + n.tiles - 1) / n.tiles;
-    const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
-    for (int s = threadIdx.x; s < wq; s += blockDim.x) S[s] = n.sabs[uint64_t(r) * wq + s];
-    __syncthreads();
-    // --- threshold positions per outer index (modulus-independent), when there is no inner leg
-    const bool cache_pos = qi < 0;
-    if (cache_pos) {
-        for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
-            bool hasL, hasR;
-            int64_t L, R;
-            merged_LR(n, r, qc, qf, qo, qi, b, o, 0, hasL, L, hasR, R);
-            const int nless = hasL ? count_lt(S, wq, uabs(L)) : 0;
-            const int nle = hasR ? count_le(S, wq, uabs(R)) : 0;
-            pos[o - o_begin] = (uint32_t)nless | ((uint32_t)nle << 16);
-        }
-    }
-    const int nt = blockDim.x;
-    const int chunk = (wq + nt - 1) / nt;
-    const int s0 = threadIdx.x * chunk, s1 = min(wq, s0 + chunk);
-    for (int k = 0; k < md.K; ++k) {
-        const uint64_t mu = md.mu[k];
-        const uint64_t m = md.m[k];
-        const uint64_t *x = msg_row(n, qc, k, r, bb, 0);
-        // --- prefix sums over the |c|-sorted order (block scan, contiguous chunks per thread)
-        uint64_t l1 = 0, l2 = 0;
-        for (int s = s0; s < s1; ++s) {      // x arrives in the |c|-sorted order (out_perm of the child)
-            const uint64_t xv = x[s];
-            l1 = mm_add(l1, xv, m);
-            l2 = mm_add(l2, mm_mul(xv, mm_i64(cs[s], m, mu), m, mu), m);
-        }
-        __syncthreads();   // previous modulus finished reading P1/P2
-        tot1[threadIdx.x] = l1;
-        tot2[threadIdx.x] = l2;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint64_t c1 = 0, c2 = 0;
-            for (int t = 0; t < nt; ++t) {
-                const uint64_t v1 = tot1[t], v2 = tot2[t];
-                tot1[t] = c1; tot2[t] = c2;
-                c1 = mm_add(c1, v1, m); c2 = mm_add(c2, v2, m);
-            }
-            P1[wq] = c1; P2[wq] = c2;
-        }
-        __syncthreads();
-        {
-            uint64_t c1 = tot1[threadIdx.x], c2 = tot2[threadIdx.x];
-            for (int s = s0; s < s1; ++s) {
-                P1[s] = c1; P2[s] = c2;
-                const uint64_t xv = x[s];
-                c1 = mm_add(c1, xv, m);
-                c2 = mm_add(c2, mm_mul(xv, mm_i64(cs[s], m, mu), m, mu), m);
-            }
-        }
-        __syncthreads();
-        // --- outputs
-        const uint64_t *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row(n, qo, k, r, bb, 0) : nullptr;
-        const uint64_t *xi2 = qi >= 0 ? msg_row(n, qi, k, r, bb, 0) : nullptr;
-        uint64_t acc = 0;
-        for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
-            uint64_t sacc = 0;
-            for (int i = 0; i < wi; ++i) {
-                bool hasL, hasR;
-                int64_t L, R;
-                merged_LR(n, r, qc, qf, qo, qi, b, o, i, hasL, L, hasR, R);
-                int nless, nle;
-                if (cache_pos) {
-                    const uint32_t pv = pos[o - o_begin];
-                    nless = (int)(pv & 0xffffu);
-                    nle = (int)(pv >> 16);
-                } else {
-                    nless = hasL ? count_lt(S, wq, uabs(L)) : 0;
-                    nle = hasR ? count_le(S, wq, uabs(R)) : 0;
-                }
-                uint64_t V = o9_value(P1, P2, wq, hasL, L, hasR, R, nless, nle, m, mu);
-                if (xi2) V = mm_mul(V, xi2[i], m, mu);
-                sacc = mm_add(sacc, V, m);
-            }
-            if (qp >= 0) {
-                const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
-                n.out[((uint64_t(k) * n.d + r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = sacc;
-            } else {
-                if (xo) sacc = mm_mul(sacc, xo[o], m, mu);
-                acc = mm_add(acc, sacc, m);
-            }
-        }
-        if (qp < 0) {
-            const uint64_t t = block_sum_mod(acc, m, red);
-            if (threadIdx.x == 0) n.out[((uint64_t(k) * n.d + r) * B + bb) * n.tiles + blockIdx.y] = t;
-        }
-    }
-}
-
 // Matrix node with one child leg and one parent leg, batched over the conditioned bucket:
 // out[b][j] = sum_i x[b][i] * M(i, j) mod m — a modular GEMM.  Residues are < 2^26, so
 // products (< 2^52) accumulate exactly in 64 bits (IMAD.WIDE.U32) for 4096 steps between
@@ -534,10 +415,381 @@ __global__ void __launch_bounds__(256) k_node_matvec(const __grid_constant__ Nod
     }
 }
 
+// ---------------------------------------------------------------- exact int128 engine
+// When the rigorous bound prod_t ||T_t||_1 is <= 2^125, every message,
+// prefix sum and partial sum of a sub-plan without matrices is a signed sum of a subset of
+// the expansion's terms, so it fits int128: the contraction runs once in exact int128
+// arithmetic instead of once per CRT modulus.  Same node model and layouts as the modular
+// kernels with K = 1 and 16-byte entries.
+typedef __int128 i128;
+
+__device__ __forceinline__ i128 shfl_xor_i128(i128 v, int o) {
+    const uint64_t lo = __shfl_xor_sync(0xffffffffu, (uint64_t)v, o);
+    const uint64_t hi = __shfl_xor_sync(0xffffffffu, (uint64_t)((unsigned __int128)v >> 64), o);
+    return (i128)(((unsigned __int128)hi << 64) | lo);
+}
+__device__ __forceinline__ i128 shfl_up_i128(i128 v, int o) {
+    const uint64_t lo = __shfl_up_sync(0xffffffffu, (uint64_t)v, o);
+    const uint64_t hi = __shfl_up_sync(0xffffffffu, (uint64_t)((unsigned __int128)v >> 64), o);
+    return (i128)(((unsigned __int128)hi << 64) | lo);
+}
+__device__ __forceinline__ i128 block_sum_i128(i128 v, i128 *red) {
+    for (int o = 16; o > 0; o >>= 1) v += shfl_xor_i128(v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    i128 t = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    return t;
+}
+__device__ __forceinline__ const i128 *msg_row_x(const Node &n, int q, int r, int bb) {
+    const int bm = n.bm[q];
+    return reinterpret_cast<const i128 *>(n.msg[q]) + (uint64_t(r) * bm + (bm > 1 ? bb : 0)) * (uint64_t)n.w[q];
+}
+
+// VEC / MAT node or merged leaf, exact.  blockIdx.x = r*B + bb, blockIdx.y = tile.
+__global__ void k_node_dense_x(const __grid_constant__ Node n) {
+    __shared__ i128 red[32];
+    const int B = n.B;
+    const int bb = blockIdx.x % B;
+    const int r = blockIdx.x / B;
+    const int64_t b = n.b0 + bb;
+    int qp = -1, qf = -1, qc0 = -1, qc1 = -1;
+    for (int q = 0; q < n.nl; ++q) {
+        if (n.role[q] == RPARENT) qp = q;
+        else if (n.role[q] == RFIXED) qf = q;
+        else if (qc0 < 0) qc0 = q;
+        else qc1 = q;
+    }
+    const int qo = qp >= 0 ? qp : qc0;
+    const int qi = qp >= 0 ? qc0 : qc1;
+    const int wo = qo >= 0 ? n.w[qo] : 1;
+    const int wi = qi >= 0 ? n.w[qi] : 1;
+    const i128 *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row_x(n, qo, r, bb) : nullptr;
+    const i128 *xi = (qi >= 0) ? msg_row_x(n, qi, r, bb) : nullptr;
+    i128 acc = 0;
+    const int per_tile = (wo + n.tiles - 1) / n.tiles;
+    const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
+    for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
+        i128 s = 0;
+        for (int i = 0; i < wi; ++i) {
+            int64_t idx[3] = {0, 0, 0};
+            if (qo >= 0) idx[qo] = o;
+            if (qi >= 0) idx[qi] = i;
+            if (qf >= 0) idx[qf] = b;
+            i128 term = (i128)tensor_val(n, r, idx);
+            if (xi) term *= xi[i];
+            s += term;
+        }
+        if (qp >= 0) {
+            const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
+            reinterpret_cast<i128 *>(n.out)[(uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = s;
+        } else {
+            if (xo) s *= xo[o];
+            acc += s;
+        }
+    }
+    if (qp < 0) {
+        const i128 t = block_sum_i128(acc, red);
+        if (threadIdx.x == 0) reinterpret_cast<i128 *>(n.out)[(uint64_t(r) * B + bb) * n.tiles + blockIdx.y] = t;
+    }
+}
+
+// per (row, outer index) threshold positions of a merged node whose contracted leg's
+// thresholds depend on the outer index only (no fixed leg, no inner leg): computed once and
+// shared by every conditioned bucket and every modulus.  pos = nless | nle << 16.
+__global__ void k_merged_pos(const __grid_constant__ Node n, int qo, uint32_t *pos) {
+    const int r = blockIdx.y;
+    const int wo = n.w[qo], wq = n.w[n.qc];
+    const uint64_t *S = n.sabs + uint64_t(r) * wq;
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < wo; o += gridDim.x * blockDim.x) {
+        bool hasL, hasR;
+        int64_t L, R;
+        merged_LR(n, r, n.qc, -1, qo, -1, 0, o, 0, hasL, L, hasR, R);
+        const int nless = hasL ? count_lt(S, wq, uabs(L)) : 0;
+        const int nle = hasR ? count_le(S, wq, uabs(R)) : 0;
+        pos[uint64_t(r) * wo + o] = (uint32_t)nless | ((uint32_t)nle << 16);
+    }
+}
+
+__device__ __forceinline__ i128 o9_value_x(const i128 *P1, const i128 *P2, int wq, bool hasL, int64_t L, bool hasR,
+                                           int64_t R, int nless, int nle) {
+    i128 V;
+    if (hasL) {
+        const int64_t win = (hasR && !(uabs(L) <= uabs(R))) ? R : L;
+        V = (i128)win * (P1[wq] - P1[nless]);
+        int endB = nless;
+        if (hasR && nle < endB) {
+            V += (i128)R * (P1[endB] - P1[nle]);
+            endB = nle;
+        }
+        V += P2[endB];
+    } else {
+        V = (i128)R * (P1[wq] - P1[nle]) + P2[nle];
+    }
+    return V;
+}
+
+// merged node, exact: prefix sums P1 (x) and P2 (x*c) over the |c|-sorted contracted leg in
+// shared memory (block scan), then O(1) per output.  pos_pre: precomputed
+// thresholds (k_merged_pos) or null (binary searches over the sorted |c| in global memory).
+constexpr int MX_T = 512;
+__global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ Node n, const uint32_t *pos_pre) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ i128 red[32];
+    __shared__ i128 tot1[MX_T], tot2[MX_T];
+    const int B = n.B;
+    const int bb = blockIdx.x % B;
+    const int r = blockIdx.x / B;
+    const int64_t b = n.b0 + bb;
+    const int qc = n.qc;
+    const int wq = n.w[qc];
+    i128 *P1 = reinterpret_cast<i128 *>(sm);
+    i128 *P2 = P1 + (wq + 1);
+    const int64_t *cs = n.csorted + uint64_t(r) * wq;
+    const uint64_t *S = n.sabs + uint64_t(r) * wq;
+    int qp = -1, qf = -1, oc[2] = {-1, -1}, noc = 0;
+    for (int q = 0; q < n.nl; ++q) {
+        if (q == qc) continue;
+        if (n.role[q] == RPARENT) qp = q;
+        else if (n.role[q] == RFIXED) qf = q;
+        else oc[noc++] = q;
+    }
+    const int qo = qp >= 0 ? qp : oc[0];
+    const int qi = qp >= 0 ? oc[0] : oc[1];
+    const int wo = qo >= 0 ? n.w[qo] : 1;
+    const int wi = qi >= 0 ? n.w[qi] : 1;
+    const int per_tile = (wo + n.tiles - 1) / n.tiles;
+    const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
+    // --- prefix sums over the |c|-sorted order: contiguous chunk per thread, then a scan of
+    //     the per-thread totals by warp 0
+    const i128 *x = msg_row_x(n, qc, r, bb);   // delivered in the |c|-sorted order
+    const int chunk = (wq + MX_T - 1) / MX_T;
+    const int s0 = threadIdx.x * chunk, s1 = min(wq, s0 + chunk);
+    i128 l1 = 0, l2 = 0;
+    for (int s = s0; s < s1; ++s) {
+        const i128 xv = x[s];
+        l1 += xv;
+        l2 += xv * (i128)cs[s];
+    }
+    tot1[threadIdx.x] = l1;
+    tot2[threadIdx.x] = l2;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        constexpr int per = MX_T / 32;
+        const int lane = threadIdx.x;
+        i128 a1 = 0, a2 = 0;
+        for (int t = 0; t < per; ++t) { a1 += tot1[lane * per + t]; a2 += tot2[lane * per + t]; }
+        i128 i1 = a1, i2 = a2;   // inclusive warp scan
+        for (int o = 1; o < 32; o <<= 1) {
+            const i128 u1 = shfl_up_i128(i1, o), u2 = shfl_up_i128(i2, o);
+            if (lane >= o) { i1 += u1; i2 += u2; }
+        }
+        i128 e1 = i1 - a1, e2 = i2 - a2;   // exclusive
+        for (int t = 0; t < per; ++t) {
+            const i128 v1 = tot1[lane * per + t], v2 = tot2[lane * per + t];
+            tot1[lane * per + t] = e1;
+            tot2[lane * per + t] = e2;
+            e1 += v1;
+            e2 += v2;
+        }
+        if (lane == 31) { P1[wq] = i1; P2[wq] = i2; }
+    }
+    __syncthreads();
+    {
+        i128 c1 = tot1[threadIdx.x], c2 = tot2[threadIdx.x];
+        for (int s = s0; s < s1; ++s) {
+            P1[s] = c1;
+            P2[s] = c2;
+            const i128 xv = x[s];
+            c1 += xv;
+            c2 += xv * (i128)cs[s];
+        }
+    }
+    __syncthreads();
+    // --- outputs
+    const i128 *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row_x(n, qo, r, bb) : nullptr;
+    const i128 *xi2 = qi >= 0 ? msg_row_x(n, qi, r, bb) : nullptr;
+    i128 acc = 0;
+    for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
+        i128 sacc = 0;
+        for (int i = 0; i < wi; ++i) {
+            bool hasL, hasR;
+            int64_t L, R;
+            merged_LR(n, r, qc, qf, qo, qi, b, o, i, hasL, L, hasR, R);
+            int nless, nle;
+            if (pos_pre) {
+                const uint32_t pv = pos_pre[uint64_t(r) * wo + o];
+                nless = (int)(pv & 0xffffu);
+                nle = (int)(pv >> 16);
+            } else {
+                nless = hasL ? count_lt(S, wq, uabs(L)) : 0;
+                nle = hasR ? count_le(S, wq, uabs(R)) : 0;
+            }
+            i128 V = o9_value_x(P1, P2, wq, hasL, L, hasR, R, nless, nle);
+            if (xi2) V *= xi2[i];
+            sacc += V;
+        }
+        if (qp >= 0) {
+            const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
+            reinterpret_cast<i128 *>(n.out)[(uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = sacc;
+        } else {
+            if (xo) sacc *= xo[o];
+            acc += sacc;
+        }
+    }
+    if (qp < 0) {
+        const i128 t = block_sum_i128(acc, red);
+        if (threadIdx.x == 0) reinterpret_cast<i128 *>(n.out)[(uint64_t(r) * B + bb) * n.tiles + blockIdx.y] = t;
+    }
+}
+
+// merged node, modular (CRT engine): the same structure as k_node_merged_x — thresholds once
+// per block (or precomputed per node), then per modulus a block scan (warp 0 scans the
+// per-thread totals with shuffles) and O(1) work per output.
+__device__ __forceinline__ uint64_t shfl_up_mod_scan(uint64_t v, int lane, uint64_t m) {
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v = mm_add(v, u, m);
+    }
+    return v;
+}
+__global__ void __launch_bounds__(MX_T) k_node_merged_m(const __grid_constant__ Node n, const __grid_constant__ Mods md,
+                                                        const uint32_t *pos_pre) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ uint64_t red[32];
+    __shared__ uint64_t tot1[MX_T], tot2[MX_T];
+    const int B = n.B;
+    const int bb = blockIdx.x % B;
+    const int r = blockIdx.x / B;
+    const int64_t b = n.b0 + bb;
+    const int qc = n.qc;
+    const int wq = n.w[qc];
+    uint64_t *P1 = reinterpret_cast<uint64_t *>(sm);
+    uint64_t *P2 = P1 + (wq + 1);
+    uint32_t *pos = reinterpret_cast<uint32_t *>(P2 + (wq + 1));   // per outer index of this tile (no inner leg)
+    const int64_t *cs = n.csorted + uint64_t(r) * wq;
+    const uint64_t *S = n.sabs + uint64_t(r) * wq;
+    int qp = -1, qf = -1, oc[2] = {-1, -1}, noc = 0;
+    for (int q = 0; q < n.nl; ++q) {
+        if (q == qc) continue;
+        if (n.role[q] == RPARENT) qp = q;
+        else if (n.role[q] == RFIXED) qf = q;
+        else oc[noc++] = q;
+    }
+    const int qo = qp >= 0 ? qp : oc[0];
+    const int qi = qp >= 0 ? oc[0] : oc[1];
+    const int wo = qo >= 0 ? n.w[qo] : 1;
+    const int wi = qi >= 0 ? n.w[qi] : 1;
+    const int per_tile = (wo + n.tiles - 1) / n.tiles;
+    const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
+    const bool cache_pos = qi < 0;
+    if (cache_pos) {
+        for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
+            if (pos_pre) { pos[o - o_begin] = pos_pre[uint64_t(r) * wo + o]; continue; }
+            bool hasL, hasR;
+            int64_t L, R;
+            merged_LR(n, r, qc, qf, qo, qi, b, o, 0, hasL, L, hasR, R);
+            const int nless = hasL ? count_lt(S, wq, uabs(L)) : 0;
+            const int nle = hasR ? count_le(S, wq, uabs(R)) : 0;
+            pos[o - o_begin] = (uint32_t)nless | ((uint32_t)nle << 16);
+        }
+    }
+    const int chunk = (wq + MX_T - 1) / MX_T;
+    const int s0 = threadIdx.x * chunk, s1 = min(wq, s0 + chunk);
+    const int lane = threadIdx.x & 31;
+    for (int k = 0; k < md.K; ++k) {
+        const uint64_t m = md.m[k], mu = md.mu[k];
+        const uint64_t *x = msg_row(n, qc, k, r, bb, 0);   // |c|-sorted order
+        uint64_t l1 = 0, l2 = 0;
+        for (int s = s0; s < s1; ++s) {
+            const uint64_t xv = x[s];
+            l1 += xv;                                   // < chunk * 2^26: reduced once below
+            l2 = mm_add(l2, mm_mul(xv, mm_i64(cs[s], m, mu), m, mu), m);
+        }
+        __syncthreads();   // previous modulus finished with P1/P2/tot
+        tot1[threadIdx.x] = mm_red(l1, m, mu);
+        tot2[threadIdx.x] = l2;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            constexpr int per = MX_T / 32;
+            uint64_t a1 = 0, a2 = 0;
+            for (int t = 0; t < per; ++t) { a1 = mm_add(a1, tot1[lane * per + t], m); a2 = mm_add(a2, tot2[lane * per + t], m); }
+            const uint64_t i1 = shfl_up_mod_scan(a1, lane, m), i2 = shfl_up_mod_scan(a2, lane, m);
+            uint64_t e1 = mm_sub(i1, a1, m), e2 = mm_sub(i2, a2, m);
+            for (int t = 0; t < per; ++t) {
+                const uint64_t v1 = tot1[lane * per + t], v2 = tot2[lane * per + t];
+                tot1[lane * per + t] = e1;
+                tot2[lane * per + t] = e2;
+                e1 = mm_add(e1, v1, m);
+                e2 = mm_add(e2, v2, m);
+            }
+            if (lane == 31) { P1[wq] = i1; P2[wq] = i2; }
+        }
+        __syncthreads();
+        {
+            uint64_t c1 = tot1[threadIdx.x], c2 = tot2[threadIdx.x];
+            for (int s = s0; s < s1; ++s) {
+                P1[s] = c1;
+                P2[s] = c2;
+                const uint64_t xv = x[s];
+                c1 = mm_add(c1, xv, m);
+                c2 = mm_add(c2, mm_mul(xv, mm_i64(cs[s], m, mu), m, mu), m);
+            }
+        }
+        __syncthreads();
+        const uint64_t *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row(n, qo, k, r, bb, 0) : nullptr;
+        const uint64_t *xi2 = qi >= 0 ? msg_row(n, qi, k, r, bb, 0) : nullptr;
+        uint64_t acc = 0;
+        for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
+            uint64_t sacc = 0;
+            for (int i = 0; i < wi; ++i) {
+                bool hasL, hasR;
+                int64_t L, R;
+                merged_LR(n, r, qc, qf, qo, qi, b, o, i, hasL, L, hasR, R);
+                int nless, nle;
+                if (cache_pos) {
+                    const uint32_t pv = pos[o - o_begin];
+                    nless = (int)(pv & 0xffffu);
+                    nle = (int)(pv >> 16);
+                } else {
+                    nless = hasL ? count_lt(S, wq, uabs(L)) : 0;
+                    nle = hasR ? count_le(S, wq, uabs(R)) : 0;
+                }
+                uint64_t V = o9_value(P1, P2, wq, hasL, L, hasR, R, nless, nle, m, mu);
+                if (xi2) V = mm_mul(V, xi2[i], m, mu);
+                sacc = mm_add(sacc, V, m);
+            }
+            if (qp >= 0) {
+                const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
+                n.out[((uint64_t(k) * n.d + r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = sacc;
+            } else {
+                if (xo) sacc = mm_mul(sacc, xo[o], m, mu);
+                acc = mm_add(acc, sacc, m);
+            }
+        }
+        if (qp < 0) {
+            const uint64_t t = block_sum_mod(acc, m, red);
+            if (threadIdx.x == 0) n.out[((uint64_t(k) * n.d + r) * B + bb) * n.tiles + blockIdx.y] = t;
+        }
+    }
+}
+
+// acc[r] += sum over slots of part[r][slot], exact
+__global__ void k_root_reduce_x(const i128 *part, i128 *acc, int slots) {
+    __shared__ i128 red[32];
+    i128 s = 0;
+    for (int i = threadIdx.x; i < slots; i += blockDim.x) s += part[uint64_t(blockIdx.x) * slots + i];
+    const i128 t = block_sum_i128(s, red);
+    if (threadIdx.x == 0) acc[blockIdx.x] += t;
+}
+
 // acc[k][r] += sum over slots of part[k][r][slot]
 __global__ void k_root_reduce(const uint64_t *part, uint64_t *acc, int slots, int d, const __grid_constant__ Mods md) {
     __shared__ uint64_t red[32];
-    const int k = blockIdx.x / d, r = blockIdx.x % d;
+    const int k = blockIdx.x / d;
     const uint64_t m = md.m[k];
     uint64_t s = 0;
     for (int i = threadIdx.x; i < slots; i += blockDim.x) s = mm_add(s, part[uint64_t(blockIdx.x) * slots + i], m);
@@ -938,11 +1190,12 @@ static double log_bound(const Plan &P, F l1of) {
 // Enqueue every kernel of one sub-plan on `stream` (no host synchronisation): per-row
 // residues -> acc[K][d] (zeroed by the caller), per-sketch-row L1 norms -> l1[n_uniq][d].
 static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const sk_sketch *> &uniq,
-                              DevPool &pool, uint64_t *acc, unsigned long long *l1, cudaStream_t stream) {
+                              DevPool &pool, uint64_t *acc, unsigned long long *l1, cudaStream_t stream,
+                              bool exact = false) {
     const int E = (int)P.edges.size();
     const int NT = (int)P.T.size();
     const int d = P.d;
-    const int K = md.K;
+    const int K = exact ? 2 : md.K;   // 64-bit words per message entry and row (exact: one int128)
     sk_status st;
     // ---- L1 norms of every sketch involved (checked against the moduli after the batch)
     for (size_t b0 = 0; b0 < uniq.size(); b0 += kMaxL1Items) {
@@ -1016,6 +1269,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
     }
     // ---- sorted orders for merged nodes' contracted legs
     std::vector<int> qc_of(NT, -1);
+    std::vector<const uint32_t *> pos_of(NT, nullptr);   // exact merged nodes: precomputed thresholds
     std::vector<const int32_t *> ord_of(NT, nullptr);
     std::vector<const uint64_t *> sabs_of(NT, nullptr);
     std::vector<const int64_t *> csorted_of(NT, nullptr);
@@ -1110,7 +1364,48 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                 if (n.role[q] == RCHILD) { ++nchild; qchild = q; }
                 if (n.role[q] == RFIXED) hasfixed = true;
             }
-            if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB == 1 && !getenv("COMPASS_EST_NO_MATVEC")) {
+            if (exact) {
+                if (t.kind == KG && qc_of[i] >= 0) {
+                    n.qc = qc_of[i];
+                    n.ord = ord_of[i];
+                    n.sabs = sabs_of[i];
+                    n.csorted = csorted_of[i];
+                    // outer leg: the parent, else the first other child (as in the kernel)
+                    int wo_max = 1, qo = -1, nother = 0;
+                    bool fixed = false;
+                    for (int q = 0; q < n.nl; ++q) {
+                        if (q == n.qc) continue;
+                        if (n.role[q] == RFIXED) { fixed = true; continue; }
+                        wo_max = std::max(wo_max, n.w[q]);
+                        if (qo < 0) qo = q;
+                        ++nother;
+                    }
+                    for (int q = 0; q < n.nl; ++q) if (q != n.qc && n.role[q] == RPARENT) qo = q;
+                    const uint32_t *pos = nullptr;
+                    if (!fixed && nother == 1 && qo >= 0) {
+                        // thresholds depend on the outer index only: once per node
+                        if (!pos_of[i]) {
+                            void *pb;
+                            if ((st = dalloc(pool, size_t(d) * n.w[qo] * 4, stream, &pb))) return st;
+                            k_merged_pos<<<dim3((n.w[qo] + 255) / 256, d), 256, 0, stream>>>(n, qo, (uint32_t *)pb); count_launch();
+                            pos_of[i] = (const uint32_t *)pb;
+                        }
+                        pos = pos_of[i];
+                    }
+                    int mtiles = 1;
+                    while (d * nB * mtiles < 296 && mtiles * MX_T < wo_max) mtiles *= 2;
+                    n.tiles = (pe >= 0) ? mtiles : 1;
+                    const size_t sm = size_t(2) * (n.w[n.qc] + 1) * 16;
+                    if (sm + 2 * MX_T * 16 + 1024 > 227 * 1024) return fail(SK_EOVERFLOW, "estimate: merged contraction too wide");
+                    SKB_CUDA(cudaFuncSetAttribute(k_node_merged_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                    k_node_merged_x<<<dim3(d * nB, n.tiles), MX_T, sm, stream>>>(n, pos); count_launch();
+                } else {
+                    int xt = 1;
+                    if (pe >= 0) while (d * nB * xt < 592 && xt * 256 < P.width[pe]) xt *= 2;
+                    n.tiles = (pe >= 0) ? xt : 1;
+                    k_node_dense_x<<<dim3(d * nB, n.tiles), 256, 0, stream>>>(n); count_launch();
+                }
+            } else if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB == 1 && !getenv("COMPASS_EST_NO_MATVEC")) {
                 k_node_matvec<<<dim3(d, (P.width[pe] + MV_OUT - 1) / MV_OUT), 256, 0, stream>>>(n, md, qchild); count_launch();
             } else if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB >= 16) {
                 const int nbt = (nB + GBM - 1) / GBM;
@@ -1121,21 +1416,41 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                 n.ord = ord_of[i];
                 n.sabs = sabs_of[i];
                 n.csorted = csorted_of[i];
-                int wo_max = 1;
-                for (int q = 0; q < n.nl; ++q) if (q != n.qc && n.role[q] != RFIXED) wo_max = std::max(wo_max, n.w[q]);
+                int wo_max = 1, qo = -1, nother = 0;
+                bool fixed = false;
+                for (int q = 0; q < n.nl; ++q) {
+                    if (q == n.qc) continue;
+                    if (n.role[q] == RFIXED) { fixed = true; continue; }
+                    wo_max = std::max(wo_max, n.w[q]);
+                    if (qo < 0) qo = q;
+                    ++nother;
+                }
+                for (int q = 0; q < n.nl; ++q) if (q != n.qc && n.role[q] == RPARENT) qo = q;
+                const uint32_t *pos = nullptr;
+                if (!fixed && nother == 1 && qo >= 0) {
+                    if (!pos_of[i]) {
+                        void *pb;
+                        if ((st = dalloc(pool, size_t(d) * n.w[qo] * 4, stream, &pb))) return st;
+                        k_merged_pos<<<dim3((n.w[qo] + 255) / 256, d), 256, 0, stream>>>(n, qo, (uint32_t *)pb); count_launch();
+                        pos_of[i] = (const uint32_t *)pb;
+                    }
+                    pos = pos_of[i];
+                }
                 int mtiles = 1;
-                while (d * nB * mtiles < 296 && mtiles * 256 < wo_max) mtiles *= 2;
+                while (d * nB * mtiles < 296 && mtiles * MX_T < wo_max) mtiles *= 2;
                 n.tiles = (pe >= 0) ? mtiles : 1;
-                const size_t sm = (size_t(2) * (n.w[n.qc] + 1) + n.w[n.qc]) * 8 + size_t(wo_max) * 4 + 16;
-                if (sm > 227 * 1024) return fail(SK_EOVERFLOW, "estimate: merged contraction too wide");
-                SKB_CUDA(cudaFuncSetAttribute(k_node_merged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-                k_node_merged<<<dim3(d * nB, n.tiles), 256, sm, stream>>>(n, md); count_launch();
+                const int per_tile = (wo_max + n.tiles - 1) / n.tiles;
+                const size_t sm = size_t(2) * (n.w[n.qc] + 1) * 8 + size_t(per_tile) * 4 + 16;
+                if (sm + 2 * MX_T * 8 + 512 > 227 * 1024) return fail(SK_EOVERFLOW, "estimate: merged contraction too wide");
+                SKB_CUDA(cudaFuncSetAttribute(k_node_merged_m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                k_node_merged_m<<<dim3(d * nB, n.tiles), MX_T, sm, stream>>>(n, md, pos); count_launch();
             } else {
                 k_node_dense<<<dim3(blocks_xy, tiles), 256, 0, stream>>>(n, md); count_launch();
             }
             SKB_CUDA_CHECK("estimate launch 4");
         }
-        k_root_reduce<<<K * d, 256, 0, stream>>>((const uint64_t *)part, acc, B * tiles_root, d, md); count_launch();
+        if (exact) { k_root_reduce_x<<<d, 256, 0, stream>>>((const i128 *)part, (i128 *)acc, B * tiles_root); count_launch(); }
+        else { k_root_reduce<<<K * d, 256, 0, stream>>>((const uint64_t *)part, acc, B * tiles_root, d, md); count_launch(); }
         SKB_CUDA_CHECK("estimate launch 5");
     }
     return SK_OK;
@@ -1223,17 +1538,26 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
     std::vector<Mods> mds(n);
     std::vector<std::vector<const sk_sketch *>> uniqs(n);
     std::vector<size_t> off_acc(n), off_l1(n);
+    std::vector<char> exact(n, 0);
     size_t words = 0;
+    const bool crt_only = getenv("COMPASS_EST_CRT_ONLY") != nullptr;
     for (size_t i = 0; i < n; ++i) {
         Plan &P = plans[i];
-        for (auto &t : P.T)
+        bool has_mat = false;
+        for (auto &t : P.T) {
+            has_mat |= t.kind == KM;
             for (auto *s : t.sk)
                 if (std::find(uniqs[i].begin(), uniqs[i].end(), s) == uniqs[i].end()) uniqs[i].push_back(s);
+        }
         const double logB = log_bound(P, [&](const sk_sketch *) { return 0.0; }) +
                             [&] { double v = 0; for (int t : P.tabs) v += log2(std::max<double>(1.0, (double)g->survivors[t])); return v; }();
         mds[i] = mods_for(logB, 1);
+        // exact int128 contraction when the survivor bound fits (verified below with the
+        // device-measured L1 norms) and the sub-plan has no matrix node
+        exact[i] = !crt_only && !has_mat && logB <= 125.0;
+        if (exact[i]) words = (words + 1) & ~size_t(1);   // int128 accumulators: 16-byte aligned
         off_acc[i] = words;
-        words += size_t(mds[i].K) * P.d;
+        words += size_t(exact[i] ? 2 : mds[i].K) * P.d;
         off_l1[i] = words;
         words += uniqs[i].size() * P.d;
     }
@@ -1245,7 +1569,7 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
     uint64_t *res = (uint64_t *)dres;
     for (size_t i = 0; i < n; ++i)
         if ((st = enqueue_plan(plans[i], mds[i], uniqs[i], pool, res + off_acc[i], (unsigned long long *)(res + off_l1[i]),
-                               stream)))
+                               stream, exact[i])))
             return st;
     std::vector<uint64_t> host(words);
     SKB_CUDA(cudaMemcpyAsync(host.data(), res, words * 8, cudaMemcpyDeviceToHost, stream));
@@ -1260,7 +1584,11 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
             return (double)mx;
         };
         const double logB = log_bound(P, l1of);
-        if (logB + 3.0 > mods_capacity(mds[i])) {
+        if (exact[i] && logB <= 125.0) {
+            for (int r = 0; r < d; ++r) rows[i].push_back(sbig_from_i128(host[off_acc[i] + 2 * r], host[off_acc[i] + 2 * r + 1]));
+            continue;
+        }
+        if (exact[i] || logB + 3.0 > mods_capacity(mds[i])) {
             // the survivor bound did not hold for these sketches: redo with the measured bound
             Mods md = mods_for(logB, 1);
             if (mods_capacity(md) < logB + 3.0)

@@ -163,7 +163,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_all_but1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 // every committed group has landed (cp.async issued since the last commit are not covered)
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 // commits the current (possibly partial) group too: every cp.async issued so far has landed
@@ -175,12 +174,6 @@ __device__ __forceinline__ void red_add_u32(uint32_t *p, uint32_t v) {
 }
 __device__ __forceinline__ void red_add_s64(int64_t *p, int64_t v) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// ------------------------------------------------------------------ column access
-__device__ __forceinline__ int64_t gval(const SCol &c, uint64_t row) {
-    if (c.bytes == 8) return __ldg(reinterpret_cast<const long long *>(c.p) + row);
-    return (int64_t)__ldg(reinterpret_cast<const int *>(c.p) + row);
 }
 
 __device__ __forceinline__ bool in_set(const int64_t *s, uint32_t n, int64_t v) {

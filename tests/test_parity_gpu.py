@@ -239,8 +239,19 @@ TOPOS = [
 ]
 
 
+@pytest.fixture(params=["default", "crt"])
+def est_engine(request, monkeypatch):
+    """Estimates through the default engine (exact int128 contraction where the bound fits,
+    int128 dot products for two-way sub-plans) and through the CRT engine alone."""
+    if request.param == "crt":
+        monkeypatch.setenv("COMPASS_EST_CRT_ONLY", "1")
+    else:
+        monkeypatch.delenv("COMPASS_EST_CRT_ONLY", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("ti", range(len(TOPOS)))
-def test_estimates_equal_oracle_on_random_networks(ti):
+def test_estimates_equal_oracle_on_random_networks(ti, est_engine):
     rng = np.random.default_rng(300 + ti)
     for trial in range(3):
         og, jg, keep = _random_graph(rng, TOPOS[ti], w=8, d=3, vmax=[3, 1000, 2**40][trial])
@@ -288,7 +299,7 @@ def _check_counters(ws, run, og, surv):
         assert np.array_equal(sk.counters.cpu().numpy(), want), (s.table, s.edge_ids)
 
 
-def test_c1_end_to_end():
+def test_c1_end_to_end(est_engine):
     ws = datagen.c1()
     run, data_h, preds = _run_workload(ws)
     og, surv = _oracle_workload(ws, data_h, preds)
@@ -322,7 +333,7 @@ def test_c2_scaled_chain_parity():
     assert order == o_order and pre == o_pre and cost == o_cost
 
 
-def test_c3_scaled_parity_all_14_subplans_and_plan():
+def test_c3_scaled_parity_all_14_subplans_and_plan(est_engine):
     ws = datagen.c3(scale=0.005, w=256)
     run, data_h, preds = _run_workload(ws)
     og, surv = _oracle_workload(ws, data_h, preds)
@@ -341,7 +352,7 @@ def test_c5_scaled_parity_all_subplans_and_plan(cycle):
     assert tuple(jg.plan_greedy()) == tuple(oracle.plan_greedy(og))
 
 
-def test_c3_full_width_triangle_sampled_row():
+def test_c3_full_width_triangle_sampled_row(est_engine):
     """C3 at its full sketch shape (d=7, w=4096), rows scaled: the triangle and the
     5-table sub-plan, row 0 only (the oracle's cost is O(w^2 log w) big-int ops)."""
     ws = datagen.c3(scale=0.01)
