@@ -198,17 +198,20 @@ __device__ __forceinline__ uint64_t lds_v64(uint32_t a) {
     return v;
 }
 __device__ __forceinline__ bool hh_add(unsigned char *tab, uint32_t log2s, uint64_t x, int cnt) {
-    uint64_t *keys = reinterpret_cast<uint64_t *>(tab);
-    int *cnts = reinterpret_cast<int *>(tab + (8u << log2s));
+    // shared-window addresses and shared-space atomics (no generic-address conversion)
+    const uint32_t ka = smem_u32(tab), ca = ka + (8u << log2s);
     const uint64_t h = x * 0x9E3779B97F4A7C15ULL;
     const uint32_t mask = (1u << log2s) - 1u;
-    const uint32_t ka = smem_u32(keys);
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
         const uint32_t sl = (uint32_t)(h >> (c ? 24 : 44)) & mask;
         uint64_t k = lds_v64(ka + sl * 8);
-        if (k == kEmpty) k = atomicCAS(reinterpret_cast<unsigned long long *>(&keys[sl]), kEmpty, x);
-        if (k == x || k == kEmpty) { atomicAdd(&cnts[sl], cnt); return true; }
+        if (k == kEmpty)
+            asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(k) : "r"(ka + sl * 8), "l"(kEmpty), "l"(x) : "memory");
+        if (k == x || k == kEmpty) {
+            asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(ca + sl * 4), "r"(cnt) : "memory");
+            return true;
+        }
     }
     return false;
 }
@@ -472,9 +475,15 @@ __device__ __forceinline__ void cp_async_key(uint32_t dst, const void *src, uint
         : "memory");
 }
 template <int W>
-__device__ __forceinline__ void cp_async_fixed(uint32_t dst, const void *src) {
-    if (W == 8) asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-    else asm volatile("cp.async.ca.shared.global.L2::64B [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+__device__ __forceinline__ void cp_async_fixed_if(bool on, uint32_t dst, const void *src) {
+    if (W == 8)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+                     "@p cp.async.ca.shared.global.L2::64B [%0], [%1], 8;\n}" ::"r"(dst), "l"(src), "r"((int)on)
+                     : "memory");
+    else
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+                     "@p cp.async.ca.shared.global.L2::64B [%0], [%1], 4;\n}" ::"r"(dst), "l"(src), "r"((int)on)
+                     : "memory");
 }
 __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
@@ -632,11 +641,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                     for (int k = 0; k < NK; ++k)
                         kb[k] = reinterpret_cast<const unsigned char *>(kptr[k]) + (row0 + r0) * (uint64_t)(KW ? KW : 8);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        if (!m[j]) continue;
+                    for (int j = 0; j < 4; ++j) {   // predicated copies: no branches
                         const uint32_t dst = q_a + ((pb[j] + __popc(bj[j] & lt)) & (cap - 1)) * (NK * 8);
 #pragma unroll
-                        for (int k = 0; k < NK; ++k) cp_async_fixed<KW ? KW : 8>(dst + k * 8, kb[k] + j * (KW ? KW : 8));
+                        for (int k = 0; k < NK; ++k)
+                            cp_async_fixed_if<KW ? KW : 8>(m[j], dst + k * 8, kb[k] + j * (KW ? KW : 8));
                     }
                     tail += wtot;
                 } else {
