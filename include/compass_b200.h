@@ -208,6 +208,44 @@ SK_API sk_status estimate_subplans(const sk_graph *g, const uint64_t *masks, uin
  * ------------------------------------------------------------------------- */
 SK_API sk_status plan_greedy(const sk_graph *g, uint32_t *order, double *prefix_card, double *cost, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * plan_enumerate — Algorithm 1 of the paper ("Fast-AGMS Sketch
+ * Join Order Enumeration") with the search-space settings of PAPER.md:662:
+ *   sources: all vertices in increasing f(v) = alpha*card(v)/max card +
+ *     beta*deg(v)/max deg (line 7; card = exact survivors, deg = incident edges,
+ *     parallel edges counted; ties: lower index);
+ *   DFS Traversal(C, cost): cost += card(C) (lines 14-15); if cost > min_cost
+ *     return (early pruning, line 17; skipped when cfg->no_prune); if |C| = |V|:
+ *     keep C if cost < min_cost (strict, first found wins), p += 1, and stop the
+ *     current source when p = max_plans (lines 19-26); else visit the
+ *     neighbours v of C in increasing card(C + v) (ties: lower index, lines 29-35);
+ *   card(S) = survivors for |S| = 1, max(Est(S), 0) otherwise;
+ *     every estimate is computed once (cache; all connected sub-plans are estimated
+ *     in one batch when there are at most 512 of them).
+ *   mode SK_ENUM_GREEDY: plan_greedy's single-source rule (PAPER.md:662 greedy);
+ *   SK_ENUM_FULL_GREEDY: max_plans = 1 from every source; SK_ENUM_LIMIT: max_plans =
+ *   cfg->max_plans (paper default 10); SK_ENUM_EXHAUSTIVE: unbounded.
+ * order/prefix_card: host arrays [n_tables] (the chosen plan and its per-prefix
+ * cards); cost: host; stats: host or NULL.  Ties by index: table index order must
+ * match the alias order.  SK_EINVAL on a NULL/ill-formed graph or config.
+ * Synchronises `stream`.
+ * ------------------------------------------------------------------------- */
+typedef enum { SK_ENUM_GREEDY = 0, SK_ENUM_FULL_GREEDY = 1, SK_ENUM_LIMIT = 2, SK_ENUM_EXHAUSTIVE = 3 } sk_enum_mode;
+typedef struct {
+    double alpha, beta;     /* f(v) weights (paper default 0.5, 0.5) */
+    uint32_t mode;          /* sk_enum_mode */
+    uint32_t max_plans;     /* SK_ENUM_LIMIT: plans per source (>= 1) */
+    uint32_t no_prune;      /* 1: disable early pruning (line 17); for checks */
+} sk_enum_config;
+typedef struct {
+    uint64_t plans_completed;   /* complete plans reached (all sources) */
+    uint64_t prunes;            /* branches cut by early pruning */
+    uint64_t estimator_calls;   /* card() evaluations (cache hits included) */
+    uint64_t distinct_estimates;/* sub-plans estimated (cache size) */
+} sk_enum_stats;
+SK_API sk_status plan_enumerate(const sk_graph *g, const sk_enum_config *cfg, uint32_t *order, double *prefix_card,
+                                double *cost, sk_enum_stats *stats, void *stream);
+
 /* Thread-local description of the last error (never NULL). */
 SK_API const char *sk_last_error(void);
 

@@ -362,6 +362,102 @@ def plan_greedy(g: Graph, est_fn=None):
     return C, prefix, cost
 
 
+def plan_enumerate(g: Graph, mode="limit", max_plans=10, alpha=0.5, beta=0.5, prune=True, est_fn=None,
+                   card_fn=None):
+    """Algorithm 1 of the paper, literally, with the search-space
+    settings of PAPER.md:662 (greedy | full-greedy | limit | exhaustive).
+
+    card(S) = survivors for |S| = 1, max(Est, 0) otherwise (SPEC.md:210, 372);
+    card_fn(S) overrides card entirely (tests: any cardinality function).
+    Sources in increasing f(v) = alpha*card(v)/max card + beta*deg(v)/max deg (line 7),
+    ties by alias; DFS Traversal adds card(C) to cost (lines 14-15), returns when
+    cost > min_cost (line 17, unless prune=False), records a complete plan if
+    cost < min_cost (lines 20-23), counts it in p and stops the current source when
+    p = max_plans (lines 24-25, per source: p is reset at line 9), and
+    visits the neighbours of C in increasing card(C + v), ties by alias (lines 29-35).
+    Returns (order, prefix_cards, cost, stats)."""
+    if mode == "greedy":
+        order, pre, cost = plan_greedy(g, est_fn)
+        return order, pre, cost, {"plans_completed": 1}
+    cache = {}
+
+    def card(S):
+        key = tuple(sorted(S))
+        if key not in cache:
+            if card_fn is not None:
+                cache[key] = float(card_fn(key))
+            elif len(key) == 1:
+                cache[key] = float(g.tables[key[0]])
+            else:
+                e = est_fn(key) if est_fn else estimate(g, key)[0]
+                cache[key] = max(float(e), 0.0)
+        return cache[key]
+
+    names = sorted(g.tables)
+    adj = {a: set() for a in names}
+    deg = {a: 0 for a in names}
+    for _, u, v in g.edges:
+        adj[u].add(v)
+        adj[v].add(u)
+        deg[u] += 1
+        deg[v] += 1
+    maxc = max(float(g.tables[a]) for a in names)
+    maxd = max(deg.values())
+
+    def f(v):
+        return (alpha * float(g.tables[v]) / maxc if maxc > 0 else 0.0) + (beta * deg[v] / maxd if maxd > 0 else 0.0)
+
+    S = sorted(names, key=lambda v: (f(v), v))
+    limit = {"full-greedy": 1, "limit": max_plans, "exhaustive": None}[mode]
+    st = {"min_cost": float("inf"), "opt": None, "p": 0, "abort": False,
+          "plans_completed": 0, "prunes": 0}
+
+    def dfs(C, cost):
+        if st["abort"]:
+            return
+        cost = cost + card(C)                                   # lines 14-15
+        if prune and cost > st["min_cost"]:                     # line 17
+            st["prunes"] += 1
+            return
+        if len(C) == len(names):                                # lines 19-26
+            if cost < st["min_cost"]:
+                st["min_cost"], st["opt"] = cost, list(C)
+            st["plans_completed"] += 1
+            st["p"] += 1
+            if limit is not None and st["p"] == limit:
+                st["abort"] = True
+            return
+        L = sorted({b for a in C for b in adj[a]} - set(C))     # line 29
+        e = {v: card(C + [v]) for v in L}                       # lines 30-32
+        for v in sorted(L, key=lambda x: (e[x], x)):            # lines 33-35
+            if st["abort"]:
+                return
+            dfs(C + [v], cost)
+
+    for v in S:                                                 # lines 8-11
+        st["p"], st["abort"] = 0, False
+        dfs([v], 0.0)
+    order = st["opt"]
+    pre = [card(order[:i + 1]) for i in range(len(order))]
+    return order, pre, st["min_cost"], {"plans_completed": st["plans_completed"], "prunes": st["prunes"]}
+
+
+def leftdeep_costs_bruteforce(names, edges, card_fn):
+    """Every valid left-deep order (each prefix connected, no cross products) with its
+    cost sum_i card(prefix_i) — the exhaustive search space of PAPER.md:662."""
+    from itertools import permutations
+    adj = {a: set() for a in names}
+    for _, u, v in edges:
+        adj[u].add(v)
+        adj[v].add(u)
+    out = {}
+    for perm in permutations(names):
+        ok = all(any(p in adj[perm[i]] for p in perm[:i]) for i in range(1, len(perm)))
+        if ok:
+            out[perm] = sum(float(card_fn(tuple(sorted(perm[:i + 1])))) for i in range(len(perm)))
+    return out
+
+
 def permutation_l1(estimates, truths) -> int:
     """Normalised-L1 numerator: sum_i |S_i - C_i|, ranks by ascending
     value, ties by stable original index."""

@@ -65,7 +65,22 @@ class sk_graph(ctypes.Structure):
 # every symbol include/compass_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = ["sketch_create", "sketch_destroy", "sketch_counters", "sketch_zero", "sketch_update_filtered",
            "sketch_merge", "estimate_join", "estimate_join_exact", "estimate_subplans", "plan_greedy",
-           "sk_last_error", "sk_version", "sk_kernel_launches"]
+           "plan_enumerate", "sk_last_error", "sk_version", "sk_kernel_launches"]
+
+# Algorithm 1 search-space settings
+ENUM_GREEDY, ENUM_FULL_GREEDY, ENUM_LIMIT, ENUM_EXHAUSTIVE = range(4)
+ENUM_MODES = {"greedy": ENUM_GREEDY, "full-greedy": ENUM_FULL_GREEDY, "limit": ENUM_LIMIT,
+              "exhaustive": ENUM_EXHAUSTIVE}
+
+
+class sk_enum_config(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_double), ("beta", ctypes.c_double), ("mode", ctypes.c_uint32),
+                ("max_plans", ctypes.c_uint32), ("no_prune", ctypes.c_uint32)]
+
+
+class sk_enum_stats(ctypes.Structure):
+    _fields_ = [("plans_completed", ctypes.c_uint64), ("prunes", ctypes.c_uint64),
+                ("estimator_calls", ctypes.c_uint64), ("distinct_estimates", ctypes.c_uint64)]
 
 _lib = None
 
@@ -103,6 +118,10 @@ def lib() -> ctypes.CDLL:
         L.plan_greedy.restype = st
         L.plan_greedy.argtypes = [ctypes.POINTER(sk_graph), ctypes.POINTER(u32), ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double), vp]
+        L.plan_enumerate.restype = st
+        L.plan_enumerate.argtypes = [ctypes.POINTER(sk_graph), ctypes.POINTER(sk_enum_config), ctypes.POINTER(u32),
+                                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(sk_enum_stats), vp]
         L.sk_last_error.restype = ctypes.c_char_p
         L.sk_last_error.argtypes = []
         L.sk_kernel_launches.restype = ctypes.c_uint64
@@ -274,6 +293,20 @@ class JoinGraph:
         _check(lib().plan_greedy(ctypes.byref(self.g), order, pre, ctypes.byref(cost),
                                  ctypes.c_void_p(_stream_ptr(stream))))
         return [self.tables[i] for i in order], list(pre), cost.value
+
+    def plan_enumerate(self, mode="limit", max_plans=10, alpha=0.5, beta=0.5, prune=True, stream=None):
+        """Algorithm 1: (order, per-prefix cards, cost, stats dict).
+        mode: greedy | full-greedy | limit (max_plans per source) | exhaustive."""
+        n = len(self.tables)
+        cfg = sk_enum_config(alpha, beta, ENUM_MODES[mode], max_plans, 0 if prune else 1)
+        order = (ctypes.c_uint32 * n)()
+        pre = (ctypes.c_double * n)()
+        cost = ctypes.c_double()
+        stats = sk_enum_stats()
+        _check(lib().plan_enumerate(ctypes.byref(self.g), ctypes.byref(cfg), order, pre, ctypes.byref(cost),
+                                    ctypes.byref(stats), ctypes.c_void_p(_stream_ptr(stream))))
+        st = {f: int(getattr(stats, f)) for f, _ in sk_enum_stats._fields_}
+        return [self.tables[i] for i in order], list(pre), cost.value, st
 
 
 def kernel_launches() -> int:

@@ -1706,17 +1706,24 @@ extern "C" sk_status estimate_subplans(const sk_graph *g, const uint64_t *masks,
     return estimate_batch(g, masks, n, est, nullptr, (cudaStream_t)stream);
 }
 
-extern "C" sk_status plan_greedy(const sk_graph *g, uint32_t *order, double *prefix_card, double *cost, void *stream) {
-    if (!g || !order) return fail(SK_EINVAL, "plan_greedy: NULL argument");
-    const uint32_t n = g->n_tables;
-    if (n == 0 || n > 64) return fail(SK_EINVAL, "plan_greedy: n_tables must be in [1,64]");
+namespace skb {
+
+// Estimate cache of one planning call: card(S) = survivors for |S| = 1,
+// max(Est(S), 0) otherwise; all connected sub-plans are estimated in one batch up front when
+// there are at most 512 of them, else on demand.
+struct CardCache {
+    const sk_graph *g;
+    cudaStream_t stream;
     std::map<uint64_t, double> cache;
     sk_status err = SK_OK;
-    // A11: evaluate every connected sub-plan in one batch when there are few of them
-    if (n <= 16) {
+    uint64_t calls = 0;
+    CardCache(const sk_graph *g_, cudaStream_t s) : g(g_), stream(s) {}
+    sk_status prefetch() {
+        const uint32_t n = g->n_tables;
+        if (n > 16) return SK_OK;
         std::vector<uint64_t> adj(n, 0);
         for (uint32_t e = 0; e < g->n_edges; ++e) {
-            if (g->edge_u[e] >= n || g->edge_v[e] >= n) return fail(SK_EINVAL, "plan_greedy: bad edge");
+            if (g->edge_u[e] >= n || g->edge_v[e] >= n) return fail(SK_EINVAL, "planner: bad edge");
             adj[g->edge_u[e]] |= 1ULL << g->edge_v[e];
             adj[g->edge_v[e]] |= 1ULL << g->edge_u[e];
         }
@@ -1733,64 +1740,149 @@ extern "C" sk_status plan_greedy(const sk_graph *g, uint32_t *order, double *pre
             }
             if (seen == m) masks.push_back(m);
         }
-        if (masks.size() <= 512) {
-            std::vector<double> est(masks.size());
-            sk_status st = estimate_batch(g, masks.data(), (uint32_t)masks.size(), est.data(), nullptr, (cudaStream_t)stream);
-            if (st) return st;
-            for (size_t i = 0; i < masks.size(); ++i) cache[masks[i]] = std::max(est[i], 0.0);
-        }
+        if (masks.size() > 512) return SK_OK;
+        std::vector<double> est(masks.size());
+        sk_status st = estimate_batch(g, masks.data(), (uint32_t)masks.size(), est.data(), nullptr, stream);
+        if (st) return st;
+        for (size_t i = 0; i < masks.size(); ++i) cache[masks[i]] = std::max(est[i], 0.0);
+        return SK_OK;
     }
-    auto card = [&](uint64_t m) -> double {
+    double card(uint64_t m) {
+        ++calls;
         auto it = cache.find(m);
         if (it != cache.end()) return it->second;
-        double e = 0;
-        sk_status st = estimate_mask(g, m, &e, nullptr, nullptr, (cudaStream_t)stream);
-        if (st && !err) err = st;
-        const double c = std::max(e, 0.0);
+        double c;
+        if (__builtin_popcountll(m) == 1) {
+            c = (double)g->survivors[__builtin_ctzll(m)];
+        } else {
+            double e = 0;
+            sk_status st = estimate_mask(g, m, &e, nullptr, nullptr, stream);
+            if (st && !err) err = st;
+            c = std::max(e, 0.0);
+        }
         cache[m] = c;
         return c;
-    };
-    std::vector<uint32_t> C;
-    double total = 0;
-    std::vector<double> pre;
+    }
+};
+
+// PAPER.md:662 greedy: cheapest two-vertex sub-plan, source = its endpoint with
+// fewer survivors, then repeatedly the cheapest neighbour extension.
+static sk_status greedy_order(CardCache &cc, std::vector<uint32_t> &C, std::vector<double> &pre) {
+    const sk_graph *g = cc.g;
+    const uint32_t n = g->n_tables;
+    C.clear();
+    pre.clear();
     if (n == 1) {
         C.push_back(0);
-        pre.push_back(card(1ULL));
-    } else {
-        // start pair: least card over adjacent pairs; ties by (min index, max index)
-        int bu = -1, bv = -1;
-        double bc = 0;
+        pre.push_back(cc.card(1ULL));
+        return cc.err;
+    }
+    int bu = -1, bv = -1;
+    double bc = 0;
+    for (uint32_t e = 0; e < g->n_edges; ++e) {
+        int u = (int)std::min(g->edge_u[e], g->edge_v[e]), v = (int)std::max(g->edge_u[e], g->edge_v[e]);
+        const double c = cc.card((1ULL << u) | (1ULL << v));
+        if (cc.err) return cc.err;
+        if (bu < 0 || c < bc || (c == bc && (u < bu || (u == bu && v < bv)))) { bu = u; bv = v; bc = c; }
+    }
+    if (bu < 0) return fail(SK_EINVAL, "planner: graph has no edges");
+    const int src = (g->survivors[bv] < g->survivors[bu]) ? bv : bu;
+    C.push_back((uint32_t)src);
+    uint64_t m = 1ULL << src;
+    pre.push_back(cc.card(m));
+    while (C.size() < n) {
+        int best = -1;
+        double bcard = 0;
         for (uint32_t e = 0; e < g->n_edges; ++e) {
-            int u = (int)std::min(g->edge_u[e], g->edge_v[e]), v = (int)std::max(g->edge_u[e], g->edge_v[e]);
-            const double c = card((1ULL << u) | (1ULL << v));
-            if (err) return err;
-            if (bu < 0 || c < bc || (c == bc && (u < bu || (u == bu && v < bv)))) { bu = u; bv = v; bc = c; }
+            const uint32_t u = g->edge_u[e], v = g->edge_v[e];
+            int cand = -1;
+            if (((m >> u) & 1ULL) && !((m >> v) & 1ULL)) cand = (int)v;
+            if (((m >> v) & 1ULL) && !((m >> u) & 1ULL)) cand = (int)u;
+            if (cand < 0) continue;
+            const double c = cc.card(m | (1ULL << cand));
+            if (cc.err) return cc.err;
+            if (best < 0 || c < bcard || (c == bcard && cand < best)) { best = cand; bcard = c; }
         }
-        if (bu < 0) return fail(SK_EINVAL, "plan_greedy: graph has no edges");
-        const int src = (g->survivors[bv] < g->survivors[bu]) ? bv : bu;
-        C.push_back((uint32_t)src);
-        uint64_t m = 1ULL << src;
-        pre.push_back(card(m));
-        while (C.size() < n) {
-            int best = -1;
-            double bcard = 0;
-            for (uint32_t e = 0; e < g->n_edges; ++e) {
-                const uint32_t u = g->edge_u[e], v = g->edge_v[e];
-                int cand = -1;
-                if (((m >> u) & 1ULL) && !((m >> v) & 1ULL)) cand = (int)v;
-                if (((m >> v) & 1ULL) && !((m >> u) & 1ULL)) cand = (int)u;
-                if (cand < 0) continue;
-                const double c = card(m | (1ULL << cand));
-                if (err) return err;
-                if (best < 0 || c < bcard || (c == bcard && cand < best)) { best = cand; bcard = c; }
-            }
-            if (best < 0) return fail(SK_EINVAL, "plan_greedy: join graph is not connected");
-            C.push_back((uint32_t)best);
-            m |= 1ULL << best;
-            pre.push_back(bcard);
+        if (best < 0) return fail(SK_EINVAL, "planner: join graph is not connected");
+        C.push_back((uint32_t)best);
+        m |= 1ULL << best;
+        pre.push_back(bcard);
+    }
+    return cc.err;
+}
+
+static sk_status check_graph(const sk_graph *g) {
+    if (!g) return fail(SK_EINVAL, "planner: NULL graph");
+    if (g->n_tables == 0 || g->n_tables > 64) return fail(SK_EINVAL, "planner: n_tables must be in [1,64]");
+    if (!g->survivors) return fail(SK_EINVAL, "planner: graph survivors missing");
+    for (uint32_t e = 0; e < g->n_edges; ++e)
+        if (g->edge_u[e] >= g->n_tables || g->edge_v[e] >= g->n_tables || g->edge_u[e] == g->edge_v[e])
+            return fail(SK_EINVAL, "planner: bad edge %u", e);
+    return SK_OK;
+}
+
+// Algorithm 1: DFS Traversal with early pruning and a per-source plan limit
+struct Enumerator {
+    CardCache &cc;
+    const sk_graph *g;
+    uint32_t n;
+    std::vector<uint64_t> adj;
+    uint64_t max_plans;      // 0 = unbounded
+    bool prune;
+    double min_cost = INFINITY;
+    std::vector<uint32_t> opt_path, C;
+    uint64_t p = 0;          // plans completed from the current source
+    bool abort_source = false;
+    sk_enum_stats st{};
+    Enumerator(CardCache &c, uint64_t mp, bool pr) : cc(c), g(c.g), n(c.g->n_tables), adj(n, 0), max_plans(mp), prune(pr) {
+        for (uint32_t e = 0; e < g->n_edges; ++e) {
+            adj[g->edge_u[e]] |= 1ULL << g->edge_v[e];
+            adj[g->edge_v[e]] |= 1ULL << g->edge_u[e];
         }
     }
-    if (err) return err;
+    void dfs(uint64_t m, double cost) {
+        if (abort_source || cc.err) return;
+        const double curr = cc.card(m);                       // line 14
+        cost += curr;                                         // line 15
+        if (prune && cost > min_cost) { ++st.prunes; return; }   // line 17
+        if (C.size() == n) {                                  // lines 19-26
+            if (cost < min_cost) { min_cost = cost; opt_path = C; }
+            ++st.plans_completed;
+            ++p;
+            if (max_plans && p == max_plans) abort_source = true;
+            return;
+        }
+        // lines 29-35: neighbours of C, in increasing card(C + v), ties by index
+        uint64_t L = 0;
+        for (uint64_t f = m; f; f &= f - 1) L |= adj[__builtin_ctzll(f)];
+        L &= ~m;
+        std::vector<std::pair<double, uint32_t>> ev;
+        for (uint64_t f = L; f; f &= f - 1) {
+            const uint32_t v = (uint32_t)__builtin_ctzll(f);
+            ev.push_back({cc.card(m | (1ULL << v)), v});
+        }
+        std::sort(ev.begin(), ev.end());
+        for (auto &e : ev) {
+            if (abort_source || cc.err) return;
+            C.push_back(e.second);
+            dfs(m | (1ULL << e.second), cost);
+            C.pop_back();
+        }
+    }
+};
+
+}  // namespace skb
+
+extern "C" sk_status plan_greedy(const sk_graph *g, uint32_t *order, double *prefix_card, double *cost, void *stream) {
+    if (!g || !order) return fail(SK_EINVAL, "plan_greedy: NULL argument");
+    sk_status st = check_graph(g);
+    if (st) return st;
+    CardCache cc(g, (cudaStream_t)stream);
+    if ((st = cc.prefetch())) return st;
+    std::vector<uint32_t> C;
+    std::vector<double> pre;
+    if ((st = greedy_order(cc, C, pre))) return st;
+    double total = 0;
     for (size_t i = 0; i < C.size(); ++i) {
         order[i] = C[i];
         if (prefix_card) prefix_card[i] = pre[i];
@@ -1798,4 +1890,64 @@ extern "C" sk_status plan_greedy(const sk_graph *g, uint32_t *order, double *pre
     }
     if (cost) *cost = total;
     return SK_OK;
+}
+
+extern "C" sk_status plan_enumerate(const sk_graph *g, const sk_enum_config *cfg, uint32_t *order, double *prefix_card,
+                                    double *cost, sk_enum_stats *stats, void *stream) {
+    if (!g || !cfg || !order) return fail(SK_EINVAL, "plan_enumerate: NULL argument");
+    sk_status st = check_graph(g);
+    if (st) return st;
+    if (cfg->mode > SK_ENUM_EXHAUSTIVE) return fail(SK_EINVAL, "plan_enumerate: unknown mode %u", cfg->mode);
+    if (cfg->mode == SK_ENUM_LIMIT && cfg->max_plans == 0) return fail(SK_EINVAL, "plan_enumerate: max_plans must be >= 1");
+    if (!(cfg->alpha >= 0) || !(cfg->beta >= 0)) return fail(SK_EINVAL, "plan_enumerate: alpha, beta must be >= 0");
+    CardCache cc(g, (cudaStream_t)stream);
+    if ((st = cc.prefetch())) return st;
+    const uint32_t n = g->n_tables;
+    std::vector<uint32_t> best;
+    double best_cost = 0;
+    sk_enum_stats es{};
+    if (cfg->mode == SK_ENUM_GREEDY) {
+        std::vector<double> pre;
+        if ((st = greedy_order(cc, best, pre))) return st;
+        for (double c : pre) best_cost += c;
+        es.plans_completed = 1;
+    } else {
+        // line 7: sources in increasing f(v), ties by index
+        std::vector<uint32_t> deg(n, 0);
+        for (uint32_t e = 0; e < g->n_edges; ++e) { ++deg[g->edge_u[e]]; ++deg[g->edge_v[e]]; }
+        double maxc = 0, maxd = 0;
+        for (uint32_t v = 0; v < n; ++v) { maxc = std::max(maxc, (double)g->survivors[v]); maxd = std::max(maxd, (double)deg[v]); }
+        std::vector<std::pair<double, uint32_t>> S;
+        for (uint32_t v = 0; v < n; ++v) {
+            const double f = (maxc > 0 ? cfg->alpha * (double)g->survivors[v] / maxc : 0.0) +
+                             (maxd > 0 ? cfg->beta * (double)deg[v] / maxd : 0.0);
+            S.push_back({f, v});
+        }
+        std::sort(S.begin(), S.end());
+        const uint64_t mp = cfg->mode == SK_ENUM_FULL_GREEDY ? 1 : cfg->mode == SK_ENUM_LIMIT ? cfg->max_plans : 0;
+        Enumerator en(cc, mp, !cfg->no_prune);
+        for (auto &sv : S) {                                   // lines 8-11
+            en.p = 0;
+            en.abort_source = false;
+            en.C.assign(1, sv.second);
+            en.dfs(1ULL << sv.second, 0.0);
+            if (cc.err) return cc.err;
+        }
+        if (en.opt_path.size() != n) return fail(SK_EINVAL, "plan_enumerate: join graph is not connected");
+        best = en.opt_path;
+        best_cost = en.min_cost;
+        es = en.st;
+    }
+    if (cc.err) return cc.err;
+    es.estimator_calls = cc.calls;
+    es.distinct_estimates = cc.cache.size();
+    uint64_t m = 0;
+    for (size_t i = 0; i < best.size(); ++i) {
+        order[i] = best[i];
+        m |= 1ULL << best[i];
+        if (prefix_card) prefix_card[i] = cc.card(m);
+    }
+    if (cost) *cost = best_cost;
+    if (stats) *stats = es;
+    return cc.err;
 }

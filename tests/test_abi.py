@@ -140,3 +140,24 @@ def test_crt_moduli_are_distinct_primes_below_2_26():
     assert len(set(primes)) == len(primes) == 28
     assert all(is_prime(p) and p < (1 << 26) for p in primes)
     assert sum(math.log2(p) for p in primes) > 700
+
+
+def test_plan_enumerate_host_validation_without_device():
+    """Algorithm 1's argument checks and a single-table graph run on the host only."""
+    import paper_2102_02440_b200 as pb
+    L = pb.lib()
+    surv = (ctypes.c_int64 * 1)(42)
+    g = pb.sk_graph()
+    g.n_tables, g.survivors, g.n_edges, g.n_mats = 1, surv, 0, 0
+    order = (ctypes.c_uint32 * 1)()
+    pre = (ctypes.c_double * 1)()
+    cost = ctypes.c_double()
+    st = pb.sk_enum_stats()
+    cfg = pb.sk_enum_config(0.5, 0.5, pb.ENUM_LIMIT, 10, 0)
+    assert L.plan_enumerate(ctypes.byref(g), None, order, pre, ctypes.byref(cost), None, None) == pb.SK_EINVAL
+    bad = pb.sk_enum_config(0.5, 0.5, pb.ENUM_LIMIT, 0, 0)
+    assert L.plan_enumerate(ctypes.byref(g), ctypes.byref(bad), order, pre, ctypes.byref(cost), None, None) == pb.SK_EINVAL
+    bad = pb.sk_enum_config(0.5, 0.5, 9, 1, 0)
+    assert L.plan_enumerate(ctypes.byref(g), ctypes.byref(bad), order, pre, ctypes.byref(cost), None, None) == pb.SK_EINVAL
+    assert L.plan_enumerate(ctypes.byref(g), ctypes.byref(cfg), order, pre, ctypes.byref(cost), ctypes.byref(st), None) == pb.SK_OK
+    assert list(order) == [0] and list(pre) == [42.0] and cost.value == 42.0 and st.plans_completed == 1

@@ -447,6 +447,76 @@ def test_greedy_cost_not_below_exhaustive_minimum():
         assert cost >= best
 
 
+# ---------------------------------------------------------------- Algorithm 1
+def _random_graph_cards(rng, T, extra):
+    names = [f"t{i}" for i in range(T)]
+    edges = [(f"{names[i]}.k|{names[j]}.k", names[i], names[j]) for i in range(1, T) for j in [int(rng.integers(0, i))]]
+    for x in range(extra):   # extra edges: cycles and parallel edges (distinct edge ids)
+        i, j = sorted(rng.choice(T, 2, replace=False).tolist())
+        edges.append((f"{names[i]}.e{x}|{names[j]}.e{x}", names[i], names[j]))
+    g = _FakeG({n: int(rng.integers(1, 100)) for n in names}, edges)
+    table = {}
+
+    def card_fn(S):   # any non-negative cardinality function (singletons included)
+        if S not in table:
+            table[S] = float(rng.integers(0, 1000))
+        return table[S]
+    return g, names, card_fn
+
+
+def test_enumerate_f_order_hand_example():
+    """SPEC.md:363 hand example: cards (8, 8, 64), degrees (1, 2, 1), alpha = beta = 0.5 ->
+    f = (0.3125, 0.5625, 0.75): DFS sources v1, v2, v3 in that order."""
+    g = _FakeG({"v1": 8, "v2": 8, "v3": 64}, [("v1.a|v2.a", "v1", "v2"), ("v2.b|v3.b", "v2", "v3")])
+    seen = []
+
+    def card_fn(S):
+        if len(S) == 1 and S[0] not in seen:
+            seen.append(S[0])
+        return {("v1",): 8, ("v2",): 8, ("v3",): 64}.get(S, 1)
+    oracle.plan_enumerate(g, mode="exhaustive", prune=False, card_fn=card_fn)
+    assert seen == ["v1", "v2", "v3"]
+
+
+def test_enumerate_hand_trace_and_prune():
+    """3-vertex path a-b-c: from source a (smallest f) the two complete plans
+    are found; the source b's first extension exceeds min_cost and is pruned."""
+    g = _FakeG({"a": 1, "b": 50, "c": 60}, [("a.x|b.x", "a", "b"), ("b.y|c.y", "b", "c")])
+    est = {("a", "b"): 2.0, ("b", "c"): 1000.0, ("a", "b", "c"): 3.0}
+    order, pre, cost, st = oracle.plan_enumerate(g, mode="exhaustive", est_fn=lambda S: est[S])
+    # a: a(1) -> a,b (2) -> a,b,c (3): cost 6; b: b(50) > 6 -> pruned; c: c(60) > 6 -> pruned
+    assert order == ["a", "b", "c"] and pre == [1.0, 2.0, 3.0] and cost == 6.0
+    assert st["plans_completed"] == 1 and st["prunes"] == 2
+
+
+def test_enumerate_exhaustive_is_optimal_and_pruning_sound():
+    """with max_plans unbounded the returned cost is the minimum over every
+    valid left-deep order (brute force), and disabling pruning changes nothing but the stats;
+    without pruning every valid order is completed exactly once."""
+    rng = np.random.default_rng(7)
+    for trial in range(40):
+        g, names, card_fn = _random_graph_cards(rng, int(rng.integers(3, 7)), int(rng.integers(0, 3)))
+        costs = oracle.leftdeep_costs_bruteforce(names, g.edges, card_fn)
+        o1, p1, c1, s1 = oracle.plan_enumerate(g, mode="exhaustive", card_fn=card_fn)
+        o2, p2, c2, s2 = oracle.plan_enumerate(g, mode="exhaustive", prune=False, card_fn=card_fn)
+        best = min(costs.values())
+        assert c1 == best and c2 == best and costs[tuple(o1)] == best and o1 == o2
+        assert s2["plans_completed"] == len(costs) and s2["prunes"] == 0
+        assert sum(p1) == c1
+
+
+def test_enumerate_search_space_nesting():
+    """exhaustive <= limit-10 <= full-greedy in cost (same estimator)."""
+    rng = np.random.default_rng(11)
+    for trial in range(40):
+        g, names, card_fn = _random_graph_cards(rng, int(rng.integers(3, 8)), int(rng.integers(0, 4)))
+        ce = oracle.plan_enumerate(g, mode="exhaustive", card_fn=card_fn)[2]
+        cl = oracle.plan_enumerate(g, mode="limit", max_plans=10, card_fn=card_fn)[2]
+        cf = oracle.plan_enumerate(g, mode="full-greedy", card_fn=card_fn)[2]
+        c1 = oracle.plan_enumerate(g, mode="limit", max_plans=1, card_fn=card_fn)[2]
+        assert ce <= cl <= cf and c1 == cf
+
+
 # ---------------------------------------------------------------- P10 C1 end to end
 def test_c1_estimate_vs_exact_join():
     import datagen

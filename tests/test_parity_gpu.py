@@ -239,6 +239,28 @@ TOPOS = [
 ]
 
 
+ENUM_CASES = [("greedy", 1, True), ("full-greedy", 1, True), ("limit", 10, True), ("limit", 2, True),
+              ("exhaustive", 0, True), ("exhaustive", 0, False)]
+
+
+def _check_enumerate(og, jg, est_cache=None):
+    """plan_enumerate (Algorithm 1) through the C-ABI == the oracle's, every mode: same
+    order, per-prefix cards, cost and traversal counters (both sides see identical estimates)."""
+    cache = dict(est_cache or {})
+
+    def est(S):
+        if S not in cache:
+            cache[S] = oracle.estimate(og, S)[0]
+        return cache[S]
+    for mode, mp, prune in ENUM_CASES:
+        o_order, o_pre, o_cost, o_st = oracle.plan_enumerate(og, mode=mode, max_plans=mp, prune=prune, est_fn=est)
+        order, pre, cost, st = jg.plan_enumerate(mode=mode, max_plans=mp, prune=prune)
+        assert (order, pre, cost) == (o_order, o_pre, o_cost), (mode, mp, prune)
+        assert st["plans_completed"] == o_st["plans_completed"], (mode, mp, prune)
+        if mode != "greedy":
+            assert st["prunes"] == o_st["prunes"], (mode, mp, prune)
+
+
 @pytest.fixture(params=["default", "crt"])
 def est_engine(request, monkeypatch):
     """Estimates through the default engine (exact int128 contraction where the bound fits,
@@ -262,6 +284,7 @@ def test_estimates_equal_oracle_on_random_networks(ti, est_engine):
             est, rows = jg.estimate_join(s)
             assert est == float(oracle.median_odd(want)) and rows == [float(v) for v in want]
         assert tuple(jg.plan_greedy()) == tuple(oracle.plan_greedy(og))
+        _check_enumerate(og, jg)
 
 
 # ------------------------------------------------------------------ workloads C1-C5
@@ -309,6 +332,7 @@ def test_c1_end_to_end(est_engine):
     est, _ = jg.estimate_join(("R", "S"))
     assert est == oracle.estimate(og, ("R", "S"))[0]
     assert list(jg.plan_greedy()[0]) == oracle.plan_greedy(og)[0]
+    _check_enumerate(og, jg)
 
 
 def _all_subplans_match(ws, run, og, rows=None):
@@ -331,6 +355,7 @@ def test_c2_scaled_chain_parity():
     order, pre, cost = jg.plan_greedy()
     o_order, o_pre, o_cost = oracle.plan_greedy(og)
     assert order == o_order and pre == o_pre and cost == o_cost
+    _check_enumerate(og, jg)
 
 
 def test_c3_scaled_parity_all_14_subplans_and_plan(est_engine):
@@ -340,6 +365,7 @@ def test_c3_scaled_parity_all_14_subplans_and_plan(est_engine):
     _check_counters(ws, run, og, surv)
     jg = _all_subplans_match(ws, run, og)
     assert tuple(jg.plan_greedy()) == tuple(oracle.plan_greedy(og))
+    _check_enumerate(og, jg)
 
 
 @pytest.mark.parametrize("cycle", [False, True])
@@ -350,6 +376,7 @@ def test_c5_scaled_parity_all_subplans_and_plan(cycle):
     _check_counters(ws, run, og, surv)
     jg = _all_subplans_match(ws, run, og)
     assert tuple(jg.plan_greedy()) == tuple(oracle.plan_greedy(og))
+    _check_enumerate(og, jg)
 
 
 def test_c3_full_width_triangle_sampled_row(est_engine):
