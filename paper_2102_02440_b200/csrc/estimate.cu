@@ -777,6 +777,175 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_m(const __grid_constant__ 
     }
 }
 
+// ---------------------------------------------------------------- absolute-value bound pass
+// |E_r| <= A_r = the same contraction with every tensor entry replaced by its absolute value
+// (a merged view's entry by min_q |v_q|).  All quantities are non-negative, so the fp64 pass
+// uses sums and products only (prefix sums of x*c and suffix sums of x — no differences):
+// V(o) = sum_s x_s min(t_o, c_s) = P2[n_t] + t_o * SUF1[n_t], t_o = min |other legs|,
+// n_t = #{c_s < t_o}.  The relative rounding error of such a computation is below 2^-26 here
+// (< 2^27 sequential additions on any path), so A_r (1 + 2^-16) bounds |E_r| rigorously; it is
+// far tighter than prod_t ||T_t||_1 (one index per edge instead of one per table leg), which
+// lets most merged sub-plans run on the exact int128 engine.
+__device__ __forceinline__ double block_sum_f64(double v, double *red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double t = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    return t;
+}
+__device__ __forceinline__ const double *msg_row_a(const Node &n, int q, int r, int bb) {
+    const int bm = n.bm[q];
+    return reinterpret_cast<const double *>(n.msg[q]) + (uint64_t(r) * bm + (bm > 1 ? bb : 0)) * (uint64_t)n.w[q];
+}
+__device__ __forceinline__ double tensor_abs(const Node &n, int r, const int64_t *idx) {
+    if (n.kind == KV) return (double)uabs(n.data[0][uint64_t(r) * n.w[0] + idx[0]]);
+    if (n.kind == KM) return (double)uabs(n.data[0][(uint64_t(r) * n.w[0] + idx[0]) * n.w[1] + idx[1]]);
+    uint64_t m = uabs(n.data[0][uint64_t(r) * n.w[0] + idx[0]]);
+    for (int q = 1; q < n.nl; ++q) m = min(m, uabs(n.data[q][uint64_t(r) * n.w[q] + idx[q]]));
+    return (double)m;
+}
+
+__global__ void k_node_dense_abs(const __grid_constant__ Node n) {
+    __shared__ double red[32];
+    const int B = n.B;
+    const int bb = blockIdx.x % B;
+    const int r = blockIdx.x / B;
+    const int64_t b = n.b0 + bb;
+    int qp = -1, qf = -1, qc0 = -1, qc1 = -1;
+    for (int q = 0; q < n.nl; ++q) {
+        if (n.role[q] == RPARENT) qp = q;
+        else if (n.role[q] == RFIXED) qf = q;
+        else if (qc0 < 0) qc0 = q;
+        else qc1 = q;
+    }
+    const int qo = qp >= 0 ? qp : qc0;
+    const int qi = qp >= 0 ? qc0 : qc1;
+    const int wo = qo >= 0 ? n.w[qo] : 1;
+    const int wi = qi >= 0 ? n.w[qi] : 1;
+    const double *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row_a(n, qo, r, bb) : nullptr;
+    const double *xi = (qi >= 0) ? msg_row_a(n, qi, r, bb) : nullptr;
+    double acc = 0;
+    const int per_tile = (wo + n.tiles - 1) / n.tiles;
+    const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
+    for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
+        double s = 0;
+        for (int i = 0; i < wi; ++i) {
+            int64_t idx[3] = {0, 0, 0};
+            if (qo >= 0) idx[qo] = o;
+            if (qi >= 0) idx[qi] = i;
+            if (qf >= 0) idx[qf] = b;
+            double term = tensor_abs(n, r, idx);
+            if (xi) term *= xi[i];
+            s += term;
+        }
+        if (qp >= 0) {
+            const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
+            reinterpret_cast<double *>(n.out)[(uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = s;
+        } else {
+            if (xo) s *= xo[o];
+            acc += s;
+        }
+    }
+    if (qp < 0) {
+        const double t = block_sum_f64(acc, red);
+        if (threadIdx.x == 0) reinterpret_cast<double *>(n.out)[(uint64_t(r) * B + bb) * n.tiles + blockIdx.y] = t;
+    }
+}
+
+__global__ void __launch_bounds__(MX_T) k_node_merged_abs(const __grid_constant__ Node n) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ double red[32];
+    __shared__ double tot1[MX_T], tot2[MX_T];
+    const int B = n.B;
+    const int bb = blockIdx.x % B;
+    const int r = blockIdx.x / B;
+    const int64_t b = n.b0 + bb;
+    const int qc = n.qc;
+    const int wq = n.w[qc];
+    double *P2 = reinterpret_cast<double *>(sm);     // prefix sums of x*|c|   [wq + 1]
+    double *S1 = P2 + (wq + 1);                      // suffix sums of x       [wq + 1]
+    const int64_t *cs = n.csorted + uint64_t(r) * wq;
+    const uint64_t *S = n.sabs + uint64_t(r) * wq;
+    int qp = -1, qf = -1, oc[2] = {-1, -1}, noc = 0;
+    for (int q = 0; q < n.nl; ++q) {
+        if (q == qc) continue;
+        if (n.role[q] == RPARENT) qp = q;
+        else if (n.role[q] == RFIXED) qf = q;
+        else oc[noc++] = q;
+    }
+    const int qo = qp >= 0 ? qp : oc[0];
+    const int qi = qp >= 0 ? oc[0] : oc[1];
+    const int wo = qo >= 0 ? n.w[qo] : 1;
+    const int wi = qi >= 0 ? n.w[qi] : 1;
+    const int per_tile = (wo + n.tiles - 1) / n.tiles;
+    const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
+    const double *x = msg_row_a(n, qc, r, bb);
+    const int chunk = (wq + MX_T - 1) / MX_T;
+    const int s0 = threadIdx.x * chunk, s1 = min(wq, s0 + chunk);
+    double l1 = 0, l2 = 0;
+    for (int s = s0; s < s1; ++s) { l1 += x[s]; l2 += x[s] * (double)uabs(cs[s]); }
+    tot1[threadIdx.x] = l1;
+    tot2[threadIdx.x] = l2;
+    __syncthreads();
+    if (threadIdx.x == 0) {   // exclusive prefix (tot2) and suffix-after (tot1) of the thread totals
+        double c2 = 0;
+        for (int t = 0; t < MX_T; ++t) { const double v = tot2[t]; tot2[t] = c2; c2 += v; }
+        P2[wq] = c2;
+        double c1 = 0;
+        for (int t = MX_T - 1; t >= 0; --t) { const double v = tot1[t]; tot1[t] = c1; c1 += v; }
+        S1[wq] = 0;
+    }
+    __syncthreads();
+    {
+        double c2 = tot2[threadIdx.x];
+        for (int s = s0; s < s1; ++s) { P2[s] = c2; c2 += x[s] * (double)uabs(cs[s]); }
+        double c1 = tot1[threadIdx.x];
+        for (int s = s1 - 1; s >= s0; --s) { c1 += x[s]; S1[s] = c1; }
+    }
+    __syncthreads();
+    const double *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row_a(n, qo, r, bb) : nullptr;
+    const double *xi2 = qi >= 0 ? msg_row_a(n, qi, r, bb) : nullptr;
+    double acc = 0;
+    for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
+        double sacc = 0;
+        for (int i = 0; i < wi; ++i) {
+            uint64_t t = ~0ULL;   // min |value| over the other legs
+            for (int q = 0; q < n.nl; ++q) {
+                if (q == qc) continue;
+                const int64_t ix = (q == qf) ? b : (q == qo ? o : i);
+                t = min(t, uabs(n.data[q][uint64_t(r) * n.w[q] + ix]));
+            }
+            const int nt = count_lt(S, wq, t);
+            double V = P2[nt] + (double)t * S1[nt];
+            if (xi2) V *= xi2[i];
+            sacc += V;
+        }
+        if (qp >= 0) {
+            const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
+            reinterpret_cast<double *>(n.out)[(uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = sacc;
+        } else {
+            if (xo) sacc *= xo[o];
+            acc += sacc;
+        }
+    }
+    if (qp < 0) {
+        const double t = block_sum_f64(acc, red);
+        if (threadIdx.x == 0) reinterpret_cast<double *>(n.out)[(uint64_t(r) * B + bb) * n.tiles + blockIdx.y] = t;
+    }
+}
+
+__global__ void k_root_reduce_abs(const double *part, double *acc, int slots) {
+    __shared__ double red[32];
+    double s = 0;
+    for (int i = threadIdx.x; i < slots; i += blockDim.x) s += part[uint64_t(blockIdx.x) * slots + i];
+    const double t = block_sum_f64(s, red);
+    if (threadIdx.x == 0) acc[blockIdx.x] += t;
+}
+
 // acc[r] += sum over slots of part[r][slot], exact
 __global__ void k_root_reduce_x(const i128 *part, i128 *acc, int slots) {
     __shared__ i128 red[32];
@@ -1191,11 +1360,13 @@ static double log_bound(const Plan &P, F l1of) {
 // residues -> acc[K][d] (zeroed by the caller), per-sketch-row L1 norms -> l1[n_uniq][d].
 static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const sk_sketch *> &uniq,
                               DevPool &pool, uint64_t *acc, unsigned long long *l1, cudaStream_t stream,
-                              bool exact = false) {
+                              int ring = 0) {
+    // ring: 0 = CRT residues, 1 = exact int128, 2 = fp64 absolute-value bound (no matrices)
+    const bool exact = ring == 1, absb = ring == 2;
     const int E = (int)P.edges.size();
     const int NT = (int)P.T.size();
     const int d = P.d;
-    const int K = exact ? 2 : md.K;   // 64-bit words per message entry and row (exact: one int128)
+    const int K = exact ? 2 : absb ? 1 : md.K;   // 64-bit words per message entry and row
     sk_status st;
     // ---- L1 norms of every sketch involved (checked against the moduli after the batch)
     for (size_t b0 = 0; b0 < uniq.size(); b0 += kMaxL1Items) {
@@ -1364,7 +1535,28 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                 if (n.role[q] == RCHILD) { ++nchild; qchild = q; }
                 if (n.role[q] == RFIXED) hasfixed = true;
             }
-            if (exact) {
+            if (absb) {
+                if (t.kind == KG && qc_of[i] >= 0) {
+                    n.qc = qc_of[i];
+                    n.ord = ord_of[i];
+                    n.sabs = sabs_of[i];
+                    n.csorted = csorted_of[i];
+                    int wo_max = 1;
+                    for (int q = 0; q < n.nl; ++q)
+                        if (q != n.qc && n.role[q] != RFIXED) wo_max = std::max(wo_max, n.w[q]);
+                    int mtiles = 1;
+                    while (d * nB * mtiles < 296 && mtiles * MX_T < wo_max) mtiles *= 2;
+                    n.tiles = (pe >= 0) ? mtiles : 1;
+                    const size_t sm = size_t(2) * (n.w[n.qc] + 1) * 8;
+                    SKB_CUDA(cudaFuncSetAttribute(k_node_merged_abs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                    k_node_merged_abs<<<dim3(d * nB, n.tiles), MX_T, sm, stream>>>(n); count_launch();
+                } else {
+                    int xt = 1;
+                    if (pe >= 0) while (d * nB * xt < 592 && xt * 256 < P.width[pe]) xt *= 2;
+                    n.tiles = (pe >= 0) ? xt : 1;
+                    k_node_dense_abs<<<dim3(d * nB, n.tiles), 256, 0, stream>>>(n); count_launch();
+                }
+            } else if (exact) {
                 if (t.kind == KG && qc_of[i] >= 0) {
                     n.qc = qc_of[i];
                     n.ord = ord_of[i];
@@ -1450,6 +1642,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
             SKB_CUDA_CHECK("estimate launch 4");
         }
         if (exact) { k_root_reduce_x<<<d, 256, 0, stream>>>((const i128 *)part, (i128 *)acc, B * tiles_root); count_launch(); }
+        else if (absb) { k_root_reduce_abs<<<d, 256, 0, stream>>>((const double *)part, (double *)acc, B * tiles_root); count_launch(); }
         else { k_root_reduce<<<K * d, 256, 0, stream>>>((const uint64_t *)part, acc, B * tiles_root, d, md); count_launch(); }
         SKB_CUDA_CHECK("estimate launch 5");
     }
@@ -1539,6 +1732,8 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
     std::vector<std::vector<const sk_sketch *>> uniqs(n);
     std::vector<size_t> off_acc(n), off_l1(n);
     std::vector<char> exact(n, 0);
+    std::vector<size_t> need_abs;
+    std::vector<double> abs_bound(n, INFINITY);   // log2 of the absolute-value bound, when computed
     size_t words = 0;
     const bool crt_only = getenv("COMPASS_EST_CRT_ONLY") != nullptr;
     for (size_t i = 0; i < n; ++i) {
@@ -1555,11 +1750,53 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
         // exact int128 contraction when the survivor bound fits (verified below with the
         // device-measured L1 norms) and the sub-plan has no matrix node
         exact[i] = !crt_only && !has_mat && logB <= 125.0;
+        if (!crt_only && !has_mat && !exact[i]) need_abs.push_back(i);
         if (exact[i]) words = (words + 1) & ~size_t(1);   // int128 accumulators: 16-byte aligned
         off_acc[i] = words;
         words += size_t(exact[i] ? 2 : mds[i].K) * P.d;
         off_l1[i] = words;
         words += uniqs[i].size() * P.d;
+    }
+    // absolute-value bound pass (one batch, one sync) for matrix-free sub-plans whose survivor
+    // bound exceeds int128: a bound A_r(1 + 2^-16) <= 2^125 on every row moves the plan to the
+    // exact engine, else the moduli are sized from it
+    if (!need_abs.empty()) {
+        DevPool apool;
+        void *dab;
+        sk_status sa;
+        const size_t aw = need_abs.size() * 64;
+        if ((sa = dalloc(apool, aw * 8 + 8 * 64 * need_abs.size() * 64, stream, &dab))) return sa;
+        SKB_CUDA(cudaMemsetAsync(dab, 0, aw * 8, stream));
+        unsigned long long *l1s = (unsigned long long *)dab + aw;
+        SKB_CUDA(cudaMemsetAsync(l1s, 0, 8 * 64 * need_abs.size() * 64, stream));
+        for (size_t j = 0; j < need_abs.size(); ++j) {
+            const size_t i = need_abs[j];
+            if (plans[i].d > 64 || uniqs[i].size() > 64) continue;
+            if ((sa = enqueue_plan(plans[i], mds[i], uniqs[i], apool, (uint64_t *)dab + j * 64, l1s + j * 64 * 64, stream, 2)))
+                return sa;
+        }
+        std::vector<double> hb(aw);
+        SKB_CUDA(cudaMemcpyAsync(hb.data(), dab, aw * 8, cudaMemcpyDeviceToHost, stream));
+        SKB_CUDA(cudaStreamSynchronize(stream));
+        size_t w2 = 0;
+        for (size_t i = 0; i < n; ++i) {
+            auto it = std::find(need_abs.begin(), need_abs.end(), i);
+            if (it != need_abs.end() && plans[i].d <= 64 && uniqs[i].size() <= 64) {
+                const size_t j = it - need_abs.begin();
+                double mx = 0;
+                for (int r = 0; r < plans[i].d; ++r) mx = std::max(mx, hb[j * 64 + r]);
+                const double lb = log2(std::max(1.0, mx * (1.0 + 1.0 / 65536.0)));
+                if (lb <= 125.0) exact[i] = 1;
+                else mds[i] = mods_for(lb, 1);
+                abs_bound[i] = lb;
+            }
+            if (exact[i]) w2 = (w2 + 1) & ~size_t(1);
+            off_acc[i] = w2;
+            w2 += size_t(exact[i] ? 2 : mds[i].K) * plans[i].d;
+            off_l1[i] = w2;
+            w2 += uniqs[i].size() * plans[i].d;
+        }
+        words = w2;
     }
     DevPool pool;
     void *dres;
@@ -1569,7 +1806,7 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
     uint64_t *res = (uint64_t *)dres;
     for (size_t i = 0; i < n; ++i)
         if ((st = enqueue_plan(plans[i], mds[i], uniqs[i], pool, res + off_acc[i], (unsigned long long *)(res + off_l1[i]),
-                               stream, exact[i])))
+                               stream, exact[i] ? 1 : 0)))
             return st;
     std::vector<uint64_t> host(words);
     SKB_CUDA(cudaMemcpyAsync(host.data(), res, words * 8, cudaMemcpyDeviceToHost, stream));
@@ -1583,7 +1820,7 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
             for (int r = 0; r < d; ++r) mx = std::max<uint64_t>(mx, host[off_l1[i] + u * d + r]);
             return (double)mx;
         };
-        const double logB = log_bound(P, l1of);
+        const double logB = std::min(log_bound(P, l1of), abs_bound[i]);
         if (exact[i] && logB <= 125.0) {
             for (int r = 0; r < d; ++r) rows[i].push_back(sbig_from_i128(host[off_acc[i] + 2 * r], host[off_acc[i] + 2 * r + 1]));
             continue;
