@@ -955,6 +955,69 @@ __global__ void k_root_reduce_x(const i128 *part, i128 *acc, int slots) {
     if (threadIdx.x == 0) acc[blockIdx.x] += t;
 }
 
+// Residues of a matrix node, child-leg major: Rc[k][r][i][o] = M(i, o) mod m_k (i = child-leg
+// index, o = parent-leg index), computed once per (matrix, orientation) per estimate batch and
+// shared by every chain sub-plan through that matrix.
+__global__ void k_mat_residues(const int64_t *T, int d, int w0, int w1, int qc, const __grid_constant__ Mods md,
+                               uint32_t *Rc) {
+    const uint64_t cells = uint64_t(w0) * w1, total = cells * d;
+    const int wi = qc == 0 ? w0 : w1, wo = qc == 0 ? w1 : w0;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t r = e / cells, c = e % cells;
+        const int i = (int)(c / wo), o = (int)(c % wo);
+        const int64_t v = qc == 0 ? T[r * cells + uint64_t(i) * w1 + o] : T[r * cells + uint64_t(o) * w1 + i];
+        const uint64_t av = uabs(v);
+        for (int k = 0; k < md.K; ++k) {
+            uint64_t rv = mm_red(av, md.m[k], md.mu[k]);
+            if (v < 0 && rv) rv = md.m[k] - rv;
+            Rc[(uint64_t(k) * d + r) * cells + c] = (uint32_t)rv;
+        }
+    }
+}
+
+// chain mat-vec from precomputed residues: grid (row, 32-output tile, group of 8 moduli);
+// 16 slices of the child index per block, combined in shared memory.
+constexpr int MR_SL = 16;
+__global__ void __launch_bounds__(512) k_node_matvec_r(const __grid_constant__ Node n, const __grid_constant__ Mods md,
+                                                       int qc, const uint32_t *Rc) {
+    __shared__ uint64_t part[MR_SL][MV_G][MV_OUT];
+    const int r = blockIdx.x;
+    const int qp = 1 - qc;
+    const int wi = n.w[qc], wo = n.w[qp];
+    const int lane = threadIdx.x & 31, sl = threadIdx.x >> 5;
+    const int o = blockIdx.y * MV_OUT + lane;
+    const int g0 = blockIdx.z * MV_G;
+    const int ng = min(MV_G, md.K - g0);
+    const uint64_t cells = uint64_t(wi) * wo;
+    const int chunk = (wi + MR_SL - 1) / MR_SL;
+    const int i0 = sl * chunk, i1 = min(wi, i0 + chunk);
+    uint64_t acc[MV_G];
+#pragma unroll
+    for (int g = 0; g < MV_G; ++g) acc[g] = 0;
+    if (o < wo) {
+#pragma unroll
+        for (int g = 0; g < MV_G; ++g) {
+            if (g >= ng) break;
+            const int k = g0 + g;
+            const uint32_t *R = Rc + (uint64_t(k) * n.d + r) * cells + o;
+            const unsigned long long *x = reinterpret_cast<const unsigned long long *>(msg_row(n, qc, k, r, 0, 0));
+            uint64_t a = 0;
+            for (int i = i0; i < i1; ++i) a += (uint64_t)__ldg(R + uint64_t(i) * wo) * __ldg(x + i);
+            acc[g] = a;   // <= chunk products of 52 bits: exact
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < MV_G; ++g) part[sl][g][lane] = g < ng ? mm_red(acc[g], md.m[g0 + g], md.mu[g0 + g]) : 0;
+    __syncthreads();
+    if (sl < ng && o < wo) {
+        const int k = g0 + sl;
+        uint64_t t = 0;
+        for (int s2 = 0; s2 < MR_SL; ++s2) t = mm_add(t, part[s2][sl][lane], md.m[k]);
+        const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
+        n.out[(uint64_t(k) * n.d + r) * n.out_bm * wo + oo] = t;
+    }
+}
+
 // acc[k][r] += sum over slots of part[k][r][slot]
 __global__ void k_root_reduce(const uint64_t *part, uint64_t *acc, int slots, int d, const __grid_constant__ Mods md) {
     __shared__ uint64_t red[32];
@@ -1360,7 +1423,8 @@ static double log_bound(const Plan &P, F l1of) {
 // residues -> acc[K][d] (zeroed by the caller), per-sketch-row L1 norms -> l1[n_uniq][d].
 static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const sk_sketch *> &uniq,
                               DevPool &pool, uint64_t *acc, unsigned long long *l1, cudaStream_t stream,
-                              int ring = 0) {
+                              int ring = 0, std::map<std::pair<const void *, int>, uint32_t *> *rescache = nullptr,
+                              const Mods *resmods = nullptr) {
     // ring: 0 = CRT residues, 1 = exact int128, 2 = fp64 absolute-value bound (no matrices)
     const bool exact = ring == 1, absb = ring == 2;
     const int E = (int)P.edges.size();
@@ -1597,6 +1661,26 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                     n.tiles = (pe >= 0) ? xt : 1;
                     k_node_dense_x<<<dim3(d * nB, n.tiles), 256, 0, stream>>>(n); count_launch();
                 }
+            } else if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB == 1 && rescache && resmods &&
+                       md.K <= resmods->K && !getenv("COMPASS_EST_NO_MATVEC")) {
+                // residues of this (folded) matrix in this orientation: once per batch
+                const auto key = std::make_pair((const void *)n.data[0], qchild);
+                auto it = rescache->find(key);
+                uint32_t *Rc;
+                if (it == rescache->end()) {
+                    void *rb;
+                    const size_t cells = size_t(n.w[0]) * n.w[1];
+                    if ((st = dalloc(pool, size_t(resmods->K) * d * cells * 4, stream, &rb))) return st;
+                    k_mat_residues<<<1184, 256, 0, stream>>>(n.data[0], d, n.w[0], n.w[1], qchild, *resmods, (uint32_t *)rb);
+                    count_launch();
+                    Rc = (uint32_t *)rb;
+                    (*rescache)[key] = Rc;
+                } else {
+                    Rc = it->second;
+                }
+                k_node_matvec_r<<<dim3(d, (P.width[pe] + MV_OUT - 1) / MV_OUT, (md.K + MV_G - 1) / MV_G), 512, 0, stream>>>(
+                    n, md, qchild, Rc);
+                count_launch();
             } else if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB == 1 && !getenv("COMPASS_EST_NO_MATVEC")) {
                 k_node_matvec<<<dim3(d, (P.width[pe] + MV_OUT - 1) / MV_OUT), 256, 0, stream>>>(n, md, qchild); count_launch();
             } else if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB >= 16) {
@@ -1804,9 +1888,16 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
     if ((st = dalloc(pool, words * 8, stream, &dres))) return st;
     SKB_CUDA(cudaMemsetAsync(dres, 0, words * 8, stream));
     uint64_t *res = (uint64_t *)dres;
+    // matrix residues shared by every CRT plan of the batch (the first K_max primes; a plan
+    // with K moduli uses the first K)
+    Mods kmax_mods;
+    kmax_mods.K = 0;
+    for (size_t i = 0; i < n; ++i)
+        if (!exact[i] && mds[i].K > kmax_mods.K) kmax_mods = mds[i];
+    std::map<std::pair<const void *, int>, uint32_t *> rescache;
     for (size_t i = 0; i < n; ++i)
         if ((st = enqueue_plan(plans[i], mds[i], uniqs[i], pool, res + off_acc[i], (unsigned long long *)(res + off_l1[i]),
-                               stream, exact[i] ? 1 : 0)))
+                               stream, exact[i] ? 1 : 0, &rescache, &kmax_mods)))
             return st;
     std::vector<uint64_t> host(words);
     SKB_CUDA(cudaMemcpyAsync(host.data(), res, words * 8, cudaMemcpyDeviceToHost, stream));
