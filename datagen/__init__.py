@@ -105,6 +105,9 @@ class Table:
     cols: list
     preds: list = field(default_factory=list)
 
+    def col(self, name: str) -> Col:
+        return next(c for c in self.cols if c.name == name)
+
     def __post_init__(self):
         # value-domain statement of each generated column (a property of the generator)
         for c in self.cols:

@@ -246,6 +246,45 @@ typedef struct {
 SK_API sk_status plan_enumerate(const sk_graph *g, const sk_enum_config *cfg, uint32_t *order, double *prefix_card,
                                 double *cost, sk_enum_stats *stats, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * exact_join_size — the exact cardinality |R_1 join ... join R_k| of an acyclic connected
+ * sub-plan, for the accuracy evaluation of the estimates (accuracy ratio est/true,
+ * PAPER.md:261; normalised L1 distance of orderings).
+ * Frequency-vector message passing on the device: a leaf table sends f(k) = number of its
+ * surviving tuples with join key k; an inner table sends, for each key of its parent edge,
+ * the sum over its surviving tuples of the product of its children's messages at the
+ * tuple's keys; the root sums that product over its surviving tuples.  Exact: every pass is
+ * modulo K primes < 2^26 (K from the bound prod_t n_rows_t) and the count is reconstructed
+ * by CRT on the host.
+ *   tables[t]: n_rows, device columns, predicates exactly as sketch_update_filtered
+ *     (survive(i) = AND of the predicates).
+ *   edge e joins table edge_u[e] column col_u[e] with table edge_v[e] column col_v[e];
+ *     every join key of a surviving tuple must lie in [key_lo[e], key_lo[e] + key_domain[e])
+ *     (SK_EINVAL otherwise; key_domain[e] <= 2^31).
+ *   vertex_mask: the sub-plan (>= 1 table; a single table gives its survivor count).
+ * dec: host buffer receiving the count in decimal (NUL-terminated, dec_len >= 2), or NULL;
+ * approx: host double (the count rounded to nearest), or NULL.
+ * SK_EOVERFLOW for cyclic sub-plans (including parallel edges) and tables with more than
+ * 4 sub-plan edges.  Synchronises `stream`.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    uint64_t n_rows;
+    const sk_column *cols;
+    uint32_t n_cols;
+    const sk_pred *preds;
+    uint32_t n_preds;
+} sk_table_data;
+typedef struct {
+    uint32_t n_tables;
+    const sk_table_data *tables;   /* [n_tables] */
+    uint32_t n_edges;
+    const uint32_t *edge_u, *edge_v, *col_u, *col_v;   /* [n_edges] */
+    const int64_t *key_lo;         /* [n_edges] */
+    const uint64_t *key_domain;    /* [n_edges] */
+} sk_join_data;
+SK_API sk_status exact_join_size(const sk_join_data *jd, uint64_t vertex_mask, char *dec, uint32_t dec_len,
+                                 double *approx, void *stream);
+
 /* Thread-local description of the last error (never NULL). */
 SK_API const char *sk_last_error(void);
 

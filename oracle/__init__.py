@@ -458,6 +458,75 @@ def leftdeep_costs_bruteforce(names, edges, card_fn):
     return out
 
 
+def exact_join_size(tables, edges, subset):
+    """Exact |join| of an acyclic connected sub-plan (the truth of the
+    accuracy ratio).  tables: {alias: (columns dict, preds)}; edges: list of
+    (u, v, col_u, col_v); subset: aliases.  Message passing over the join tree with Python
+    integers: a table sends, per key of its parent edge, the sum over its surviving tuples of
+    the product of its children's messages at the tuple's keys.  Pinned by
+    exact_join_size_bruteforce."""
+    S = sorted(set(subset))
+    E = [e for e in edges if e[0] in S and e[1] in S]
+    if len(E) != len(S) - 1:
+        raise ValueError("cyclic or disconnected sub-plan")
+    masks = {t: filter_mask(tables[t][0], tables[t][1])[0] for t in S}
+    root = S[0]
+
+    def send(t, parent_edge):
+        cols = tables[t][0]
+        rows = np.nonzero(masks[t])[0]
+        child = []
+        for e in E:
+            if e is parent_edge or t not in (e[0], e[1]):
+                continue
+            c, col = (e[1], e[2]) if e[0] == t else (e[0], e[3])
+            child.append((col, send(c, e)))
+        out = {}
+        pcol = None if parent_edge is None else (parent_edge[2] if parent_edge[0] == t else parent_edge[3])
+        total = 0
+        for i in rows:
+            v = 1
+            for col, m in child:
+                v *= m.get(int(cols[col][i]), 0)
+                if v == 0:
+                    break
+            if pcol is None:
+                total += v
+            elif v:
+                k = int(cols[pcol][i])
+                out[k] = out.get(k, 0) + v
+        return total if pcol is None else out
+    return send(root, None)
+
+
+def exact_join_size_bruteforce(tables, edges, subset) -> int:
+    """The literal definition (tiny inputs only): the number of combinations of one surviving
+    tuple per table that agree on every induced join edge."""
+    from itertools import product
+    S = sorted(set(subset))
+    E = [e for e in edges if e[0] in S and e[1] in S]
+    rows = {t: np.nonzero(filter_mask(tables[t][0], tables[t][1])[0])[0].tolist() for t in S}
+    n = 0
+    for combo in product(*[rows[t] for t in S]):
+        pick = dict(zip(S, combo))
+        if all(int(tables[u][0][cu][pick[u]]) == int(tables[v][0][cv][pick[v]]) for u, v, cu, cv in E):
+            n += 1
+    return n
+
+
+def accuracy_report(estimates: dict, truths: dict):
+    """PAPER.md:261 accuracy ratio est/true per sub-plan, and PAPER.md:294 normalised L1
+    distance per sub-plan size (permutation_l1 / number of sub-plans of that size).
+    estimates, truths: {sub-plan (tuple of aliases): value}.  Returns {size: (ratios, l1)}."""
+    out = {}
+    for size in sorted({len(s) for s in truths}):
+        keys = sorted(s for s in truths if len(s) == size)
+        ratios = [float(estimates[s]) / float(truths[s]) if truths[s] else float("inf") for s in keys]
+        l1 = permutation_l1([estimates[s] for s in keys], [truths[s] for s in keys]) / len(keys)
+        out[size] = (ratios, l1)
+    return out
+
+
 def permutation_l1(estimates, truths) -> int:
     """Normalised-L1 numerator: sum_i |S_i - C_i|, ranks by ascending
     value, ties by stable original index."""

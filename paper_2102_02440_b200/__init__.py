@@ -65,7 +65,7 @@ class sk_graph(ctypes.Structure):
 # every symbol include/compass_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = ["sketch_create", "sketch_destroy", "sketch_counters", "sketch_zero", "sketch_update_filtered",
            "sketch_merge", "estimate_join", "estimate_join_exact", "estimate_subplans", "plan_greedy",
-           "plan_enumerate", "sk_last_error", "sk_version", "sk_kernel_launches"]
+           "plan_enumerate", "exact_join_size", "sk_last_error", "sk_version", "sk_kernel_launches"]
 
 # Algorithm 1 search-space settings
 ENUM_GREEDY, ENUM_FULL_GREEDY, ENUM_LIMIT, ENUM_EXHAUSTIVE = range(4)
@@ -76,6 +76,19 @@ ENUM_MODES = {"greedy": ENUM_GREEDY, "full-greedy": ENUM_FULL_GREEDY, "limit": E
 class sk_enum_config(ctypes.Structure):
     _fields_ = [("alpha", ctypes.c_double), ("beta", ctypes.c_double), ("mode", ctypes.c_uint32),
                 ("max_plans", ctypes.c_uint32), ("no_prune", ctypes.c_uint32)]
+
+
+class sk_table_data(ctypes.Structure):
+    _fields_ = [("n_rows", ctypes.c_uint64), ("cols", ctypes.POINTER(sk_column)), ("n_cols", ctypes.c_uint32),
+                ("preds", ctypes.POINTER(sk_pred)), ("n_preds", ctypes.c_uint32)]
+
+
+class sk_join_data(ctypes.Structure):
+    _fields_ = [("n_tables", ctypes.c_uint32), ("tables", ctypes.POINTER(sk_table_data)),
+                ("n_edges", ctypes.c_uint32), ("edge_u", ctypes.POINTER(ctypes.c_uint32)),
+                ("edge_v", ctypes.POINTER(ctypes.c_uint32)), ("col_u", ctypes.POINTER(ctypes.c_uint32)),
+                ("col_v", ctypes.POINTER(ctypes.c_uint32)), ("key_lo", ctypes.POINTER(ctypes.c_int64)),
+                ("key_domain", ctypes.POINTER(ctypes.c_uint64))]
 
 
 class sk_enum_stats(ctypes.Structure):
@@ -122,6 +135,9 @@ def lib() -> ctypes.CDLL:
         L.plan_enumerate.argtypes = [ctypes.POINTER(sk_graph), ctypes.POINTER(sk_enum_config), ctypes.POINTER(u32),
                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(sk_enum_stats), vp]
+        L.exact_join_size.restype = st
+        L.exact_join_size.argtypes = [ctypes.POINTER(sk_join_data), u64, ctypes.c_char_p, u32,
+                                      ctypes.POINTER(ctypes.c_double), vp]
         L.sk_last_error.restype = ctypes.c_char_p
         L.sk_last_error.argtypes = []
         L.sk_kernel_launches.restype = ctypes.c_uint64
@@ -222,6 +238,56 @@ def sketch_update_filtered(columns, n_rows: int, preds, targets, survivors: torc
     sp = ctypes.c_void_p(survivors.data_ptr()) if survivors is not None else None
     _check(lib().sketch_update_filtered(cols, ncol, n_rows, pr, len(preds), tg, len(targets), sp,
                                         ctypes.c_void_p(_stream_ptr(stream))))
+
+
+def _columns(columns, domains=None):
+    cols = (sk_column * max(1, len(columns)))()
+    for i, c in enumerate(columns):
+        assert c.is_cuda and c.dtype in (torch.int32, torch.int64) and c.is_contiguous()
+        cols[i].data = c.data_ptr()
+        cols[i].dtype = SK_INT64 if c.dtype == torch.int64 else SK_INT32
+        cols[i].domain = int(domains[i]) if domains else 0
+    return cols
+
+
+def _preds(preds, keep):
+    pr = (sk_pred * max(1, len(preds)))()
+    for i, p in enumerate(preds):
+        p = tuple(p) + (None,) * (5 - len(p))
+        pr[i].col, pr[i].kind, pr[i].lo, pr[i].hi = p[0], p[1], p[2], p[3]
+        if p[1] == SUBSET:
+            vals = list(p[4] or [])
+            arr = (ctypes.c_int64 * max(1, len(vals)))(*vals)
+            keep.append(arr)
+            pr[i].set = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int64))
+            pr[i].set_size = len(vals)
+    return pr
+
+
+def exact_join_size(tables, edges, subset_mask: int, stream=None) -> int:
+    """Exact |join| of an acyclic connected sub-plan (accuracy evaluation).
+    tables: list of (columns [int32/int64 CUDA tensors], preds as in sketch_update_filtered);
+    edges: list of (u, v, col_u, col_v, key_lo, key_domain); subset_mask: bit t = table t."""
+    keep = []
+    tds = (sk_table_data * len(tables))()
+    for i, (cols, preds) in enumerate(tables):
+        c = _columns(cols)
+        p = _preds(preds, keep)
+        keep += [c, p]
+        tds[i].n_rows = int(cols[0].numel()) if cols else 0
+        tds[i].cols, tds[i].n_cols = ctypes.cast(c, ctypes.POINTER(sk_column)), len(cols)
+        tds[i].preds, tds[i].n_preds = ctypes.cast(p, ctypes.POINTER(sk_pred)), len(preds)
+    E = len(edges)
+    arr = lambda t, vals: (t * max(1, E))(*vals)
+    eu, ev = arr(ctypes.c_uint32, [e[0] for e in edges]), arr(ctypes.c_uint32, [e[1] for e in edges])
+    cu, cv = arr(ctypes.c_uint32, [e[2] for e in edges]), arr(ctypes.c_uint32, [e[3] for e in edges])
+    lo, dom = arr(ctypes.c_int64, [e[4] for e in edges]), arr(ctypes.c_uint64, [e[5] for e in edges])
+    jd = sk_join_data(len(tables), tds, E, eu, ev, cu, cv, lo, dom)
+    buf = ctypes.create_string_buffer(256)
+    approx = ctypes.c_double()
+    _check(lib().exact_join_size(ctypes.byref(jd), subset_mask, buf, 256, ctypes.byref(approx),
+                                 ctypes.c_void_p(_stream_ptr(stream))))
+    return int(buf.value.decode())
 
 
 def sketch_merge(dst: Sketch, src: Sketch, stream=None):

@@ -1076,6 +1076,88 @@ __global__ void __launch_bounds__(512) k_dot128(const __grid_constant__ DotItems
     }
 }
 
+// ---------------------------------------------------------------- exact join size (accuracy evaluation)
+// Frequency-vector message passing modulo one prime per blockIdx.y:
+// messages [K][dom] hold lazily summed residues (< 2^26 each, so 2^38 additions fit in 64
+// bits) and are reduced once after the node's pass.
+constexpr int kXCols = 8, kXPreds = 8, kXChild = 4;
+struct XPred { uint32_t col, kind; int64_t lo, hi; const int64_t *set; uint32_t n; };
+struct XChild { const uint64_t *msg; uint32_t col; int64_t lo; uint64_t dom; };
+struct XNode {
+    const void *col[kXCols];
+    uint32_t col64;
+    uint64_t n_rows;
+    uint32_t n_preds;
+    XPred pred[kXPreds];
+    uint32_t n_child;
+    XChild ch[kXChild];
+    int has_parent;
+    uint32_t pcol;
+    int64_t plo;
+    uint64_t pdom;
+    uint64_t *out;       // parent message [K][pdom], or the root's residues [K]
+};
+__device__ __forceinline__ int64_t xval(const XNode &n, uint32_t c, uint64_t row) {
+    if ((n.col64 >> c) & 1u) return __ldg(reinterpret_cast<const long long *>(n.col[c]) + row);
+    return (int64_t)__ldg(reinterpret_cast<const int *>(n.col[c]) + row);
+}
+__device__ __forceinline__ bool xin_set(const int64_t *s, uint32_t n, int64_t v) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(reinterpret_cast<const long long *>(s) + mid) < v) lo = mid + 1; else hi = mid;
+    }
+    return lo < n && __ldg(reinterpret_cast<const long long *>(s) + lo) == v;
+}
+__global__ void k_exact_node(const __grid_constant__ XNode n, const __grid_constant__ Mods md, unsigned int *err) {
+    __shared__ uint64_t red[32];
+    const int k = blockIdx.y;
+    const uint64_t m = md.m[k], mu = md.mu[k];
+    uint64_t acc = 0;
+    for (uint64_t row = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < n.n_rows;
+         row += uint64_t(gridDim.x) * blockDim.x) {
+        bool ok = true;
+        for (uint32_t q = 0; q < n.n_preds && ok; ++q) {
+            const XPred &pr = n.pred[q];
+            const int64_t v = xval(n, pr.col, row);
+            if (pr.kind == SK_PRED_POINT) ok = v == pr.lo;
+            else if (pr.kind == SK_PRED_RANGE) ok = pr.lo <= v && v <= pr.hi;
+            else ok = xin_set(pr.set, pr.n, v);
+        }
+        if (!ok) continue;
+        uint64_t v = 1;
+        for (uint32_t c = 0; c < n.n_child; ++c) {
+            const uint64_t key = (uint64_t)(xval(n, n.ch[c].col, row) - n.ch[c].lo);
+            if (key >= n.ch[c].dom) { atomicOr(err, 1u); v = 0; break; }
+            v = mm_mul(v, n.ch[c].msg[uint64_t(k) * n.ch[c].dom + key], m, mu);
+        }
+        if (n.has_parent) {
+            const uint64_t key = (uint64_t)(xval(n, n.pcol, row) - n.plo);
+            if (key >= n.pdom) { atomicOr(err, 1u); continue; }
+            if (v) atomicAdd(reinterpret_cast<unsigned long long *>(n.out + uint64_t(k) * n.pdom + key), (unsigned long long)v);
+        } else {
+            acc += v;   // < 2^26 per row
+        }
+    }
+    if (!n.has_parent) {
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        if (lane == 0) red[wid] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t t = 0;
+            for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+            atomicAdd(reinterpret_cast<unsigned long long *>(n.out + k), (unsigned long long)mm_red(t, m, mu));
+        }
+    }
+}
+// msg[k][i] mod m_k
+__global__ void k_mod_reduce(uint64_t *msg, uint64_t dom, const __grid_constant__ Mods md) {
+    const int k = blockIdx.y;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < dom; i += uint64_t(gridDim.x) * blockDim.x)
+        msg[uint64_t(k) * dom + i] = mm_red(msg[uint64_t(k) * dom + i], md.m[k], md.mu[k]);
+}
+
 // ---------------------------------------------------------------- host big integers (Garner)
 struct UBig {
     std::vector<uint64_t> l;  // little-endian limbs
@@ -2278,4 +2360,151 @@ extern "C" sk_status plan_enumerate(const sk_graph *g, const sk_enum_config *cfg
     if (cost) *cost = best_cost;
     if (stats) *stats = es;
     return cc.err;
+}
+
+extern "C" sk_status exact_join_size(const sk_join_data *jd, uint64_t mask, char *dec, uint32_t dec_len, double *approx,
+                                     void *stream_) {
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (!jd || !jd->tables) return fail(SK_EINVAL, "exact_join_size: NULL argument");
+    if (dec && dec_len < 2) return fail(SK_EINVAL, "exact_join_size: dec_len must be >= 2");
+    const uint32_t T = jd->n_tables;
+    if (T == 0 || T > 64) return fail(SK_EINVAL, "exact_join_size: n_tables must be in [1,64]");
+    if (mask == 0 || (T < 64 && (mask >> T))) return fail(SK_EINVAL, "exact_join_size: bad vertex mask");
+    for (uint32_t t = 0; t < T; ++t) {
+        const sk_table_data &td = jd->tables[t];
+        if (td.n_cols > (uint32_t)kXCols || td.n_preds > (uint32_t)kXPreds)
+            return fail(SK_EINVAL, "exact_join_size: table %u has too many columns/predicates", t);
+        if ((td.n_cols && !td.cols) || (td.n_preds && !td.preds)) return fail(SK_EINVAL, "exact_join_size: NULL array");
+        for (uint32_t q = 0; q < td.n_preds; ++q)
+            if (td.preds[q].col >= td.n_cols || td.preds[q].kind > SK_PRED_SUBSET)
+                return fail(SK_EINVAL, "exact_join_size: table %u predicate %u invalid", t, q);
+    }
+    // induced edges; acyclic and connected (|E_C| = |C| - 1)
+    std::vector<uint32_t> ed;
+    for (uint32_t e = 0; e < jd->n_edges; ++e) {
+        const uint32_t u = jd->edge_u[e], v = jd->edge_v[e];
+        if (u >= T || v >= T || u == v) return fail(SK_EINVAL, "exact_join_size: bad edge %u", e);
+        if (jd->col_u[e] >= jd->tables[u].n_cols || jd->col_v[e] >= jd->tables[v].n_cols)
+            return fail(SK_EINVAL, "exact_join_size: edge %u column out of range", e);
+        if (jd->key_domain[e] == 0 || jd->key_domain[e] > (1ULL << 31))
+            return fail(SK_EINVAL, "exact_join_size: edge %u key domain must be in [1, 2^31]", e);
+        if (((mask >> u) & 1ULL) && ((mask >> v) & 1ULL)) ed.push_back(e);
+    }
+    const int nC = __builtin_popcountll(mask);
+    if ((int)ed.size() != nC - 1) {
+        if ((int)ed.size() > nC - 1) return fail(SK_EOVERFLOW, "exact_join_size: cyclic sub-plans are unsupported");
+        return fail(SK_EINVAL, "exact_join_size: sub-plan is not connected");
+    }
+    const int root = __builtin_ctzll(mask);
+    // DFS from the root: parent edge per table, post-order
+    std::vector<int> pe(T, -2), order;
+    {
+        std::vector<int> st{root}, pre;
+        pe[root] = -1;
+        while (!st.empty()) {
+            const int x = st.back();
+            st.pop_back();
+            pre.push_back(x);
+            for (uint32_t e : ed) {
+                const int u = (int)jd->edge_u[e], v = (int)jd->edge_v[e];
+                const int y = u == x ? v : (v == x ? u : -1);
+                if (y < 0 || pe[y] != -2) continue;
+                pe[y] = (int)e;
+                st.push_back(y);
+            }
+        }
+        if ((int)pre.size() != nC) return fail(SK_EINVAL, "exact_join_size: sub-plan is not connected");
+        order.assign(pre.rbegin(), pre.rend());
+    }
+    double logB = 1;
+    for (int t : order) logB += log2(std::max<double>(1.0, (double)jd->tables[t].n_rows));
+    const Mods md = mods_for(logB, 1);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    DevPool pool;
+    sk_status st;
+    void *derr, *dacc;
+    if ((st = dalloc(pool, 16, stream, &derr))) return st;
+    if ((st = dalloc(pool, size_t(md.K) * 8, stream, &dacc))) return st;
+    SKB_CUDA(cudaMemsetAsync(derr, 0, 16, stream));
+    SKB_CUDA(cudaMemsetAsync(dacc, 0, size_t(md.K) * 8, stream));
+    std::vector<uint64_t *> msg(jd->n_edges, nullptr);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, prev);
+    for (int t : order) {
+        const sk_table_data &td = jd->tables[t];
+        XNode n;
+        memset(&n, 0, sizeof(n));
+        n.n_rows = td.n_rows;
+        for (uint32_t c = 0; c < td.n_cols; ++c) {
+            if (!td.cols[c].data && td.n_rows) return fail(SK_EINVAL, "exact_join_size: table %d column %u is NULL", t, c);
+            n.col[c] = td.cols[c].data;
+            if (td.cols[c].dtype == SK_INT64) n.col64 |= 1u << c;
+            else if (td.cols[c].dtype != SK_INT32) return fail(SK_EINVAL, "exact_join_size: bad dtype");
+        }
+        n.n_preds = td.n_preds;
+        for (uint32_t q = 0; q < td.n_preds; ++q) {
+            const sk_pred &pr = td.preds[q];
+            n.pred[q] = XPred{pr.col, pr.kind, pr.lo, pr.hi, nullptr, 0};
+            if (pr.kind == SK_PRED_SUBSET) {
+                if (pr.set_size && !pr.set) return fail(SK_EINVAL, "exact_join_size: NULL subset");
+                std::vector<int64_t> sv(pr.set, pr.set + pr.set_size);
+                std::sort(sv.begin(), sv.end());
+                sv.erase(std::unique(sv.begin(), sv.end()), sv.end());
+                n.pred[q].n = (uint32_t)sv.size();
+                if (!sv.empty()) {
+                    void *ds;
+                    if ((st = dalloc(pool, sv.size() * 8, stream, &ds))) return st;
+                    SKB_CUDA(cudaMemcpyAsync(ds, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice, stream));
+                    n.pred[q].set = (const int64_t *)ds;
+                }
+            }
+        }
+        for (uint32_t e : ed) {
+            if ((int)e == pe[t]) continue;
+            const bool at_u = (int)jd->edge_u[e] == t, at_v = (int)jd->edge_v[e] == t;
+            if (!at_u && !at_v) continue;
+            if (n.n_child == (uint32_t)kXChild) return fail(SK_EOVERFLOW, "exact_join_size: table %d has > 4 sub-plan edges", t);
+            n.ch[n.n_child++] = XChild{msg[e], at_u ? jd->col_u[e] : jd->col_v[e], jd->key_lo[e], jd->key_domain[e]};
+        }
+        if (pe[t] >= 0) {
+            const uint32_t e = (uint32_t)pe[t];
+            void *mb;
+            if ((st = dalloc(pool, size_t(md.K) * jd->key_domain[e] * 8, stream, &mb))) return st;
+            SKB_CUDA(cudaMemsetAsync(mb, 0, size_t(md.K) * jd->key_domain[e] * 8, stream));
+            msg[e] = (uint64_t *)mb;
+            n.has_parent = 1;
+            n.pcol = (int)jd->edge_u[e] == t ? jd->col_u[e] : jd->col_v[e];
+            n.plo = jd->key_lo[e];
+            n.pdom = jd->key_domain[e];
+            n.out = msg[e];
+        } else {
+            n.out = (uint64_t *)dacc;
+        }
+        const unsigned gx = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(sms) * 4, (td.n_rows + 255) / 256));
+        k_exact_node<<<dim3(gx, md.K), 256, 0, stream>>>(n, md, (unsigned int *)derr); count_launch();
+        SKB_CUDA_CHECK("k_exact_node launch");
+        if (pe[t] >= 0) {
+            const uint64_t dom = jd->key_domain[pe[t]];
+            k_mod_reduce<<<dim3((unsigned)std::min<uint64_t>(uint64_t(sms) * 4, (dom + 255) / 256), md.K), 256, 0, stream>>>(
+                msg[pe[t]], dom, md);
+            count_launch();
+        }
+    }
+    uint64_t herr[2] = {0, 0};
+    std::vector<uint64_t> hacc(md.K);
+    SKB_CUDA(cudaMemcpyAsync(herr, derr, 16, cudaMemcpyDeviceToHost, stream));
+    SKB_CUDA(cudaMemcpyAsync(hacc.data(), dacc, size_t(md.K) * 8, cudaMemcpyDeviceToHost, stream));
+    SKB_CUDA(cudaStreamSynchronize(stream));
+    if (herr[0] & 0xffffffffu) return fail(SK_EINVAL, "exact_join_size: a join key lies outside its edge's key domain");
+    for (int k = 0; k < md.K; ++k) hacc[k] %= md.m[k];
+    const SBig v = crt_signed(hacc.data(), md);
+    if (v.neg && !v.mag.zero()) return fail(SK_ECUDA, "exact_join_size: negative count (internal error)");
+    if (dec) {
+        const std::string sd = v.to_dec();
+        if (sd.size() + 1 > dec_len) return fail(SK_EINVAL, "exact_join_size: dec_len too small");
+        memcpy(dec, sd.c_str(), sd.size() + 1);
+    }
+    if (approx) *approx = v.to_double();
+    return SK_OK;
 }

@@ -517,6 +517,47 @@ def test_enumerate_search_space_nesting():
         assert ce <= cl <= cf and c1 == cf
 
 
+# ---------------------------------------------------------------- exact join sizes (accuracy truth)
+def _tiny_tables(rng, names, n):
+    T = {}
+    for t in names:
+        cols = {"k": rng.integers(0, 3, n), "j": rng.integers(0, 3, n), "p": rng.integers(0, 10, n)}
+        preds = [[], [("p", RANGE, 2, 8)], [("p", SUBSET, 0, 0, [1, 3, 5, 7, 9])], [("p", POINT, 4, 4)]][int(rng.integers(0, 4))]
+        T[t] = (cols, preds)
+    return T
+
+
+def test_exact_join_size_equals_nested_loop_definition():
+    """Message passing == the literal definition (every combination of one surviving tuple per
+    table that agrees on every join edge), on random chains, stars and trees with predicates."""
+    rng = np.random.default_rng(21)
+    shapes = [[("A", "B", "k", "k")], [("A", "B", "k", "k"), ("B", "C", "j", "j")],
+              [("A", "B", "k", "k"), ("A", "C", "j", "k"), ("A", "D", "k", "j")],
+              [("A", "B", "k", "j"), ("B", "C", "k", "k"), ("C", "D", "j", "j")]]
+    for trial in range(30):
+        E = shapes[trial % len(shapes)]
+        names = sorted({x for e in E for x in e[:2]})
+        T = _tiny_tables(rng, names, int(rng.integers(1, 7)))
+        for k in range(1, len(names) + 1):
+            for sub in __import__("itertools").combinations(names, k):
+                induced = [e for e in E if e[0] in sub and e[1] in sub]
+                if len(induced) != len(sub) - 1:
+                    continue
+                if len(sub) > 1 and not oracle.connected(_FakeG({x: 1 for x in names}, [(f"{u}|{v}", u, v) for u, v, *_ in E]), sub):
+                    continue
+                assert oracle.exact_join_size(T, E, sub) == oracle.exact_join_size_bruteforce(T, E, sub), (trial, sub)
+
+
+def test_accuracy_l1_paper_example():
+    """PAPER.md:294 / Table 2: the 4-way joins of JOB 6a, true (6, 1194, 1224) vs sketch
+    merging (198, 18M, 6.5M): L1 distance 0 + 1 + 1 = 2, normalised by the 3 sub-plans."""
+    truths = {("ci", "k", "mk", "n"): 6, ("ci", "mk", "n", "t"): 1194, ("ci", "k", "mk", "t"): 1224}
+    est = {("ci", "k", "mk", "n"): 198, ("ci", "mk", "n", "t"): 18_000_000, ("ci", "k", "mk", "t"): 6_500_000}
+    rep = oracle.accuracy_report(est, truths)
+    assert rep[4][1] == 2 / 3
+    assert rep[4][0] == [198 / 6, 6_500_000 / 1224, 18_000_000 / 1194]
+
+
 # ---------------------------------------------------------------- P10 C1 end to end
 def test_c1_estimate_vs_exact_join():
     import datagen

@@ -389,3 +389,87 @@ def test_c3_full_width_triangle_sampled_row(est_engine):
     jg = run.graph()
     for s in [("CI", "MK", "T"), ("CI", "K", "MK", "N", "T")]:
         assert jg.estimate_join_exact(s)[0] == oracle.estimate_rows(og, s, rows=[0])[0]
+
+
+# ------------------------------------------------------------------ exact join sizes (accuracy, §8(f) 2)
+XSHAPES = [[("A", "B", "k", "k")], [("A", "B", "k", "k"), ("B", "C", "j", "j"), ("C", "D", "k", "j")],
+           [("A", "B", "k", "k"), ("A", "C", "j", "k"), ("A", "D", "k", "j"), ("D", "E", "k", "k")]]
+
+
+def _xtables(rng, names, n, dom):
+    T = {}
+    for t in names:
+        cols = {"k": rng.integers(0, dom, n).astype(np.int32), "j": rng.integers(0, dom, n).astype(np.int64),
+                "p": rng.integers(0, 100, n).astype(np.int32)}
+        preds = [[], [("p", pb.RANGE, 5, 90)], [("p", pb.SUBSET, 0, 0, list(range(0, 100, 3)))],
+                 [("p", pb.POINT, 7, 7)]][int(rng.integers(0, 4))]
+        T[t] = (cols, preds)
+    return T
+
+
+def _x_gpu_args(T, E, names, dom):
+    tables, cpos = [], {}
+    for t in names:
+        cols, preds = T[t]
+        cn = list(cols)
+        cpos[t] = {c: i for i, c in enumerate(cn)}
+        tables.append(([torch.from_numpy(cols[c]).to(_dev()) for c in cn],
+                       [(cn.index(p[0]),) + tuple(p[1:]) for p in preds]))
+    edges = [(names.index(u), names.index(v), cpos[u][cu], cpos[v][cv], 0, dom) for u, v, cu, cv in E]
+    return tables, edges
+
+
+@pytest.mark.parametrize("si", range(len(XSHAPES)))
+def test_exact_join_size_equals_oracle(si):
+    """Every acyclic connected sub-plan of random trees (counts far beyond 2^64 on the larger
+    cases: several CRT moduli) — exact decimal equality with the oracle's Python integers."""
+    from paper_2102_02440_b200 import accuracy
+    rng = np.random.default_rng(400 + si)
+    E = XSHAPES[si]
+    names = sorted({x for e in E for x in e[:2]})
+    for n, dom in [(1, 4), (2000, 16), (50_000, 64)]:
+        T = _xtables(rng, names, n, dom)
+        tables, edges = _x_gpu_args(T, E, names, dom)
+        for sub in accuracy.acyclic_connected_subplans(names, edges, min_size=1):
+            got = pb.exact_join_size(tables, edges, sum(1 << names.index(t) for t in sub))
+            assert got == oracle.exact_join_size(T, E, sub), (si, n, sub)
+
+
+def test_exact_join_size_errors():
+    rng = np.random.default_rng(5)
+    E = [("A", "B", "k", "k"), ("B", "C", "j", "j"), ("A", "C", "j", "k")]   # a triangle
+    names = ["A", "B", "C"]
+    T = _xtables(rng, names, 100, 8)
+    tables, edges = _x_gpu_args(T, E, names, 8)
+    with pytest.raises(pb.SkError) as ei:
+        pb.exact_join_size(tables, edges, 0b111)
+    assert ei.value.status == pb.SK_EOVERFLOW
+    tables, edges = _x_gpu_args(T, E, names, 4)          # keys in [0, 8) outside the domain [0, 4)
+    with pytest.raises(pb.SkError) as ei:
+        pb.exact_join_size(tables, edges, 0b011)
+    assert ei.value.status == pb.SK_EINVAL
+
+
+@pytest.mark.parametrize("which", ["C2", "C5"])
+def test_accuracy_report_equals_oracle(which):
+    """The accuracy evaluation of PAPER.md:261/294 on scaled C2 and C5-chain: GPU estimates and
+    GPU exact counts give the same ratios and normalised L1 distances as the oracle's."""
+    from paper_2102_02440_b200 import accuracy
+    ws = datagen.c2(scale=0.01) if which == "C2" else datagen.c5(scale=2e-4, w=128, wm=64)
+    run, data_h, preds = _run_workload(ws)
+    og, surv = _oracle_workload(ws, data_h, preds)
+    data_d = {t.name: {k: torch.from_numpy(v).to(_dev()) for k, v in data_h[t.name].items()} for t in ws.tables}
+    tables, edges, names = accuracy.join_data(ws, data_d, preds)
+    subs = accuracy.acyclic_connected_subplans(names, edges)
+    truths = accuracy.exact_counts(tables, edges, names, subs)
+    jg = run.graph()
+    ests = dict(zip(subs, jg.estimate_subplans(subs)))
+    got = accuracy.report(ests, truths)
+    # oracle side
+    T = {t.name: (data_h[t.name], preds[t.name]) for t in ws.tables}
+    keycol = {(s.table, s.edge_ids[0]): s.key_cols[0] for s in ws.sketches if len(s.edge_ids) == 1}
+    OE = [(u, v, keycol[(u, e)], keycol[(v, e)]) for e, u, v in ws.edges]
+    o_truths = {s: oracle.exact_join_size(T, OE, s) for s in subs}
+    assert o_truths == truths
+    want = oracle.accuracy_report({s: oracle.estimate(og, s)[0] for s in subs}, o_truths)
+    assert got == want
