@@ -163,6 +163,8 @@ extern "C" sk_status sketch_destroy(sk_sketch *sk) {
     cudaDeviceSynchronize();
     if (sk->owned && sk->counters) cudaFree(sk->counters);
     if (sk->seeds_dev) cudaFree(sk->seeds_dev);
+    for (int q = 0; q < 2; ++q)
+        if (sk->lut[q]) cudaFree(sk->lut[q]);
     cudaSetDevice(prev);
     delete sk;
     return SK_OK;

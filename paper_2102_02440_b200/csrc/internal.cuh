@@ -23,6 +23,11 @@ struct sk_sketch {
     // per dimension q, per row r: {a0, a1, a2, a3, b0, b1} (H2), on device and host
     uint64_t *seeds_dev = nullptr;
     std::vector<uint64_t> seeds_host;
+    // per dimension q: hash lookup table over a hinted key domain [0, lut_dom[q]):
+    // lut[q][x * d + r] = (h_r(x) & (w_q - 1)) << 1 | (xi_r(x) < 0); built on first use
+    // (the seeds never change), freed with the sketch
+    uint32_t *lut[2] = {nullptr, nullptr};
+    uint64_t lut_dom[2] = {0, 0};
 };
 
 namespace skb {

@@ -90,6 +90,8 @@ struct STarget {
     int32_t smem_off;     // int32 offset of privatised copy, -1 = global
     uint32_t cells;
     uint32_t seed_off;
+    const uint32_t *lut0, *lut1;   // matrices: per-dimension hash lookup tables (or null)
+    uint64_t lut_dom0, lut_dom1;
 };
 struct SParams {
     SCol col[kMaxSCols];
@@ -250,6 +252,19 @@ __device__ __forceinline__ void update_2d_t(const STarget &tg, const uint64_t *s
 }
 __device__ __forceinline__ void update_2d(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, uint64_t y,
                                           int cnt) {
+    if (tg.lut0 && x < tg.lut_dom0 && y < tg.lut_dom1) {
+        // hinted key domains: (bucket, sign) per row from the lookup tables (the same values
+        // the hash polynomials give; built once per sketch by k_lut_build)
+        const uint32_t *la = tg.lut0 + x * tg.d, *lb = tg.lut1 + y * tg.d;
+        for (uint32_t r = 0; r < tg.d; ++r) {
+            const uint32_t ea = __ldg(la + r), eb = __ldg(lb + r);
+            const uint32_t cell = ((ea >> 1) << tg.lw1) | (eb >> 1);
+            const int v = ((ea ^ eb) & 1u) ? -cnt : cnt;
+            if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
+            else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
+        }
+        return;
+    }
     if ((x | y) < (1ULL << 32)) update_2d_t<true>(tg, seed, sc, x, y, cnt);
     else update_2d_t<false>(tg, seed, sc, x, y, cnt);
 }
@@ -849,6 +864,20 @@ __global__ void __launch_bounds__(512) k_hist_epilogue(const __grid_constant__ E
     }
 }
 
+// hash lookup table of one sketch dimension over keys [0, dom): lut[x * d + r] =
+// (h_r(x) & wmask) << 1 | (xi_r(x) < 0)   (H3/H4 for x < 2^32: the narrow path)
+__global__ void k_lut_build(const uint64_t *seeds, uint32_t d, uint32_t wmask, uint64_t dom, uint32_t *lut) {
+    const uint64_t total = dom * d;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t x = e / d;
+        const uint32_t r = (uint32_t)(e % d);
+        const uint64_t *a = seeds + r * 6;
+        const uint32_t b = (uint32_t)(hash_g61_t<true>(__ldg(a + 4), __ldg(a + 5), x) & wmask);
+        uint64_t sa[4] = {__ldg(a), __ldg(a + 1), __ldg(a + 2), __ldg(a + 3)};
+        lut[e] = (b << 1) | (xi_sign61_t<true>(sa, x) < 0 ? 1u : 0u);
+    }
+}
+
 typedef void (*ScanKernel)(const SParams);
 
 template <int NK, int NP>
@@ -1014,6 +1043,37 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     }
     P.smem_counters = sc_count;
     avail -= (sc_count * 4 + 15) & ~15u;
+    // hash lookup tables for matrix dimensions whose key column has a domain hint (the table
+    // stays L2-resident: dom * d * 4 bytes <= 64 MB per dimension); built once per sketch
+    if (!(getenv("COMPASS_LUT") && strcmp(getenv("COMPASS_LUT"), "0") == 0)) {
+        int dev_l = 0, sms_l = 148;
+        cudaGetDevice(&dev_l);
+        cudaDeviceGetAttribute(&sms_l, cudaDevAttrMultiProcessorCount, dev_l);
+        for (uint32_t t = 0; t < c.n_targets; ++t) {
+            STarget &tg = P.tgt[t];
+            tg.lut0 = tg.lut1 = nullptr;
+            if (tg.ndim != 2 || !c.tgt_sketch[t]) continue;
+            sk_sketch *sk = c.tgt_sketch[t];
+            const uint64_t dom[2] = {c.col_domain[c.tgt_key[t][0]], c.col_domain[c.tgt_key[t][1]]};
+            bool ok = true;
+            for (int q = 0; q < 2; ++q) ok &= dom[q] > 0 && dom[q] <= (1ULL << 31) && dom[q] * sk->d * 4 <= (64ULL << 20);
+            if (!ok) continue;
+            for (int q = 0; q < 2; ++q) {
+                if (sk->lut[q] && sk->lut_dom[q] >= dom[q]) continue;
+                if (sk->lut[q]) { cudaFree(sk->lut[q]); sk->lut[q] = nullptr; }
+                SKB_CUDA(cudaMalloc(&sk->lut[q], dom[q] * sk->d * 4));
+                k_lut_build<<<(unsigned)std::min<uint64_t>(uint64_t(sms_l) * 8, (dom[q] * sk->d + 255) / 256), 256, 0, stream>>>(
+                    sk->seeds_dev + size_t(q) * sk->d * 6, sk->d, sk->w[q] - 1, dom[q], sk->lut[q]);
+                SKB_CUDA(cudaGetLastError());
+                count_launch();
+                sk->lut_dom[q] = dom[q];
+            }
+            tg.lut0 = sk->lut[0];
+            tg.lut1 = sk->lut[1];
+            tg.lut_dom0 = dom[0];
+            tg.lut_dom1 = dom[1];
+        }
+    }
     // trio detection: matrix M whose dimension-q hash rows equal those of a privatised 1-D
     // sketch on the same key (exact comparison of the coefficient rows; same d)
     P.trio_on = 0;

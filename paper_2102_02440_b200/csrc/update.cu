@@ -274,6 +274,7 @@ extern "C" sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_co
             sc.tgt_key[t][1] = sk->ndim == 2 ? targets[t].key_col[1] : 0;
             sc.tgt_seeds[t] = sk->seeds_dev;
             sc.tgt_seeds_host[t] = sk->seeds_host.data();
+            sc.tgt_sketch[t] = const_cast<sk_sketch *>(sk);
         }
         sc.survivors = p.survivors;
         bool launched = false;
