@@ -171,7 +171,11 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 // commits the current (possibly partial) group too: every cp.async issued so far has landed
 __device__ __forceinline__ void cp_commit_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_lag() { asm volatile("cp.async.wait_group 3;" ::: "memory"); }
+#ifndef SCAN_LAG
+#define SCAN_LAG 3
+#endif
+constexpr int kLag = SCAN_LAG;   // a tile's gathered keys are consumed kLag tiles later
+__device__ __forceinline__ void cp_wait_lag() { asm volatile("cp.async.wait_group %0;" ::"n"(kLag) : "memory"); }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 __device__ __forceinline__ void red_add_u32(uint32_t *p, uint32_t v) {
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -621,7 +625,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
     const uint32_t q_a = smem_u32(q);
     const uint32_t rl_a = smem_u32(smem + P.off_rows) + warp * 256;   // this warp's survivor row list
     uint32_t head = 0, tail = 0;             // ring positions (monotone)
-    uint32_t t1 = 0, t2 = 0, t3 = 0;         // ring tail after the previous 1, 2, 3 tiles
+    uint32_t tl[kLag];                       // ring tail after each of the previous kLag tiles
+#pragma unroll
+    for (int i = 0; i < kLag; ++i) tl[i] = 0;
     const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t n_tiles = (uint32_t)P.n_tiles;
@@ -686,7 +692,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                                 drain_batch<NK>(P, smem, q, kbytes, head, n);
                                 head += n;
                             }
-                            t1 = t2 = t3 = tail;
+#pragma unroll
+                            for (int i = 0; i < kLag; ++i) tl[i] = tail;
                         }
                         const uint32_t n = min(wtot - e0, cap - (tail - head));   // a tile may exceed cap
                         for (uint32_t e = lane; e < n; e += 32) {
@@ -708,8 +715,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             // one cp.async group per tile (possibly empty): wait_group kLag then guarantees the
             // entries appended kLag tiles ago (t3) have landed; the latency hides behind 3 tiles
             cp_commit();
-            const uint32_t ready_end = t3;
-            t3 = t2; t2 = t1; t1 = tail;
+            const uint32_t ready_end = tl[kLag - 1];
+#pragma unroll
+            for (int i = kLag - 1; i > 0; --i) tl[i] = tl[i - 1];
+            tl[0] = tail;
             if (ready_end - head >= 32) {
                 cp_wait_lag();
                 __syncwarp();
