@@ -15,7 +15,6 @@ import pytest
 import torch
 
 import datagen
-import paper_2102_02440_b200 as pb
 from paper_2102_02440_b200.query import QueryRun
 
 pytestmark = pytest.mark.gpu
