@@ -1483,22 +1483,39 @@ static double mods_capacity(const Mods &md) {
     return have;
 }
 
-// log2 of the bound prod_t ||T_t||_1 from per-sketch L1 values (merged views: the best
-// constituent times the widths of the other legs)
+// log2 of a rigorous bound on |E_r| from per-sketch L1 values, the smaller of
+//  (a) prod_t ||T_t||_1 (every term of the expansion is one choice of an entry per tensor),
+//      a merged view's L1 taken as its best constituent's times the other legs' widths;
+//  (b) prod_t F_t, F_t = ||T_t||_1 for vectors and matrices and max_q ||v_q||_1 for a merged
+//      view: in message passing a node's output L1 is at most (sum over its parent leg of
+//      |entries| <= F_t) times its children's message L1s, and a root's value at most
+//      max|entry| <= F_t times them, since |min-abs(v_1, ..)| <= |v_q| for every constituent;
+//      a conditioned cycle adds the factor w of the conditioned edge (sum over its buckets).
 template <typename F>
 static double log_bound(const Plan &P, F l1of) {
-    double logB = 0;
+    double a = 0, b = 0;
+    bool has_kg = false;
     for (auto &t : P.T) {
-        if (t.kind != KG) { logB += log2(std::max(1.0, l1of(t.sk[0]))); continue; }
-        double best = 1e300;
+        if (t.kind != KG) {
+            const double v = log2(std::max(1.0, l1of(t.sk[0])));
+            a += v;
+            b += v;
+            continue;
+        }
+        has_kg = true;
+        double best = 1e300, mx = 0;
         for (size_t q = 0; q < t.legs.size(); ++q) {
-            double v = log2(std::max(1.0, l1of(t.sk[q])));
+            const double l = log2(std::max(1.0, l1of(t.sk[q])));
+            double v = l;
             for (size_t q2 = 0; q2 < t.legs.size(); ++q2) if (q2 != q) v += log2((double)P.width[t.legs[q2]]);
             best = std::min(best, v);
+            mx = std::max(mx, l);
         }
-        logB += best;
+        a += best;
+        b += mx;
     }
-    return logB;
+    if (P.cond >= 0 && has_kg) b += log2((double)P.width[P.cond]);
+    return std::min(a, b);
 }
 
 // Enqueue every kernel of one sub-plan on `stream` (no host synchronisation): per-row
