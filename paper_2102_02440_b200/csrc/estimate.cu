@@ -514,20 +514,38 @@ __global__ void k_merged_pos(const __grid_constant__ Node n, int qo, uint32_t *p
     }
 }
 
-__device__ __forceinline__ i128 o9_value_x(const i128 *P1, const i128 *P2, int wq, bool hasL, int64_t L, bool hasR,
-                                           int64_t R, int nless, int nle) {
-    i128 V;
+__device__ __forceinline__ i128 shfl_up_w(i128 v, int o) { return shfl_up_i128(v, o); }
+__device__ __forceinline__ int64_t shfl_up_w(int64_t v, int o) { return __shfl_up_sync(0xffffffffu, (long long)v, o); }
+__device__ __forceinline__ i128 shfl_xor_w(i128 v, int o) { return shfl_xor_i128(v, o); }
+__device__ __forceinline__ int64_t shfl_xor_w(int64_t v, int o) { return __shfl_xor_sync(0xffffffffu, (long long)v, o); }
+template <typename W>
+__device__ __forceinline__ W block_sum_w(W v, W *red) {
+    for (int o = 16; o > 0; o >>= 1) v += shfl_xor_w(v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    W t = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    return t;
+}
+
+template <typename W>
+__device__ __forceinline__ W o9_value_x(const W *P1, const W *P2, int wq, bool hasL, int64_t L, bool hasR,
+                                        int64_t R, int nless, int nle) {
+    W V;
     if (hasL) {
         const int64_t win = (hasR && !(uabs(L) <= uabs(R))) ? R : L;
-        V = (i128)win * (P1[wq] - P1[nless]);
+        V = (W)win * (P1[wq] - P1[nless]);
         int endB = nless;
         if (hasR && nle < endB) {
-            V += (i128)R * (P1[endB] - P1[nle]);
+            V += (W)R * (P1[endB] - P1[nle]);
             endB = nle;
         }
         V += P2[endB];
     } else {
-        V = (i128)R * (P1[wq] - P1[nle]) + P2[nle];
+        V = (W)R * (P1[wq] - P1[nle]) + P2[nle];
     }
     return V;
 }
@@ -536,18 +554,22 @@ __device__ __forceinline__ i128 o9_value_x(const i128 *P1, const i128 *P2, int w
 // shared memory (block scan), then O(1) per output.  pos_pre: precomputed
 // thresholds (k_merged_pos) or null (binary searches over the sorted |c| in global memory).
 constexpr int MX_T = 512;
+// W = i128, or int64_t when the node's message-passing bound (F_t x its children's message
+// bounds) is below 2^62: half the shared memory (two CTAs per SM) and 64-bit
+// arithmetic; messages in memory stay int128.
+template <typename W>
 __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ Node n, const uint32_t *pos_pre) {
     extern __shared__ __align__(16) unsigned char sm[];
-    __shared__ i128 red[32];
-    __shared__ i128 tot1[MX_T], tot2[MX_T];
+    __shared__ W red[32];
+    __shared__ W tot1[MX_T], tot2[MX_T];
     const int B = n.B;
     const int bb = blockIdx.x % B;
     const int r = blockIdx.x / B;
     const int64_t b = n.b0 + bb;
     const int qc = n.qc;
     const int wq = n.w[qc];
-    i128 *P1 = reinterpret_cast<i128 *>(sm);
-    i128 *P2 = P1 + (wq + 1);
+    W *P1 = reinterpret_cast<W *>(sm);
+    W *P2 = P1 + (wq + 1);
     const int64_t *cs = n.csorted + uint64_t(r) * wq;
     const uint64_t *S = n.sabs + uint64_t(r) * wq;
     int qp = -1, qf = -1, oc[2] = {-1, -1}, noc = 0;
@@ -568,11 +590,11 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
     const i128 *x = msg_row_x(n, qc, r, bb);   // delivered in the |c|-sorted order
     const int chunk = (wq + MX_T - 1) / MX_T;
     const int s0 = threadIdx.x * chunk, s1 = min(wq, s0 + chunk);
-    i128 l1 = 0, l2 = 0;
+    W l1 = 0, l2 = 0;
     for (int s = s0; s < s1; ++s) {
-        const i128 xv = x[s];
+        const W xv = (W)x[s];
         l1 += xv;
-        l2 += xv * (i128)cs[s];
+        l2 += xv * (W)cs[s];
     }
     tot1[threadIdx.x] = l1;
     tot2[threadIdx.x] = l2;
@@ -580,16 +602,16 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
     if (threadIdx.x < 32) {
         constexpr int per = MX_T / 32;
         const int lane = threadIdx.x;
-        i128 a1 = 0, a2 = 0;
+        W a1 = 0, a2 = 0;
         for (int t = 0; t < per; ++t) { a1 += tot1[lane * per + t]; a2 += tot2[lane * per + t]; }
-        i128 i1 = a1, i2 = a2;   // inclusive warp scan
+        W i1 = a1, i2 = a2;   // inclusive warp scan
         for (int o = 1; o < 32; o <<= 1) {
-            const i128 u1 = shfl_up_i128(i1, o), u2 = shfl_up_i128(i2, o);
+            const W u1 = shfl_up_w(i1, o), u2 = shfl_up_w(i2, o);
             if (lane >= o) { i1 += u1; i2 += u2; }
         }
-        i128 e1 = i1 - a1, e2 = i2 - a2;   // exclusive
+        W e1 = i1 - a1, e2 = i2 - a2;   // exclusive
         for (int t = 0; t < per; ++t) {
-            const i128 v1 = tot1[lane * per + t], v2 = tot2[lane * per + t];
+            const W v1 = tot1[lane * per + t], v2 = tot2[lane * per + t];
             tot1[lane * per + t] = e1;
             tot2[lane * per + t] = e2;
             e1 += v1;
@@ -599,22 +621,22 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
     }
     __syncthreads();
     {
-        i128 c1 = tot1[threadIdx.x], c2 = tot2[threadIdx.x];
+        W c1 = tot1[threadIdx.x], c2 = tot2[threadIdx.x];
         for (int s = s0; s < s1; ++s) {
             P1[s] = c1;
             P2[s] = c2;
-            const i128 xv = x[s];
+            const W xv = (W)x[s];
             c1 += xv;
-            c2 += xv * (i128)cs[s];
+            c2 += xv * (W)cs[s];
         }
     }
     __syncthreads();
     // --- outputs
     const i128 *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row_x(n, qo, r, bb) : nullptr;
     const i128 *xi2 = qi >= 0 ? msg_row_x(n, qi, r, bb) : nullptr;
-    i128 acc = 0;
+    W acc = 0;
     for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
-        i128 sacc = 0;
+        W sacc = 0;
         for (int i = 0; i < wi; ++i) {
             bool hasL, hasR;
             int64_t L, R;
@@ -628,21 +650,21 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
                 nless = hasL ? count_lt(S, wq, uabs(L)) : 0;
                 nle = hasR ? count_le(S, wq, uabs(R)) : 0;
             }
-            i128 V = o9_value_x(P1, P2, wq, hasL, L, hasR, R, nless, nle);
-            if (xi2) V *= xi2[i];
+            W V = o9_value_x<W>(P1, P2, wq, hasL, L, hasR, R, nless, nle);
+            if (xi2) V *= (W)xi2[i];
             sacc += V;
         }
         if (qp >= 0) {
             const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
-            reinterpret_cast<i128 *>(n.out)[(uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = sacc;
+            reinterpret_cast<i128 *>(n.out)[(uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = (i128)sacc;
         } else {
-            if (xo) sacc *= xo[o];
+            if (xo) sacc *= (W)xo[o];
             acc += sacc;
         }
     }
     if (qp < 0) {
-        const i128 t = block_sum_i128(acc, red);
-        if (threadIdx.x == 0) reinterpret_cast<i128 *>(n.out)[(uint64_t(r) * B + bb) * n.tiles + blockIdx.y] = t;
+        const W t = block_sum_w(acc, red);
+        if (threadIdx.x == 0) reinterpret_cast<i128 *>(n.out)[(uint64_t(r) * B + bb) * n.tiles + blockIdx.y] = (i128)t;
     }
 }
 
@@ -1518,12 +1540,54 @@ static double log_bound(const Plan &P, F l1of) {
     return std::min(a, b);
 }
 
+// Spanning tree of a plan rooted at local table 0 without the conditioned edge: parent edge
+// per table (-1 at the root) and a post-order for message passing.
+static void spanning_tree(const Plan &P, std::vector<int> &parent_edge, std::vector<int> &order) {
+    const int NT = (int)P.T.size();
+    parent_edge.assign(NT, -2);
+    std::vector<std::pair<int, int>> st2{{0, -1}};
+    std::vector<int> vis(NT, 0), pre;
+    while (!st2.empty()) {
+        auto [i, pe] = st2.back();
+        st2.pop_back();
+        if (vis[i]) continue;
+        vis[i] = 1;
+        parent_edge[i] = pe;
+        pre.push_back(i);
+        for (int le : P.T[i].legs) {
+            if (le == pe || le == P.cond) continue;
+            const int j = P.ends[le].first == i ? P.ends[le].second : P.ends[le].first;
+            if (!vis[j]) st2.push_back({j, le});
+        }
+    }
+    order.assign(pre.rbegin(), pre.rend());
+}
+
+// log2 bound of each node's output (message, per conditioned bucket; the root's value) in
+// message passing: F_t x the bounds of its children's messages (see log_bound (b)).
+// logF: per local table.  A merged node whose bound is <= 61 runs in 64-bit arithmetic.
+static void node_logbounds(const Plan &P, const std::vector<double> &logF, std::vector<double> &lb) {
+    std::vector<int> parent_edge, order;
+    spanning_tree(P, parent_edge, order);
+    const int NT = (int)P.T.size();
+    lb.assign(NT, 0.0);
+    for (int i : order) {
+        double v = logF[i];
+        for (int le : P.T[i].legs) {
+            if (le == parent_edge[i] || le == P.cond) continue;
+            const int j = P.ends[le].first == i ? P.ends[le].second : P.ends[le].first;
+            v += lb[j];
+        }
+        lb[i] = v;
+    }
+}
+
 // Enqueue every kernel of one sub-plan on `stream` (no host synchronisation): per-row
 // residues -> acc[K][d] (zeroed by the caller), per-sketch-row L1 norms -> l1[n_uniq][d].
 static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const sk_sketch *> &uniq,
                               DevPool &pool, uint64_t *acc, unsigned long long *l1, cudaStream_t stream,
                               int ring = 0, std::map<std::pair<const void *, int>, uint32_t *> *rescache = nullptr,
-                              const Mods *resmods = nullptr) {
+                              const Mods *resmods = nullptr, const std::vector<char> *narrow = nullptr) {
     // ring: 0 = CRT residues, 1 = exact int128, 2 = fp64 absolute-value bound (no matrices)
     const bool exact = ring == 1, absb = ring == 2;
     const int E = (int)P.edges.size();
@@ -1571,26 +1635,8 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
     }
     SKB_CUDA_CHECK("estimate launch 2");
     // ---- spanning tree rooted at local table 0 (DFS), post-order
-    std::vector<int> parent_edge(NT, -2), order;
-    {
-        std::vector<std::pair<int, int>> st2{{0, -1}};
-        std::vector<int> vis(NT, 0);
-        // iterative DFS producing pre-order; reverse gives a valid post-order for message passing
-        std::vector<int> pre;
-        while (!st2.empty()) {
-            auto [i, pe] = st2.back(); st2.pop_back();
-            if (vis[i]) continue;
-            vis[i] = 1;
-            parent_edge[i] = pe;
-            pre.push_back(i);
-            for (int le : P.T[i].legs) {
-                if (le == pe || le == P.cond) continue;
-                const int j = P.ends[le].first == i ? P.ends[le].second : P.ends[le].first;
-                if (!vis[j]) st2.push_back({j, le});
-            }
-        }
-        order.assign(pre.rbegin(), pre.rend());
-    }
+    std::vector<int> parent_edge, order;
+    spanning_tree(P, parent_edge, order);
     // does the subtree of node i contain an endpoint of the conditioned edge?
     std::vector<int> depb(NT, 0);
     for (int i : order) {
@@ -1750,10 +1796,17 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                     int mtiles = 1;
                     while (d * nB * mtiles < 296 && mtiles * MX_T < wo_max) mtiles *= 2;
                     n.tiles = (pe >= 0) ? mtiles : 1;
-                    const size_t sm = size_t(2) * (n.w[n.qc] + 1) * 16;
+                    const bool nw = narrow && (*narrow)[i] && !getenv("COMPASS_EST_NO_NARROW");
+                    const size_t sm = size_t(2) * (n.w[n.qc] + 1) * (nw ? 8 : 16);
                     if (sm + 2 * MX_T * 16 + 1024 > 227 * 1024) return fail(SK_EOVERFLOW, "estimate: merged contraction too wide");
-                    SKB_CUDA(cudaFuncSetAttribute(k_node_merged_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-                    k_node_merged_x<<<dim3(d * nB, n.tiles), MX_T, sm, stream>>>(n, pos); count_launch();
+                    if (nw) {
+                        SKB_CUDA(cudaFuncSetAttribute(k_node_merged_x<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                        k_node_merged_x<int64_t><<<dim3(d * nB, n.tiles), MX_T, sm, stream>>>(n, pos);
+                    } else {
+                        SKB_CUDA(cudaFuncSetAttribute(k_node_merged_x<i128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                        k_node_merged_x<i128><<<dim3(d * nB, n.tiles), MX_T, sm, stream>>>(n, pos);
+                    }
+                    count_launch();
                 } else {
                     int xt = 1;
                     if (pe >= 0) while (d * nB * xt < 592 && xt * 256 < P.width[pe]) xt *= 2;
@@ -1994,9 +2047,31 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
     for (size_t i = 0; i < n; ++i)
         if (!exact[i] && mds[i].K > kmax_mods.K) kmax_mods = mds[i];
     std::map<std::pair<const void *, int>, uint32_t *> rescache;
+    // exact plans: 64-bit merged nodes where the survivor-based node bound is <= 2^61
+    // (re-checked below with the measured L1 norms)
+    std::vector<std::vector<char>> narrow(n);
+    auto logF_of = [&](const Plan &P, auto l1of) {
+        std::vector<double> f;
+        for (auto &t : P.T) {
+            double m = 0;
+            for (auto *sk : t.sk) m = std::max(m, log2(std::max(1.0, l1of(sk))));
+            f.push_back(m);
+        }
+        return f;
+    };
+    for (size_t i = 0; i < n; ++i) {
+        if (!exact[i]) continue;
+        const Plan &P = plans[i];
+        std::vector<double> f;
+        for (auto &t : P.T) f.push_back(log2(std::max<double>(1.0, (double)g->survivors[t.t])));
+        std::vector<double> lb;
+        node_logbounds(P, f, lb);
+        narrow[i].assign(P.T.size(), 0);
+        for (size_t j = 0; j < P.T.size(); ++j) narrow[i][j] = P.T[j].kind == KG && lb[j] <= 61.0;
+    }
     for (size_t i = 0; i < n; ++i)
         if ((st = enqueue_plan(plans[i], mds[i], uniqs[i], pool, res + off_acc[i], (unsigned long long *)(res + off_l1[i]),
-                               stream, exact[i] ? 1 : 0, &rescache, &kmax_mods)))
+                               stream, exact[i] ? 1 : 0, &rescache, &kmax_mods, exact[i] ? &narrow[i] : nullptr)))
             return st;
     std::vector<uint64_t> host(words);
     SKB_CUDA(cudaMemcpyAsync(host.data(), res, words * 8, cudaMemcpyDeviceToHost, stream));
@@ -2011,7 +2086,14 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
             return (double)mx;
         };
         const double logB = std::min(log_bound(P, l1of), abs_bound[i]);
-        if (exact[i] && logB <= 125.0) {
+        bool narrow_ok = true;
+        if (exact[i]) {   // 64-bit nodes must also hold under the measured norms
+            std::vector<double> lb;
+            node_logbounds(P, logF_of(P, l1of), lb);
+            for (size_t j = 0; j < P.T.size(); ++j)
+                if (narrow[i][j] && lb[j] > 61.0) narrow_ok = false;   // re-run on the CRT engine below
+        }
+        if (exact[i] && narrow_ok && logB <= 125.0) {
             for (int r = 0; r < d; ++r) rows[i].push_back(sbig_from_i128(host[off_acc[i] + 2 * r], host[off_acc[i] + 2 * r + 1]));
             continue;
         }
