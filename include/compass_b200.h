@@ -108,7 +108,8 @@ SK_API sk_status sketch_zero(sk_sketch *sk, void *stream);
  *   *survivors_dev (device int64, may be NULL) += number of surviving tuples
  *   (the exact selection cardinality).
  * cols: device pointers, each n_rows elements of int32 or int64, 16-byte aligned
- *   recommended.  Counters are accumulated (+=), so calls over row shards add up
+ *   recommended.  A key column of a table with predicates may also be pinned, mapped host
+ *   memory (UVA): the scan reads only the survivors' key sectors in place over PCIe.  Counters are accumulated (+=), so calls over row shards add up
  *   (linearity).
  * Limits: n_cols <= 16, n_preds <= 8, n_targets <= 16, all targets on one device.
  * ------------------------------------------------------------------------- */

@@ -215,7 +215,9 @@ def sketch_update_filtered(columns, n_rows: int, preds, targets, survivors: torc
     ncol = len(columns)
     cols = (sk_column * max(1, ncol))()
     for i, c in enumerate(columns):
-        assert c.is_cuda and c.dtype in (torch.int32, torch.int64) and c.is_contiguous()
+        # device tensors, or pinned host tensors (mapped, read in place over PCIe) for key
+        # columns of tables with predicates: only the survivors' keys are then transferred
+        assert (c.is_cuda or c.is_pinned()) and c.dtype in (torch.int32, torch.int64) and c.is_contiguous()
         cols[i].data = c.data_ptr()
         cols[i].dtype = SK_INT64 if c.dtype == torch.int64 else SK_INT32
         cols[i].domain = int(domains[i]) if domains else 0
