@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <deque>
 #include <map>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -1587,7 +1588,8 @@ static void node_logbounds(const Plan &P, const std::vector<double> &logF, std::
 static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const sk_sketch *> &uniq,
                               DevPool &pool, uint64_t *acc, unsigned long long *l1, cudaStream_t stream,
                               int ring = 0, std::map<std::pair<const void *, int>, uint32_t *> *rescache = nullptr,
-                              const Mods *resmods = nullptr, const std::vector<char> *narrow = nullptr) {
+                              const Mods *resmods = nullptr, const std::vector<char> *narrow = nullptr,
+                              std::map<std::tuple<const void *, int, int>, const int64_t *> *foldcache = nullptr) {
     // ring: 0 = CRT residues, 1 = exact int128, 2 = fp64 absolute-value bound (no matrices)
     const bool exact = ring == 1, absb = ring == 2;
     const int E = (int)P.edges.size();
@@ -1595,8 +1597,9 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
     const int d = P.d;
     const int K = exact ? 2 : absb ? 1 : md.K;   // 64-bit words per message entry and row
     sk_status st;
-    // ---- L1 norms of every sketch involved (checked against the moduli after the batch)
-    for (size_t b0 = 0; b0 < uniq.size(); b0 += kMaxL1Items) {
+    // ---- L1 norms of every sketch involved (checked against the moduli after the batch;
+    //      skipped when the caller computes them once for the whole batch: l1 == null)
+    for (size_t b0 = 0; l1 && b0 < uniq.size(); b0 += kMaxL1Items) {
         L1Items items;
         items.n = (int)std::min<size_t>(kMaxL1Items, uniq.size() - b0);
         uint32_t maxcells = 1;
@@ -1617,19 +1620,25 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
             const sk_sketch *s = t.sk[0];
             const int w0 = P.width[t.legs[0]], w1 = P.width[t.legs[1]];
             if ((int)s->w[0] == w0 && (int)s->w[1] == w1) { data[i].push_back(s->counters); continue; }
+            const auto key = std::make_tuple((const void *)s, w0, w1);
+            if (foldcache && foldcache->count(key)) { data[i].push_back((*foldcache)[key]); continue; }
             void *f;
             if ((st = dalloc(pool, size_t(d) * w0 * w1 * 8, stream, &f))) return st;
             k_fold<<<1184, 256, 0, stream>>>(s->counters, (int64_t *)f, d, s->w[0], s->w[1], w0, w1); count_launch();
             data[i].push_back((const int64_t *)f);
+            if (foldcache) (*foldcache)[key] = (const int64_t *)f;
         } else {
             for (size_t q = 0; q < t.sk.size(); ++q) {
                 const sk_sketch *s = t.sk[q];
                 const int w = P.width[t.legs[q]];
                 if ((int)s->w[0] == w) { data[i].push_back(s->counters); continue; }
+                const auto key = std::make_tuple((const void *)s, 1, w);
+                if (foldcache && foldcache->count(key)) { data[i].push_back((*foldcache)[key]); continue; }
                 void *f;
                 if ((st = dalloc(pool, size_t(d) * w * 8, stream, &f))) return st;
                 k_fold<<<592, 256, 0, stream>>>(s->counters, (int64_t *)f, d, 1, s->w[0], 1, w); count_launch();
                 data[i].push_back((const int64_t *)f);
+                if (foldcache) (*foldcache)[key] = (const int64_t *)f;
             }
         }
     }
@@ -2069,13 +2078,44 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
         narrow[i].assign(P.T.size(), 0);
         for (size_t j = 0; j < P.T.size(); ++j) narrow[i][j] = P.T[j].kind == KG && lb[j] <= 61.0;
     }
+    // L1 norms once per distinct sketch of the batch (one k_l1 launch per 48 sketches), then
+    // scattered into each plan's slots on the host after the copy
+    std::vector<const sk_sketch *> guniq;
+    std::map<const sk_sketch *, size_t> gidx;
     for (size_t i = 0; i < n; ++i)
-        if ((st = enqueue_plan(plans[i], mds[i], uniqs[i], pool, res + off_acc[i], (unsigned long long *)(res + off_l1[i]),
-                               stream, exact[i] ? 1 : 0, &rescache, &kmax_mods, exact[i] ? &narrow[i] : nullptr)))
+        for (auto *sk : uniqs[i])
+            if (!gidx.count(sk)) { gidx[sk] = guniq.size(); guniq.push_back(sk); }
+    int dmax = 1;
+    for (auto &P : plans) dmax = std::max(dmax, P.d);
+    void *dl1;
+    if ((st = dalloc(pool, guniq.size() * dmax * 8 + 8, stream, &dl1))) return st;
+    SKB_CUDA(cudaMemsetAsync(dl1, 0, guniq.size() * dmax * 8 + 8, stream));
+    for (size_t b0 = 0; b0 < guniq.size(); b0 += kMaxL1Items) {
+        L1Items items;
+        items.n = (int)std::min<size_t>(kMaxL1Items, guniq.size() - b0);
+        uint32_t maxcells = 1;
+        for (int j = 0; j < items.n; ++j) {
+            const sk_sketch *sk = guniq[b0 + j];
+            items.it[j] = {sk->counters, sk->d, (uint32_t)(sk->n_counters / sk->d)};
+            maxcells = std::max(maxcells, items.it[j].cells);
+        }
+        const unsigned chunks = std::min<unsigned>(64, (maxcells + 8191) / 8192);
+        k_l1<<<dim3(items.n, dmax, chunks), 256, 0, stream>>>(items, (unsigned long long *)dl1 + b0 * dmax, dmax);
+        count_launch();
+        SKB_CUDA_CHECK("estimate launch l1");
+    }
+    std::map<std::tuple<const void *, int, int>, const int64_t *> foldcache;
+    for (size_t i = 0; i < n; ++i)
+        if ((st = enqueue_plan(plans[i], mds[i], uniqs[i], pool, res + off_acc[i], nullptr, stream, exact[i] ? 1 : 0,
+                               &rescache, &kmax_mods, exact[i] ? &narrow[i] : nullptr, &foldcache)))
             return st;
-    std::vector<uint64_t> host(words);
+    std::vector<uint64_t> host(words), hl1(guniq.size() * dmax);
     SKB_CUDA(cudaMemcpyAsync(host.data(), res, words * 8, cudaMemcpyDeviceToHost, stream));
+    if (!hl1.empty()) SKB_CUDA(cudaMemcpyAsync(hl1.data(), dl1, hl1.size() * 8, cudaMemcpyDeviceToHost, stream));
     SKB_CUDA(cudaStreamSynchronize(stream));
+    for (size_t i = 0; i < n; ++i)   // each plan's L1 slots, as enqueue_plan would have written them
+        for (size_t u = 0; u < uniqs[i].size(); ++u)
+            for (int r = 0; r < plans[i].d; ++r) host[off_l1[i] + u * plans[i].d + r] = hl1[gidx[uniqs[i][u]] * dmax + r];
     for (size_t i = 0; i < n; ++i) {
         const Plan &P = plans[i];
         const int d = P.d;
