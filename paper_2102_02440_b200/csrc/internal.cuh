@@ -24,7 +24,8 @@ struct sk_sketch {
     uint64_t *seeds_dev = nullptr;
     std::vector<uint64_t> seeds_host;
     // per dimension q: hash lookup table over a hinted key domain [0, lut_dom[q]):
-    // lut[q][x * d + r] = (h_r(x) & (w_q - 1)) << 1 | (xi_r(x) < 0); built on first use
+    // lut[q][x * dp + r] = (h_r(x) & (w_q - 1)) << 1 | (xi_r(x) < 0), dp = d rounded up to a
+    // multiple of 4 (d <= 8); built on first use
     // (the seeds never change), freed with the sketch
     uint32_t *lut[2] = {nullptr, nullptr};
     uint64_t lut_dom[2] = {0, 0};

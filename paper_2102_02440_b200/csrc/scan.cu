@@ -259,9 +259,17 @@ __device__ __forceinline__ void update_2d(const STarget &tg, const uint64_t *see
     if (tg.lut0 && x < tg.lut_dom0 && y < tg.lut_dom1) {
         // hinted key domains: (bucket, sign) per row from the lookup tables (the same values
         // the hash polynomials give; built once per sketch by k_lut_build)
-        const uint32_t *la = tg.lut0 + x * tg.d, *lb = tg.lut1 + y * tg.d;
-        for (uint32_t r = 0; r < tg.d; ++r) {
-            const uint32_t ea = __ldg(la + r), eb = __ldg(lb + r);
+        // rows padded to a multiple of 4: the entries of both keys arrive in 128-bit loads,
+        // all issued before the first use
+        const uint32_t dp = (tg.d + 3) & ~3u;
+        const uint4 *la = reinterpret_cast<const uint4 *>(tg.lut0 + x * dp), *lb = reinterpret_cast<const uint4 *>(tg.lut1 + y * dp);
+        uint4 va[2], vb[2];
+        va[0] = __ldg(la); vb[0] = __ldg(lb);
+        if (dp > 4) { va[1] = __ldg(la + 1); vb[1] = __ldg(lb + 1); }
+        for (uint32_t r = 0; r < tg.d && r < 8; ++r) {
+            const uint4 &qa = va[r >> 2], &qb = vb[r >> 2];
+            const uint32_t ea = (r & 3) == 0 ? qa.x : (r & 3) == 1 ? qa.y : (r & 3) == 2 ? qa.z : qa.w;
+            const uint32_t eb = (r & 3) == 0 ? qb.x : (r & 3) == 1 ? qb.y : (r & 3) == 2 ? qb.z : qb.w;
             const uint32_t cell = ((ea >> 1) << tg.lw1) | (eb >> 1);
             const int v = ((ea ^ eb) & 1u) ? -cnt : cnt;
             if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
@@ -876,10 +884,12 @@ __global__ void __launch_bounds__(512) k_hist_epilogue(const __grid_constant__ E
 // hash lookup table of one sketch dimension over keys [0, dom): lut[x * d + r] =
 // (h_r(x) & wmask) << 1 | (xi_r(x) < 0)   (H3/H4 for x < 2^32: the narrow path)
 __global__ void k_lut_build(const uint64_t *seeds, uint32_t d, uint32_t wmask, uint64_t dom, uint32_t *lut) {
-    const uint64_t total = dom * d;
+    const uint32_t dp = (d + 3) & ~3u;   // rows padded to a multiple of 4 (128-bit loads)
+    const uint64_t total = dom * dp;
     for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t x = e / d;
-        const uint32_t r = (uint32_t)(e % d);
+        const uint64_t x = e / dp;
+        const uint32_t r = (uint32_t)(e % dp);
+        if (r >= d) { lut[e] = 0; continue; }
         const uint64_t *a = seeds + r * 6;
         const uint32_t b = (uint32_t)(hash_g61_t<true>(__ldg(a + 4), __ldg(a + 5), x) & wmask);
         uint64_t sa[4] = {__ldg(a), __ldg(a + 1), __ldg(a + 2), __ldg(a + 3)};
@@ -1065,13 +1075,14 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
             sk_sketch *sk = c.tgt_sketch[t];
             const uint64_t dom[2] = {c.col_domain[c.tgt_key[t][0]], c.col_domain[c.tgt_key[t][1]]};
             bool ok = true;
-            for (int q = 0; q < 2; ++q) ok &= dom[q] > 0 && dom[q] <= (1ULL << 31) && dom[q] * sk->d * 4 <= (64ULL << 20);
+            const uint64_t dp = (sk->d + 3) & ~3u;
+            for (int q = 0; q < 2; ++q) ok &= sk->d <= 8 && dom[q] > 0 && dom[q] <= (1ULL << 31) && dom[q] * dp * 4 <= (64ULL << 20);
             if (!ok) continue;
             for (int q = 0; q < 2; ++q) {
                 if (sk->lut[q] && sk->lut_dom[q] >= dom[q]) continue;
                 if (sk->lut[q]) { cudaFree(sk->lut[q]); sk->lut[q] = nullptr; }
-                SKB_CUDA(cudaMalloc(&sk->lut[q], dom[q] * sk->d * 4));
-                k_lut_build<<<(unsigned)std::min<uint64_t>(uint64_t(sms_l) * 8, (dom[q] * sk->d + 255) / 256), 256, 0, stream>>>(
+                SKB_CUDA(cudaMalloc(&sk->lut[q], dom[q] * dp * 4));
+                k_lut_build<<<(unsigned)std::min<uint64_t>(uint64_t(sms_l) * 8, (dom[q] * dp + 255) / 256), 256, 0, stream>>>(
                     sk->seeds_dev + size_t(q) * sk->d * 6, sk->d, sk->w[q] - 1, dom[q], sk->lut[q]);
                 SKB_CUDA(cudaGetLastError());
                 count_launch();
