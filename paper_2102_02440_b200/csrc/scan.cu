@@ -21,6 +21,7 @@
 //   A7  CTA flush: int32 smem counters and heavy-hitter counts -> int64 HBM
 //       sketch with red.global.add (order-independent, bit-exact).
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -117,6 +118,7 @@ struct SParams {
     // values).
     uint32_t trio_on, trio_ka, trio_kb, trio_a, trio_b, trio_m;
     uint32_t off_miss, off_missn;   // per-warp miss buffers (x, count) and fill counts
+    uint32_t off_hstat;             // per key: heavy-hitter probes, hits, disabled flag (histogram keys)
     uint32_t off_rows;              // per-warp survivor row-offset list (128 x uint16)
     uint32_t tile_rows;             // rows per ring stage
     uint32_t n_full_tiles;          // tiles with tile_rows rows (staged by TMA)
@@ -332,11 +334,18 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
             if ((uint32_t)k == P.trio_ka) { la = leader; ca = cnt; }
             if ((uint32_t)k == P.trio_kb) { lb = leader; cb = cnt; }
         }
+        // histogram keys: the CTA stops probing the heavy-hitter table once it no longer pays
+        // (fewer than 1 hit in 4 probes after 8192 probes: a flat key distribution); what the
+        // table holds is still flushed at the end, so the counts stay exact either way
+        uint32_t *hstat = reinterpret_cast<uint32_t *>(smem + P.off_hstat) + k * 4;
+        const bool use_hh = P.key[k].hh_off >= 0 && (!P.key[k].hist || *reinterpret_cast<volatile uint32_t *>(hstat + 2) == 0);
+        bool hh_hit = false;
         if (leader) {
             if (P.key[k].hist) {
                 // histogram mode: count the key (heavy-hitter table first, then the L2 histogram);
                 // all 1-D sketches of this key are built from the counts after the scan
-                bool done = P.key[k].hh_off >= 0 && hh_add(smem + P.key[k].hh_off, P.hh_log2, x[k], cnt);
+                bool done = use_hh && hh_add(smem + P.key[k].hh_off, P.hh_log2, x[k], cnt);
+                hh_hit = done;
                 if (!done && x[k] < P.key[k].domain) { red_add_u32(P.key[k].hist + x[k], (uint32_t)cnt); done = true; }
                 if (!done) {   // outside the hinted domain: direct updates
                     miss = P.key[k].hasglob;
@@ -352,6 +361,14 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
                     const STarget &tg = P.tgt[__ffs(tm) - 1];
                     update_1d(tg, seeds + tg.seed_off, sc, x[k], cnt);
                 }
+            }
+        }
+        if (P.key[k].hist && use_hh) {
+            const uint32_t np = __popc(__ballot_sync(0xffffffffu, leader));
+            const uint32_t nh = __popc(__ballot_sync(0xffffffffu, hh_hit));
+            if (lane == 0 && np) {
+                const uint32_t p0 = atomicAdd(hstat, np), h0 = atomicAdd(hstat + 1, nh);
+                if (p0 + np >= 8192 && (h0 + nh) * 4 < p0 + np) hstat[2] = 1;
             }
         }
         if (P.key[k].hasglob) {
@@ -578,6 +595,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
         }
         uint32_t *nm = reinterpret_cast<uint32_t *>(smem + P.off_missn);
         for (uint32_t i = tid; i < kWarps * P.n_keys; i += kThreads) nm[i] = 0;
+        uint32_t *hs = reinterpret_cast<uint32_t *>(smem + P.off_hstat);
+        for (uint32_t i = tid; i < kMaxKeys * 4; i += kThreads) hs[i] = 0;
     }
     __syncthreads();
 
@@ -1017,7 +1036,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         P.kb_bytes = P.cap * P.n_keys * 8;
     }
     const uint32_t min_stages = 3;
-    const uint32_t miss_bytes = kWarps * P.n_keys * 32 * 12 + ((kWarps * P.n_keys * 4 + 15) & ~15u);
+    const uint32_t miss_bytes = kWarps * P.n_keys * 32 * 12 + ((kWarps * P.n_keys * 4 + 15) & ~15u) + kMaxKeys * 16 + 16;
     const uint32_t kBarBytes = 2 * kGroups * kMaxStages * 8;
     const uint32_t ring_stage = kGroups * P.stage_bytes;   // one stage of every group's ring
     const uint32_t fixed = kBarBytes + min_stages * ring_stage + ring_warps * P.kb_bytes + seed_bytes + miss_bytes +
@@ -1155,6 +1174,8 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     off = P.off_miss + kWarps * P.n_keys * 32 * 12;
     P.off_missn = (off + 15) & ~15u;
     off = P.off_missn + kWarps * P.n_keys * 4;
+    P.off_hstat = (off + 15) & ~15u;
+    off = P.off_hstat + kMaxKeys * 4 * 4;
     P.off_seed = (off + 15) & ~15u;
     off = P.off_seed + seed_bytes;
     if (off > kBudget) return SK_OK;
@@ -1189,6 +1210,10 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     if (getenv("COMPASS_SCAN_KW0")) kw = 0;   // experiments / parity of the generic variant
     ScanKernel kern = pick_kernel(P.n_keys, P.n_preds, kw);
     const int threads = kThreads;
+    if (getenv("COMPASS_SCAN_DEBUG"))
+        fprintf(stderr, "k_scan plan: keys %u preds %u kw %d stages %u hh_log2 %u cap %u smem %u (ring %u, counters %u)\n",
+                P.n_keys, P.n_preds, kw, P.stages, P.hh_log2, P.cap, off, P.stages * kGroups * P.stage_bytes,
+                P.smem_counters * 4);
     SKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)off));
     kern<<<(unsigned)grid, threads, off, stream>>>(P);
     SKB_CUDA(cudaGetLastError());
