@@ -1016,6 +1016,16 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     for (uint32_t q = 0; q < c.n_preds; ++q) stage_col(c.pred_col[q]);
     if (!P.gather) for (uint32_t k : keys) stage_col(k);
     P.stage_bytes = soff;
+    // staged columns are read by TMA bulk copies: they must be device memory (a mapped host
+    // column — allowed for gathered key columns — sends the call to the grid-stride kernel)
+    for (uint32_t ci = 0; ci < c.n_cols; ++ci) {
+        if (P.col[ci].soff < 0) continue;
+        cudaPointerAttributes pa;
+        if (cudaPointerGetAttributes(&pa, c.col_ptr[ci]) != cudaSuccess || pa.type != cudaMemoryTypeDevice) {
+            cudaGetLastError();
+            return SK_OK;
+        }
+    }
     // ---- shared-memory plan (227 KB): barriers | TMA ring (stages x stage) | per-warp key
     //      rings | privatised counters | heavy-hitter tables | seeds.  Tunables via env
     //      (COMPASS_STAGES, COMPASS_HH_LOG2) for experiments only.

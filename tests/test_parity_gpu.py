@@ -499,3 +499,24 @@ def test_zero_copy_key_columns_equal_device_build(kw):
     assert int(surv.item()) == gs == os_
     for sk, a, b in zip(sks, g, o):
         assert np.array_equal(sk.counters.cpu().numpy(), a) and np.array_equal(a, b)
+
+
+def test_mapped_host_predicate_column_takes_the_generic_kernel():
+    """A predicate column in pinned host memory cannot be staged by TMA: the call falls back
+    to the grid-stride kernel and the counters are still exact."""
+    n = 200_003
+    cols = _rand_cols(n, 77)
+    preds = [("p", pb.RANGE, 10, 69)]
+    targets = TARGETS[:3]
+    names = list(cols)
+    host_or_dev = [torch.from_numpy(cols[c]).pin_memory() for c in names]
+    sks = [pb.Sketch(d, w, e, 42, _dev()) for (_, d, w, e) in targets]
+    surv = torch.zeros(1, dtype=torch.int64, device=_dev())
+    pr = [(names.index(p[0]),) + tuple(p[1:]) for p in preds]
+    tg = [(sk, [names.index(k) for k in t[0]]) for sk, t in zip(sks, targets)]
+    pb.sketch_update_filtered(host_or_dev, n, pr, tg, survivors=surv)
+    torch.cuda.synchronize()
+    o, os_ = _oracle_build(cols, preds, targets)
+    assert int(surv.item()) == os_
+    for sk, b in zip(sks, o):
+        assert np.array_equal(sk.counters.cpu().numpy(), b)
