@@ -340,7 +340,10 @@ def main():
             "kernel": "k_scan (persistent TMA-ring fused filter+hash+update+flush)",
             "alg_bytes_per_step": ab["alg"], "kernel_ms_per_step": round(kms, 4),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "_fallback" not in peaks else "fallback 6.65 TB/s",
-            "frac_of_nominal_8TBs": round(achieved / 8000.0, 4)}
+            "frac_of_nominal_8TBs": round(achieved / 8000.0, 4),
+            # third denominator of SURVEY.md §8(d): the measured read-only TMA-ring stream of 12 GB
+            # (tools/stream_micro.cu: 7.3 TB/s on these B200s)
+            "frac_of_read_stream_7300GBs": round(achieved / 7300.0, 4)}
 
     line = {"metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
@@ -353,6 +356,9 @@ def main():
             "roofline": roof, "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "survivors": run.survivors.tolist(), "estimates": ests[:8] if ests else None,
+            "rates": {"survivors_per_s": sum(run.survivors.tolist()) / (ms / 1e3),
+                      "row_updates_per_s": sum(surv_n * sum(s.d for s in ws.sketches_of(t.name))
+                                               for t, surv_n in zip(ws.tables, run.survivors.tolist())) / (ms / 1e3)},
             "plan": plan[0] if plan else None}
 
     # end to end through the public API with pinned host buffers (H2D inside the timed region)
