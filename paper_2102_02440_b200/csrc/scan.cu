@@ -8,16 +8,22 @@
 //       with cp.async.bulk (TMA bulk copies, UBLKCP) into a 4-8 stage ring
 //       guarded by mbarriers (full: tx-count; empty: consumer release).
 //   A2  Consumers read 4 rows per lane with 128-bit shared loads and evaluate
-//       the conjunction of point / range / subset predicates.
-//   A3  Survivors are compacted per warp (popc prefix) into a per-tile list; the
-//       key columns of survivors only are gathered with cp.async (LDGSTS,
-//       sector-granular HBM traffic) one tile ahead of their use.
-//   A4  Hashes mod 2^61-1 on the integer pipe (hash.cuh).
+//       the conjunction of point / range / subset predicates (one predicate
+//       register per row slot; KW variants: all int32 ranges, one key width).
+//   A3  One ballot per row slot; survivors' ring positions are popcs of the
+//       ballots; only the survivors' key sectors are gathered with predicated
+//       cp.async (LDGSTS, .L2::64B) into a per-warp ring, consumed 3 tiles later.
+//   A4  Hashes mod 2^61-1 on the integer pipe (hash.cuh; 64x32 lazy Horner for
+//       keys < 2^32), or per-sketch lookup tables for matrices over hinted domains.
 //   A5  Keys are aggregated per warp with __match_any_sync (leader adds
 //       count * xi, exact by linearity).  1-D sketches that fit
-//       are privatised as int32 in smem; others get a per-CTA heavy-hitter
-//       table (canonical key -> count) flushed once, misses go to L2 atomics.
-//   A6  Matrix sketches: per-survivor cell update, smem or L2.
+//       are privatised as int32 in smem; others get a per-CTA two-choice
+//       heavy-hitter table (canonical key -> count) flushed once, misses are
+//       buffered per warp and applied 32 at a time with L2 atomics; hinted key
+//       domains go through a histogram (hashed once per distinct key).
+//   A6  Matrix sketches: per equal-key-pair leader, one cell per
+//       row, smem or L2 (trio loop when the hash families equal two privatised
+//       1-D sketches').
 //   A7  CTA flush: int32 smem counters and heavy-hitter counts -> int64 HBM
 //       sketch with red.global.add (order-independent, bit-exact).
 #include <stdint.h>
