@@ -171,14 +171,53 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _relaunch(n: int) -> int:
+    """`bench.py --gpus N` run as one process: re-executes itself under torchrun with N ranks
+    on this node (one process per GPU, NCCL over NVLink), rendezvous on 127.0.0.1."""
+    import socket
+    if torch.cuda.device_count() < n:
+        print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {torch.cuda.device_count()}", file=sys.stderr)
+        return 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+NCCL_LOG = "/tmp/compass_bench_nccl.%h.%p.log"
+
+
 def _setup_dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        # NCCL's communicator line (rank count, NVLS / channels) is kept so the JSON line can
+        # show the collective really spanned every rank
+        if "NCCL_DEBUG" not in os.environ:
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+            os.environ["NCCL_DEBUG_FILE"] = NCCL_LOG
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
+
+
+def _nccl_comm_line() -> str | None:
+    """The 'comm ... nRanks N' INIT line NCCL wrote for this process (NCCL_DEBUG_FILE)."""
+    import glob
+    import socket
+    path = NCCL_LOG.replace("%h", socket.gethostname()).replace("%p", str(os.getpid()))
+    for f in [path] + glob.glob("/tmp/compass_bench_nccl.*.%d.log" % os.getpid()):
+        try:
+            for line in open(f):
+                if "nRanks" in line or "nranks" in line:
+                    return line.strip()[:300]
+        except OSError:
+            continue
+    return None
 
 
 def _barrier(world):
@@ -194,27 +233,61 @@ def _max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
-def cpu_oracle_sample(ws, rows_budget: int, device) -> dict:
-    """Time the oracle (O1 filter + O2/O3 builds) on the first rows of every table
-    (proportional sample), single-threaded, on this host."""
+def _oracle_pass(ws, cols_by_table, preds_by_table, threads: int) -> float:
+    """One timed oracle pass (O1 filter + O2/O3 builds, SURVEY.md §8(d) "Oracle timing
+    beside it") over the sampled rows.  threads > 1: the rows of every table are split into
+    `threads` contiguous ranges, each thread filters and builds private sketches for its range
+    (the oracle's C routines run outside the GIL), and the private sketches are merged by int64
+    addition (O4).  The oracle's arithmetic is used as it stands."""
     import oracle
+    from concurrent.futures import ThreadPoolExecutor
+
+    def part(tname, a, b):
+        cols = {c: v[a:b] for c, v in cols_by_table[tname].items()}
+        mask, _ = oracle.filter_mask(cols, preds_by_table[tname])
+        return [oracle.build([cols[k] for k in s.key_cols], mask, s.d, s.w, s.edge_ids, master=ws.master_seed)
+                for s in ws.sketches_of(tname)]
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        for t in ws.tables:
+            n = len(next(iter(cols_by_table[t.name].values())))
+            cuts = [n * i // threads for i in range(threads + 1)]
+            parts = list(ex.map(lambda ab: part(t.name, *ab), zip(cuts[:-1], cuts[1:])))
+            merged = parts[0]
+            for p_ in parts[1:]:
+                for m, q in zip(merged, p_):
+                    m += q
+    return time.perf_counter() - t0
+
+
+def cpu_oracle_sample(ws, rows_budget: int, device, threads: int | None = None, single: bool = True) -> dict:
+    """Time the oracle (O1 filter + O2/O3 builds) on the first rows of every table
+    (proportional sample) on this host: all hardware threads (private sketches merged by
+    int64 addition) and, on a smaller sample, single-threaded."""
+    cores = threads or os.cpu_count() or 1
     total = ws.total_rows
     frac = min(1.0, rows_budget / total)
-    scanned = 0
-    t_oracle = 0.0
+    cols, preds, scanned = {}, {}, 0
     for t in ws.tables:
         n = max(1, int(t.n_rows * frac))
-        cols = {c.name: datagen._gen_column(ws, t, c, 0, n, device).cpu().numpy() for c in t.cols}
-        preds = datagen.resolve_preds(ws, t.name)
-        t0 = time.perf_counter()
-        mask, _ = oracle.filter_mask(cols, preds)
-        for s in ws.sketches_of(t.name):
-            oracle.build([cols[k] for k in s.key_cols], mask, s.d, s.w, s.edge_ids, master=ws.master_seed)
-        t_oracle += time.perf_counter() - t0
+        cols[t.name] = {c.name: datagen._gen_column(ws, t, c, 0, n, device).cpu().numpy() for c in t.cols}
+        preds[t.name] = datagen.resolve_preds(ws, t.name)
         scanned += n
-    return {"value": scanned / t_oracle, "unit": "tuples/s", "cores": 1, "kind": "oracle",
-            "sample": f"first {frac:.3%} of every table of {ws.name} ({scanned} rows), filter + sketch builds, "
-                      f"single-threaded plain C oracle, {t_oracle:.1f} s"}
+    t_mt = _oracle_pass(ws, cols, preds, cores)
+    out = {"value": scanned / t_mt, "unit": "tuples/s", "cores": cores, "kind": "oracle", "seconds": round(t_mt, 4),
+           "sample": f"first {frac:.3%} of every table of {ws.name} ({scanned} rows), filter + sketch builds, "
+                     f"plain C oracle on {cores} threads (row ranges, private sketches merged by int64 addition), "
+                     f"{t_mt:.1f} s"}
+    if single:
+        # single-threaded leg on the first 1/cores of the same sample (bounded CPU time)
+        frac1 = 1.0 / cores
+        cols1 = {tn: {c: v[:max(1, int(len(v) * frac1))] for c, v in cc.items()} for tn, cc in cols.items()}
+        scanned1 = sum(len(next(iter(cc.values()))) for cc in cols1.values())
+        t_st = _oracle_pass(ws, cols1, preds, 1)
+        out["single_thread"] = {"value": scanned1 / t_st, "unit": "tuples/s", "cores": 1,
+                                "sample": f"first {scanned1} rows of the same sample, {t_st:.1f} s"}
+    return out
 
 
 def run_reference(args, world, rank):
@@ -224,16 +297,18 @@ def run_reference(args, world, rank):
     ws = _workload(args.workload, args.scale)
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     budget = args.ref_rows
-    samples = []
+    samples, secs = [], []
     base = None
     for i in range(args.warmup + args.steps):
-        r = cpu_oracle_sample(ws, budget, dev)
+        r = cpu_oracle_sample(ws, budget, dev, single=False)
         if i >= args.warmup:
             samples.append(r["value"])
+            secs.append(r["seconds"])
         base = r
     v = sorted(samples)[len(samples) // 2]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tuples/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sum(secs) / len(secs), 3),
+            "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": ws.name, "rows": ws.total_rows, "sample_rows_per_step": budget},
             "cpu_baseline": {"value": v, "unit": "tuples/s", "cores": base["cores"], "kind": "oracle",
@@ -255,6 +330,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch(args.gpus))
     world, rank, local = _setup_dist()
     if args.impl == "reference":
         run_reference(args, world, rank)
@@ -274,28 +351,34 @@ def main():
     subplans = _subplans(ws) if ws.kind == "graph" else None
     stream = torch.cuda.current_stream()
     kev = []  # (start, end) events around each fused-scan launch
+    pev = []  # per step: (start, build done = sketches resident after the all-reduce, end)
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
 
     def step(record=False):
+        s0 = ev() if record else None
         run.zero_()
         for t in ws.tables:
-            if record:
-                a = torch.cuda.Event(enable_timing=True)
-                b = torch.cuda.Event(enable_timing=True)
-                a.record(stream)
+            a = ev() if record else None
             run.build_table(t.name, data[t.name], preds[t.name], stream=stream)
             if record:
-                b.record(stream)
-                kev.append((a, b))
+                kev.append((a, ev()))
         run.allreduce()
+        s1 = ev() if record else None
         g = run.graph()
         if subplans is None:
             # C4: self-join size of each key sketch, one batched estimate call
             ests = g.estimate_subplans([(g.tables[2 * i], g.tables[2 * i + 1]) for i in range(len(g.tables) // 2)])
             plan = None
         else:
-            # plan_greedy evaluates every connected sub-plan in one batch (A11), then plans (A12)
+            # plan_greedy evaluates the connected sub-plans it needs (A11), then plans (A12)
             ests = None
             plan = g.plan_greedy()
+        if record:
+            pev.append((s0, s1, ev()))
         return ests, plan
 
     for _ in range(args.warmup):
@@ -321,8 +404,12 @@ def main():
     ms = _max_over_ranks(ms, world)
     kms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
     kms = _max_over_ranks(kms, world)
+    # t_build: first kernel of the step -> final int64 sketches resident
+    # (after the all-reduce for N > 1); max over ranks
+    bms = _max_over_ranks(sum(a.elapsed_time(b) for a, b, _ in pev) / args.steps, world)
+    ems = _max_over_ranks(sum(b.elapsed_time(c) for _, b, c in pev) / args.steps, world)
     rows_all = ws.total_rows
-    value = rows_all / (ms / 1e3)
+    value = rows_all / (bms / 1e3)
 
     # roofline of the dominant kernel (the fused scan), algorithmic bytes per launch set
     ab = algorithmic_bytes(ws, data, preds, run)
@@ -347,6 +434,10 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+            "timing": {"value_is": "rows of all ranks / t_build (SURVEY.md 8(d)): zero + fused scans + "
+                                   "all-reduce, max over ranks; every step also runs the estimates and the plan",
+                       "build_ms_per_step": round(bms, 4), "estimate_plan_ms_per_step": round(ems, 4),
+                       "step_ms": round(ms, 4), "step_tuples_per_s": rows_all / (ms / 1e3)},
             "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded counter-based generator, datagen/)",
             "config": {"workload": ws.name, "rows": rows_all, "tables": len(ws.tables),
                        "sketches": [f"{s.table}:{'x'.join(map(str, s.w))}xd{s.d}" for s in ws.sketches],
@@ -356,9 +447,9 @@ def main():
             "roofline": roof, "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "survivors": run.survivors.tolist(), "estimates": ests[:8] if ests else None,
-            "rates": {"survivors_per_s": sum(run.survivors.tolist()) / (ms / 1e3),
+            "rates": {"survivors_per_s": sum(run.survivors.tolist()) / (bms / 1e3),
                       "row_updates_per_s": sum(surv_n * sum(s.d for s in ws.sketches_of(t.name))
-                                               for t, surv_n in zip(ws.tables, run.survivors.tolist())) / (ms / 1e3)},
+                                               for t, surv_n in zip(ws.tables, run.survivors.tolist())) / (bms / 1e3)},
             "plan": plan[0] if plan else None}
 
     # end to end through the public API with pinned host buffers (H2D inside the timed region)
@@ -372,6 +463,11 @@ def main():
             line["cpu_baseline"] = cpu_oracle_sample(ws, args.cpu_rows, dev)
         except Exception as ex:
             line["cpu_baseline"] = {"unavailable": f"{type(ex).__name__}: {ex}"[:300]}
+    if world > 1:
+        comm = _nccl_comm_line()
+        line["nccl"] = {"comm": comm, "world_size": dist.get_world_size()}
+        if rank == 0 and comm:
+            print(comm, flush=True)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

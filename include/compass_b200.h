@@ -189,7 +189,8 @@ typedef struct {
 SK_API sk_status estimate_join(const sk_graph *g, uint64_t vertex_mask, double *est, double *row_est, void *stream);
 
 /* Same, but writes each row's exact E_r as a decimal string into
- * buf[r*stride .. r*stride+stride) (NUL-terminated); stride >= 160 recommended. */
+ * buf[r*stride .. r*stride+stride) (NUL-terminated); stride >= 160 recommended.
+ * A singleton mask has no rows: its exact survivor count is written once, at buf[0]. */
 SK_API sk_status estimate_join_exact(const sk_graph *g, uint64_t vertex_mask, char *buf, uint32_t stride, void *stream);
 
 /* Batched estimates of n sub-plans: est[i] for masks[i]. */

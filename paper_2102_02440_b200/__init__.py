@@ -344,7 +344,10 @@ class JoinGraph:
         _check(lib().estimate_join_exact(ctypes.byref(self.g), self.mask(subset), buf, stride,
                                          ctypes.c_void_p(_stream_ptr(stream))))
         raw = buf.raw
-        return [int(raw[r * stride:(r + 1) * stride].split(b"\0", 1)[0].decode()) for r in range(self.d)]
+        # a singleton's value is its exact survivor count, written once (row 0)
+        rows = 1 if bin(self.mask(subset)).count("1") == 1 else self.d
+        vals = [int(raw[r * stride:(r + 1) * stride].split(b"\0", 1)[0].decode()) for r in range(rows)]
+        return vals * self.d if rows == 1 else vals
 
     def estimate_subplans(self, subsets, stream=None) -> list[float]:
         n = len(subsets)

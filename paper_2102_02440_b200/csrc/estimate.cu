@@ -2,13 +2,15 @@
 // (PAPER.md:197-201 two-way; PAPER.md:221-225 partitioned; PAPER.md:234-240
 // merging) and the greedy enumerator.
 //
-// Exactness.  E_r is an integer (a sum of products of integer counters).  The
-// GPU evaluates it modulo K pairwise-coprime Mersenne numbers m_k = 2^{a_k} - 1
-// (a_k in {61,59,57,55,53,49,47,43,41,37}; gcd(2^a-1, 2^b-1) = 2^gcd(a,b)-1 = 1),
-// where reduction is two shift-and-add folds.  K is chosen from a rigorous bound
-// |E_r| <= prod_t ||T_t||_1 (L1 norms measured on the device), and the host
-// reconstructs E_r exactly by Garner's mixed-radix CRT, takes the median over
-// rows, and rounds once to fp64 (round-to-nearest-even).
+// Exactness.  E_r is an integer (a sum of products of integer counters), computed
+// exactly by one of three engines: (1) two-way sub-plans, an int128 dot product per row
+// (k_dot128; rows not provably inside int128 are flagged and redone by (3)); (2) matrix-
+// free multi-way sub-plans whose rigorous bound (message-passing node bounds from the
+// survivor counts, re-verified with L1 norms measured on the device) is <= 2^125, an
+// int128 (or int64, when a node's bound is <= 2^61) message-passing engine; (3) every
+// other sub-plan, modulo K primes below 2^26 (Barrett reduction, kMods), K chosen from the
+// same bound, reconstructed on the host by Garner's mixed-radix CRT.  The host takes the
+// median over rows and rounds it once to fp64 (round-to-nearest-even).
 //
 // Contraction.  The sub-plan's tensor network is contracted by message passing
 // over a spanning tree rooted at the lowest-index table; a single cycle is
@@ -1054,9 +1056,12 @@ __global__ void k_root_reduce(const uint64_t *part, uint64_t *acc, int slots, in
 
 // ---------------------------------------------------------------- two-way estimate (A9)
 // E_r = sum_j A[r][j] * B[r][j] in exact int128:
-// |A[r][j] B[r][j]| <= N_A N_B < 2^126 for any pair of sketches built from < 2^63 tuples,
-// so the sum over a row never leaves int128 — no moduli, no bound check.  Both legs are
-// folded to the common width w inline (O5): A'[j] = sum_s A[j + s w].
+// |A[r][j] B[r][j]| <= N_A N_B < 2^126 for any pair of sketches built from < 2^63 tuples.
+// Counter buffers are caller-owned (merged, all-reduced, or written by the caller), so the
+// kernel does not rely on that: it also accumulates U = sum_j |A'_j| |B'_j| (unsigned, carry
+// detected) and flags the row if a fold overflows int64 or U >= 2^127; a flagged plan is
+// re-evaluated by the CRT engine (exact for any int64 counters).  Both legs are folded to
+// the common width w inline (O5): A'[j] = sum_s A[j + s w].
 struct DotItem {
     const int64_t *a, *b;
     uint32_t wa, wb, w;
@@ -1070,32 +1075,62 @@ __device__ __forceinline__ void add128(uint64_t &lo, uint64_t &hi, uint64_t l2, 
     lo = t;
 }
 
-// one CTA per (item, row): out[(item*d + r)*2 + {0,1}] = {lo, hi} of the two's-complement sum
+// one CTA per (item, row): out[(item*d + r)*3 + {0,1}] = {lo, hi} of the two's-complement
+// sum, out[... + 2] = 1 if the row is flagged (not provably exact in int128), else 0
+__device__ __forceinline__ bool fold_add(int64_t &x, int64_t v) {
+    const int64_t t = (int64_t)((uint64_t)x + (uint64_t)v);
+    const bool ovf = ((x ^ t) & (v ^ t)) < 0;
+    x = t;
+    return ovf;
+}
+__device__ __forceinline__ bool uadd128(uint64_t &lo, uint64_t &hi, uint64_t l2, uint64_t h2) {
+    const uint64_t t = lo + l2;
+    const uint64_t c = t < lo;
+    const uint64_t h = hi + h2;
+    const bool ovf = h < hi || h + c < h;
+    hi = h + c;
+    lo = t;
+    return ovf;
+}
 __global__ void __launch_bounds__(512) k_dot128(const __grid_constant__ DotItems items, uint64_t *out) {
     const int item = blockIdx.x / items.d, r = blockIdx.x % items.d;
     const DotItem it = items.it[item];
     const int64_t *A = it.a + uint64_t(r) * it.wa, *B = it.b + uint64_t(r) * it.wb;
-    uint64_t lo = 0, hi = 0;
+    uint64_t lo = 0, hi = 0, ulo = 0, uhi = 0;
+    bool bad = false;
     for (uint32_t j = threadIdx.x; j < it.w; j += blockDim.x) {
         int64_t x = 0, y = 0;
-        for (uint32_t s = j; s < it.wa; s += it.w) x += __ldg(reinterpret_cast<const long long *>(A) + s);
-        for (uint32_t s = j; s < it.wb; s += it.w) y += __ldg(reinterpret_cast<const long long *>(B) + s);
+        for (uint32_t s = j; s < it.wa; s += it.w) bad |= fold_add(x, __ldg(reinterpret_cast<const long long *>(A) + s));
+        for (uint32_t s = j; s < it.wb; s += it.w) bad |= fold_add(y, __ldg(reinterpret_cast<const long long *>(B) + s));
         const __int128 p = (__int128)x * (__int128)y;
         add128(lo, hi, (uint64_t)p, (uint64_t)((unsigned __int128)p >> 64));
+        const uint64_t ax = x < 0 ? 0ull - (uint64_t)x : (uint64_t)x, ay = y < 0 ? 0ull - (uint64_t)y : (uint64_t)y;
+        const unsigned __int128 up = (unsigned __int128)ax * ay;
+        bad |= uadd128(ulo, uhi, (uint64_t)up, (uint64_t)(up >> 64));
     }
     for (int o = 16; o > 0; o >>= 1) {
         const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
         add128(lo, hi, l2, h2);
+        const uint64_t u2 = __shfl_xor_sync(0xffffffffu, ulo, o), v2 = __shfl_xor_sync(0xffffffffu, uhi, o);
+        bad |= uadd128(ulo, uhi, u2, v2);
     }
-    __shared__ uint64_t slo[16], shi[16];
+    bad = __any_sync(0xffffffffu, bad);
+    __shared__ uint64_t slo[16], shi[16], sul[16], suh[16];
+    __shared__ int sbad[16];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) { slo[wid] = lo; shi[wid] = hi; }
+    if (lane == 0) { slo[wid] = lo; shi[wid] = hi; sul[wid] = ulo; suh[wid] = uhi; sbad[wid] = bad; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        uint64_t L = 0, H = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) add128(L, H, slo[i], shi[i]);
-        out[uint64_t(blockIdx.x) * 2] = L;
-        out[uint64_t(blockIdx.x) * 2 + 1] = H;
+        uint64_t L = 0, H = 0, UL = 0, UH = 0;
+        bool B = false;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+            add128(L, H, slo[i], shi[i]);
+            B |= uadd128(UL, UH, sul[i], suh[i]) || sbad[i];
+        }
+        B |= (UH >> 63) != 0;   // U >= 2^127: the signed sum may not fit int128
+        out[uint64_t(blockIdx.x) * 3] = L;
+        out[uint64_t(blockIdx.x) * 3 + 1] = H;
+        out[uint64_t(blockIdx.x) * 3 + 2] = B ? 1 : 0;
     }
 }
 
@@ -1899,16 +1934,17 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
 // ||row||_1 <= N); the device-measured L1 norms verify it, else the plan is redone.
 static bool is_two_way(const Plan &P) { return P.T.size() == 2 && P.T[0].kind == KV && P.T[1].kind == KV; }
 
-// all two-way plans of a batch: one k_dot128 launch per kMaxDot plans, one copy, one sync
+// all two-way plans of a batch: one k_dot128 launch per kMaxDot plans, one copy, one sync.
+// Plans with a flagged row are returned in `redo` (evaluated by the general engine).
 static sk_status run_two_way(std::vector<Plan> &plans, const std::vector<size_t> &idx,
-                             std::vector<std::vector<SBig>> &rows, cudaStream_t stream) {
+                             std::vector<std::vector<SBig>> &rows, std::vector<size_t> &redo, cudaStream_t stream) {
     if (idx.empty()) return SK_OK;
     int d = plans[idx[0]].d;
     for (size_t i : idx) d = std::max(d, plans[i].d);
     DevPool pool;
     void *dout;
     sk_status st;
-    if ((st = dalloc(pool, idx.size() * d * 16, stream, &dout))) return st;
+    if ((st = dalloc(pool, idx.size() * d * 24, stream, &dout))) return st;
     uint64_t *out = (uint64_t *)dout;
     for (size_t b0 = 0; b0 < idx.size();) {
         // one launch per run of plans with equal d (grid = items x d)
@@ -1922,14 +1958,14 @@ static sk_status run_two_way(std::vector<Plan> &plans, const std::vector<size_t>
             items.it[items.n++] = {a->counters, b->counters, a->w[0], b->w[0], (uint32_t)P.width[0]};
             ++b1;
         }
-        k_dot128<<<items.n * items.d, 512, 0, stream>>>(items, out + b0 * d * 2); count_launch();
+        k_dot128<<<items.n * items.d, 512, 0, stream>>>(items, out + b0 * d * 3); count_launch();
         SKB_CUDA_CHECK("k_dot128 launch");
         b0 = b1;
     }
-    std::vector<uint64_t> host(idx.size() * d * 2);
+    std::vector<uint64_t> host(idx.size() * d * 3);
     SKB_CUDA(cudaMemcpyAsync(host.data(), out, host.size() * 8, cudaMemcpyDeviceToHost, stream));
     SKB_CUDA(cudaStreamSynchronize(stream));
-    // items of one launch are laid out [item][d_launch][2] from the launch's base b0 * d * 2
+    // items of one launch are laid out [item][d_launch][3] from the launch's base b0 * d * 3
     for (size_t b0 = 0; b0 < idx.size();) {
         const int dl = plans[idx[b0]].d;
         size_t b1 = b0;
@@ -1937,8 +1973,13 @@ static sk_status run_two_way(std::vector<Plan> &plans, const std::vector<size_t>
         for (size_t j = b0; j < b1; ++j) {
             auto &rr = rows[idx[j]];
             rr.clear();
-            const uint64_t *h = host.data() + b0 * d * 2 + (j - b0) * dl * 2;
-            for (int r = 0; r < dl; ++r) rr.push_back(sbig_from_i128(h[2 * r], h[2 * r + 1]));
+            const uint64_t *h = host.data() + b0 * d * 3 + (j - b0) * dl * 3;
+            bool bad = false;
+            for (int r = 0; r < dl; ++r) {
+                rr.push_back(sbig_from_i128(h[3 * r], h[3 * r + 1]));
+                bad |= h[3 * r + 2] != 0;
+            }
+            if (bad) { rr.clear(); redo.push_back(idx[j]); }
         }
         b0 = b1;
     }
@@ -1946,7 +1987,7 @@ static sk_status run_two_way(std::vector<Plan> &plans, const std::vector<size_t>
 }
 
 static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vector<std::vector<SBig>> &rows,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, bool no_two_way = false) {
     const size_t n = plans.size();
     rows.assign(n, {});
     if (!n) return SK_OK;
@@ -1956,16 +1997,18 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
         std::vector<Plan> rest;
         std::vector<size_t> rest_idx;
         for (size_t i = 0; i < n; ++i) {
-            if (is_two_way(plans[i]) && !getenv("COMPASS_EST_CRT_ONLY")) tw.push_back(i);
+            if (!no_two_way && is_two_way(plans[i]) && !getenv("COMPASS_EST_CRT_ONLY")) tw.push_back(i);
             else rest_idx.push_back(i);
         }
         if (!tw.empty()) {
-            sk_status st = run_two_way(plans, tw, rows, stream);
+            std::vector<size_t> redo;
+            sk_status st = run_two_way(plans, tw, rows, redo, stream);
             if (st) return st;
+            for (size_t i : redo) rest_idx.push_back(i);   // not provably exact in int128: CRT engine
             if (rest_idx.empty()) return SK_OK;
             for (size_t i : rest_idx) rest.push_back(std::move(plans[i]));
             std::vector<std::vector<SBig>> rrows;
-            st = run_batch(g, rest, rrows, stream);
+            st = run_batch(g, rest, rrows, stream, /*no_two_way=*/true);
             for (size_t j = 0; j < rest_idx.size(); ++j) {
                 plans[rest_idx[j]] = std::move(rest[j]);
                 rows[rest_idx[j]] = std::move(rrows[j]);

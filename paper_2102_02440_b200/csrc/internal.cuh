@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -29,6 +30,10 @@ struct sk_sketch {
     // (the seeds never change), freed with the sketch
     uint32_t *lut[2] = {nullptr, nullptr};
     uint64_t lut_dom[2] = {0, 0};
+    // the tables are built on the first caller's stream: later calls on any stream wait on
+    // this event (recorded after the build); the mutex guards the cache fields
+    cudaEvent_t lut_ready = nullptr;
+    std::mutex lut_mu;
 };
 
 namespace skb {

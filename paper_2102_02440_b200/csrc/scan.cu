@@ -33,6 +33,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <mutex>
 #include <vector>
 
 #include "hash.cuh"
@@ -344,7 +345,12 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
         // (fewer than 1 hit in 4 probes after 8192 probes: a flat key distribution); what the
         // table holds is still flushed at the end, so the counts stay exact either way
         uint32_t *hstat = reinterpret_cast<uint32_t *>(smem + P.off_hstat) + k * 4;
-        const bool use_hh = P.key[k].hh_off >= 0 && (!P.key[k].hist || *reinterpret_cast<volatile uint32_t *>(hstat + 2) == 0);
+        // the flag is written concurrently by other warps: lane 0's read is broadcast so the
+        // full-mask ballots below are reached by every lane or by none (warp-uniform branch)
+        uint32_t hh_off_flag = 0;
+        if (P.key[k].hist && P.key[k].hh_off >= 0)
+            hh_off_flag = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile uint32_t *>(hstat + 2), 0);
+        const bool use_hh = P.key[k].hh_off >= 0 && (!P.key[k].hist || hh_off_flag == 0);
         bool hh_hit = false;
         if (leader) {
             if (P.key[k].hist) {
@@ -1113,15 +1119,28 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
             const uint64_t dp = (sk->d + 3) & ~3u;
             for (int q = 0; q < 2; ++q) ok &= sk->d <= 8 && dom[q] > 0 && dom[q] <= (1ULL << 31) && dom[q] * dp * 4 <= (64ULL << 20);
             if (!ok) continue;
+            std::lock_guard<std::mutex> lk(sk->lut_mu);
+            bool built = false;
             for (int q = 0; q < 2; ++q) {
                 if (sk->lut[q] && sk->lut_dom[q] >= dom[q]) continue;
-                if (sk->lut[q]) { cudaFree(sk->lut[q]); sk->lut[q] = nullptr; }
+                if (sk->lut[q]) {   // a wider table replaces it: no reader of the old one may be in flight
+                    SKB_CUDA(cudaDeviceSynchronize());
+                    cudaFree(sk->lut[q]);
+                    sk->lut[q] = nullptr;
+                }
                 SKB_CUDA(cudaMalloc(&sk->lut[q], dom[q] * dp * 4));
                 k_lut_build<<<(unsigned)std::min<uint64_t>(uint64_t(sms_l) * 8, (dom[q] * dp + 255) / 256), 256, 0, stream>>>(
                     sk->seeds_dev + size_t(q) * sk->d * 6, sk->d, sk->w[q] - 1, dom[q], sk->lut[q]);
                 SKB_CUDA(cudaGetLastError());
                 count_launch();
                 sk->lut_dom[q] = dom[q];
+                built = true;
+            }
+            if (built) {
+                if (!sk->lut_ready) SKB_CUDA(cudaEventCreateWithFlags(&sk->lut_ready, cudaEventDisableTiming));
+                SKB_CUDA(cudaEventRecord(sk->lut_ready, stream));
+            } else if (sk->lut_ready) {
+                SKB_CUDA(cudaStreamWaitEvent(stream, sk->lut_ready, 0));   // built on another stream
             }
             tg.lut0 = sk->lut[0];
             tg.lut1 = sk->lut[1];
@@ -1234,15 +1253,19 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     kern<<<(unsigned)grid, threads, off, stream>>>(P);
     SKB_CUDA(cudaGetLastError());
     count_launch();
-    // histogram -> sketches, then release the histograms (stream-ordered)
+    // histogram -> sketches, then release the histograms (stream-ordered).  Every 1-D target
+    // on a histogram key gets its in-domain counts only here, so all of them must be served:
+    // the targets go in chunks of kMaxEpiTargets, one epilogue launch per chunk.
     for (uint32_t k = 0; k < P.n_keys; ++k) {
         if (!P.key[k].hist) continue;
+      for (uint32_t t_next = 0; t_next < c.n_targets;) {
         EpiParams E;
         memset(&E, 0, sizeof(E));
         E.hist = P.key[k].hist;
         E.domain = P.key[k].domain;
         uint32_t sc2 = 0;
-        for (uint32_t t = 0; t < c.n_targets && E.n_targets < kMaxEpiTargets; ++t) {
+        uint32_t t = t_next;
+        for (; t < c.n_targets && E.n_targets < kMaxEpiTargets; ++t) {
             if (c.tgt_ndim[t] != 1 || c.tgt_key[t][0] != keys[k]) continue;
             EpiTarget &et = E.tgt[E.n_targets++];
             et.counters = c.tgt_counters[t];
@@ -1254,6 +1277,8 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
             if ((sc2 + need) * 4 <= 200 * 1024) { et.smem_off = (int32_t)sc2; sc2 += need; }
             else et.smem_off = -1;
         }
+        t_next = t;
+        if (!E.n_targets) break;
         E.smem_counters = sc2;
         const size_t esm = size_t(sc2) * 4;
         SKB_CUDA(cudaFuncSetAttribute(k_hist_epilogue, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm));
@@ -1261,6 +1286,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         k_hist_epilogue<<<std::max(1u, eg), 512, esm, stream>>>(E);
         SKB_CUDA(cudaGetLastError());
         count_launch();
+      }
     }
     for (void *h : hists) cudaFreeAsync(h, stream);
     *launched = true;

@@ -55,6 +55,40 @@ def test_l1_paper_example():
     assert oracle.permutation_l1([3, 2, 1], [1, 2, 3]) == 4
 
 
+@pytest.mark.parametrize("vals,expect", [
+    # hand-sorted by eye: [-3, 1, 5, 7, 9] -> 5 (mean 3.8, unsorted middle 7)
+    ([9, -3, 7, 1, 5], 5),
+    # [-10^25, -4, 0, 2, 3, 8, 10^30] -> 2 (unsorted middle 3; the mean is ~1.4e29)
+    ([10**30, -4, 0, 3, -10**25, 8, 2], 2),
+    # ties: [1, 2, 2, 2, 3] -> 2
+    ([2, 2, 1, 3, 2], 2),
+    # all negative, d = 3: [-9, -5, -1] -> -5
+    ([-1, -9, -5], -5),
+    ([42], 42),
+])
+def test_median_odd_hand_values(vals, expect):
+    """PAPER.md:201 (Fast-AGMS estimate = median over the d rows), d odd (reading R5):
+    element (d-1)/2 of the ascending order, checked on hand-sorted unsorted rows where the
+    mean and the unsorted middle element both differ from the median."""
+    assert oracle.median_odd(vals) == expect
+
+
+def test_median_odd_rejects_even_d():
+    with pytest.raises(AssertionError):
+        oracle.median_odd([1, 2])
+
+
+def test_estimate_is_median_of_rows_hand_example():
+    """Two-way estimate of hand-written 5-row sketches (w = 2): per-row dot products by
+    hand, then the median."""
+    A = np.array([[1, 2], [3, -1], [0, 4], [-2, -2], [5, 0]], dtype=np.int64)
+    B = np.array([[2, 1], [1, 1], [1, 1], [3, 1], [1, 7]], dtype=np.int64)
+    # rows: 1*2+2*1=4, 3-1=2, 0+4=4, -6-2=-8, 5+0=5  -> sorted [-8, 2, 4, 4, 5] -> 4
+    g = oracle.Graph({"A": 10, "B": 10}, [("A.k|B.k", "A", "B")], {("A", "A.k|B.k"): A, ("B", "A.k|B.k"): B})
+    est, rows = oracle.estimate(g, ("A", "B"))
+    assert rows == [4, 2, 4, -8, 5] and est == 4.0
+
+
 # ---------------------------------------------------------------- exact arithmetic
 def test_bignum_exact_vs_python_int():
     L = oracle.lib()
