@@ -171,6 +171,54 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _measured_roofs() -> dict:
+    """Roofs 2 and 3 of SURVEY.md §8(d) and the read-only stream, measured on a B200 by
+    tools/roofs_micro.cu (MEASURED_ROOFS.json, beside the driver's MEASURED_PEAKS.json)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_ROOFS.json")))
+    except Exception:
+        return {}
+
+
+def _int_update_roofs(ws, survivors, kernel_ms, roofs) -> dict:
+    """Algorithmic hash and update work of the scans (SURVEY.md §8(d) roofs 2 and 3), counted
+    without the exact levers (every survivor hashed and counted once per sketch row):
+      hash pairs  I = sum_t survivors_t * sum_{s of t} d_s * ndim_s   ((xi, h) per key and row)
+      updates     U = sum_t survivors_t * sum_{s of t} d_s            (counter increments)
+    achieved = I / t (U / t) over the scans' time; peak = the measured roof (narrow / wide hash
+    path by key width; shared-memory atomics for sketches that fit a CTA, L2 red otherwise).
+    frac > 1 means the levers (key aggregation, heavy hitters, histograms, lookup tables)
+    beat the naive roof."""
+    if not roofs:
+        return {"int_frac": None, "update_frac": None, "roofs_source": "MEASURED_ROOFS.json missing"}
+    t = kernel_ms / 1e3
+    pairs_n = pairs_w = 0
+    t_upd = 0.0
+    upd = 0
+    for tb, sv in zip(ws.tables, survivors):
+        wide = any(c.dtype == "int64" for c in tb.cols)
+        for s in ws.sketches_of(tb.name):
+            cells = 1
+            for w in s.w:
+                cells *= w
+            pr = sv * s.d * len(s.w)
+            if wide:
+                pairs_w += pr
+            else:
+                pairs_n += pr
+            u = sv * s.d
+            upd += u
+            fits = s.d * cells * 4 <= 96 * 1024
+            t_upd += u / (roofs["atoms_smem_per_s"] if fits else roofs["red_l2_u64_mat10mb_per_s"])
+    t_hash = pairs_n / roofs["hash_narrow_pairs_per_s"] + pairs_w / roofs["hash_wide_pairs_per_s"]
+    return {"int": {"hash_pairs": pairs_n + pairs_w, "achieved_pairs_per_s": (pairs_n + pairs_w) / t,
+                    "roof_time_ms": round(t_hash * 1e3, 4), "frac": round(t_hash / t, 4)},
+            "update": {"counter_increments": upd, "achieved_per_s": upd / t,
+                       "roof_time_ms": round(t_upd * 1e3, 4), "frac": round(t_upd / t, 4)},
+            "int_frac": round(t_hash / t, 4), "update_frac": round(t_upd / t, 4),
+            "roofs_source": "MEASURED_ROOFS.json (tools/roofs_micro.cu)"}
+
+
 def _relaunch(n: int) -> int:
     """`bench.py --gpus N` run as one process: re-executes itself under torchrun with N ranks
     on this node (one process per GPU, NCCL over NVLink), rendezvous on 127.0.0.1."""
@@ -422,16 +470,19 @@ def main():
         traffic = tf.get(ws.name)
     except Exception:
         pass
+    roofs = _measured_roofs()
+    read_peak = roofs.get("read_stream_gbs")
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
             "kernel": "k_scan (persistent TMA-ring fused filter+hash+update+flush)",
             "alg_bytes_per_step": ab["alg"], "kernel_ms_per_step": round(kms, 4),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "_fallback" not in peaks else "fallback 6.65 TB/s",
-            "frac_of_nominal_8TBs": round(achieved / 8000.0, 4),
-            # third denominator of SURVEY.md §8(d): the measured read-only TMA-ring stream of 12 GB
-            # (tools/stream_micro.cu: 7.3 TB/s on these B200s)
-            "frac_of_read_stream_7300GBs": round(achieved / 7300.0, 4)}
-
+            "frac_of_nominal_8TBs": round(achieved / 8000.0, 4)}
+    if read_peak:
+        # third denominator of SURVEY.md §8(d): the measured read-only stream (MEASURED_ROOFS.json)
+        roof["read_stream_gbs"] = read_peak
+        roof["frac_of_read_stream"] = round(achieved / read_peak, 4)
+    roof.update(_int_update_roofs(ws, run.survivors.tolist(), kms, roofs))
     line = {"metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
             "timing": {"value_is": "rows of all ranks / t_build (SURVEY.md 8(d)): zero + fused scans + "

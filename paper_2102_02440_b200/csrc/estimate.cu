@@ -80,7 +80,13 @@ __device__ __forceinline__ uint64_t mm_i64(int64_t v, uint64_t m, uint64_t mu) {
 }
 
 // ---------------------------------------------------------------- small kernels
-// per (item, row): sum |v| over `cells` counters (blockIdx.z = chunk; atomically accumulated)
+// per (item, row): sum |v| over `cells` counters (blockIdx.z = chunk; atomically accumulated).
+// Saturating: a row whose L1 reaches 2^64 (caller-owned counters can hold any int64) reads
+// UINT64_MAX, which the host takes as the worst case 2^63 * cells (the bound stays rigorous).
+__device__ __forceinline__ unsigned long long sat_add(unsigned long long a, unsigned long long b) {
+    const unsigned long long c = a + b;
+    return c < a ? ~0ULL : c;
+}
 struct L1Item { const int64_t *p; uint32_t d; uint32_t cells; };
 constexpr int kMaxL1Items = 48;
 struct L1Items { L1Item it[kMaxL1Items]; int n; };
@@ -91,15 +97,19 @@ __global__ void k_l1(const __grid_constant__ L1Items items, unsigned long long *
     const uint32_t chunk = (it.cells + gridDim.z - 1) / gridDim.z;
     const uint32_t c0 = blockIdx.z * chunk, c1 = min(it.cells, c0 + chunk);
     unsigned long long s = 0;
-    for (uint32_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) s += uabs(it.p[uint64_t(r) * it.cells + i]);
+    for (uint32_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) s = sat_add(s, uabs(it.p[uint64_t(r) * it.cells + i]));
     __shared__ unsigned long long red[32];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    for (int o = 16; o > 0; o >>= 1) s = sat_add(s, __shfl_xor_sync(0xffffffffu, s, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long t = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
-        if (t) atomicAdd(&out[blockIdx.x * maxd + r], t);
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = sat_add(t, red[i]);
+        if (t) {
+            unsigned long long *p = &out[blockIdx.x * maxd + r];
+            unsigned long long old = *p, seen;
+            while ((seen = atomicCAS(p, old, sat_add(old, t))) != old) old = seen;
+        }
     }
 }
 
@@ -2166,6 +2176,8 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
             const size_t u = std::find(uniqs[i].begin(), uniqs[i].end(), s) - uniqs[i].begin();
             uint64_t mx = 0;
             for (int r = 0; r < d; ++r) mx = std::max<uint64_t>(mx, host[off_l1[i] + u * d + r]);
+            // saturated (>= 2^64): the worst case for int64 counters, 2^63 per cell
+            if (mx == ~0ULL) return ldexp((double)(s->n_counters / s->d), 63);
             return (double)mx;
         };
         const double logB = std::min(log_bound(P, l1of), abs_bound[i]);

@@ -30,6 +30,12 @@ struct sk_sketch {
     // (the seeds never change), freed with the sketch
     uint32_t *lut[2] = {nullptr, nullptr};
     uint64_t lut_dom[2] = {0, 0};
+    // 1-D sketches: packed 64-bit lookup table over a hinted key domain [0, lut64_dom) for
+    // the scan's lookup-table path: lut64[x] = sum_r ((h_r(x) & (w - 1)) << 1 | (xi_r(x) < 0))
+    // << (r * lut64_bits), lut64_bits = log2(w) + 1, d * lut64_bits <= 64 (H3/H4)
+    uint64_t *lut64 = nullptr;
+    uint64_t lut64_dom = 0;
+    uint32_t lut64_bits = 0;
     // the tables are built on the first caller's stream: later calls on any stream wait on
     // this event (recorded after the build); the mutex guards the cache fields
     cudaEvent_t lut_ready = nullptr;

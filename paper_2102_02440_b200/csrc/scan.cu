@@ -26,842 +26,16 @@
 //       1-D sketches').
 //   A7  CTA flush: int32 smem counters and heavy-hitter counts -> int64 HBM
 //       sketch with red.global.add (order-independent, bit-exact).
-#include <stdint.h>
-#include <stdio.h>
-#include <stdlib.h>
-#include <string.h>
+#include "scan_kernel.cuh"
 
-#include <algorithm>
-#include <climits>
-#include <mutex>
-#include <vector>
-
-#include "hash.cuh"
-#include "internal.cuh"
-#include "scan.cuh"
-
-using namespace skb;
+namespace skb {
+const void *scan_pick_nk1(uint32_t np, int kw, bool fast);   // scan_k1.cu
+const void *scan_pick_nk2(uint32_t np, int kw, bool fast);   // scan_k2.cu
+const void *scan_pick_nk3(uint32_t np, int kw, bool fast);   // scan_k3.cu
+const void *scan_pick_nk4(uint32_t np, int kw, bool fast);   // scan_k4.cu
+}  // namespace skb
 
 namespace {
-
-#ifndef SCAN_WAIT_HINT
-#define SCAN_WAIT_HINT 1
-#endif
-#ifndef SCAN_CAP2
-#define SCAN_CAP2 64
-#endif
-#ifndef SCAN_WARPS
-#define SCAN_WARPS 20
-#endif
-#ifndef SCAN_GROUPS
-#define SCAN_GROUPS 4
-#endif
-constexpr int kWarps = SCAN_WARPS;           // consumer warps per CTA
-constexpr int kGroups = SCAN_GROUPS;         // independent ring groups per CTA (one producer warp each)
-constexpr int kGW = kWarps / kGroups;        // consumer warps per group
-constexpr int kTile = kGW * 128;             // rows per group tile (one ring stage)
-static_assert(kWarps % kGroups == 0, "warps must split evenly into ring groups");
-
-constexpr int kConsumers = kWarps * 32;
-constexpr int kThreads = kConsumers + 32 * kGroups;
-constexpr int kMaxStages = 8;
-constexpr int kMaxSCols = 8, kMaxSPreds = 8, kMaxKeys = 4, kMaxSTargets = 16;
-constexpr uint64_t kEmpty = ~0ULL;   // canonical keys are < 2^61: never equal
-
-struct SCol {
-    const void *p;
-    uint32_t bytes;       // 4 or 8
-    int32_t soff;         // byte offset inside a stage, -1 = not staged
-};
-enum { PR_R32 = 0, PR_R64 = 1, PR_SET = 2, PR_NONE = 3 };
-struct SPred {
-    uint32_t col, kind;   // PR_R32: (uint32)(v - lo32) <= span32; PR_R64: (uint64)(v - lo) <= span; PR_NONE: no row
-    int64_t lo;           // POINT c is RANGE [c, c]
-    uint64_t span;
-    const int64_t *set;
-    uint32_t n;
-};
-struct SKey {
-    uint32_t col;
-    int32_t hh_off;       // byte offset of this key's heavy-hitter table, -1 = none
-    uint32_t has1d;       // some 1-D target hashes this key
-    uint32_t hasglob;     // some non-privatised 1-D target hashes this key
-    uint32_t *hist;       // histogram mode: per-key counts over [0, domain), else null
-    uint64_t domain;
-    uint32_t priv1d;      // bit t: 1-D target t on this key, privatised in smem
-    uint32_t glob1d;      // bit t: 1-D target t on this key, updated in HBM/L2
-};
-struct STarget {
-    int64_t *counters;
-    uint32_t ndim, d, wmask0, wmask1, lw1;
-    uint32_t k0, k1;      // indices into keys[]
-    int32_t smem_off;     // int32 offset of privatised copy, -1 = global
-    uint32_t cells;
-    uint32_t seed_off;
-    const uint32_t *lut0, *lut1;   // matrices: per-dimension hash lookup tables (or null)
-    uint64_t lut_dom0, lut_dom1;
-};
-struct SParams {
-    SCol col[kMaxSCols];
-    SPred pred[kMaxSPreds];
-    SKey key[kMaxKeys];
-    STarget tgt[kMaxSTargets];
-    const uint64_t *seeds[kMaxSTargets];
-    uint32_t n_cols, n_preds, n_keys, n_targets;
-    uint64_t n_rows, n_tiles;
-    uint32_t stage_bytes;
-    uint32_t stages;      // ring depth (<= kMaxStages)
-    uint32_t gather;      // 1: survivors' keys gathered, 0: keys staged (no predicate)
-    uint32_t cap;         // entries of each warp's survivor-key ring (power of two)
-    uint32_t kb_bytes;    // bytes of one warp's ring
-    uint32_t hh_log2;     // heavy-hitter slots per key = 1 << hh_log2
-    // smem layout (byte offsets)
-    uint32_t off_ring, off_kbuf, off_hh, off_sc, off_seed;
-    uint32_t smem_counters, seed_words;
-    uint32_t has2d;       // some target is a matrix
-    // trio: a matrix M on key columns (ka, kb) whose two hash families equal those of the
-    // privatised 1-D sketches A on ka and B on kb (same edges, same d).  One row loop hashes
-    // each survivor's two keys once and updates A, B and M (the matrix reuses the 1-D hash
-    // values).
-    uint32_t trio_on, trio_ka, trio_kb, trio_a, trio_b, trio_m;
-    uint32_t off_miss, off_missn;   // per-warp miss buffers (x, count) and fill counts
-    uint32_t off_hstat;             // per key: heavy-hitter probes, hits, disabled flag (histogram keys)
-    uint32_t off_rows;              // per-warp survivor row-offset list (128 x uint16)
-    uint32_t tile_rows;             // rows per ring stage
-    uint32_t n_full_tiles;          // tiles with tile_rows rows (staged by TMA)
-    unsigned long long *survivors;
-};
-
-// ------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity), "r"(0x989680u) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
-#if SCAN_WAIT_HINT
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-        "@!P1 bra WAIT_%=;\n}" ::"r"(bar), "r"(parity), "r"(0x989680u) : "memory");
-#else
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
-#endif
-}
-__device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-// every committed group has landed (cp.async issued since the last commit are not covered)
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-// commits the current (possibly partial) group too: every cp.async issued so far has landed
-__device__ __forceinline__ void cp_commit_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-#ifndef SCAN_LAG
-#define SCAN_LAG 3
-#endif
-constexpr int kLag = SCAN_LAG;   // a tile's gathered keys are consumed kLag tiles later
-__device__ __forceinline__ void cp_wait_lag() { asm volatile("cp.async.wait_group %0;" ::"n"(kLag) : "memory"); }
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
-__device__ __forceinline__ void red_add_u32(uint32_t *p, uint32_t v) {
-    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void red_add_s64(int64_t *p, int64_t v) {
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ bool in_set(const int64_t *s, uint32_t n, int64_t v) {
-    uint32_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(reinterpret_cast<const long long *>(s) + mid) < v) lo = mid + 1; else hi = mid;
-    }
-    return lo < n && __ldg(reinterpret_cast<const long long *>(s) + lo) == v;
-}
-
-// ------------------------------------------------------------------ heavy-hitter table
-// Two-choice table of 2^log2s slots (canonical key -> int32 count): a key lives in slot
-// s1(x) or s2(x); a probe is one 64-bit shared load and compare per choice, so a hit on
-// the first choice (every hot key: they arrive first) costs a handful of instructions.
-// Slots are never freed, so a key found in s2 cannot also sit in s1.  Two warps may
-// still insert one key twice in a race; both counts are flushed, which is exact by
-// linearity.
-__device__ __forceinline__ uint64_t lds_v64(uint32_t a) {
-    uint64_t v;
-    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ bool hh_add(unsigned char *tab, uint32_t log2s, uint64_t x, int cnt) {
-    // shared-window addresses and shared-space atomics (no generic-address conversion)
-    const uint32_t ka = smem_u32(tab), ca = ka + (8u << log2s);
-    const uint64_t h = x * 0x9E3779B97F4A7C15ULL;
-    const uint32_t mask = (1u << log2s) - 1u;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-        const uint32_t sl = (uint32_t)(h >> (c ? 24 : 44)) & mask;
-        uint64_t k = lds_v64(ka + sl * 8);
-        if (k == kEmpty)
-            asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(k) : "r"(ka + sl * 8), "l"(kEmpty), "l"(x) : "memory");
-        if (k == x || k == kEmpty) {
-            asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(ca + sl * 4), "r"(cnt) : "memory");
-            return true;
-        }
-    }
-    return false;
-}
-
-// ------------------------------------------------------------------ sketch updates
-// 1-D target t: row r gets cnt * xi_r(x) at bucket h_r(x)
-template <bool N>
-__device__ __forceinline__ void update_1d_t(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, int cnt) {
-    for (uint32_t r = 0; r < tg.d; ++r) {
-        const uint64_t *a = seed + r * 6;
-        const uint32_t cell = (uint32_t)(hash_g61_t<N>(a[4], a[5], x) & tg.wmask0);
-        const int v = xi_sign61_t<N>(a, x) * cnt;
-        if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
-        else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
-    }
-}
-__device__ __forceinline__ void update_1d(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, int cnt) {
-    if (x < (1ULL << 32)) update_1d_t<true>(tg, seed, sc, x, cnt);
-    else update_1d_t<false>(tg, seed, sc, x, cnt);
-}
-
-template <bool N>
-__device__ __forceinline__ void update_2d_t(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, uint64_t y,
-                                            int cnt) {
-    const uint64_t *s1 = seed + tg.d * 6;
-    for (uint32_t r = 0; r < tg.d; ++r) {
-        const uint64_t *a = seed + r * 6, *b = s1 + r * 6;
-        const uint32_t cell = ((uint32_t)(hash_g61_t<N>(a[4], a[5], x) & tg.wmask0) << tg.lw1) |
-                              (uint32_t)(hash_g61_t<N>(b[4], b[5], y) & tg.wmask1);
-        const int v = xi_sign61_t<N>(a, x) * xi_sign61_t<N>(b, y) * cnt;
-        if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
-        else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
-    }
-}
-__device__ __forceinline__ void update_2d(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, uint64_t y,
-                                          int cnt) {
-    if (tg.lut0 && x < tg.lut_dom0 && y < tg.lut_dom1) {
-        // hinted key domains: (bucket, sign) per row from the lookup tables (the same values
-        // the hash polynomials give; built once per sketch by k_lut_build)
-        // rows padded to a multiple of 4: the entries of both keys arrive in 128-bit loads,
-        // all issued before the first use
-        const uint32_t dp = (tg.d + 3) & ~3u;
-        const uint4 *la = reinterpret_cast<const uint4 *>(tg.lut0 + x * dp), *lb = reinterpret_cast<const uint4 *>(tg.lut1 + y * dp);
-        uint4 va[2], vb[2];
-        va[0] = __ldg(la); vb[0] = __ldg(lb);
-        if (dp > 4) { va[1] = __ldg(la + 1); vb[1] = __ldg(lb + 1); }
-        for (uint32_t r = 0; r < tg.d && r < 8; ++r) {
-            const uint4 &qa = va[r >> 2], &qb = vb[r >> 2];
-            const uint32_t ea = (r & 3) == 0 ? qa.x : (r & 3) == 1 ? qa.y : (r & 3) == 2 ? qa.z : qa.w;
-            const uint32_t eb = (r & 3) == 0 ? qb.x : (r & 3) == 1 ? qb.y : (r & 3) == 2 ? qb.z : qb.w;
-            const uint32_t cell = ((ea >> 1) << tg.lw1) | (eb >> 1);
-            const int v = ((ea ^ eb) & 1u) ? -cnt : cnt;
-            if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
-            else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
-        }
-        return;
-    }
-    if ((x | y) < (1ULL << 32)) update_2d_t<true>(tg, seed, sc, x, y, cnt);
-    else update_2d_t<false>(tg, seed, sc, x, y, cnt);
-}
-
-// x[idx] with compile-time indexing only (keeps the key array in registers)
-template <int NK>
-__device__ __forceinline__ uint64_t pick(const uint64_t (&x)[NK], uint32_t idx) {
-    uint64_t v = x[0];
-#pragma unroll
-    for (int k = 1; k < NK; ++k)
-        if (idx == (uint32_t)k) v = x[k];
-    return v;
-}
-
-// all lanes: lane i < n applies buffered miss i (key x, count c) to every non-privatised
-// 1-D sketch hashed on key column k
-__device__ __forceinline__ void flush_misses(const SParams &P, const uint64_t *seeds, const uint64_t *mx, const int *mc,
-                                             uint32_t n, uint32_t k) {
-    const int lane = threadIdx.x & 31;
-    if ((uint32_t)lane < n) {
-        const uint64_t xv = mx[lane];
-        const int cv = mc[lane];
-        for (uint32_t tm = P.key[k].glob1d; tm; tm &= tm - 1) {
-            const STarget &tg = P.tgt[__ffs(tm) - 1];
-            update_1d(tg, seeds + tg.seed_off, nullptr, xv, cv);
-        }
-    }
-    __syncwarp();
-}
-
-// one warp-wide batch: lanes with `valid` hold one surviving tuple each, canonical keys x[k]
-template <int NK>
-__device__ __forceinline__ void process_batch(const SParams &P, unsigned char *smem, bool valid, const uint64_t (&x)[NK]) {
-    const uint32_t act = __ballot_sync(0xffffffffu, valid);
-    if (!act) return;
-    int32_t *sc = reinterpret_cast<int32_t *>(smem + P.off_sc);
-    const uint64_t *seeds = reinterpret_cast<const uint64_t *>(smem + P.off_seed);
-    const int lane = threadIdx.x & 31;
-    bool la = false, lb = false;   // trio keys: this lane leads its key group (size ca / cb)
-    int ca = 0, cb = 0;
-#pragma unroll
-    for (int k = 0; k < NK; ++k) {
-        if (!P.key[k].has1d) continue;
-        // aggregate equal keys of the warp (match_any); the leader updates with the count
-        bool leader = false, miss = false;
-        int cnt = 0;
-        if (valid) {
-            const uint32_t grp = __match_any_sync(act, x[k]);
-            leader = lane == __ffs(grp) - 1;
-            cnt = __popc(grp);
-        }
-        if (P.trio_on) {
-            if ((uint32_t)k == P.trio_ka) { la = leader; ca = cnt; }
-            if ((uint32_t)k == P.trio_kb) { lb = leader; cb = cnt; }
-        }
-        // histogram keys: the CTA stops probing the heavy-hitter table once it no longer pays
-        // (fewer than 1 hit in 4 probes after 8192 probes: a flat key distribution); what the
-        // table holds is still flushed at the end, so the counts stay exact either way
-        uint32_t *hstat = reinterpret_cast<uint32_t *>(smem + P.off_hstat) + k * 4;
-        // the flag is written concurrently by other warps: lane 0's read is broadcast so the
-        // full-mask ballots below are reached by every lane or by none (warp-uniform branch)
-        uint32_t hh_off_flag = 0;
-        if (P.key[k].hist && P.key[k].hh_off >= 0)
-            hh_off_flag = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile uint32_t *>(hstat + 2), 0);
-        const bool use_hh = P.key[k].hh_off >= 0 && (!P.key[k].hist || hh_off_flag == 0);
-        bool hh_hit = false;
-        if (leader) {
-            if (P.key[k].hist) {
-                // histogram mode: count the key (heavy-hitter table first, then the L2 histogram);
-                // all 1-D sketches of this key are built from the counts after the scan
-                bool done = use_hh && hh_add(smem + P.key[k].hh_off, P.hh_log2, x[k], cnt);
-                hh_hit = done;
-                if (!done && x[k] < P.key[k].domain) { red_add_u32(P.key[k].hist + x[k], (uint32_t)cnt); done = true; }
-                if (!done) {   // outside the hinted domain: direct updates
-                    miss = P.key[k].hasglob;
-                    for (uint32_t tm = P.key[k].priv1d; tm; tm &= tm - 1) {
-                        const STarget &tg = P.tgt[__ffs(tm) - 1];
-                        update_1d(tg, seeds + tg.seed_off, sc, x[k], cnt);
-                    }
-                }
-            } else {
-                if (P.key[k].hh_off >= 0) miss = !hh_add(smem + P.key[k].hh_off, P.hh_log2, x[k], cnt);
-                else miss = P.key[k].hasglob;
-                for (uint32_t tm = P.key[k].priv1d; tm; tm &= tm - 1) {   // privatised: always direct
-                    const STarget &tg = P.tgt[__ffs(tm) - 1];
-                    update_1d(tg, seeds + tg.seed_off, sc, x[k], cnt);
-                }
-            }
-        }
-        if (P.key[k].hist && use_hh) {
-            const uint32_t np = __popc(__ballot_sync(0xffffffffu, leader));
-            const uint32_t nh = __popc(__ballot_sync(0xffffffffu, hh_hit));
-            if (lane == 0 && np) {
-                const uint32_t p0 = atomicAdd(hstat, np), h0 = atomicAdd(hstat + 1, nh);
-                if (p0 + np >= 8192 && (h0 + nh) * 4 < p0 + np) hstat[2] = 1;
-            }
-        }
-        if (P.key[k].hasglob) {
-            // keys without a heavy-hitter slot go to this warp's miss buffer; 32 buffered
-            // misses are flushed together so every lane hashes (SIMT-efficient L2 updates)
-            const uint32_t mb = __ballot_sync(0xffffffffu, miss);
-            if (mb) {
-                const uint32_t mi = (threadIdx.x >> 5) * P.n_keys + k;
-                uint64_t *mx = reinterpret_cast<uint64_t *>(smem + P.off_miss) + mi * 32;
-                int *mc = reinterpret_cast<int *>(smem + P.off_miss + kWarps * P.n_keys * 32 * 8) + mi * 32;
-                uint32_t *nm = reinterpret_cast<uint32_t *>(smem + P.off_missn) + mi;
-                uint32_t fill = *nm;
-                const uint32_t nnew = __popc(mb);
-                if (fill + nnew > 32) {
-                    __syncwarp();
-                    flush_misses(P, seeds, mx, mc, fill, (uint32_t)k);
-                    fill = 0;
-                }
-                if (miss) {
-                    const uint32_t pos = fill + __popc(mb & ((1u << lane) - 1u));
-                    mx[pos] = x[k];
-                    mc[pos] = cnt;
-                }
-                __syncwarp();
-                if (lane == 0) *nm = fill + nnew;
-                __syncwarp();
-            }
-        }
-    }
-    // matrix targets: equal key pairs of the warp aggregated (two match_any), the leader
-    // updates one cell per row with count * xi * xi
-    if (valid && P.has2d) {
-        for (uint32_t t = 0; t < P.n_targets; ++t) {
-            const STarget &tg = P.tgt[t];
-            if (tg.ndim != 2 || (P.trio_on && t == P.trio_m)) continue;
-            const uint64_t xa = pick<NK>(x, tg.k0), xb = pick<NK>(x, tg.k1);
-            const uint32_t grp = __match_any_sync(act, xa) & __match_any_sync(act, xb);
-            if (lane == __ffs(grp) - 1) update_2d(tg, seeds + tg.seed_off, sc, xa, xb, __popc(grp));
-        }
-    }
-    if (valid && P.trio_on) {
-        const uint64_t xa = pick<NK>(x, P.trio_ka), xb = pick<NK>(x, P.trio_kb);
-        const uint32_t grp = __match_any_sync(act, xa) & __match_any_sync(act, xb);
-        const bool lm = lane == __ffs(grp) - 1;
-        const int cm = __popc(grp);
-        if (la || lb || lm) {
-            const STarget &A = P.tgt[P.trio_a], &B = P.tgt[P.trio_b], &M = P.tgt[P.trio_m];
-            const uint64_t *sa = seeds + A.seed_off, *sb = seeds + B.seed_off;
-            const bool narrow = (xa | xb) < (1ULL << 32);
-            for (uint32_t r = 0; r < M.d; ++r) {
-                const uint64_t *a = sa + r * 6, *b = sb + r * 6;
-                uint32_t ga, gb;
-                int xia, xib;
-                if (narrow) {
-                    ga = (uint32_t)hash_g61_t<true>(a[4], a[5], xa);
-                    gb = (uint32_t)hash_g61_t<true>(b[4], b[5], xb);
-                    xia = xi_sign61_t<true>(a, xa);
-                    xib = xi_sign61_t<true>(b, xb);
-                } else {
-                    ga = (uint32_t)hash_g61_t<false>(a[4], a[5], xa);
-                    gb = (uint32_t)hash_g61_t<false>(b[4], b[5], xb);
-                    xia = xi_sign61_t<false>(a, xa);
-                    xib = xi_sign61_t<false>(b, xb);
-                }
-                if (la) atomicAdd(&sc[A.smem_off + r * A.cells + (ga & A.wmask0)], xia * ca);
-                if (lb) atomicAdd(&sc[B.smem_off + r * B.cells + (gb & B.wmask0)], xib * cb);
-                if (lm) {
-                    const uint32_t cell = ((ga & M.wmask0) << M.lw1) | (gb & M.wmask1);
-                    const int v = xia * xib * cm;
-                    if (M.smem_off >= 0) atomicAdd(&sc[M.smem_off + r * M.cells + cell], v);
-                    else red_add_s64(M.counters + uint64_t(r) * M.cells + cell, (int64_t)v);
-                }
-            }
-        }
-    }
-}
-
-// register copy of one predicate (A2)
-struct PR {
-    uint32_t kind, bytes, n;
-    int32_t soff;
-    int64_t lo;
-    uint64_t span;
-    const void *p;
-    const int64_t *set;
-};
-
-// conjunction of the predicates over this lane's 4 rows r0..r0+3 -> m[j] (A2).  FULL: the
-// rows come from the staged tile (128-bit shared loads); otherwise from global memory,
-// rows past the end are false.  R32: every predicate is an int32 range (no kind branches):
-// one unsigned subtract-compare per row, ANDed into a predicate register.
-template <int NP, bool R32, bool FULL>
-__device__ __forceinline__ void eval_preds(const PR (&pr)[NP], const unsigned char *stage, uint64_t row0, int r0,
-                                           int valid, bool (&m)[4]) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) m[j] = FULL || j < valid;
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-        if (R32 || pr[q].kind == PR_R32) {
-            int4 v;
-            if (FULL) v = *reinterpret_cast<const int4 *>(stage + pr[q].soff + r0 * 4);
-            else {
-                const int *g = reinterpret_cast<const int *>(pr[q].p) + row0 + r0;
-                v.x = valid > 0 ? __ldg(g) : 0; v.y = valid > 1 ? __ldg(g + 1) : 0;
-                v.z = valid > 2 ? __ldg(g + 2) : 0; v.w = valid > 3 ? __ldg(g + 3) : 0;
-            }
-            const uint32_t lo = (uint32_t)pr[q].lo, sp = (uint32_t)pr[q].span;
-            m[0] = m[0] & ((uint32_t)v.x - lo <= sp);
-            m[1] = m[1] & ((uint32_t)v.y - lo <= sp);
-            m[2] = m[2] & ((uint32_t)v.z - lo <= sp);
-            m[3] = m[3] & ((uint32_t)v.w - lo <= sp);
-        } else if (pr[q].kind == PR_R64) {
-            int64_t v[4];
-            if (FULL) {
-                const longlong2 a = *reinterpret_cast<const longlong2 *>(stage + pr[q].soff + r0 * 8);
-                const longlong2 b = *reinterpret_cast<const longlong2 *>(stage + pr[q].soff + r0 * 8 + 16);
-                v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-            } else {
-                const long long *g = reinterpret_cast<const long long *>(pr[q].p) + row0 + r0;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) v[j] = j < valid ? __ldg(g + j) : 0;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) m[j] = m[j] & ((uint64_t)v[j] - (uint64_t)pr[q].lo <= pr[q].span);
-        } else if (pr[q].kind == PR_SET) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (!m[j]) continue;
-                int64_t v;
-                if (FULL) v = pr[q].bytes == 8 ? *reinterpret_cast<const int64_t *>(stage + pr[q].soff + (r0 + j) * 8)
-                                               : (int64_t) * reinterpret_cast<const int *>(stage + pr[q].soff + (r0 + j) * 4);
-                else v = pr[q].bytes == 8 ? __ldg(reinterpret_cast<const long long *>(pr[q].p) + row0 + r0 + j)
-                                          : (int64_t)__ldg(reinterpret_cast<const int *>(pr[q].p) + row0 + r0 + j);
-                m[j] = in_set(pr[q].set, pr[q].n, v);
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) m[j] = false;
-        }
-    }
-}
-
-// A3: one sector-granular gather of a survivor's key into the ring; the copy size (4 or 8
-// bytes) is chosen by a predicate so one address computation serves both key widths
-__device__ __forceinline__ void cp_async_key(uint32_t dst, const void *src, uint32_t is8) {
-    asm volatile(
-        "{\n\t.reg .pred p8;\n\tsetp.ne.u32 p8, %2, 0;\n\t"
-        "@p8 cp.async.ca.shared.global.L2::64B [%0], [%1], 8;\n\t"
-        "@!p8 cp.async.ca.shared.global.L2::64B [%0], [%1], 4;\n}" ::"r"(dst), "l"(src), "r"(is8)
-        : "memory");
-}
-template <int W>
-__device__ __forceinline__ void cp_async_fixed_if(bool on, uint32_t dst, const void *src) {
-    if (W == 8)
-        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
-                     "@p cp.async.ca.shared.global.L2::64B [%0], [%1], 8;\n}" ::"r"(dst), "l"(src), "r"((int)on)
-                     : "memory");
-    else
-        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
-                     "@p cp.async.ca.shared.global.L2::64B [%0], [%1], 4;\n}" ::"r"(dst), "l"(src), "r"((int)on)
-                     : "memory");
-}
-__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
-}
-__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
-    unsigned short v;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
-    return v;
-}
-
-template <int NK>
-__device__ __forceinline__ void drain_batch(const SParams &P, unsigned char *smem, const unsigned char *q,
-                                            const uint32_t (&kbytes)[NK], uint32_t head, uint32_t n) {
-#ifdef SCAN_NOHASH   // timing experiments only (tools/build_variant.sh): results are wrong
-    return;
-#endif
-    const int lane = threadIdx.x & 31;
-    const bool valid = (uint32_t)lane < n;
-    uint64_t xk[NK];
-    const unsigned char *e = q + ((head + lane) & (P.cap - 1)) * (NK * 8);
-#pragma unroll
-    for (int k = 0; k < NK; ++k)
-        xk[k] = valid ? canon61(kbytes[k] == 8 ? *reinterpret_cast<const int64_t *>(e + k * 8)
-                                               : (int64_t) * reinterpret_cast<const int32_t *>(e + k * 8))
-                      : 0;
-    process_batch<NK>(P, smem, valid, xk);
-}
-
-// KW = 0: generic (any predicate kinds, key widths read at run time); KW = 4 / 8: every
-// predicate is an int32 range and every key column is KW bytes wide (no kind or width
-// branches; survivors' keys are gathered straight from the ballots)
-template <int NK, int NP, int KW>
-__global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SParams P) {
-    constexpr bool R32 = KW != 0;
-    extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t *full_all = reinterpret_cast<uint64_t *>(smem);   // [kGroups][kMaxStages]
-    uint64_t *empty_all = full_all + kGroups * kMaxStages;     // [kGroups][kMaxStages]
-    const uint32_t kStages = P.stages;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // ring group of this warp (producers are warps kWarps .. kWarps + kGroups - 1)
-    const int grp = warp < kWarps ? warp / kGW : warp - kWarps;
-    uint64_t *full = full_all + grp * kMaxStages, *empty = empty_all + grp * kMaxStages;
-    const uint32_t G = gridDim.x * kGroups, gid = blockIdx.x * kGroups + grp;   // this group's tiles: gid + k*G
-
-    // ---- setup: barriers, smem counters, heavy-hitter tables, seeds
-    if (tid == 0) {
-        for (uint32_t s = 0; s < kGroups * kMaxStages; ++s) { mbar_init(&full_all[s], 1); mbar_init(&empty_all[s], kGW); }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    {
-        int32_t *sc = reinterpret_cast<int32_t *>(smem + P.off_sc);
-        for (uint32_t i = tid; i < P.smem_counters; i += kThreads) sc[i] = 0;
-        for (uint32_t k = 0; k < P.n_keys; ++k) {
-            if (P.key[k].hh_off < 0) continue;
-            uint64_t *keys = reinterpret_cast<uint64_t *>(smem + P.key[k].hh_off);
-            int *cnts = reinterpret_cast<int *>(smem + P.key[k].hh_off + (8u << P.hh_log2));
-            for (uint32_t i = tid; i < (1u << P.hh_log2); i += kThreads) { keys[i] = kEmpty; cnts[i] = 0; }
-        }
-        uint64_t *sseed = reinterpret_cast<uint64_t *>(smem + P.off_seed);
-        for (uint32_t t = 0; t < P.n_targets; ++t) {
-            const uint32_t words = P.tgt[t].ndim * P.tgt[t].d * 6;
-            for (uint32_t i = tid; i < words; i += kThreads) sseed[P.tgt[t].seed_off + i] = P.seeds[t][i];
-        }
-        uint32_t *nm = reinterpret_cast<uint32_t *>(smem + P.off_missn);
-        for (uint32_t i = tid; i < kWarps * P.n_keys; i += kThreads) nm[i] = 0;
-        uint32_t *hs = reinterpret_cast<uint32_t *>(smem + P.off_hstat);
-        for (uint32_t i = tid; i < kMaxKeys * 4; i += kThreads) hs[i] = 0;
-    }
-    __syncthreads();
-
-    if (warp >= kWarps) {
-        // ================= producer warp of ring group grp: TMA bulk copies of staged columns
-        if (lane == 0) {
-            uint32_t s = 0, ph = 0;
-            bool wrapped = false;
-            for (uint64_t t = gid; t < P.n_tiles; t += G) {
-                if (wrapped) mbar_wait(&empty[s], ph ^ 1);
-                const uint64_t row0 = t * P.tile_rows;
-                const bool fulltile = row0 + P.tile_rows <= P.n_rows;
-                if (fulltile && P.stage_bytes) {
-                    mbar_arrive_tx(&full[s], P.stage_bytes);
-                    unsigned char *stage = smem + P.off_ring + (grp * kStages + s) * P.stage_bytes;
-                    for (uint32_t c = 0; c < P.n_cols; ++c) {
-                        if (P.col[c].soff < 0) continue;
-                        const uint32_t b = P.col[c].bytes;
-                        bulk_g2s(stage + P.col[c].soff, reinterpret_cast<const unsigned char *>(P.col[c].p) + row0 * b,
-                                 P.tile_rows * b, &full[s]);
-                    }
-                } else {
-                    mbar_arrive(&full[s]);
-                }
-                if (++s == kStages) { s = 0; ph ^= 1; wrapped = true; }
-            }
-        }
-        return;
-    }
-
-    // ================= consumer warps: independent pipelines, no CTA-wide barrier in the loop
-    PR pr[(NP > 0) ? NP : 1];
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-        const SPred &sp = P.pred[q];
-        const SCol &c = P.col[sp.col];
-        pr[q] = PR{sp.kind, c.bytes, sp.n, c.soff, sp.lo, sp.span, c.p, sp.set};
-    }
-    const void *kptr[NK];
-    uint32_t kbytes[NK];
-    int32_t ksoff[NK];
-#pragma unroll
-    for (int k = 0; k < NK; ++k) {
-        const SCol &c = P.col[P.key[k].col];
-        kptr[k] = c.p;
-        kbytes[k] = c.bytes;
-        ksoff[k] = c.soff;
-    }
-    const uint32_t cap = P.cap;
-    uint32_t surv = 0;                       // warp-uniform exact survivor count
-    const int r0 = (warp % kGW) * 128 + lane * 4;   // this lane's 4 rows inside its group's tile
-    unsigned char *q = smem + P.off_kbuf + warp * P.kb_bytes;   // this warp's survivor-key ring
-    const uint32_t q_a = smem_u32(q);
-    const uint32_t rl_a = smem_u32(smem + P.off_rows) + warp * 256;   // this warp's survivor row list
-    uint32_t head = 0, tail = 0;             // ring positions (monotone)
-    uint32_t tl[kLag];                       // ring tail after each of the previous kLag tiles
-#pragma unroll
-    for (int i = 0; i < kLag; ++i) tl[i] = 0;
-    const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
-    const uint32_t lt = (1u << lane) - 1u;
-    const uint32_t n_tiles = (uint32_t)P.n_tiles;
-    constexpr int NPX = (NP > 0) ? NP : 1;
-    uint32_t s = 0, ph = 0;
-    for (uint32_t t = gid; t < n_tiles; t += G) {
-        const uint64_t row0 = uint64_t(t) * kTile;
-        mbar_wait_a(full_a + s * 8, ph);
-        const unsigned char *stage = smem + P.off_ring + (grp * kStages + s) * P.stage_bytes;
-        const bool full_tile = t < P.n_full_tiles;   // staged by the producer
-        if (NP > 0) {
-            bool m[4];
-            if (full_tile) eval_preds<NPX, R32, true>(pr, stage, row0, r0, 4, m);
-            else {
-                const int64_t rem = (int64_t)P.n_rows - (int64_t)(row0 + r0);
-                eval_preds<NPX, R32, false>(pr, stage, row0, r0, rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem), m);
-            }
-            // one ballot per row slot; the ballots also order every lane's shared reads of
-            // stage s before lane 0 releases it
-            const uint32_t B0 = __ballot_sync(0xffffffffu, m[0]), B1 = __ballot_sync(0xffffffffu, m[1]);
-            const uint32_t B2 = __ballot_sync(0xffffffffu, m[2]), B3 = __ballot_sync(0xffffffffu, m[3]);
-            if (lane == 0) mbar_arrive_a(empty_a + s * 8);
-            const uint32_t c0 = __popc(B0), c1 = __popc(B1), c2 = __popc(B2), c3 = __popc(B3);
-            const uint32_t wtot = c0 + c1 + c2 + c3;
-            surv += wtot;
-            if (wtot) {
-                if (KW != 0 && tail - head + wtot <= cap) {
-                    // survivors in slot-major order (slot j of every lane, then slot j+1): ring
-                    // position = popc of one ballot, gathered straight from the owning lane
-                    const uint32_t pb[4] = {tail, tail + c0, tail + c0 + c1, tail + c0 + c1 + c2};
-                    const uint32_t bj[4] = {B0, B1, B2, B3};
-                    const unsigned char *kb[NK];
-#pragma unroll
-                    for (int k = 0; k < NK; ++k)
-                        kb[k] = reinterpret_cast<const unsigned char *>(kptr[k]) + (row0 + r0) * (uint64_t)(KW ? KW : 8);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {   // predicated copies: no branches
-                        const uint32_t dst = q_a + ((pb[j] + __popc(bj[j] & lt)) & (cap - 1)) * (NK * 8);
-#pragma unroll
-                        for (int k = 0; k < NK; ++k)
-                            cp_async_fixed_if<KW ? KW : 8>(m[j], dst + k * 8, kb[k] + j * (KW ? KW : 8));
-                    }
-                    tail += wtot;
-                } else {
-                    // generic / ring-full path: each survivor's tile offset goes to the warp's
-                    // row list (same slot-major order), then the gathers run converged over the
-                    // list, in rounds that fit the ring (a tile may hold more survivors than it)
-                    if (m[0]) sts_u16(rl_a + 2 * __popc(B0 & lt), r0);
-                    if (m[1]) sts_u16(rl_a + 2 * (c0 + __popc(B1 & lt)), r0 + 1);
-                    if (m[2]) sts_u16(rl_a + 2 * (c0 + c1 + __popc(B2 & lt)), r0 + 2);
-                    if (m[3]) sts_u16(rl_a + 2 * (c0 + c1 + c2 + __popc(B3 & lt)), r0 + 3);
-                    __syncwarp();
-                    for (uint32_t e0 = 0; e0 < wtot;) {
-                        if (tail - head == cap || (e0 == 0 && tail - head + wtot > cap)) {
-                            // ring would overflow: finish outstanding gathers and drain it completely
-                            // (mid-tile, the gathers just issued are not committed yet)
-                            if (e0 == 0) cp_wait_all();
-                            else cp_commit_wait_all();
-                            __syncwarp();
-                            while (tail != head) {
-                                const uint32_t n = min(32u, tail - head);
-                                drain_batch<NK>(P, smem, q, kbytes, head, n);
-                                head += n;
-                            }
-#pragma unroll
-                            for (int i = 0; i < kLag; ++i) tl[i] = tail;
-                        }
-                        const uint32_t n = min(wtot - e0, cap - (tail - head));   // a tile may exceed cap
-                        for (uint32_t e = lane; e < n; e += 32) {
-                            const uint64_t row = row0 + lds_u16(rl_a + 2 * (e0 + e));
-                            const uint32_t dst = q_a + ((tail + e) & (cap - 1)) * (NK * 8);
-#ifndef SCAN_NOGATHER   // timing experiments only (tools/build_variant.sh): results are wrong
-#pragma unroll
-                            for (int k = 0; k < NK; ++k)
-                                cp_async_key(dst + k * 8, reinterpret_cast<const unsigned char *>(kptr[k]) + row * kbytes[k],
-                                             kbytes[k] == 8);
-#endif
-                        }
-                        tail += n;
-                        e0 += n;
-                    }
-                    __syncwarp();
-                }
-            }
-            // one cp.async group per tile (possibly empty): wait_group kLag then guarantees the
-            // entries appended kLag tiles ago (t3) have landed; the latency hides behind 3 tiles
-            cp_commit();
-            const uint32_t ready_end = tl[kLag - 1];
-#pragma unroll
-            for (int i = kLag - 1; i > 0; --i) tl[i] = tl[i - 1];
-            tl[0] = tail;
-            if (ready_end - head >= 32) {
-                cp_wait_lag();
-                __syncwarp();
-                while (ready_end - head >= 32) { drain_batch<NK>(P, smem, q, kbytes, head, 32); head += 32; }
-            }
-        } else {
-            // keys are staged (no predicate): aggregate and update straight from the stage
-            const int64_t rem = (int64_t)P.n_rows - (int64_t)(row0 + r0);
-            const int valid = rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem);
-            const uint32_t bits = (1u << valid) - 1u;
-            surv += __reduce_add_sync(0xffffffffu, (uint32_t)valid);
-            uint64_t xs[4][NK];
-#pragma unroll
-            for (int k = 0; k < NK; ++k) {
-                if (kbytes[k] == 4) {
-                    int4 v;
-                    if (full_tile) v = *reinterpret_cast<const int4 *>(stage + ksoff[k] + r0 * 4);
-                    else {
-                        const int *g = reinterpret_cast<const int *>(kptr[k]) + row0 + r0;
-                        v.x = valid > 0 ? __ldg(g) : 0; v.y = valid > 1 ? __ldg(g + 1) : 0;
-                        v.z = valid > 2 ? __ldg(g + 2) : 0; v.w = valid > 3 ? __ldg(g + 3) : 0;
-                    }
-                    xs[0][k] = canon61(v.x); xs[1][k] = canon61(v.y); xs[2][k] = canon61(v.z); xs[3][k] = canon61(v.w);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        int64_t v = 0;
-                        if (full_tile) v = *reinterpret_cast<const int64_t *>(stage + ksoff[k] + (r0 + j) * 8);
-                        else if (j < valid) v = __ldg(reinterpret_cast<const long long *>(kptr[k]) + row0 + r0 + j);
-                        xs[j][k] = canon61(v);
-                    }
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) process_batch<NK>(P, smem, (bits >> j) & 1u, xs[j]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive_a(empty_a + s * 8);
-        }
-        if (++s == kStages) { s = 0; ph ^= 1; }
-    }
-    if (NP > 0) {
-        cp_wait_all();
-        __syncwarp();
-        while (tail - head > 0) {
-            const uint32_t n = min(32u, tail - head);
-            drain_batch<NK>(P, smem, q, kbytes, head, n);
-            head += n;
-        }
-    }
-
-    // ---- this warp's buffered heavy-hitter misses
-    {
-        const uint64_t *seeds = reinterpret_cast<const uint64_t *>(smem + P.off_seed);
-        __syncwarp();
-        for (uint32_t k = 0; k < P.n_keys; ++k) {
-            if (!P.key[k].hasglob) continue;
-            const uint32_t mi = warp * P.n_keys + k;
-            const uint32_t n = reinterpret_cast<volatile uint32_t *>(smem + P.off_missn)[mi];
-            if (n) flush_misses(P, seeds, reinterpret_cast<const uint64_t *>(smem + P.off_miss) + mi * 32,
-                                reinterpret_cast<const int *>(smem + P.off_miss + kWarps * P.n_keys * 32 * 8) + mi * 32, n, k);
-        }
-    }
-    // ---- exact survivor count
-    if (lane == 0 && surv && P.survivors) atomicAdd(P.survivors, (unsigned long long)surv);
-    consumer_sync();
-    // ---- flush heavy-hitter tables (one hash evaluation per distinct key per CTA)
-    int32_t *sc = reinterpret_cast<int32_t *>(smem + P.off_sc);
-    const uint64_t *seeds = reinterpret_cast<const uint64_t *>(smem + P.off_seed);
-    for (uint32_t k = 0; k < P.n_keys; ++k) {
-        if (P.key[k].hh_off < 0) continue;
-        const uint64_t *keys = reinterpret_cast<const uint64_t *>(smem + P.key[k].hh_off);
-        const int *cnts = reinterpret_cast<const int *>(smem + P.key[k].hh_off + (8u << P.hh_log2));
-        for (uint32_t s = tid; s < (1u << P.hh_log2); s += kConsumers) {
-            const uint64_t x = keys[s];
-            const int c = cnts[s];
-            if (x == kEmpty || c == 0) continue;
-            if (P.key[k].hist) {
-                if (x < P.key[k].domain) { red_add_u32(P.key[k].hist + x, (uint32_t)c); continue; }
-                for (uint32_t tt = 0; tt < P.n_targets; ++tt) {   // outside the domain: all targets directly
-                    const STarget &tg = P.tgt[tt];
-                    if (tg.ndim != 1 || tg.k0 != k) continue;
-                    update_1d(tg, seeds + tg.seed_off, sc, x, c);
-                }
-                continue;
-            }
-            for (uint32_t tt = 0; tt < P.n_targets; ++tt) {
-                const STarget &tg = P.tgt[tt];
-                if (tg.ndim != 1 || tg.k0 != k || tg.smem_off >= 0) continue;
-                update_1d(tg, seeds + tg.seed_off, sc, x, c);
-            }
-        }
-    }
-    consumer_sync();
-    // ---- flush privatised int32 counters into the int64 sketches
-    for (uint32_t tt = 0; tt < P.n_targets; ++tt) {
-        const STarget &tg = P.tgt[tt];
-        if (tg.smem_off < 0) continue;
-        const uint32_t n = tg.d * tg.cells;
-        for (uint32_t qq = tid; qq < n; qq += kConsumers) {
-            const int32_t v = sc[tg.smem_off + qq];
-            if (v) red_add_s64(tg.counters + qq, (int64_t)v);
-        }
-    }
-}
 
 // Histogram-then-sketch epilogue (SURVEY.md §8(d) lever f): every key x with count c in
 // [0, domain) adds c * xi_r(x) at bucket h_r(x) of each 1-D sketch on that key column.
@@ -928,31 +102,27 @@ __global__ void k_lut_build(const uint64_t *seeds, uint32_t d, uint32_t wmask, u
     }
 }
 
-typedef void (*ScanKernel)(const SParams);
-
-template <int NK, int NP>
-static ScanKernel pick_kw(int kw) {
-    if (NP == 0) return k_scan<NK, NP, 0>;
-    return kw == 4 ? k_scan<NK, NP, 4> : kw == 8 ? k_scan<NK, NP, 8> : k_scan<NK, NP, 0>;
-}
-
-template <int NK>
-static ScanKernel pick_np(uint32_t np, int kw) {
-    switch (np) {
-        case 0: return pick_kw<NK, 0>(kw);
-        case 1: return pick_kw<NK, 1>(kw);
-        case 2: return pick_kw<NK, 2>(kw);
-        case 3: return pick_kw<NK, 3>(kw);
-        default: return pick_kw<NK, 4>(kw);
+// packed 64-bit lookup table of one hash family over keys [0, dom) (see Pend / process_fast):
+// lut[x] = sum_r ((h_r(x) & wmask) << 1 | (xi_r(x) < 0)) << (r * B)   (H3/H4, narrow path)
+__global__ void k_lut64_build(const uint64_t *seeds, uint32_t d, uint32_t B, uint32_t wmask, uint64_t dom, uint64_t *lut) {
+    for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < dom; x += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t e = 0;
+        for (uint32_t r = 0; r < d; ++r) {
+            const uint64_t *a = seeds + r * 6;
+            const uint64_t b = hash_g61_t<true>(__ldg(a + 4), __ldg(a + 5), x) & wmask;
+            uint64_t sa[4] = {__ldg(a), __ldg(a + 1), __ldg(a + 2), __ldg(a + 3)};
+            e |= ((b << 1) | (xi_sign61_t<true>(sa, x) < 0 ? 1ull : 0ull)) << (r * B);
+        }
+        lut[x] = e;
     }
 }
 
-static ScanKernel pick_kernel(uint32_t nk, uint32_t np, int kw) {
+static const void *pick_kernel(uint32_t nk, uint32_t np, int kw, bool fast) {
     switch (nk) {
-        case 1: return pick_np<1>(np, kw);
-        case 2: return pick_np<2>(np, kw);
-        case 3: return pick_np<3>(np, kw);
-        default: return pick_np<4>(np, kw);
+        case 1: return skb::scan_pick_nk1(np, kw, fast);
+        case 2: return skb::scan_pick_nk2(np, kw, fast);
+        case 3: return skb::scan_pick_nk3(np, kw, fast);
+        default: return skb::scan_pick_nk4(np, kw, fast);
     }
 }
 
@@ -1012,6 +182,70 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
             pr.kind = PR_R64;
             pr.lo = lo;
             pr.span = (uint64_t)hi - (uint64_t)lo;
+        }
+    }
+    // ---- lookup-table path (FAST, see process_fast): every key column int32 with a hinted
+    //      domain <= 2^22; on each key column one hash family (all its 1-D sketches and matrix
+    //      dimensions share d and the seed rows, i.e. the same edge), with d * (log2 w + 1) <= 64
+    //      for the widest 1-D sketch on it, whose handle caches the packed table
+    bool fast = !(getenv("COMPASS_FAST") && strcmp(getenv("COMPASS_FAST"), "0") == 0) && P.n_keys <= 2 &&
+                c.n_preds <= 2 && c.n_rows < (1ULL << 31);
+    for (uint32_t q = 0; fast && q < c.n_preds; ++q) fast = P.pred[q].kind == PR_R32;
+    int fam_t[kMaxKeys] = {-1, -1, -1, -1};
+    uint32_t fam_bits[kMaxKeys] = {0, 0, 0, 0};
+    for (uint32_t k = 0; fast && k < P.n_keys; ++k) {
+        const uint32_t col = keys[k];
+        const uint64_t dom = c.col_domain[col];
+        fast = c.col_bytes[col] == 4 && dom > 0 && dom <= (1ULL << 22);
+        int best = -1;
+        for (uint32_t t = 0; fast && t < c.n_targets; ++t)
+            if (c.tgt_ndim[t] == 1 && c.tgt_key[t][0] == col && c.tgt_sketch[t] &&
+                (best < 0 || c.tgt_w[t][0] > c.tgt_w[best][0]))
+                best = (int)t;
+        if (!fast || best < 0) { fast = false; break; }
+        const uint32_t d = c.tgt_d[best], wmax = c.tgt_w[best][0];
+        const uint32_t B = (uint32_t)__builtin_ctz(wmax) + 1;
+        fast = d * B <= 64;
+        for (uint32_t t = 0; fast && t < c.n_targets; ++t)
+            for (uint32_t q = 0; q < c.tgt_ndim[t]; ++q) {
+                if (c.tgt_key[t][q] != col) continue;
+                if (c.tgt_d[t] != d || c.tgt_w[t][q] > wmax ||
+                    memcmp(c.tgt_seeds_host[t] + size_t(q) * d * 6, c.tgt_seeds_host[best], size_t(d) * 6 * 8) != 0)
+                    fast = false;
+            }
+        fam_t[k] = best;
+        fam_bits[k] = B;
+    }
+    if (fast) {
+        int dev_f = 0, sms_f = 148;
+        cudaGetDevice(&dev_f);
+        cudaDeviceGetAttribute(&sms_f, cudaDevAttrMultiProcessorCount, dev_f);
+        for (uint32_t k = 0; k < P.n_keys; ++k) {
+            hist_key[k] = false;
+            sk_sketch *sk = c.tgt_sketch[fam_t[k]];
+            const uint64_t dom = c.col_domain[keys[k]];
+            std::lock_guard<std::mutex> lk(sk->lut_mu);
+            if (!sk->lut64 || sk->lut64_dom < dom || sk->lut64_bits != fam_bits[k]) {
+                if (sk->lut64) {   // replaced: no reader of the old table may be in flight
+                    SKB_CUDA(cudaDeviceSynchronize());
+                    cudaFree(sk->lut64);
+                    sk->lut64 = nullptr;
+                }
+                SKB_CUDA(cudaMalloc(&sk->lut64, dom * 8));
+                k_lut64_build<<<(unsigned)std::min<uint64_t>(uint64_t(sms_f) * 8, (dom + 255) / 256), 256, 0, stream>>>(
+                    sk->seeds_dev, sk->d, fam_bits[k], sk->w[0] - 1, dom, sk->lut64);
+                SKB_CUDA(cudaGetLastError());
+                count_launch();
+                sk->lut64_dom = dom;
+                sk->lut64_bits = fam_bits[k];
+                if (!sk->lut_ready) SKB_CUDA(cudaEventCreateWithFlags(&sk->lut_ready, cudaEventDisableTiming));
+                SKB_CUDA(cudaEventRecord(sk->lut_ready, stream));
+            } else if (sk->lut_ready) {
+                SKB_CUDA(cudaStreamWaitEvent(stream, sk->lut_ready, 0));   // built on another stream
+            }
+            P.klut[k] = sk->lut64;
+            P.klut_dom[k] = sk->lut64_dom;
+            P.klut_bits[k] = fam_bits[k];
         }
     }
     P.gather = c.n_preds > 0 ? 1u : 0u;
@@ -1103,9 +337,11 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     }
     P.smem_counters = sc_count;
     avail -= (sc_count * 4 + 15) & ~15u;
+    if (fast)   // the lookup-table path updates non-privatised sketches directly (no heavy hitters)
+        for (uint32_t k = 0; k < P.n_keys; ++k) { key_needs_hh[k] = false; P.key[k].hasglob = 0; }
     // hash lookup tables for matrix dimensions whose key column has a domain hint (the table
     // stays L2-resident: dom * d * 4 bytes <= 64 MB per dimension); built once per sketch
-    if (!(getenv("COMPASS_LUT") && strcmp(getenv("COMPASS_LUT"), "0") == 0)) {
+    if (!fast && !(getenv("COMPASS_LUT") && strcmp(getenv("COMPASS_LUT"), "0") == 0)) {
         int dev_l = 0, sms_l = 148;
         cudaGetDevice(&dev_l);
         cudaDeviceGetAttribute(&sms_l, cudaDevAttrMultiProcessorCount, dev_l);
@@ -1151,7 +387,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     // trio detection: matrix M whose dimension-q hash rows equal those of a privatised 1-D
     // sketch on the same key (exact comparison of the coefficient rows; same d)
     P.trio_on = 0;
-    for (uint32_t m = 0; m < c.n_targets && !P.trio_on; ++m) {
+    for (uint32_t m = 0; !fast && m < c.n_targets && !P.trio_on; ++m) {
         const STarget &M = P.tgt[m];
         if (M.ndim != 2 || M.k0 == M.k1) continue;
         int ab[2] = {-1, -1};
@@ -1243,15 +479,15 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     for (uint32_t q = 0; q < P.n_preds; ++q)
         if (P.pred[q].kind != PR_R32) kw = 0;
     if (getenv("COMPASS_SCAN_KW0")) kw = 0;   // experiments / parity of the generic variant
-    ScanKernel kern = pick_kernel(P.n_keys, P.n_preds, kw);
+    const void *kern = pick_kernel(P.n_keys, P.n_preds, kw, fast);
     const int threads = kThreads;
     if (getenv("COMPASS_SCAN_DEBUG"))
-        fprintf(stderr, "k_scan plan: keys %u preds %u kw %d stages %u hh_log2 %u cap %u smem %u (ring %u, counters %u)\n",
-                P.n_keys, P.n_preds, kw, P.stages, P.hh_log2, P.cap, off, P.stages * kGroups * P.stage_bytes,
+        fprintf(stderr, "k_scan plan: keys %u preds %u kw %d fast %d stages %u hh_log2 %u cap %u smem %u (ring %u, counters %u)\n",
+                P.n_keys, P.n_preds, kw, (int)fast, P.stages, P.hh_log2, P.cap, off, P.stages * kGroups * P.stage_bytes,
                 P.smem_counters * 4);
     SKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)off));
-    kern<<<(unsigned)grid, threads, off, stream>>>(P);
-    SKB_CUDA(cudaGetLastError());
+    void *kargs[] = {&P};
+    SKB_CUDA(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(threads), kargs, off, stream));
     count_launch();
     // histogram -> sketches, then release the histograms (stream-ordered).  Every 1-D target
     // on a histogram key gets its in-domain counts only here, so all of them must be served:

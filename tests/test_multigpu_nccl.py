@@ -1,0 +1,79 @@
+"""Multi-GPU path on real devices: N ranks, one GPU each, NCCL
+process group; every rank builds its contiguous row shard of every table with the CUDA scan
+into the query's packed int64 buffer, then QueryRun.allreduce() merges them (one NCCL SUM).
+The merged buffer must equal the oracle's single-process build bit for bit, and every rank
+must produce the same greedy plan.  Skipped when fewer than 2 GPUs are visible (the gpurun
+pool has one); the same host logic runs on CPU under gloo in tests/test_multirank_gloo.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cfg, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    import datagen
+    from paper_2102_02440_b200.query import QueryRun
+    ws = getattr(datagen, cfg[0])(**cfg[1])
+    run = QueryRun(ws, dev)
+    for t in ws.tables:
+        data = datagen.generate_table(ws, t.name, dev, rank=rank, world=world)
+        run.build_table(t.name, data, datagen.resolve_preds(ws, t.name))
+    run.allreduce()
+    plan = run.graph().plan_greedy() if ws.kind == "graph" else None
+    plans = [None] * world
+    dist.all_gather_object(plans, plan)
+    if rank == 0:
+        torch.save({"buf": run.buffer.cpu(), "plans": plans}, out_path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _oracle_packed(ws):
+    import datagen
+    import oracle
+    from paper_2102_02440_b200.query import packed_layout
+    total, lay = packed_layout(ws)
+    buf = np.zeros(total, dtype=np.int64)
+    for ti, t in enumerate(ws.tables):
+        cols = {k: v.numpy() for k, v in datagen.generate_table(ws, t.name, "cpu").items()}
+        mask, cnt = oracle.filter_mask(cols, datagen.resolve_preds(ws, t.name))
+        buf[ti] = cnt
+        for (off, n), s in zip(lay, ws.sketches):
+            if s.table == t.name:
+                buf[off:off + n] = oracle.build([cols[k] for k in s.key_cols], mask, s.d, s.w, s.edge_ids,
+                                                master=ws.master_seed).reshape(-1)
+    return buf
+
+
+@pytest.mark.parametrize("cfg", [("c1", {}), ("c5", {"scale": 2e-4, "w": 128, "wm": 64}),
+                                 ("c4", {"scale": 0.002})])
+def test_nccl_ranks_merge_equals_oracle_build(cfg, tmp_path):
+    world = torch.cuda.device_count()
+    if world < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(world, 8)
+    import datagen
+    out = str(tmp_path / "merged.pt")
+    mp.start_processes(_worker, args=(world, _free_port(), cfg, out), nprocs=world, join=True, start_method="spawn")
+    res = torch.load(out)
+    ws = getattr(datagen, cfg[0])(**cfg[1])
+    assert np.array_equal(res["buf"].numpy(), _oracle_packed(ws))
+    assert all(p == res["plans"][0] for p in res["plans"])

@@ -161,3 +161,49 @@ def test_c3_full_size_all_14_subplans_row0():
     assert len(subs) == 14
     for s in subs:
         assert jg.estimate_join_exact(s)[0] == oracle.estimate_rows(og, s, rows=[0])[0], s
+
+
+# ------------------------------------------------------------------ lookup-table scan (FAST)
+def _fast_cols(n, seed, skew):
+    rng = np.random.default_rng(seed)
+    if skew == "flat":
+        a = rng.integers(0, 1 << 20, n)
+        b = rng.integers(0, 1 << 20, n)
+    else:                                   # Zipf 2.0-like: most lanes of a warp share a key
+        a = rng.zipf(2.0, n) % (1 << 20)
+        b = rng.zipf(1.3, n) % (1 << 20)
+    a = a.astype(np.int32)
+    b = b.astype(np.int32)
+    if n > 64:                              # keys outside the hinted domain: fallback hashing
+        a[::53] = -rng.integers(1, 1 << 30, a[::53].shape[0])
+        b[::59] = (1 << 20) + rng.integers(0, 1 << 30, b[::59].shape[0])
+        a[:4] = [-1, 7, -(1 << 31), (1 << 31) - 1]   # -1 and 7 share a canonical key (H1)
+    return {"a": a, "b": b, "p": rng.integers(0, 1000, n).astype(np.int32)}
+
+
+FAST_TARGETS = [  # one hash family per key column (edge), matrices on the same families
+    (["a"], 5, [1024], ["T1.b|T2.a"]),
+    (["b"], 5, [1024], ["T2.b|T3.a"]),
+    (["a", "b"], 5, [512, 512], ["T1.b|T2.a", "T2.b|T3.a"]),
+    (["a"], 5, [256], ["T1.b|T2.a"]),        # narrower sketch of the same family
+]
+
+
+@pytest.mark.parametrize("n", [1, 4097, 1_000_003])
+@pytest.mark.parametrize("skew", ["flat", "zipf"])
+@pytest.mark.parametrize("preds", [[], [("p", pb.RANGE, 0, 499)], [("p", pb.RANGE, 0, 9), ("a", pb.RANGE, -(1 << 31), 1 << 19)]])
+@pytest.mark.parametrize("fast", ["1", "0"])
+def test_lookup_table_scan_equals_oracle(n, skew, preds, fast, capfd, monkeypatch):
+    """int32 keys with domain hints (C5 / C2 shape): the lookup-table scan (and, as a second
+    witness, the hashing scan with COMPASS_FAST=0) against the oracle, bit for bit."""
+    monkeypatch.setenv("COMPASS_FAST", fast)
+    monkeypatch.setenv("COMPASS_SCAN_DEBUG", "1")
+    cols = _fast_cols(n, 9000 + n, skew)
+    g, gs = _build(cols, preds, FAST_TARGETS, domains={"a": 1 << 20, "b": 1 << 20})
+    err = capfd.readouterr().err
+    if fast == "1":
+        assert "fast 1" in err, err
+    o, os_ = _oracle(cols, preds, FAST_TARGETS)
+    assert gs == os_
+    for t, (x, y) in enumerate(zip(g, o)):
+        assert np.array_equal(x, y), f"target {t} differs"
