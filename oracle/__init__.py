@@ -499,6 +499,73 @@ def exact_join_size(tables, edges, subset):
     return send(root, None)
 
 
+def exact_join_size_any(tables, edges, subset) -> int:
+    """Exact |join| of any connected sub-plan, cycles and parallel edges included (SURVEY.md
+    §8(f) 2; PAPER.md:261 needs the truth of "all the enumerated sub-plans", and the paper's
+    running example has a triangle).  A hash join with multiplicities: tables
+    are joined one at a time (each new table adjacent to the joined set); the partial result
+    is a map from the values of the joined tables' columns that still have edges to unjoined
+    tables to the number of partial tuple combinations carrying them; a new table's surviving
+    row extends exactly the entries whose values agree with it on EVERY edge between the new
+    table and the joined set (an edge closing a cycle is one more equality checked).  Plain
+    Python integers.  Pinned by exact_join_size_bruteforce on tiny cyclic graphs."""
+    S = sorted(set(subset))
+    E = [e for e in edges if e[0] in S and e[1] in S]
+    masks = {t: filter_mask(tables[t][0], tables[t][1])[0] for t in S}
+    order = [S[0]]
+    while len(order) < len(S):
+        nxt = [t for t in S if t not in order and any((u in order and v == t) or (v in order and u == t)
+                                                     for u, v, _, _ in E)]
+        if not nxt:
+            raise ValueError("disconnected sub-plan")
+        order.append(nxt[0])
+
+    def open_cols(joined):
+        """(table, col) of joined tables with an edge to a table not joined yet (sorted)."""
+        out = set()
+        for u, v, cu, cv in E:
+            if u in joined and v not in joined:
+                out.add((u, cu))
+            if v in joined and u not in joined:
+                out.add((v, cv))
+        return sorted(out)
+
+    joined = {order[0]}
+    t0 = order[0]
+    cols0 = tables[t0][0]
+    oc = open_cols(joined)
+    state = {}
+    for i in np.nonzero(masks[t0])[0]:
+        key = tuple(int(tables[t][0][c][i]) for t, c in oc)
+        state[key] = state.get(key, 0) + 1
+    for t in order[1:]:
+        cols = tables[t][0]
+        # edges between t and the joined set: (open-column position, column of t)
+        links = []
+        for u, v, cu, cv in E:
+            if u == t and v in joined:
+                links.append((oc.index((v, cv)), cu))
+            elif v == t and u in joined:
+                links.append((oc.index((u, cu)), cv))
+        joined.add(t)
+        oc_new = open_cols(joined)
+        idx = {}   # state entries by the values the new table must match
+        for key, cnt in state.items():
+            idx.setdefault(tuple(key[p] for p, _ in links), []).append((key, cnt))
+        new = {}
+        for i in np.nonzero(masks[t])[0]:
+            want = tuple(int(cols[c][i]) for _, c in links)
+            for key, cnt in idx.get(want, ()):
+                full = {tc: key[j] for j, tc in enumerate(oc)}
+                for tt, c in oc_new:
+                    if tt == t:
+                        full[(t, c)] = int(cols[c][i])
+                nk = tuple(full[tc] for tc in oc_new)
+                new[nk] = new.get(nk, 0) + cnt
+        state, oc = new, oc_new
+    return sum(state.values())
+
+
 def exact_join_size_bruteforce(tables, edges, subset) -> int:
     """The literal definition (tiny inputs only): the number of combinations of one surviving
     tuple per table that agree on every induced join edge."""

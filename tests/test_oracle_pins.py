@@ -582,6 +582,53 @@ def test_exact_join_size_equals_nested_loop_definition():
                 assert oracle.exact_join_size(T, E, sub) == oracle.exact_join_size_bruteforce(T, E, sub), (trial, sub)
 
 
+CYCLIC_SHAPES = [
+    # triangle on one shared key column per table (the C3 shape: T.id, MK.mid, CI.mid)
+    [("A", "B", "k", "k"), ("A", "C", "k", "k"), ("B", "C", "k", "k")],
+    # triangle with a different column per table and edge (a genuine cycle)
+    [("A", "B", "k", "j"), ("B", "C", "k", "j"), ("C", "A", "k", "j")],
+    # 4-cycle (C5-cycle shape: each table joins on 'k' one way and 'j' the other)
+    [("A", "B", "j", "k"), ("B", "C", "j", "k"), ("C", "D", "j", "k"), ("D", "A", "j", "k")],
+    # parallel edges between two tables, plus a pendant
+    [("A", "B", "k", "k"), ("A", "B", "j", "j"), ("B", "C", "k", "j")],
+    # triangle plus two pendants (the C3 graph)
+    [("K", "M", "k", "j"), ("M", "T", "k", "k"), ("C", "T", "k", "k"), ("C", "M", "k", "k"), ("C", "N", "j", "k")],
+    # trees too (the general routine is not restricted to cycles)
+    [("A", "B", "k", "k"), ("B", "C", "j", "j")],
+]
+
+
+def test_exact_join_size_any_equals_nested_loop_definition_with_cycles():
+    """exact_join_size_any (hash join with multiplicities) == the literal definition on tiny
+    graphs with cycles (one-key and genuine triangles, a 4-cycle, parallel edges, the C3
+    graph), every connected sub-plan, random predicates; and == message passing on trees."""
+    import itertools
+    rng = np.random.default_rng(2102)
+    for trial in range(36):
+        E = CYCLIC_SHAPES[trial % len(CYCLIC_SHAPES)]
+        names = sorted({x for e in E for x in e[:2]})
+        T = _tiny_tables(rng, names, int(rng.integers(1, 6)))
+        G = _FakeG({x: 1 for x in names}, [(f"{u}.{cu}|{v}.{cv}#{i}", u, v) for i, (u, v, cu, cv) in enumerate(E)])
+        for k in range(1, len(names) + 1):
+            for sub in itertools.combinations(names, k):
+                if len(sub) > 1 and not oracle.connected(G, sub):
+                    continue
+                want = oracle.exact_join_size_bruteforce(T, E, sub)
+                assert oracle.exact_join_size_any(T, E, sub) == want, (trial, sub)
+                induced = [e for e in E if e[0] in sub and e[1] in sub]
+                if len(induced) == len(sub) - 1:
+                    assert oracle.exact_join_size(T, E, sub) == want
+
+
+def test_exact_join_size_any_hand_triangle():
+    """A hand-counted triangle: A(k) = [1, 1, 2], B(k) = [1, 2, 2], C(k) = [1, 2]; all three
+    equal on k: key 1 -> 2*1*1 = 2, key 2 -> 1*2*1 = 2, total 4."""
+    T = {"A": ({"k": np.array([1, 1, 2])}, []), "B": ({"k": np.array([1, 2, 2])}, []),
+         "C": ({"k": np.array([1, 2])}, [])}
+    E = [("A", "B", "k", "k"), ("A", "C", "k", "k"), ("B", "C", "k", "k")]
+    assert oracle.exact_join_size_any(T, E, ("A", "B", "C")) == 4
+
+
 def test_accuracy_l1_paper_example():
     """PAPER.md:294 / Table 2: the 4-way joins of JOB 6a, true (6, 1194, 1224) vs sketch
     merging (198, 18M, 6.5M): L1 distance 0 + 1 + 1 = 2, normalised by the 3 sub-plans."""
