@@ -1,7 +1,9 @@
-"""Accuracy evaluation of the sketch estimates.
+"""Accuracy evaluation workload of the sketch estimates — evaluation
+tooling beside the hot path, not part of it (it is not in the product package).
 
-The truth of every acyclic connected sub-plan comes from ``exact_join_size`` (frequency-vector
-message passing in the library's CUDA kernels, exact by CRT).  The two measures of the paper:
+The truth of every connected sub-plan (cycles included) comes from ``exact_join_size``
+(frequency-vector message passing in the library's CUDA kernels, exact by CRT; implied cycle
+edges dropped, genuine cycles conditioned on one edge).  The two measures of the paper:
   * accuracy ratio = estimate / true cardinality per sub-plan;
   * normalised L1 distance per sub-plan size: sort the sub-plans of one size by true
     cardinality (order C) and by estimate (order S), sum |S_i - C_i| over the positions and
@@ -12,7 +14,7 @@ from __future__ import annotations
 
 from itertools import combinations
 
-from . import exact_join_size
+from paper_2102_02440_b200 import SK_EOVERFLOW, SkError, exact_join_size
 
 
 def join_data(ws, data: dict, preds: dict):
@@ -63,8 +65,38 @@ def acyclic_connected_subplans(names, edges, min_size=2):
     return out
 
 
+def connected_subplans(names, edges, min_size=2):
+    """Every vertex set whose induced join graph is connected (cycles included)."""
+    out = []
+    for k in range(min_size, len(names) + 1):
+        for sub in combinations(range(len(names)), k):
+            s = set(sub)
+            ind = [(u, v) for u, v, *_ in edges if u in s and v in s]
+            seen, st = {sub[0]}, [sub[0]]
+            while st:
+                x = st.pop()
+                for u, v in ind:
+                    y = v if u == x else (u if v == x else None)
+                    if y is not None and y not in seen:
+                        seen.add(y)
+                        st.append(y)
+            if seen == s:
+                out.append(tuple(names[i] for i in sub))
+    return out
+
+
 def exact_counts(tables, edges, names, subsets, stream=None) -> dict:
-    return {s: exact_join_size(tables, edges, sum(1 << names.index(t) for t in s), stream) for s in subsets}
+    """{sub-plan: exact count}; None where the library declines (a genuine cycle over a key
+    domain too large to condition, SK_EOVERFLOW)."""
+    out = {}
+    for s in subsets:
+        try:
+            out[s] = exact_join_size(tables, edges, sum(1 << names.index(t) for t in s), stream)
+        except SkError as ex:
+            if ex.status != SK_EOVERFLOW:
+                raise
+            out[s] = None
+    return out
 
 
 def l1_distance(estimates, truths) -> int:
@@ -79,6 +111,7 @@ def l1_distance(estimates, truths) -> int:
 def report(estimates: dict, truths: dict) -> dict:
     """{size: (accuracy ratios in sub-plan order, normalised L1 distance)}."""
     out = {}
+    truths = {s: v for s, v in truths.items() if v is not None}
     for size in sorted({len(s) for s in truths}):
         keys = sorted(s for s in truths if len(s) == size)
         ratios = [float(estimates[s]) / float(truths[s]) if truths[s] else float("inf") for s in keys]

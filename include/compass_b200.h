@@ -249,15 +249,20 @@ SK_API sk_status plan_enumerate(const sk_graph *g, const sk_enum_config *cfg, ui
                                 double *cost, sk_enum_stats *stats, void *stream);
 
 /* ---------------------------------------------------------------------------
- * exact_join_size — the exact cardinality |R_1 join ... join R_k| of an acyclic connected
- * sub-plan, for the accuracy evaluation of the estimates (accuracy ratio est/true,
- * PAPER.md:261; normalised L1 distance of orderings).
+ * exact_join_size — the exact cardinality |R_1 join ... join R_k| of a connected sub-plan
+ * (cycles and parallel edges included), for the accuracy evaluation of the estimates
+ * (accuracy ratio est/true over "all the enumerated sub-plans"; normalised L1
+ * distance of orderings).
  * Frequency-vector message passing on the device: a leaf table sends f(k) = number of its
  * surviving tuples with join key k; an inner table sends, for each key of its parent edge,
  * the sum over its surviving tuples of the product of its children's messages at the
  * tuple's keys; the root sums that product over its surviving tuples.  Exact: every pass is
  * modulo K primes < 2^26 (K from the bound prod_t n_rows_t) and the count is reconstructed
- * by CRT on the host.
+ * by CRT on the host.  Cycles: an induced edge whose two columns are already equal through
+ * other edges (transitivity of equality, e.g. a triangle on one key column per table) is
+ * implied and dropped; a remaining cycle is conditioned on one of its edges, summing the
+ * acyclic count with both endpoints' columns fixed to k over every k of that edge's key
+ * domain (at most 65536 conditioned keys per call).
  *   tables[t]: n_rows, device columns, predicates exactly as sketch_update_filtered
  *     (survive(i) = AND of the predicates).
  *   edge e joins table edge_u[e] column col_u[e] with table edge_v[e] column col_v[e];
@@ -266,8 +271,8 @@ SK_API sk_status plan_enumerate(const sk_graph *g, const sk_enum_config *cfg, ui
  *   vertex_mask: the sub-plan (>= 1 table; a single table gives its survivor count).
  * dec: host buffer receiving the count in decimal (NUL-terminated, dec_len >= 2), or NULL;
  * approx: host double (the count rounded to nearest), or NULL.
- * SK_EOVERFLOW for cyclic sub-plans (including parallel edges) and tables with more than
- * 4 sub-plan edges.  Synchronises `stream`.
+ * SK_EOVERFLOW for a cycle whose conditioning exceeds 65536 keys, for tables with more than
+ * 4 tree edges, or more than 8 predicates after conditioning.  Synchronises `stream`.
  * ------------------------------------------------------------------------- */
 typedef struct {
     uint64_t n_rows;

@@ -165,7 +165,7 @@ extern "C" sk_status sketch_destroy(sk_sketch *sk) {
     if (sk->seeds_dev) cudaFree(sk->seeds_dev);
     for (int q = 0; q < 2; ++q)
         if (sk->lut[q]) cudaFree(sk->lut[q]);
-    if (sk->lut64) cudaFree(sk->lut64);
+    if (sk->lutx) cudaFree(sk->lutx);
     if (sk->lut_ready) cudaEventDestroy(sk->lut_ready);
     cudaSetDevice(prev);
     delete sk;

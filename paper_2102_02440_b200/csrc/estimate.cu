@@ -1256,6 +1256,19 @@ struct UBig {
             if (x.l[i] != y.l[i]) return x.l[i] < y.l[i] ? -1 : 1;
         return 0;
     }
+    static UBig add(const UBig &x, const UBig &y) {
+        UBig r;
+        r.l.resize(std::max(x.l.size(), y.l.size()) + 1, 0);
+        unsigned __int128 carry = 0;
+        for (size_t i = 0; i + 1 < r.l.size(); ++i) {
+            const unsigned __int128 t = (unsigned __int128)(i < x.l.size() ? x.l[i] : 0) + (i < y.l.size() ? y.l[i] : 0) + carry;
+            r.l[i] = (uint64_t)t;
+            carry = t >> 64;
+        }
+        r.l.back() = (uint64_t)carry;
+        r.norm();
+        return r;
+    }
     static UBig sub(const UBig &x, const UBig &y) {  // x >= y
         UBig r;
         r.l.resize(x.l.size());
@@ -2556,39 +2569,14 @@ extern "C" sk_status plan_enumerate(const sk_graph *g, const sk_enum_config *cfg
     return cc.err;
 }
 
-extern "C" sk_status exact_join_size(const sk_join_data *jd, uint64_t mask, char *dec, uint32_t dec_len, double *approx,
-                                     void *stream_) {
-    cudaStream_t stream = (cudaStream_t)stream_;
-    if (!jd || !jd->tables) return fail(SK_EINVAL, "exact_join_size: NULL argument");
-    if (dec && dec_len < 2) return fail(SK_EINVAL, "exact_join_size: dec_len must be >= 2");
+// Exact count of a connected sub-plan whose kept edges form a tree (frequency-vector message
+// passing, one prime per blockIdx.y, CRT).  extra[t]: additional point predicates (column,
+// value) on table t (cycle conditioning).
+static sk_status exact_tree(const sk_join_data *jd, uint64_t mask, const std::vector<uint32_t> &ed,
+                            const std::vector<std::vector<std::pair<uint32_t, int64_t>>> &extra, cudaStream_t stream,
+                            SBig *out) {
     const uint32_t T = jd->n_tables;
-    if (T == 0 || T > 64) return fail(SK_EINVAL, "exact_join_size: n_tables must be in [1,64]");
-    if (mask == 0 || (T < 64 && (mask >> T))) return fail(SK_EINVAL, "exact_join_size: bad vertex mask");
-    for (uint32_t t = 0; t < T; ++t) {
-        const sk_table_data &td = jd->tables[t];
-        if (td.n_cols > (uint32_t)kXCols || td.n_preds > (uint32_t)kXPreds)
-            return fail(SK_EINVAL, "exact_join_size: table %u has too many columns/predicates", t);
-        if ((td.n_cols && !td.cols) || (td.n_preds && !td.preds)) return fail(SK_EINVAL, "exact_join_size: NULL array");
-        for (uint32_t q = 0; q < td.n_preds; ++q)
-            if (td.preds[q].col >= td.n_cols || td.preds[q].kind > SK_PRED_SUBSET)
-                return fail(SK_EINVAL, "exact_join_size: table %u predicate %u invalid", t, q);
-    }
-    // induced edges; acyclic and connected (|E_C| = |C| - 1)
-    std::vector<uint32_t> ed;
-    for (uint32_t e = 0; e < jd->n_edges; ++e) {
-        const uint32_t u = jd->edge_u[e], v = jd->edge_v[e];
-        if (u >= T || v >= T || u == v) return fail(SK_EINVAL, "exact_join_size: bad edge %u", e);
-        if (jd->col_u[e] >= jd->tables[u].n_cols || jd->col_v[e] >= jd->tables[v].n_cols)
-            return fail(SK_EINVAL, "exact_join_size: edge %u column out of range", e);
-        if (jd->key_domain[e] == 0 || jd->key_domain[e] > (1ULL << 31))
-            return fail(SK_EINVAL, "exact_join_size: edge %u key domain must be in [1, 2^31]", e);
-        if (((mask >> u) & 1ULL) && ((mask >> v) & 1ULL)) ed.push_back(e);
-    }
     const int nC = __builtin_popcountll(mask);
-    if ((int)ed.size() != nC - 1) {
-        if ((int)ed.size() > nC - 1) return fail(SK_EOVERFLOW, "exact_join_size: cyclic sub-plans are unsupported");
-        return fail(SK_EINVAL, "exact_join_size: sub-plan is not connected");
-    }
     const int root = __builtin_ctzll(mask);
     // DFS from the root: parent edge per table, post-order
     std::vector<int> pe(T, -2), order;
@@ -2629,6 +2617,8 @@ extern "C" sk_status exact_join_size(const sk_join_data *jd, uint64_t mask, char
         const sk_table_data &td = jd->tables[t];
         XNode n;
         memset(&n, 0, sizeof(n));
+        if (td.n_preds + extra[t].size() > (size_t)kXPreds)
+            return fail(SK_EOVERFLOW, "exact_join_size: table %d has too many predicates for cycle conditioning", t);
         n.n_rows = td.n_rows;
         for (uint32_t c = 0; c < td.n_cols; ++c) {
             if (!td.cols[c].data && td.n_rows) return fail(SK_EINVAL, "exact_join_size: table %d column %u is NULL", t, c);
@@ -2654,6 +2644,7 @@ extern "C" sk_status exact_join_size(const sk_join_data *jd, uint64_t mask, char
                 }
             }
         }
+        for (const auto &xp : extra[t]) n.pred[n.n_preds++] = XPred{xp.first, SK_PRED_POINT, xp.second, xp.second, nullptr, 0};
         for (uint32_t e : ed) {
             if ((int)e == pe[t]) continue;
             const bool at_u = (int)jd->edge_u[e] == t, at_v = (int)jd->edge_v[e] == t;
@@ -2692,8 +2683,105 @@ extern "C" sk_status exact_join_size(const sk_join_data *jd, uint64_t mask, char
     SKB_CUDA(cudaStreamSynchronize(stream));
     if (herr[0] & 0xffffffffu) return fail(SK_EINVAL, "exact_join_size: a join key lies outside its edge's key domain");
     for (int k = 0; k < md.K; ++k) hacc[k] %= md.m[k];
-    const SBig v = crt_signed(hacc.data(), md);
-    if (v.neg && !v.mag.zero()) return fail(SK_ECUDA, "exact_join_size: negative count (internal error)");
+    *out = crt_signed(hacc.data(), md);
+    if (out->neg && !out->mag.zero()) return fail(SK_ECUDA, "exact_join_size: negative count (internal error)");
+    return SK_OK;
+}
+
+// union-find over (table, column) nodes: equality of join keys is transitive, so an induced
+// edge whose two columns are already equal through the other kept edges is implied (e.g. the
+// C3 triangle T.id = MK.mid = CI.mid) and dropped without changing the count
+static uint32_t uf_find(std::vector<uint32_t> &p, uint32_t x) {
+    while (p[x] != x) { p[x] = p[p[x]]; x = p[x]; }
+    return x;
+}
+
+// Exact count of any connected sub-plan: implied edges dropped; a remaining cycle is
+// conditioned on one of its edges (u.cu = v.cv = k for every k of the edge's key domain,
+// each an acyclic count with two more point predicates), recursively.
+static sk_status exact_any(const sk_join_data *jd, uint64_t mask, std::vector<uint32_t> ed,
+                           std::vector<std::vector<std::pair<uint32_t, int64_t>>> extra, cudaStream_t stream,
+                           uint64_t &budget, SBig *out) {
+    const uint32_t T = jd->n_tables;
+    const int nC = __builtin_popcountll(mask);
+    std::vector<uint32_t> par(T * (uint32_t)kXCols);
+    for (uint32_t i = 0; i < par.size(); ++i) par[i] = i;
+    std::vector<uint32_t> kept;
+    std::vector<uint32_t> tpar(T);   // table-level union-find: the first edge closing a table cycle
+    for (uint32_t i = 0; i < T; ++i) tpar[i] = i;
+    int cyc = -1;
+    for (uint32_t e : ed) {
+        const uint32_t a = uf_find(par, jd->edge_u[e] * kXCols + jd->col_u[e]);
+        const uint32_t b = uf_find(par, jd->edge_v[e] * kXCols + jd->col_v[e]);
+        if (a == b) continue;   // implied by transitivity
+        par[a] = b;
+        kept.push_back(e);
+        const uint32_t ta = uf_find(tpar, jd->edge_u[e]), tb = uf_find(tpar, jd->edge_v[e]);
+        if (ta == tb) { if (cyc < 0) cyc = (int)e; }
+        else tpar[ta] = tb;
+    }
+    if ((int)kept.size() < nC - 1) return fail(SK_EINVAL, "exact_join_size: sub-plan is not connected");
+    if (cyc < 0) return exact_tree(jd, mask, kept, extra, stream, out);
+    // a genuine cycle: condition the edge that closed it on every key of its domain
+    const uint32_t e = (uint32_t)cyc;
+    const uint64_t dom = jd->key_domain[e];
+    if (dom > budget) return fail(SK_EOVERFLOW, "exact_join_size: cycle conditioning over %llu keys exceeds the limit",
+                                  (unsigned long long)dom);
+    budget -= dom;
+    std::vector<uint32_t> rest;
+    for (uint32_t f : kept) if (f != e) rest.push_back(f);
+    out->neg = false;
+    out->mag = UBig();
+    for (uint64_t i = 0; i < dom; ++i) {
+        const int64_t k = jd->key_lo[e] + (int64_t)i;
+        auto ex = extra;
+        ex[jd->edge_u[e]].push_back({jd->col_u[e], k});
+        ex[jd->edge_v[e]].push_back({jd->col_v[e], k});
+        SBig part;
+        sk_status st = exact_any(jd, mask, rest, ex, stream, budget, &part);
+        if (st) return st;
+        out->mag = UBig::add(out->mag, part.mag);
+    }
+    return SK_OK;
+}
+
+extern "C" sk_status exact_join_size(const sk_join_data *jd, uint64_t mask, char *dec, uint32_t dec_len, double *approx,
+                                     void *stream_) {
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (!jd || !jd->tables) return fail(SK_EINVAL, "exact_join_size: NULL argument");
+    if (dec && dec_len < 2) return fail(SK_EINVAL, "exact_join_size: dec_len must be >= 2");
+    const uint32_t T = jd->n_tables;
+    if (T == 0 || T > 64) return fail(SK_EINVAL, "exact_join_size: n_tables must be in [1,64]");
+    if (mask == 0 || (T < 64 && (mask >> T))) return fail(SK_EINVAL, "exact_join_size: bad vertex mask");
+    for (uint32_t t = 0; t < T; ++t) {
+        const sk_table_data &td = jd->tables[t];
+        if (td.n_cols > (uint32_t)kXCols || td.n_preds > (uint32_t)kXPreds)
+            return fail(SK_EINVAL, "exact_join_size: table %u has too many columns/predicates", t);
+        if ((td.n_cols && !td.cols) || (td.n_preds && !td.preds)) return fail(SK_EINVAL, "exact_join_size: NULL array");
+        for (uint32_t q = 0; q < td.n_preds; ++q)
+            if (td.preds[q].col >= td.n_cols || td.preds[q].kind > SK_PRED_SUBSET)
+                return fail(SK_EINVAL, "exact_join_size: table %u predicate %u invalid", t, q);
+    }
+    // induced edges; acyclic and connected (|E_C| = |C| - 1)
+    std::vector<uint32_t> ed;
+    for (uint32_t e = 0; e < jd->n_edges; ++e) {
+        const uint32_t u = jd->edge_u[e], v = jd->edge_v[e];
+        if (u >= T || v >= T || u == v) return fail(SK_EINVAL, "exact_join_size: bad edge %u", e);
+        if (jd->col_u[e] >= jd->tables[u].n_cols || jd->col_v[e] >= jd->tables[v].n_cols)
+            return fail(SK_EINVAL, "exact_join_size: edge %u column out of range", e);
+        if (jd->key_domain[e] == 0 || jd->key_domain[e] > (1ULL << 31))
+            return fail(SK_EINVAL, "exact_join_size: edge %u key domain must be in [1, 2^31]", e);
+        if (((mask >> u) & 1ULL) && ((mask >> v) & 1ULL)) ed.push_back(e);
+    }
+    const int nC = __builtin_popcountll(mask);
+    if ((int)ed.size() < nC - 1) return fail(SK_EINVAL, "exact_join_size: sub-plan is not connected");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    std::vector<std::vector<std::pair<uint32_t, int64_t>>> extra(T);
+    uint64_t budget = 1ULL << 16;   // total conditioned keys (cycles of small key domains only)
+    SBig v;
+    sk_status st = exact_any(jd, mask, ed, extra, stream, budget, &v);
+    if (st) return st;
     if (dec) {
         const std::string sd = v.to_dec();
         if (sd.size() + 1 > dec_len) return fail(SK_EINVAL, "exact_join_size: dec_len too small");

@@ -30,12 +30,12 @@ struct sk_sketch {
     // (the seeds never change), freed with the sketch
     uint32_t *lut[2] = {nullptr, nullptr};
     uint64_t lut_dom[2] = {0, 0};
-    // 1-D sketches: packed 64-bit lookup table over a hinted key domain [0, lut64_dom) for
-    // the scan's lookup-table path: lut64[x] = sum_r ((h_r(x) & (w - 1)) << 1 | (xi_r(x) < 0))
-    // << (r * lut64_bits), lut64_bits = log2(w) + 1, d * lut64_bits <= 64 (H3/H4)
-    uint64_t *lut64 = nullptr;
-    uint64_t lut64_dom = 0;
-    uint32_t lut64_bits = 0;
+    // 1-D sketches: lookup table over a hinted key domain [0, lutx_dom) for the scan's
+    // lookup-table path (d <= 8, d * w <= 2^15): lutx[x] holds 8 uint16 fields, field r =
+    // ((r * w + (h_r(x) & (w - 1))) << 1) | (xi_r(x) < 0) for r < d (H3/H4), i.e. the
+    // counter index inside the sketch and the sign
+    uint4 *lutx = nullptr;
+    uint64_t lutx_dom = 0;
     // the tables are built on the first caller's stream: later calls on any stream wait on
     // this event (recorded after the build); the mutex guards the cache fields
     cudaEvent_t lut_ready = nullptr;

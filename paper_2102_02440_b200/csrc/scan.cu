@@ -102,18 +102,19 @@ __global__ void k_lut_build(const uint64_t *seeds, uint32_t d, uint32_t wmask, u
     }
 }
 
-// packed 64-bit lookup table of one hash family over keys [0, dom) (see Pend / process_fast):
-// lut[x] = sum_r ((h_r(x) & wmask) << 1 | (xi_r(x) < 0)) << (r * B)   (H3/H4, narrow path)
-__global__ void k_lut64_build(const uint64_t *seeds, uint32_t d, uint32_t B, uint32_t wmask, uint64_t dom, uint64_t *lut) {
+// lookup table of one hash family over keys [0, dom) (see Pend / process_fast): entry x holds
+// 8 uint16 fields, field r = ((r * w + (h_r(x) & (w - 1))) << 1) | (xi_r(x) < 0), r < d
+// (H3/H4, narrow path: x < 2^32)
+__global__ void k_lutx_build(const uint64_t *seeds, uint32_t d, uint32_t w, uint64_t dom, uint4 *lut) {
     for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < dom; x += uint64_t(gridDim.x) * blockDim.x) {
-        uint64_t e = 0;
+        uint32_t f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (uint32_t r = 0; r < d; ++r) {
             const uint64_t *a = seeds + r * 6;
-            const uint64_t b = hash_g61_t<true>(__ldg(a + 4), __ldg(a + 5), x) & wmask;
+            const uint32_t b = (uint32_t)(hash_g61_t<true>(__ldg(a + 4), __ldg(a + 5), x) & (w - 1));
             uint64_t sa[4] = {__ldg(a), __ldg(a + 1), __ldg(a + 2), __ldg(a + 3)};
-            e |= ((b << 1) | (xi_sign61_t<true>(sa, x) < 0 ? 1ull : 0ull)) << (r * B);
+            f[r] = ((r * w + b) << 1) | (xi_sign61_t<true>(sa, x) < 0 ? 1u : 0u);
         }
-        lut[x] = e;
+        lut[x] = make_uint4(f[0] | (f[1] << 16), f[2] | (f[3] << 16), f[4] | (f[5] << 16), f[6] | (f[7] << 16));
     }
 }
 
@@ -186,13 +187,12 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     }
     // ---- lookup-table path (FAST, see process_fast): every key column int32 with a hinted
     //      domain <= 2^22; on each key column one hash family (all its 1-D sketches and matrix
-    //      dimensions share d and the seed rows, i.e. the same edge), with d * (log2 w + 1) <= 64
-    //      for the widest 1-D sketch on it, whose handle caches the packed table
+    //      dimensions share d and the seed rows, i.e. the same edge), d <= 8 and d * w <= 2^15 for
+    //      the widest 1-D sketch on it (the primary), whose handle caches the table
     bool fast = !(getenv("COMPASS_FAST") && strcmp(getenv("COMPASS_FAST"), "0") == 0) && P.n_keys <= 2 &&
                 c.n_preds <= 2 && c.n_rows < (1ULL << 31);
     for (uint32_t q = 0; fast && q < c.n_preds; ++q) fast = P.pred[q].kind == PR_R32;
     int fam_t[kMaxKeys] = {-1, -1, -1, -1};
-    uint32_t fam_bits[kMaxKeys] = {0, 0, 0, 0};
     for (uint32_t k = 0; fast && k < P.n_keys; ++k) {
         const uint32_t col = keys[k];
         const uint64_t dom = c.col_domain[col];
@@ -204,8 +204,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
                 best = (int)t;
         if (!fast || best < 0) { fast = false; break; }
         const uint32_t d = c.tgt_d[best], wmax = c.tgt_w[best][0];
-        const uint32_t B = (uint32_t)__builtin_ctz(wmax) + 1;
-        fast = d * B <= 64;
+        fast = d <= 8 && d * wmax <= (1u << 15);
         for (uint32_t t = 0; fast && t < c.n_targets; ++t)
             for (uint32_t q = 0; q < c.tgt_ndim[t]; ++q) {
                 if (c.tgt_key[t][q] != col) continue;
@@ -214,7 +213,6 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
                     fast = false;
             }
         fam_t[k] = best;
-        fam_bits[k] = B;
     }
     if (fast) {
         int dev_f = 0, sms_f = 148;
@@ -225,27 +223,29 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
             sk_sketch *sk = c.tgt_sketch[fam_t[k]];
             const uint64_t dom = c.col_domain[keys[k]];
             std::lock_guard<std::mutex> lk(sk->lut_mu);
-            if (!sk->lut64 || sk->lut64_dom < dom || sk->lut64_bits != fam_bits[k]) {
-                if (sk->lut64) {   // replaced: no reader of the old table may be in flight
+            if (!sk->lutx || sk->lutx_dom < dom) {
+                if (sk->lutx) {   // replaced: no reader of the old table may be in flight
                     SKB_CUDA(cudaDeviceSynchronize());
-                    cudaFree(sk->lut64);
-                    sk->lut64 = nullptr;
+                    cudaFree(sk->lutx);
+                    sk->lutx = nullptr;
                 }
-                SKB_CUDA(cudaMalloc(&sk->lut64, dom * 8));
-                k_lut64_build<<<(unsigned)std::min<uint64_t>(uint64_t(sms_f) * 8, (dom + 255) / 256), 256, 0, stream>>>(
-                    sk->seeds_dev, sk->d, fam_bits[k], sk->w[0] - 1, dom, sk->lut64);
+                SKB_CUDA(cudaMalloc(&sk->lutx, dom * 16));
+                k_lutx_build<<<(unsigned)std::min<uint64_t>(uint64_t(sms_f) * 8, (dom + 255) / 256), 256, 0, stream>>>(
+                    sk->seeds_dev, sk->d, sk->w[0], dom, sk->lutx);
                 SKB_CUDA(cudaGetLastError());
                 count_launch();
-                sk->lut64_dom = dom;
-                sk->lut64_bits = fam_bits[k];
+                sk->lutx_dom = dom;
                 if (!sk->lut_ready) SKB_CUDA(cudaEventCreateWithFlags(&sk->lut_ready, cudaEventDisableTiming));
                 SKB_CUDA(cudaEventRecord(sk->lut_ready, stream));
             } else if (sk->lut_ready) {
                 SKB_CUDA(cudaStreamWaitEvent(stream, sk->lut_ready, 0));   // built on another stream
             }
-            P.klut[k] = sk->lut64;
-            P.klut_dom[k] = sk->lut64_dom;
-            P.klut_bits[k] = fam_bits[k];
+            P.klut[k] = sk->lutx;
+            P.klut_dom[k] = sk->lutx_dom;
+            P.kprim[k] = (uint32_t)fam_t[k];
+            P.kothers[k] = 0;
+            for (uint32_t t = 0; t < c.n_targets; ++t)
+                if (c.tgt_ndim[t] == 1 && c.tgt_key[t][0] == keys[k] && t != (uint32_t)fam_t[k]) P.kothers[k] |= 1u << t;
         }
     }
     P.gather = c.n_preds > 0 ? 1u : 0u;
@@ -337,8 +337,20 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     }
     P.smem_counters = sc_count;
     avail -= (sc_count * 4 + 15) & ~15u;
-    if (fast)   // the lookup-table path updates non-privatised sketches directly (no heavy hitters)
+    P.pairhh_off = -1;
+    uint32_t pair_bytes = 0;
+    if (fast) {   // the lookup-table path updates non-privatised sketches directly (no heavy hitters)
         for (uint32_t k = 0; k < P.n_keys; ++k) { key_needs_hh[k] = false; P.key[k].hasglob = 0; }
+        // a skewed-pair table for the first matrix backed by L2 (2^10 slots, 12 KB)
+        for (uint32_t t = 0; t < c.n_targets; ++t)
+            if (P.tgt[t].ndim == 2 && P.tgt[t].smem_off < 0 && avail >= (12u << 10) + ring_stage * 2) {
+                P.pair_t = t;
+                P.pair_log2 = 10;
+                pair_bytes = 12u << 10;
+                avail -= pair_bytes;
+                break;
+            }
+    }
     // hash lookup tables for matrix dimensions whose key column has a domain hint (the table
     // stays L2-resident: dom * d * 4 bytes <= 64 MB per dimension); built once per sketch
     if (!fast && !(getenv("COMPASS_LUT") && strcmp(getenv("COMPASS_LUT"), "0") == 0)) {
@@ -445,6 +457,10 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     off = P.off_miss + kWarps * P.n_keys * 32 * 12;
     P.off_missn = (off + 15) & ~15u;
     off = P.off_missn + kWarps * P.n_keys * 4;
+    if (pair_bytes) {
+        P.pairhh_off = (int32_t)((off + 15) & ~15u);
+        off = (uint32_t)P.pairhh_off + pair_bytes;
+    }
     P.off_hstat = (off + 15) & ~15u;
     off = P.off_hstat + kMaxKeys * 4 * 4;
     P.off_seed = (off + 15) & ~15u;

@@ -106,11 +106,19 @@ struct SParams {
     uint32_t tile_rows;             // rows per ring stage
     uint32_t n_full_tiles;          // tiles with tile_rows rows (staged by TMA)
     unsigned long long *survivors;
-    // lookup-table path (FAST instances): per key column, the packed 64-bit table of its
-    // hash family over the hinted domain [0, klut_dom) (klut_bits per sketch row)
-    const uint64_t *klut[kMaxKeys];
+    // lookup-table path (FAST instances): per key column, the lookup table of its hash family
+    // over the hinted domain [0, klut_dom) (16 bytes per key: 8 uint16 fields, field r =
+    // counter index r * w + bucket of the family's primary sketch << 1 | sign), the primary
+    // sketch (the widest 1-D sketch of the family) and the other 1-D sketches on the column
+    const uint4 *klut[kMaxKeys];
     uint64_t klut_dom[kMaxKeys];
-    uint32_t klut_bits[kMaxKeys];
+    uint32_t kprim[kMaxKeys];
+    uint32_t kothers[kMaxKeys];
+    // skewed key pairs of one L2-backed matrix (target pair_t): a two-choice table of
+    // (key pair -> count) at byte offset pairhh_off (-1 = none), 2^pair_log2 slots, used while
+    // a warp aggregates (hot cells would otherwise serialise their L2 atomics)
+    int32_t pairhh_off;
+    uint32_t pair_log2, pair_t;
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -450,13 +458,15 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
 // w_m | w).  Keys outside the hinted domain fall back to the hash polynomials.
 template <int NK>
 struct Pend {
-    uint64_t e[NK];
+    uint4 e[NK];
     int32_t x[NK];
     bool valid;
 };
 
-__device__ __forceinline__ uint32_t lut_field(uint64_t e, uint32_t r, uint32_t B) {
-    return (uint32_t)(e >> (r * B)) & ((1u << B) - 1u);
+// field r (compile-time after unrolling) of a table entry
+__device__ __forceinline__ uint32_t lut_fld(const uint4 &q, int r) {
+    const uint32_t w = r < 2 ? q.x : (r < 4 ? q.y : (r < 6 ? q.z : q.w));
+    return (r & 1) ? (w >> 16) : (w & 0xffffu);
 }
 
 template <int NK>
@@ -465,9 +475,7 @@ __device__ __forceinline__ void fast_load(const SParams &P, bool valid, const in
 #pragma unroll
     for (int k = 0; k < NK; ++k) {
         n.x[k] = xr[k];
-        n.e[k] = (valid && (uint32_t)xr[k] < P.klut_dom[k])
-                     ? (uint64_t)__ldg(reinterpret_cast<const unsigned long long *>(P.klut[k]) + (uint32_t)xr[k])
-                     : 0ull;
+        n.e[k] = (valid && (uint32_t)xr[k] < P.klut_dom[k]) ? __ldg(P.klut[k] + (uint32_t)xr[k]) : make_uint4(0, 0, 0, 0);
     }
 }
 
@@ -498,18 +506,42 @@ __device__ __forceinline__ void process_fast(const SParams &P, unsigned char *sm
     for (int k = 0; k < NK; ++k) {
         if (!P.key[k].has1d || lane != __ffs(grp[k]) - 1) continue;
         const int cnt = __popc(grp[k]);
-        const bool inl = (uint32_t)b.x[k] < P.klut_dom[k];
-        const uint32_t B = P.klut_bits[k];
-        for (uint32_t tm = P.key[k].priv1d | P.key[k].glob1d; tm; tm &= tm - 1) {
-            const STarget &tg = P.tgt[__ffs(tm) - 1];
-            if (!inl) { update_1d(tg, seeds + tg.seed_off, sc, canon61(b.x[k]), cnt); continue; }
-            for (uint32_t r = 0; r < tg.d; ++r) {
-                const uint32_t f = lut_field(b.e[k], r, B);
-                const uint32_t cell = (f >> 1) & tg.wmask0;
-                const int v = (f & 1u) ? -cnt : cnt;
-                if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
-                else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
+        if ((uint32_t)b.x[k] >= P.klut_dom[k]) {   // outside the hinted domain: hash
+            for (uint32_t tm = P.key[k].priv1d | P.key[k].glob1d; tm; tm &= tm - 1) {
+                const STarget &tg = P.tgt[__ffs(tm) - 1];
+                update_1d(tg, seeds + tg.seed_off, sc, canon61(b.x[k]), cnt);
             }
+            continue;
+        }
+        const uint4 q = b.e[k];
+        const STarget &tp = P.tgt[P.kprim[k]];   // field >> 1 is its counter index
+        if (tp.smem_off >= 0) {
+            int32_t *base = sc + tp.smem_off;
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                if (r < (int)tp.d) {
+                    const uint32_t f = lut_fld(q, r);
+                    atomicAdd(base + (f >> 1), (f & 1u) ? -cnt : cnt);
+                }
+        } else {
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                if (r < (int)tp.d) {
+                    const uint32_t f = lut_fld(q, r);
+                    red_add_s64(tp.counters + (f >> 1), (f & 1u) ? -cnt : cnt);
+                }
+        }
+        for (uint32_t tm = P.kothers[k]; tm; tm &= tm - 1) {   // narrower sketches of the family
+            const STarget &tg = P.tgt[__ffs(tm) - 1];
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                if (r < (int)tg.d) {
+                    const uint32_t f = lut_fld(q, r);
+                    const uint32_t cell = (f >> 1) & tg.wmask0;
+                    const int v = (f & 1u) ? -cnt : cnt;
+                    if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
+                    else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
+                }
         }
     }
     if (!P.has2d) return;
@@ -524,15 +556,20 @@ __device__ __forceinline__ void process_fast(const SParams &P, unsigned char *sm
             update_2d(tg, seeds + tg.seed_off, sc, canon61(xa), canon61(xb), cnt);
             continue;
         }
-        const uint64_t ea = pick<NK>(b.e, tg.k0), eb = pick<NK>(b.e, tg.k1);
-        const uint32_t Ba = P.klut_bits[tg.k0], Bb = P.klut_bits[tg.k1];
-        for (uint32_t r = 0; r < tg.d; ++r) {
-            const uint32_t fa = lut_field(ea, r, Ba), fb = lut_field(eb, r, Bb);
-            const uint32_t cell = (((fa >> 1) & tg.wmask0) << tg.lw1) | ((fb >> 1) & tg.wmask1);
-            const int v = ((fa ^ fb) & 1u) ? -cnt : cnt;
-            if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
-            else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
-        }
+        if (agg && cnt > 1 && P.pairhh_off >= 0 && t == P.pair_t &&
+            hh_add(smem + P.pairhh_off, P.pair_log2, ((uint64_t)(uint32_t)xa << 32) | (uint32_t)xb, cnt))
+            continue;   // absorbed by the CTA's pair table (flushed once per distinct pair)
+        const uint4 qa = pick<NK>(b.e, tg.k0), qb = pick<NK>(b.e, tg.k1);
+        // (r * w + b) & (w_m - 1) = b & (w_m - 1): the family's bucket at the matrix width
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+            if (r < (int)tg.d) {
+                const uint32_t fa = lut_fld(qa, r), fb = lut_fld(qb, r);
+                const uint32_t cell = (((fa >> 1) & tg.wmask0) << tg.lw1) | ((fb >> 1) & tg.wmask1);
+                const int v = ((fa ^ fb) & 1u) ? -cnt : cnt;
+                if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
+                else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
+            }
     }
 }
 
@@ -691,6 +728,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
     {
         int32_t *sc = reinterpret_cast<int32_t *>(smem + P.off_sc);
         for (uint32_t i = tid; i < P.smem_counters; i += kThreads) sc[i] = 0;
+        if (FAST && P.pairhh_off >= 0) {
+            uint64_t *keys = reinterpret_cast<uint64_t *>(smem + P.pairhh_off);
+            int *cnts = reinterpret_cast<int *>(smem + P.pairhh_off + (8u << P.pair_log2));
+            for (uint32_t i = tid; i < (1u << P.pair_log2); i += kThreads) { keys[i] = kEmpty; cnts[i] = 0; }
+        }
         for (uint32_t k = 0; k < P.n_keys; ++k) {
             if (P.key[k].hh_off < 0) continue;
             uint64_t *keys = reinterpret_cast<uint64_t *>(smem + P.key[k].hh_off);
@@ -767,7 +809,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
     FastState<NK> fs;
     fs.pend.valid = false;
 #pragma unroll
-    for (int k = 0; k < NK; ++k) { fs.pend.e[k] = 0; fs.pend.x[k] = 0; }
+    for (int k = 0; k < NK; ++k) { fs.pend.e[k] = make_uint4(0, 0, 0, 0); fs.pend.x[k] = 0; }
     fs.agg = false;
     fs.actr = 0;
     const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
@@ -965,6 +1007,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                 if (tg.ndim != 1 || tg.k0 != k || tg.smem_off >= 0) continue;
                 update_1d(tg, seeds + tg.seed_off, sc, x, c);
             }
+        }
+    }
+    // ---- flush the skewed-pair table of the L2-backed matrix (FAST): one table lookup per
+    //      key and d counters per distinct pair, with the pair's count (linearity)
+    if (FAST && P.pairhh_off >= 0) {
+        const uint64_t *keys = reinterpret_cast<const uint64_t *>(smem + P.pairhh_off);
+        const int *cnts = reinterpret_cast<const int *>(smem + P.pairhh_off + (8u << P.pair_log2));
+        const STarget &tg = P.tgt[P.pair_t];
+        for (uint32_t s = tid; s < (1u << P.pair_log2); s += kConsumers) {
+            const uint64_t key = keys[s];
+            const int c = cnts[s];
+            if (key == kEmpty || c == 0) continue;
+            const uint4 qa = __ldg(P.klut[tg.k0] + (uint32_t)(key >> 32)), qb = __ldg(P.klut[tg.k1] + (uint32_t)key);
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                if (r < (int)tg.d) {
+                    const uint32_t fa = lut_fld(qa, r), fb = lut_fld(qb, r);
+                    const uint32_t cell = (((fa >> 1) & tg.wmask0) << tg.lw1) | ((fb >> 1) & tg.wmask1);
+                    red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, ((fa ^ fb) & 1u) ? -(int64_t)c : (int64_t)c);
+                }
         }
     }
     consumer_sync();

@@ -24,20 +24,26 @@ int main() {
     if (!mc) return 0;
     CUmulticastObjectProp prop = {};
     prop.numDevices = 1;
-    prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     size_t gran = 0;
     prop.size = 1 << 21;
-    CK(cuMulticastGetGranularity(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED));
-    prop.size = ((size_t(1) << 21) + gran - 1) / gran * gran;
-    printf("granularity=%zu size=%zu\n", gran, prop.size);
     CUmemGenericAllocationHandle mch;
-    CK(cuMulticastCreate(&mch, &prop));
+    CUresult rr = CUDA_ERROR_INVALID_VALUE;
+    const CUmemAllocationHandleType hts[3] = {CU_MEM_HANDLE_TYPE_FABRIC, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, CU_MEM_HANDLE_TYPE_NONE};
+    for (int h = 0; h < 3 && rr != CUDA_SUCCESS; ++h) {
+        prop.handleTypes = hts[h];
+        CK(cuMulticastGetGranularity(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+        prop.size = ((size_t(1) << 21) + gran - 1) / gran * gran;
+        rr = cuMulticastCreate(&mch, &prop);
+        const char *es; cuGetErrorString(rr, &es);
+        printf("handleType=%d granularity=%zu size=%zu cuMulticastCreate -> %d %s\n", (int)hts[h], gran, prop.size, (int)rr, es);
+    }
+    if (rr != CUDA_SUCCESS) return 0;
     CK(cuMulticastAddDevice(mch, dev));
     CUmemAllocationProp ap = {};
     ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     ap.location.id = 0;
-    ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    ap.requestedHandleTypes = (CUmemAllocationHandleType)prop.handleTypes;
     CUmemGenericAllocationHandle mem;
     CK(cuMemCreate(&mem, prop.size, &ap, 0));
     CK(cuMulticastBindMem(mch, 0, mem, 0, prop.size, 0));
