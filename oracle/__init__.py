@@ -31,7 +31,7 @@ _SRC = os.path.join(_HERE, "compass_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 POINT, RANGE, SUBSET = 0, 1, 2
-K_VEC, K_MAT, K_MERGED = 0, 1, 2
+K_VEC, K_MAT, K_MERGED, K_TEN3 = 0, 1, 2, 3   # K_TEN3: 3-D partitioned tensor
 INT64_MIN = -(1 << 63)
 INT64_MAX = (1 << 63) - 1
 
@@ -63,6 +63,8 @@ def lib():
         L.or_filter.argtypes = [i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp]
         L.or_build.restype = i32
         L.or_build.argtypes = [i64, vp, vp, i32, vp, i32, i32, i32, vp, cp, cp, u64, vp]
+        L.or_build_nd.restype = i32
+        L.or_build_nd.argtypes = [i64, vp, i32, vp, vp, i32, vp, vp, u64, vp]
         L.or_contract_row.restype = i32
         L.or_contract_row.argtypes = [i32, vp, vp, vp, vp, i32, vp, cp, i32, vp]
         L.or_contract_brute_row.restype = i32
@@ -132,18 +134,29 @@ def filter_mask(columns: dict, preds: list) -> tuple[np.ndarray, int]:
 
 
 def build(keys: list, mask, d: int, w: list, edge_ids: list, master: int = 42, out=None) -> np.ndarray:
-    """Fast-AGMS sketch (ndim = len(keys) = 1) or partitioned matrix (ndim 2), O2/O3."""
+    """Fast-AGMS sketch (ndim = len(keys) = 1), partitioned matrix (ndim 2), O2/O3, or 3-D
+    partitioned tensor (ndim 3), dims in the given (canonical) edge order."""
     ndim = len(keys)
-    assert ndim in (1, 2) and len(w) == ndim and len(edge_ids) == ndim
-    k0 = np.ascontiguousarray(keys[0])
-    k1 = np.ascontiguousarray(keys[1]) if ndim == 2 else k0
-    n = len(k0)
-    shape = (d, w[0]) if ndim == 1 else (d, w[0], w[1])
+    assert ndim in (1, 2, 3) and len(w) == ndim and len(edge_ids) == ndim
+    n = len(keys[0])
+    shape = (d, *w)
     if out is None:
         out = np.zeros(shape, dtype=np.int64)
     assert out.shape == shape and out.dtype == np.int64 and out.flags.c_contiguous
     m = np.ascontiguousarray(mask, dtype=np.uint8) if mask is not None else None
     wa = np.array(w, dtype=np.int64)
+    if ndim == 3:
+        ks = [np.ascontiguousarray(k) for k in keys]
+        kp = (ctypes.c_void_p * 3)(*[_ptr(k) for k in ks])
+        is64 = np.array([int(k.dtype == np.int64) for k in ks], dtype=np.int32)
+        eb = [e.encode() for e in edge_ids]
+        ep = (ctypes.c_char_p * 3)(*eb)
+        rc = lib().or_build_nd(n, _ptr(m) if m is not None else 0, 3, ctypes.cast(kp, ctypes.c_void_p), _ptr(is64), d,
+                               _ptr(wa), ctypes.cast(ep, ctypes.c_void_p), master, _ptr(out))
+        assert rc == 0
+        return out
+    k0 = np.ascontiguousarray(keys[0])
+    k1 = np.ascontiguousarray(keys[1]) if ndim == 2 else k0
     rc = lib().or_build(n, _ptr(m) if m is not None else 0,
                         _ptr(k0), int(k0.dtype == np.int64), _ptr(k1), int(k1.dtype == np.int64),
                         d, ndim, _ptr(wa), edge_ids[0].encode(), edge_ids[-1].encode(), master, _ptr(out))
@@ -216,7 +229,8 @@ class Graph:
     """Join graph with its built sketches (SURVEY.md §8(b) sk_graph, oracle side).
 
     tables: {alias: survivors}; edges: list of (edge_id, u, v);
-    vec: {(alias, edge_id): int64[d][w]}; mat: {(alias, (e_lo, e_hi)): int64[d][w_lo][w_hi]}.
+    vec: {(alias, edge_id): int64[d][w]}; mat: {(alias, (e_lo, e_hi)): int64[d][w_lo][w_hi]} and
+    3-D tensors {(alias, (e_0, e_1, e_2)): int64[d][w_0][w_1][w_2]}, edges canonical.
     """
 
     def __init__(self, tables, edges, vec, mat=None):
@@ -244,13 +258,15 @@ def subplan_tensors(g: Graph, subset):
             specs.append((t, K_VEC, inc, [g.vec[(t, inc[0])]]))
         elif len(inc) == 2 and (t, (inc[0], inc[1])) in g.mat:
             specs.append((t, K_MAT, inc, [g.mat[(t, (inc[0], inc[1]))]]))
+        elif len(inc) == 3 and (t, tuple(inc)) in g.mat:          # PAPER.md:225 3-D tensor
+            specs.append((t, K_TEN3, inc, [g.mat[(t, tuple(inc))]]))
         else:
             specs.append((t, K_MERGED, inc, [g.vec[(t, e)] for e in inc]))
     # widths: narrowest native width seen on each edge
     widths = [None] * len(E)
     for t, kind, inc, arrs in specs:
         for q, e in enumerate(inc):
-            if kind == K_MAT:
+            if kind in (K_MAT, K_TEN3):
                 wn = arrs[0].shape[1 + q]
             elif kind == K_VEC:
                 wn = arrs[0].shape[1]
@@ -261,10 +277,10 @@ def subplan_tensors(g: Graph, subset):
     # fold every leg to its edge width (O5)
     folded = []
     for t, kind, inc, arrs in specs:
-        if kind == K_MAT:
+        if kind in (K_MAT, K_TEN3):
             m = arrs[0]
-            m = fold(m, widths[eidx[inc[0]]], axis=1)
-            m = fold(m, widths[eidx[inc[1]]], axis=2)
+            for q, e in enumerate(inc):
+                m = fold(m, widths[eidx[e]], axis=1 + q)
             folded.append((kind, [eidx[e] for e in inc], [m]))
         elif kind == K_VEC:
             folded.append((kind, [eidx[inc[0]]], [fold(arrs[0], widths[eidx[inc[0]]], axis=1)]))
@@ -281,7 +297,7 @@ def estimate_rows(g: Graph, subset, brute: bool = False, rows=None):
     for r in (range(g.d) if rows is None else rows):
         tens = []
         for kind, legs, arrs in folded:
-            if kind == K_MAT:
+            if kind in (K_MAT, K_TEN3):
                 tens.append((kind, legs, [arrs[0][r].reshape(-1)]))
             else:
                 tens.append((kind, legs, [a[r] for a in arrs]))

@@ -196,6 +196,39 @@ int or_build(int64_t n_rows, const uint8_t *mask,
 }
 
 /* ------------------------------------------------------------------------- */
+/* O3' (n-D partitioned tensor, "a table with 3 joins has a 3-D tensor
+ * as its sketch, with one dimension for every join attribute"): for every surviving
+ * tuple and row r, the cell [h^{e_0}_r(x_0)]..[h^{e_{n-1}}_r(x_{n-1})] gets
+ * prod_q xi^{e_q}_r(x_q); dims in canonical edge order (SURVEY.md H6 generalised).
+ * keys[q] / key_is64[q] / edges[q] / w[q] per dimension, 1 <= ndim <= 3; adds into
+ * `out` (int64, [d][w_0]..[w_{ndim-1}], row-major).  Returns 0, or -1.        */
+/* ------------------------------------------------------------------------- */
+int or_build_nd(int64_t n_rows, const uint8_t *mask, int ndim, const void *const *keys, const int *key_is64,
+                int d, const int64_t *w, const char *const *edges, uint64_t master, int64_t *out) {
+    if (d < 1 || ndim < 1 || ndim > 3) return -1;
+    row_seed *s = (row_seed *)malloc((size_t)d * 3 * sizeof(row_seed));
+    for (int q = 0; q < ndim; ++q)
+        for (int r = 0; r < d; ++r) derive_row_seed(master, edges[q], (uint32_t)r, &s[q * d + r]);
+    int64_t cells = 1;
+    for (int q = 0; q < ndim; ++q) cells *= w[q];
+    for (int64_t i = 0; i < n_rows; ++i) {
+        if (mask && !mask[i]) continue;
+        for (int r = 0; r < d; ++r) {
+            int64_t cell = 0;
+            int sign = 1;
+            for (int q = 0; q < ndim; ++q) {
+                uint64_t x = or_canon(col_value(keys[q], key_is64[q], i));
+                cell = cell * w[q] + (int64_t)(g_eval(s[q * d + r].b, x) % (uint64_t)w[q]);
+                sign *= xi_eval(s[q * d + r].a, x);
+            }
+            out[(int64_t)r * cells + cell] += sign;
+        }
+    }
+    free(s);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
 /* Exact signed big integers (sign-magnitude, BN_L x 32-bit limbs).            */
 /* ------------------------------------------------------------------------- */
 
@@ -429,7 +462,7 @@ double or_bn_selftest_to_double(int n, const int64_t *xs) {
  */
 /* ------------------------------------------------------------------------- */
 
-enum { K_VEC = 0, K_MAT = 1, K_MERGED = 2 };
+enum { K_VEC = 0, K_MAT = 1, K_MERGED = 2, K_TEN3 = 3 };   /* K_TEN3: 3-D partitioned tensor */
 
 typedef struct {
     int T, E;
@@ -456,6 +489,7 @@ static int64_t tensor_at(const net *g, int t, const int64_t *idx) {
     const int *lg = &g->legs[3 * t];
     if (g->kind[t] == K_VEC) return g->data[3 * t][idx[0]];
     if (g->kind[t] == K_MAT) return g->data[3 * t][idx[0] * g->w[lg[1]] + idx[1]];
+    if (g->kind[t] == K_TEN3) return g->data[3 * t][(idx[0] * g->w[lg[1]] + idx[1]) * g->w[lg[2]] + idx[2]];
     int64_t vals[3] = {0, 0, 0};
     for (int q = 0; q < k; ++q) vals[q] = g->data[3 * t + q][idx[q]];
     return fold_minabs(vals, k);
@@ -470,6 +504,7 @@ static int net_init(net *g, int T, const int *kind, const int *nlegs, const int 
         if (nlegs[t] < 1 || nlegs[t] > 3) return -1;
         if (kind[t] == K_VEC && nlegs[t] != 1) return -1;
         if (kind[t] == K_MAT && nlegs[t] != 2) return -1;
+        if (kind[t] == K_TEN3 && nlegs[t] != 3) return -1;
         for (int q = 0; q < nlegs[t]; ++q) {
             int e = legs[3 * t + q];
             if (e < 0 || e >= E || cnt[e] >= 2) return -1;

@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import oracle
-from oracle import K_MAT, K_MERGED, K_VEC, POINT, RANGE, SUBSET
+from oracle import K_MAT, K_MERGED, K_TEN3, K_VEC, POINT, RANGE, SUBSET
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = json.load(open(os.path.join(HERE, "golden", "paper_pins.json")))
@@ -657,3 +657,119 @@ def test_c1_estimate_vs_exact_join():
     est = oracle.median_odd(rows)
     sigma = math.sqrt((float((fR ** 2).sum()) * float((fS ** 2).sum()) + J * J) / 1024)
     assert abs(est - J) < 4 * sigma, (est, J, sigma)
+
+
+# ---------------------------------------------------------------- §8(f) 3: n-D partitioned tensors
+def test_tensor3_build_single_tuple_definition():
+    """PAPER.md:225 ("a table with 3 joins has a 3-D tensor as its sketch, with one dimension
+    for every join attribute"): one tuple (x, y, z) puts exactly prod_q xi^{e_q}_r(x_q) at
+    [h^{e_0}_r(x)][h^{e_1}_r(y)][h^{e_2}_r(z)] of every row r and nothing elsewhere; the
+    hash primitives are the pinned H3/H4 ones (oracle.xi, oracle.bucket)."""
+    es = ["A.x|C.x", "B.y|C.y", "C.z|D.z"]
+    w = [8, 4, 16]
+    for (x, y, z) in [(5, -3, 1 << 40), (0, 0, 0), (-(1 << 63), (1 << 61) - 1, 7)]:
+        T = oracle.build([np.array([x], np.int64), np.array([y], np.int64), np.array([z], np.int64)], None, 3, w, es,
+                         master=77)
+        for r in range(3):
+            want = np.zeros(w, dtype=np.int64)
+            idx = tuple(oracle.bucket(77, e, r, k, wq) for e, k, wq in zip(es, (x, y, z), w))
+            want[idx] = oracle.xi(77, es[0], r, x) * oracle.xi(77, es[1], r, y) * oracle.xi(77, es[2], r, z)
+            assert np.array_equal(T[r], want), (x, y, z, r)
+
+
+def test_tensor3_linearity_and_fold():
+    """P1 (PAPER.md:86) and P6 (SPEC.md:147-155) for 3-D tensors: shards sum bit-exactly;
+    folding any axis of build(w) equals build at the narrower width."""
+    rng = np.random.default_rng(301)
+    n = 3000
+    keys = [rng.integers(-50, 50, n).astype(np.int64), rng.integers(0, 20, n).astype(np.int32),
+            rng.zipf(1.4, n).astype(np.int64)]
+    mask = (rng.random(n) < 0.7).astype(np.uint8)
+    es = ["A.x|C.x", "B.y|C.y", "C.z|D.z"]
+    full = oracle.build(keys, mask, 5, [16, 8, 32], es)
+    cuts = sorted(rng.choice(np.arange(1, n), 4, replace=False))
+    acc = np.zeros_like(full)
+    for a, b in zip([0] + cuts, cuts + [n]):
+        acc += oracle.build([k[a:b] for k in keys], mask[a:b], 5, [16, 8, 32], es)
+    assert np.array_equal(acc, full)
+    narrow = oracle.build(keys, mask, 5, [4, 8, 2], es)
+    f = oracle.fold(oracle.fold(full, 4, axis=1), 2, axis=3)
+    assert np.array_equal(f, narrow)
+
+
+def _star3(rng, keys):
+    """center C(x, y, z) with leaves A(x), B(y), D(z); random multiplicities on `keys`."""
+    k = len(keys)
+    fA, fB, fD = rng.integers(0, 4, k), rng.integers(0, 4, k), rng.integers(0, 4, k)
+    fC = rng.integers(0, 3, (k, k, k))
+    kA = np.repeat(keys, fA).astype(np.int64)
+    kB = np.repeat(keys, fB).astype(np.int32)
+    kD = np.repeat(keys, fD).astype(np.int64)
+    trip = [(keys[i], keys[j], keys[l]) for i in range(k) for j in range(k) for l in range(k) for _ in range(fC[i, j, l])]
+    kC = [np.array([t[q] for t in trip], dtype=np.int64) for q in range(3)]
+    J = int(np.einsum("i,j,l,ijl->", fA, fB, fD, fC))
+    return kA, kB, kD, kC, J
+
+
+def test_tensor3_star_exact_with_injective_hashes():
+    """SURVEY P2 generalised to a 3-D tensor: with every h_r injective on the key domain (at
+    the tensor width, and at the vectors' width before folding), every row of the 4-table
+    star estimate equals the exact join size sum fA(x) fB(y) fD(z) fC(x, y, z)."""
+    rng = np.random.default_rng(302)
+    keys = list(range(200, 206))
+    es = ["A.x|C.x", "B.y|C.y", "C.z|D.z"]
+    d = 3
+    seed = _injective_seed(keys, [(e, w) for e in es for w in (256, 16)], d)
+    kA, kB, kD, kC, J = _star3(rng, keys)
+    vec = {("A", es[0]): oracle.build([kA], None, d, [256], [es[0]], master=seed),
+           ("B", es[1]): oracle.build([kB], None, d, [256], [es[1]], master=seed),
+           ("D", es[2]): oracle.build([kD], None, d, [256], [es[2]], master=seed)}
+    for q, e in enumerate(es):
+        vec[("C", e)] = oracle.build([kC[q]], None, d, [256], [e], master=seed)
+    T = oracle.build(kC, None, d, [16, 16, 16], es, master=seed)
+    g = oracle.Graph({"A": len(kA), "B": len(kB), "C": len(kC[0]), "D": len(kD)},
+                     [(es[0], "A", "C"), (es[1], "B", "C"), (es[2], "C", "D")], vec, {("C", tuple(es)): T})
+    rows = oracle.estimate_rows(g, ("A", "B", "C", "D"))
+    assert rows == [J] * d
+    assert oracle.estimate_rows(g, ("A", "B", "C", "D"), brute=True) == rows
+
+
+def test_tensor3_star_unbiased():
+    """SURVEY P3 for the 3-D partitioned estimator ("this procedure can be
+    generalized to any number of join attributes"): over 2000 master seeds the mean of the
+    per-row estimate is within 4 standard errors of the exact join size."""
+    rng = np.random.default_rng(303)
+    kA, kB, kD, kC, J = _star3(rng, list(range(5)))
+    es = ["A.x|C.x", "B.y|C.y", "C.z|D.z"]
+    ests = []
+    for s in range(2000):
+        A = oracle.build([kA], None, 1, [4], [es[0]], master=20000 + s)[0]
+        B = oracle.build([kB], None, 1, [4], [es[1]], master=20000 + s)[0]
+        D = oracle.build([kD], None, 1, [4], [es[2]], master=20000 + s)[0]
+        T = oracle.build(kC, None, 1, [4, 4, 4], es, master=20000 + s)[0]
+        ests.append(int(np.einsum("i,j,l,ijl->", A, B, D, T)))
+    m, se = _mean_se(ests)
+    assert abs(m - J) < 4 * se, (m, J, se)
+
+
+def test_tensor3_message_passing_equals_literal_definition():
+    """P5 with 3-D tensor nodes: in a star (3 children), at a leaf-bearing tree node, and
+    inside a cycle (the conditioned edge fixes one leg) — message passing == definition."""
+    rng = np.random.default_rng(304)
+    topos = [[(0, 1), (0, 2), (0, 3)],                   # node 0: 3-D star centre
+             [(0, 1), (1, 2), (2, 0), (1, 3)],           # node 1: 3-D inside the triangle
+             [(1, 0), (0, 2), (1, 2), (2, 3), (1, 4)]]   # C3 shape: nodes 1 and 2 are 3-D
+    for trial in range(150):
+        topo = topos[trial % len(topos)]
+        T = 1 + max(max(e) for e in topo)
+        widths = [int(rng.integers(1, 4)) for _ in topo]
+        tens = []
+        for t in range(T):
+            inc = [i for i, e in enumerate(topo) if t in e]
+            if len(inc) == 3:
+                tens.append((K_TEN3, inc, [rng.integers(-3, 4, widths[inc[0]] * widths[inc[1]] * widths[inc[2]])]))
+            elif len(inc) == 2:
+                tens.append((K_MAT, inc, [rng.integers(-3, 4, widths[inc[0]] * widths[inc[1]])]))
+            else:
+                tens.append((K_VEC, inc, [rng.integers(-3, 4, widths[inc[0]])]))
+        assert oracle.contract_row(tens, widths) == oracle.contract_row(tens, widths, brute=True), (trial, topo)
