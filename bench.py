@@ -371,12 +371,14 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C4", choices=["C1", "C2", "C3", "C4", "C5", "C5-cycle"])
+    ap.add_argument("--workload", default="C4", choices=["C1", "C2", "C3", "C3t", "C4", "C5", "C5-cycle"])
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--cpu-rows", type=int, default=150_000_000)
     ap.add_argument("--ref-rows", type=int, default=20_000_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--wire", default="i32", choices=["i32", "i64"], help="all-reduce wire format (N > 1)")
+    ap.add_argument("--no-overlap", action="store_true", help="one trailing all-reduce instead of per-table ones")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(_relaunch(args.gpus))
@@ -395,7 +397,9 @@ def main():
     preds = {t.name: datagen.resolve_preds(ws, t.name) for t in ws.tables}
     data = {t.name: datagen.generate_table(ws, t.name, dev, rank=rank, world=world) for t in ws.tables}
     torch.cuda.synchronize()
-    run = QueryRun(ws, dev)
+    # N > 1: int32 wire and per-table all-reduces overlapped with the next table's scan
+    # (SURVEY.md §8(e) levers i and ii); N = 1 has no collective
+    run = QueryRun(ws, dev, wire=args.wire, overlap=not args.no_overlap)
     subplans = _subplans(ws) if ws.kind == "graph" else None
     stream = torch.cuda.current_stream()
     kev = []  # (start, end) events around each fused-scan launch
@@ -494,7 +498,9 @@ def main():
                        "sketches": [f"{s.table}:{'x'.join(map(str, s.w))}xd{s.d}" for s in ws.sketches],
                        "subplans": len(subplans) if subplans else len(ests),
                        "l2": "inputs larger than L2 (no flush)" if ab["full"] > 4 * 126e6 else "inputs L2-resident",
-                       "parallelism": f"row-sharded x{world} + NCCL int64 all-reduce"},
+                       "parallelism": f"row-sharded x{world}" + (f" + NCCL SUM all-reduce ({run.merge.wire} wire, "
+                                                                  f"{'per-table overlapped' if run.merge.overlap else 'one trailing'})"
+                                                                  if world > 1 else "")},
             "roofline": roof, "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "survivors": run.survivors.tolist(), "estimates": ests[:8] if ests else None,

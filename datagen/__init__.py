@@ -291,6 +291,23 @@ def c3(scale: float = 1.0, w: int = 4096, d: int = 7) -> Workload:
     return ws
 
 
+def c3t(scale: float = 1.0, w: int = 4096, d: int = 7, wt: int = 64) -> Workload:
+    """C3 with partitioned sketches for its multi-join tables (PAPER.md:225
+    "a table with 3 joins has a 3-D tensor as its sketch, with one dimension for every join
+    attribute"): MK and CI get d x wt^3 tensors over their three edges, T a wt x wt matrix over
+    its two; dimensions in canonical edge order.  Same tables, data and 1-D sketches as C3."""
+    ws = c3(scale=scale, w=w, d=d)
+    e = {nm: ed for ed, u, v in ws.edges for nm in [(u, v)]}
+    e1, e2, e3, e4, e5 = e[("K", "MK")], e[("MK", "T")], e[("CI", "T")], e[("CI", "MK")], e[("CI", "N")]
+    col_of = {("MK", e1): "kid", ("MK", e2): "mid", ("MK", e4): "mid",
+              ("CI", e3): "mid", ("CI", e4): "mid", ("CI", e5): "pid", ("T", e2): "id", ("T", e3): "id"}
+    for t, es in [("MK", [e1, e2, e4]), ("CI", [e3, e4, e5]), ("T", [e2, e3])]:
+        es = sorted(es)
+        ws.sketches.append(Sketch(t, [col_of[(t, x)] for x in es], es, d, [wt] * len(es)))
+    ws.name = "C3t"
+    return ws
+
+
 def c4(scale: float = 1.0, w: int = 16384, d: int = 9) -> Workload:
     n = max(1, int(1_000_000_000 * scale))
     dom = 100_000_000
@@ -340,4 +357,4 @@ def c5(scale: float = 1.0, cycle: bool = False, w: int = 1024, wm: int = 512, d:
     return Workload("C5-cycle" if cycle else "C5-chain", tables, edges, sk, data_seed=210202440 + 4)
 
 
-CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5}
+CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C3t": c3t, "C4": c4, "C5": c5}

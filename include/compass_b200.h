@@ -54,6 +54,9 @@ typedef struct sk_sketch sk_sketch;   /* opaque */
  *                (PAPER.md:192 rows; median needs odd d).
  *   ndim         1: Fast-AGMS vector  sk[r][j]
  *                2: partitioned matrix M[r][i][j]
+ *                3: partitioned tensor T[r][i][j][k]  ("a table with 3 joins
+ *                   has a 3-D tensor as its sketch, with one dimension for every join
+ *                   attribute")
  *   w[0..ndim)   buckets per dimension, powers of two in [2, 2^24]
  *                (PAPER.md:395 uses 1023; powers of two enable folding).
  *   master_seed  seed of the hash family (default 42).
@@ -69,12 +72,14 @@ typedef struct sk_sketch sk_sketch;   /* opaque */
 typedef struct {
     uint32_t d;
     uint32_t ndim;
-    uint32_t w[2];
+    uint32_t w[3];
     uint64_t master_seed;
-    const char *edge_id[2];
+    const char *edge_id[3];
 } sk_desc;
 
-/* Counter layout: int64, row-major, [d][w0] (ndim 1) or [d][w0][w1] (ndim 2). */
+/* Counter layout: int64, row-major, [d][w0], [d][w0][w1] or [d][w0][w1][w2]; the
+ * dimensions of a matrix or tensor are in canonical edge order (edge_id[0] < edge_id[1]
+ * < edge_id[2]), else SK_EINVAL. */
 
 /* Create a sketch on CUDA `device`.  counters_dev: caller-owned device buffer of
  * d*w0(*w1) int64 (must already be zeroed if a fresh sketch is wanted), or NULL
@@ -135,7 +140,7 @@ typedef struct {
 
 typedef struct {
     sk_sketch *sketch;
-    uint32_t key_col[2]; /* key column per sketch dimension */
+    uint32_t key_col[3]; /* key column per sketch dimension */
 } sk_target;
 
 SK_API sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_cols, uint64_t n_rows,
@@ -148,13 +153,27 @@ SK_API sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_cols, 
  * Cross-GPU merge: all-reduce (SUM, int64) the counter buffers with NCCL. */
 SK_API sk_status sketch_merge(sk_sketch *dst, const sk_sketch *src, void *stream);
 
+/* int32 wire format of the cross-GPU merge (SURVEY.md §8(e) lever i): the
+ * all-reduce moves half the bytes when every partial and merged counter fits int32, which
+ * holds whenever every table has < 2^31 rows (|counter| <= survivors <= rows).
+ *   sketch_wire_pack:   wire_dev[i] = (int32) counters_dev[i], i < n; a value outside int32
+ *                       sets *overflow_dev to 1 (device uint32, optional, never cleared).
+ *   sketch_wire_unpack: counters_dev[i] = (int64) wire_dev[i], i < n.
+ * Device buffers, caller-owned; asynchronous on `stream`; SK_EINVAL on NULL buffers with n > 0. */
+SK_API sk_status sketch_wire_pack(const int64_t *counters_dev, int32_t *wire_dev, uint64_t n, unsigned int *overflow_dev,
+                                  void *stream);
+SK_API sk_status sketch_wire_unpack(const int32_t *wire_dev, int64_t *counters_dev, uint64_t n, void *stream);
+
 /* ---------------------------------------------------------------------------
  * Join graph of one query: tables are vertices carrying their
  * exact post-selection cardinality; edge e joins tables edge_u[e] and edge_v[e]
  * and carries one 1-D sketch per side (vec_u[e] built on table edge_u[e]'s join
  * column, vec_v[e] on edge_v[e]'s), both with the edge's id and seed.  Optional
- * partitioned matrices: mat[m] is table mat_table[m]'s 2-D sketch over edges
- * (mat_e0[m], mat_e1[m]) (dimension 0 = mat_e0, the canonically first edge).
+ * partitioned sketches: mat[m] is table mat_table[m]'s 2-D matrix over edges
+ * (mat_e0[m], mat_e1[m]) (dimension 0 = mat_e0, the canonically first edge), or its 3-D
+ * tensor (ndim 3; mat_e0/mat_e1 = its first two edges).  A table uses its
+ * matrix or tensor in a sub-plan whose edges at that table are exactly the sketch's edges
+ * (matched by edge id), else the min-abs merged view of its 1-D sketches.
  * All arrays are host arrays; sketches live on one device.  n_tables <= 64.
  * ------------------------------------------------------------------------- */
 typedef struct {

@@ -36,8 +36,8 @@ class SkError(RuntimeError):
 
 
 class sk_desc(ctypes.Structure):
-    _fields_ = [("d", ctypes.c_uint32), ("ndim", ctypes.c_uint32), ("w", ctypes.c_uint32 * 2),
-                ("master_seed", ctypes.c_uint64), ("edge_id", ctypes.c_char_p * 2)]
+    _fields_ = [("d", ctypes.c_uint32), ("ndim", ctypes.c_uint32), ("w", ctypes.c_uint32 * 3),
+                ("master_seed", ctypes.c_uint64), ("edge_id", ctypes.c_char_p * 3)]
 
 
 class sk_column(ctypes.Structure):
@@ -50,7 +50,7 @@ class sk_pred(ctypes.Structure):
 
 
 class sk_target(ctypes.Structure):
-    _fields_ = [("sketch", ctypes.c_void_p), ("key_col", ctypes.c_uint32 * 2)]
+    _fields_ = [("sketch", ctypes.c_void_p), ("key_col", ctypes.c_uint32 * 3)]
 
 
 class sk_graph(ctypes.Structure):
@@ -64,7 +64,7 @@ class sk_graph(ctypes.Structure):
 
 # every symbol include/compass_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = ["sketch_create", "sketch_destroy", "sketch_counters", "sketch_zero", "sketch_update_filtered",
-           "sketch_merge", "estimate_join", "estimate_join_exact", "estimate_subplans", "plan_greedy",
+           "sketch_merge", "sketch_wire_pack", "sketch_wire_unpack", "estimate_join", "estimate_join_exact", "estimate_subplans", "plan_greedy",
            "plan_enumerate", "exact_join_size", "sk_last_error", "sk_version", "sk_kernel_launches"]
 
 # Algorithm 1 search-space settings
@@ -123,6 +123,11 @@ def lib() -> ctypes.CDLL:
         L.estimate_join.restype = st
         L.estimate_join.argtypes = [ctypes.POINTER(sk_graph), u64, ctypes.POINTER(ctypes.c_double),
                                     ctypes.POINTER(ctypes.c_double), vp]
+        if hasattr(L, "sketch_wire_pack"):   # (experimental builds of older revisions lack it)
+            L.sketch_wire_pack.restype = st
+            L.sketch_wire_pack.argtypes = [vp, vp, u64, vp, vp]
+            L.sketch_wire_unpack.restype = st
+            L.sketch_wire_unpack.argtypes = [vp, vp, u64, vp]
         L.estimate_join_exact.restype = st
         L.estimate_join_exact.argtypes = [ctypes.POINTER(sk_graph), u64, ctypes.c_char_p, u32, vp]
         L.estimate_subplans.restype = st
@@ -160,13 +165,14 @@ def _stream_ptr(stream) -> int:
 
 
 class Sketch:
-    """A Fast-AGMS vector (ndim 1) or partitioned matrix (ndim 2) sketch whose
-    int64 counters are a caller-owned torch tensor (``self.counters``)."""
+    """A Fast-AGMS vector (ndim 1), partitioned matrix (ndim 2) or 3-D partitioned tensor
+    (ndim 3) sketch whose int64 counters are a caller-owned torch tensor
+    (``self.counters``); the dimensions are in canonical edge order."""
 
     def __init__(self, d: int, w, edge_ids, master_seed: int = 42, device=None, counters: torch.Tensor | None = None):
         w = list(w)
         edge_ids = list(edge_ids)
-        assert len(w) == len(edge_ids) and len(w) in (1, 2)
+        assert len(w) == len(edge_ids) and len(w) in (1, 2, 3)
         self.d, self.w, self.edge_ids, self.master_seed = d, w, edge_ids, master_seed
         device = torch.device(device if device is not None else "cuda")
         if device.index is None:
@@ -296,10 +302,28 @@ def sketch_merge(dst: Sketch, src: Sketch, stream=None):
     _check(lib().sketch_merge(dst.handle, src.handle, ctypes.c_void_p(_stream_ptr(stream))))
 
 
+def sketch_wire_pack(counters: torch.Tensor, wire: torch.Tensor, overflow: torch.Tensor | None = None, stream=None):
+    """int64 counters -> int32 wire buffer (same length), for the int32 all-reduce."""
+    assert counters.dtype == torch.int64 and wire.dtype == torch.int32 and counters.numel() == wire.numel()
+    assert counters.is_contiguous() and wire.is_contiguous()
+    _check(lib().sketch_wire_pack(ctypes.c_void_p(counters.data_ptr()), ctypes.c_void_p(wire.data_ptr()),
+                                  counters.numel(), ctypes.c_void_p(overflow.data_ptr() if overflow is not None else 0),
+                                  ctypes.c_void_p(_stream_ptr(stream))))
+
+
+def sketch_wire_unpack(wire: torch.Tensor, counters: torch.Tensor, stream=None):
+    """int32 wire buffer -> int64 counters (same length)."""
+    assert counters.dtype == torch.int64 and wire.dtype == torch.int32 and counters.numel() == wire.numel()
+    assert counters.is_contiguous() and wire.is_contiguous()
+    _check(lib().sketch_wire_unpack(ctypes.c_void_p(wire.data_ptr()), ctypes.c_void_p(counters.data_ptr()),
+                                    counters.numel(), ctypes.c_void_p(_stream_ptr(stream))))
+
+
 class JoinGraph:
     """sk_graph wrapper.  tables: list of aliases (index order = tie order);
     survivors: list of ints; edges: list of (u, v, Sketch_u, Sketch_v);
-    mats: list of (table, e0, e1, Sketch)."""
+    mats: list of (table, e0, e1, Sketch) — matrices, and 3-D tensors (e0, e1 = their first
+    two edges)."""
 
     def __init__(self, tables, survivors, edges, mats=()):
         self.tables = list(tables)

@@ -95,7 +95,7 @@ extern "C" sk_status sketch_create(const sk_desc *desc, int device, int64_t *cou
     *out = nullptr;
     if (desc->d < 1 || desc->d > 63 || (desc->d % 2) == 0)
         return fail(SK_EINVAL, "sketch_create: d=%u must be odd in [1,63]", desc->d);
-    if (desc->ndim != 1 && desc->ndim != 2) return fail(SK_EINVAL, "sketch_create: ndim must be 1 or 2");
+    if (desc->ndim < 1 || desc->ndim > 3) return fail(SK_EINVAL, "sketch_create: ndim must be 1, 2 or 3");
     uint64_t cells = 1;
     for (uint32_t q = 0; q < desc->ndim; ++q) {
         if (!is_pow2(desc->w[q]) || desc->w[q] > (1u << 24))
@@ -103,8 +103,9 @@ extern "C" sk_status sketch_create(const sk_desc *desc, int device, int64_t *cou
         if (!desc->edge_id[q] || !desc->edge_id[q][0]) return fail(SK_EINVAL, "sketch_create: empty edge id");
         cells *= desc->w[q];
     }
-    if (desc->ndim == 2 && strcmp(desc->edge_id[0], desc->edge_id[1]) >= 0)
-        return fail(SK_EINVAL, "sketch_create: matrix dims must be in canonical edge order (edge_id[0] < edge_id[1])");
+    for (uint32_t q = 1; q < desc->ndim; ++q)
+        if (strcmp(desc->edge_id[q - 1], desc->edge_id[q]) >= 0)
+            return fail(SK_EINVAL, "sketch_create: dims must be in canonical edge order (edge_id[q-1] < edge_id[q])");
     if (cells * desc->d > (1ULL << 31)) return fail(SK_EINVAL, "sketch_create: sketch too large");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(SK_ECUDA, "sketch_create: no CUDA device");
@@ -202,6 +203,44 @@ __global__ void k_merge_add(int64_t *__restrict__ dst, const int64_t *__restrict
         reinterpret_cast<longlong2 *>(dst)[i] = a;
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) dst[n - 1] += src[n - 1];
+}
+
+// int32 wire format of the cross-GPU merge (SURVEY.md §8(e) lever i): exact while every
+// partial and merged counter lies in int32, i.e. every table has < 2^31 rows (|counter| <=
+// survivors).  A value outside int32 sets *overflow (device flag, never cleared here).
+__global__ void k_wire_pack(const int64_t *src, int32_t *dst, uint64_t n, unsigned int *overflow) {
+    bool bad = false;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const int64_t v = src[i];
+        bad |= v != (int64_t)(int32_t)v;
+        dst[i] = (int32_t)v;
+    }
+    if (bad && overflow) atomicOr(overflow, 1u);
+}
+__global__ void k_wire_unpack(const int32_t *src, int64_t *dst, uint64_t n) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        dst[i] = (int64_t)src[i];
+}
+
+extern "C" sk_status sketch_wire_pack(const int64_t *counters_dev, int32_t *wire_dev, uint64_t n, unsigned int *overflow_dev,
+                                      void *stream) {
+    if (n && (!counters_dev || !wire_dev)) return fail(SK_EINVAL, "sketch_wire_pack: NULL buffer");
+    if (!n) return SK_OK;
+    const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 8);
+    k_wire_pack<<<blocks, 256, 0, (cudaStream_t)stream>>>(counters_dev, wire_dev, n, overflow_dev);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SK_OK : cuda_fail(e, "sketch_wire_pack launch");
+}
+
+extern "C" sk_status sketch_wire_unpack(const int32_t *wire_dev, int64_t *counters_dev, uint64_t n, void *stream) {
+    if (n && (!counters_dev || !wire_dev)) return fail(SK_EINVAL, "sketch_wire_unpack: NULL buffer");
+    if (!n) return SK_OK;
+    const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 8);
+    k_wire_unpack<<<blocks, 256, 0, (cudaStream_t)stream>>>(wire_dev, counters_dev, n);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SK_OK : cuda_fail(e, "sketch_wire_unpack launch");
 }
 
 extern "C" sk_status sketch_merge(sk_sketch *dst, const sk_sketch *src, void *stream) {

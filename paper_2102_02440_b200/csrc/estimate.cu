@@ -45,7 +45,7 @@ const uint32_t kPrimes[kMaxMod] = {67108859, 67108837, 67108819, 67108777, 67108
                                    67108747, 67108739, 67108729, 67108721, 67108709, 67108693, 67108669,
                                    67108667, 67108661, 67108649, 67108633, 67108597, 67108579, 67108529,
                                    67108511, 67108507, 67108493, 67108471, 67108463, 67108453, 67108439};
-enum { KV = 0, KM = 1, KG = 2 };          // vector, matrix, merged
+enum { KV = 0, KM = 1, KG = 2, KT = 3 };  // vector, matrix, merged, 3-D tensor
 enum { RCHILD = 0, RPARENT = 1, RFIXED = 2 };
 
 struct Mods {
@@ -127,6 +127,23 @@ __global__ void k_fold(const int64_t *in, int64_t *out, uint32_t d, uint32_t wn0
     }
 }
 
+// fold [d][wn0][wn1][wn2] -> [d][w0][w1][w2] along every axis (O5 per dimension)
+__global__ void k_fold3(const int64_t *in, int64_t *out, uint32_t d, uint32_t wn0, uint32_t wn1, uint32_t wn2, uint32_t w0,
+                        uint32_t w1, uint32_t w2) {
+    const uint64_t total = uint64_t(d) * w0 * w1 * w2;
+    for (uint64_t o = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; o < total; o += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t k = (uint32_t)(o % w2);
+        const uint32_t j = (uint32_t)((o / w2) % w1);
+        const uint32_t i = (uint32_t)((o / (uint64_t(w1) * w2)) % w0);
+        const uint32_t r = (uint32_t)(o / (uint64_t(w0) * w1 * w2));
+        int64_t s = 0;
+        for (uint32_t a = i; a < wn0; a += w0)
+            for (uint32_t b = j; b < wn1; b += w1)
+                for (uint32_t c = k; c < wn2; c += w2) s += in[((uint64_t(r) * wn0 + a) * wn1 + b) * wn2 + c];
+        out[o] = s;
+    }
+}
+
 // per row: sort indices by |c| ascending (bitonic, w a power of two, w <= 8192)
 __global__ void k_sort_abs(const int64_t *c, uint32_t w, int32_t *ord, uint64_t *sabs, int32_t *rank, int64_t *csorted) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -203,6 +220,7 @@ __device__ __forceinline__ uint64_t block_sum_mod(uint64_t v, uint64_t m, uint64
 __device__ __forceinline__ int64_t tensor_val(const Node &n, int r, const int64_t *idx) {
     if (n.kind == KV) return n.data[0][uint64_t(r) * n.w[0] + idx[0]];
     if (n.kind == KM) return n.data[0][(uint64_t(r) * n.w[0] + idx[0]) * n.w[1] + idx[1]];
+    if (n.kind == KT) return n.data[0][((uint64_t(r) * n.w[0] + idx[0]) * n.w[1] + idx[1]) * n.w[2] + idx[2]];
     int64_t acc = n.data[0][uint64_t(r) * n.w[0] + idx[0]];
     for (int q = 1; q < n.nl; ++q) {
         const int64_t v = n.data[q][uint64_t(r) * n.w[q] + idx[q]];
@@ -221,33 +239,42 @@ __global__ void k_node_dense(const __grid_constant__ Node n, const __grid_consta
     const uint64_t mu = md.mu[k];
     const uint64_t m = md.m[k];
     const int64_t b = n.b0 + bb;
-    int qp = -1, qf = -1, qc0 = -1, qc1 = -1;
+    int qp = -1, qf = -1, qc0 = -1, qc1 = -1, qc2 = -1;
     for (int q = 0; q < n.nl; ++q) {
         if (n.role[q] == RPARENT) qp = q;
         else if (n.role[q] == RFIXED) qf = q;
         else if (qc0 < 0) qc0 = q;
-        else qc1 = q;
+        else if (qc1 < 0) qc1 = q;
+        else qc2 = q;
     }
-    // outer leg: parent if any, else first child; inner leg: the (other) child if any
+    // outer leg: parent if any, else first child; inner legs: the (other) children, a second
+    // one only for a 3-D tensor with three free legs
     const int qo = qp >= 0 ? qp : qc0;
     const int qi = qp >= 0 ? qc0 : qc1;
+    const int qj = qp >= 0 ? qc1 : qc2;
     const int wo = qo >= 0 ? n.w[qo] : 1;
     const int wi = qi >= 0 ? n.w[qi] : 1;
+    const int wj = qj >= 0 ? n.w[qj] : 1;
     const uint64_t *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row(n, qo, k, r, bb, 0) : nullptr;
     const uint64_t *xi = (qi >= 0) ? msg_row(n, qi, k, r, bb, 0) : nullptr;
+    const uint64_t *xj = (qj >= 0) ? msg_row(n, qj, k, r, bb, 0) : nullptr;
     uint64_t acc = 0;
     const int per_tile = (wo + n.tiles - 1) / n.tiles;
     const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
     for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
         uint64_t s = 0;
         for (int i = 0; i < wi; ++i) {
-            int64_t idx[3] = {0, 0, 0};
-            if (qo >= 0) idx[qo] = o;
-            if (qi >= 0) idx[qi] = i;
-            if (qf >= 0) idx[qf] = b;
-            uint64_t term = mm_i64(tensor_val(n, r, idx), m, mu);
-            if (xi) term = mm_mul(term, xi[i], m, mu);
-            s = mm_add(s, term, m);
+            for (int j = 0; j < wj; ++j) {
+                int64_t idx[3] = {0, 0, 0};
+                if (qo >= 0) idx[qo] = o;
+                if (qi >= 0) idx[qi] = i;
+                if (qj >= 0) idx[qj] = j;
+                if (qf >= 0) idx[qf] = b;
+                uint64_t term = mm_i64(tensor_val(n, r, idx), m, mu);
+                if (xi) term = mm_mul(term, xi[i], m, mu);
+                if (xj) term = mm_mul(term, xj[j], m, mu);
+                s = mm_add(s, term, m);
+            }
         }
         if (qp >= 0) {
             const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
@@ -1463,14 +1490,18 @@ static sk_status build_plan(const sk_graph *g, uint64_t mask, Plan &P) {
             tt.kind = KV;
             tt.sk.push_back(side(tt.legs[0]));
         } else {
+            // a built matrix (2 legs) or 3-D tensor (3 legs) over
+            // exactly this table's sub-plan edges (reading R8), else the merged view
             const sk_sketch *mat = nullptr;
-            if (tt.legs.size() == 2)
-                for (uint32_t mi = 0; mi < g->n_mats; ++mi) {
-                    if ((int)g->mat_table[mi] != t || !g->mat[mi]) continue;
-                    const sk_sketch *ms = g->mat[mi];
-                    if (ms->ndim == 2 && ms->edge[0] == P.eid[tt.legs[0]] && ms->edge[1] == P.eid[tt.legs[1]]) mat = ms;
-                }
-            if (mat) { tt.kind = KM; tt.sk.push_back(mat); }
+            for (uint32_t mi = 0; mi < g->n_mats; ++mi) {
+                if ((int)g->mat_table[mi] != t || !g->mat[mi]) continue;
+                const sk_sketch *ms = g->mat[mi];
+                if (ms->ndim != tt.legs.size()) continue;
+                bool same = true;
+                for (size_t q = 0; q < tt.legs.size(); ++q) same &= ms->edge[q] == P.eid[tt.legs[q]];
+                if (same) mat = ms;
+            }
+            if (mat) { tt.kind = mat->ndim == 3 ? KT : KM; tt.sk.push_back(mat); }
             else { tt.kind = KG; for (int le : tt.legs) tt.sk.push_back(side(le)); }
         }
         for (const sk_sketch *s : tt.sk) {
@@ -1479,7 +1510,7 @@ static sk_status build_plan(const sk_graph *g, uint64_t mask, Plan &P) {
             if (s->master != ref->master) return fail(SK_EMISMATCH, "estimate: sketches disagree on master seed");
         }
         for (size_t q = 0; q < tt.legs.size(); ++q) {
-            const int wn = tt.kind == KM ? (int)tt.sk[0]->w[q] : (int)tt.sk[tt.kind == KV ? 0 : q]->w[0];
+            const int wn = (tt.kind == KM || tt.kind == KT) ? (int)tt.sk[0]->w[q] : (int)tt.sk[tt.kind == KV ? 0 : q]->w[0];
             P.width[tt.legs[q]] = std::min(P.width[tt.legs[q]], wn);
         }
         P.T.push_back(tt);
@@ -1674,7 +1705,16 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
     std::vector<std::vector<const int64_t *>> data(NT);
     for (int i = 0; i < NT; ++i) {
         const TabT &t = P.T[i];
-        if (t.kind == KM) {
+        if (t.kind == KT) {
+            const sk_sketch *s = t.sk[0];
+            const int w0 = P.width[t.legs[0]], w1 = P.width[t.legs[1]], w2 = P.width[t.legs[2]];
+            if ((int)s->w[0] == w0 && (int)s->w[1] == w1 && (int)s->w[2] == w2) { data[i].push_back(s->counters); continue; }
+            void *f;
+            if ((st = dalloc(pool, size_t(d) * w0 * w1 * w2 * 8, stream, &f))) return st;
+            k_fold3<<<1184, 256, 0, stream>>>(s->counters, (int64_t *)f, d, s->w[0], s->w[1], s->w[2], w0, w1, w2);
+            count_launch();
+            data[i].push_back((const int64_t *)f);
+        } else if (t.kind == KM) {
             const sk_sketch *s = t.sk[0];
             const int w0 = P.width[t.legs[0]], w1 = P.width[t.legs[1]];
             if ((int)s->w[0] == w0 && (int)s->w[1] == w1) { data[i].push_back(s->counters); continue; }
@@ -2051,7 +2091,7 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
         Plan &P = plans[i];
         bool has_mat = false;
         for (auto &t : P.T) {
-            has_mat |= t.kind == KM;
+            has_mat |= t.kind == KM || t.kind == KT;
             for (auto *s : t.sk)
                 if (std::find(uniqs[i].begin(), uniqs[i].end(), s) == uniqs[i].end()) uniqs[i].push_back(s);
         }
@@ -2364,6 +2404,21 @@ struct CardCache {
         for (size_t i = 0; i < masks.size(); ++i) cache[masks[i]] = std::max(est[i], 0.0);
         return SK_OK;
     }
+    // one batch for the given sub-plans that are not cached yet (greedy: one batch per level,
+    // only the sub-plans the enumeration reads)
+    sk_status prefetch_masks(const std::vector<uint64_t> &want) {
+        std::vector<uint64_t> masks;
+        for (uint64_t m : want)
+            if (__builtin_popcountll(m) >= 2 && !cache.count(m) &&
+                std::find(masks.begin(), masks.end(), m) == masks.end())
+                masks.push_back(m);
+        if (masks.empty()) return SK_OK;
+        std::vector<double> est(masks.size());
+        sk_status st = estimate_batch(g, masks.data(), (uint32_t)masks.size(), est.data(), nullptr, stream);
+        if (st) return st;
+        for (size_t i = 0; i < masks.size(); ++i) cache[masks[i]] = std::max(est[i], 0.0);
+        return SK_OK;
+    }
     double card(uint64_t m) {
         ++calls;
         auto it = cache.find(m);
@@ -2396,6 +2451,12 @@ static sk_status greedy_order(CardCache &cc, std::vector<uint32_t> &C, std::vect
     }
     int bu = -1, bv = -1;
     double bc = 0;
+    {
+        std::vector<uint64_t> lvl;
+        for (uint32_t e = 0; e < g->n_edges; ++e) lvl.push_back((1ULL << g->edge_u[e]) | (1ULL << g->edge_v[e]));
+        sk_status st = cc.prefetch_masks(lvl);
+        if (st) return st;
+    }
     for (uint32_t e = 0; e < g->n_edges; ++e) {
         int u = (int)std::min(g->edge_u[e], g->edge_v[e]), v = (int)std::max(g->edge_u[e], g->edge_v[e]);
         const double c = cc.card((1ULL << u) | (1ULL << v));
@@ -2410,6 +2471,16 @@ static sk_status greedy_order(CardCache &cc, std::vector<uint32_t> &C, std::vect
     while (C.size() < n) {
         int best = -1;
         double bcard = 0;
+        {
+            std::vector<uint64_t> lvl;   // every extension of C by one neighbour, one batch
+            for (uint32_t e = 0; e < g->n_edges; ++e) {
+                const uint32_t u = g->edge_u[e], v = g->edge_v[e];
+                if (((m >> u) & 1ULL) && !((m >> v) & 1ULL)) lvl.push_back(m | (1ULL << v));
+                if (((m >> v) & 1ULL) && !((m >> u) & 1ULL)) lvl.push_back(m | (1ULL << u));
+            }
+            sk_status st = cc.prefetch_masks(lvl);
+            if (st) return st;
+        }
         for (uint32_t e = 0; e < g->n_edges; ++e) {
             const uint32_t u = g->edge_u[e], v = g->edge_v[e];
             int cand = -1;
@@ -2494,8 +2565,7 @@ extern "C" sk_status plan_greedy(const sk_graph *g, uint32_t *order, double *pre
     if (!g || !order) return fail(SK_EINVAL, "plan_greedy: NULL argument");
     sk_status st = check_graph(g);
     if (st) return st;
-    CardCache cc(g, (cudaStream_t)stream);
-    if ((st = cc.prefetch())) return st;
+    CardCache cc(g, (cudaStream_t)stream);   // greedy batches its reads level by level
     std::vector<uint32_t> C;
     std::vector<double> pre;
     if ((st = greedy_order(cc, C, pre))) return st;

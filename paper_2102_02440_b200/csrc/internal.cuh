@@ -14,9 +14,9 @@
 #define SKP_MERSENNE61 0x1FFFFFFFFFFFFFFFULL
 
 struct sk_sketch {
-    uint32_t d = 0, ndim = 0, w[2] = {0, 0};
+    uint32_t d = 0, ndim = 0, w[3] = {0, 0, 0};
     uint64_t master = 0;
-    std::string edge[2];
+    std::string edge[3];
     int device = 0;
     int64_t *counters = nullptr;
     bool owned = false;

@@ -29,10 +29,10 @@
 #include "scan_kernel.cuh"
 
 namespace skb {
-const void *scan_pick_nk1(uint32_t np, int kw, bool fast);   // scan_k1.cu
-const void *scan_pick_nk2(uint32_t np, int kw, bool fast);   // scan_k2.cu
-const void *scan_pick_nk3(uint32_t np, int kw, bool fast);   // scan_k3.cu
-const void *scan_pick_nk4(uint32_t np, int kw, bool fast);   // scan_k4.cu
+const void *scan_pick_nk1(uint32_t np, int kw, bool fast, int sub);   // scan_k1.cu
+const void *scan_pick_nk2(uint32_t np, int kw, bool fast, int sub);   // scan_k2.cu
+const void *scan_pick_nk3(uint32_t np, int kw, bool fast, int sub);   // scan_k3.cu
+const void *scan_pick_nk4(uint32_t np, int kw, bool fast, int sub);   // scan_k4.cu
 }  // namespace skb
 
 namespace {
@@ -118,12 +118,12 @@ __global__ void k_lutx_build(const uint64_t *seeds, uint32_t d, uint32_t w, uint
     }
 }
 
-static const void *pick_kernel(uint32_t nk, uint32_t np, int kw, bool fast) {
+static const void *pick_kernel(uint32_t nk, uint32_t np, int kw, bool fast, int sub) {
     switch (nk) {
-        case 1: return skb::scan_pick_nk1(np, kw, fast);
-        case 2: return skb::scan_pick_nk2(np, kw, fast);
-        case 3: return skb::scan_pick_nk3(np, kw, fast);
-        default: return skb::scan_pick_nk4(np, kw, fast);
+        case 1: return skb::scan_pick_nk1(np, kw, fast, sub);
+        case 2: return skb::scan_pick_nk2(np, kw, fast, sub);
+        case 3: return skb::scan_pick_nk3(np, kw, fast, sub);
+        default: return skb::scan_pick_nk4(np, kw, fast, sub);
     }
 }
 
@@ -190,7 +190,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     //      dimensions share d and the seed rows, i.e. the same edge), d <= 8 and d * w <= 2^15 for
     //      the widest 1-D sketch on it (the primary), whose handle caches the table
     bool fast = !(getenv("COMPASS_FAST") && strcmp(getenv("COMPASS_FAST"), "0") == 0) && P.n_keys <= 2 &&
-                c.n_preds <= 2 && c.n_rows < (1ULL << 31);
+                c.n_preds <= 2 && c.n_rows < (1ULL << 31) && !getenv("COMPASS_SCAN_KW0");
     for (uint32_t q = 0; fast && q < c.n_preds; ++q) fast = P.pred[q].kind == PR_R32;
     int fam_t[kMaxKeys] = {-1, -1, -1, -1};
     for (uint32_t k = 0; fast && k < P.n_keys; ++k) {
@@ -249,7 +249,38 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         }
     }
     P.gather = c.n_preds > 0 ? 1u : 0u;
-    P.tile_rows = kTile;
+    // predicate path: stages of up to 4 sub-tiles, ~10 KB of predicate columns per stage and
+    // group (a single int32 column gets 4 sub-tiles: the per-stage work is amortised over more
+    // rows); COMPASS_SUB overrides (experiments)
+    {
+        uint32_t pbytes = 0;
+        std::vector<uint32_t> pc;
+        for (uint32_t q = 0; q < c.n_preds; ++q)
+            if (std::find(pc.begin(), pc.end(), c.pred_col[q]) == pc.end()) { pc.push_back(c.pred_col[q]); pbytes += c.col_bytes[c.pred_col[q]]; }
+        // sub-tiles pay only where most sub-tiles hold no survivor: the expected selectivity
+        // from the columns' value-domain hints (uniform reading of each predicate's share of
+        // the domain; no hint = 1) must be below 1 %
+        double est = 1.0;
+        for (uint32_t q = 0; q < c.n_preds; ++q) {
+            const double dom = (double)c.col_domain[c.pred_col[q]];
+            if (dom <= 0) continue;
+            double f = 1.0;
+            if (c.pred_kind[q] == SK_PRED_SUBSET) f = c.pred_n[q] / dom;
+            else {
+                const int64_t hi = c.pred_kind[q] == SK_PRED_POINT ? c.pred_lo[q] : c.pred_hi[q];
+                const double lo = std::max<double>(0.0, (double)c.pred_lo[q]), h = std::min<double>(dom - 1, (double)hi);
+                f = h >= lo ? (h - lo + 1) / dom : 0.0;
+            }
+            est *= std::min(1.0, f);
+        }
+        // 4 sub-tiles (instances exist for the lookup-table path with an int32 predicate
+        // column: ~10 KB per stage and group, three stages within 3/5 of the budget), else 1
+        uint32_t sub = (P.gather && fast && pbytes == 4 && est < 0.01) ? 4u : 1u;
+        if (const char *es = getenv("COMPASS_SUB")) sub = (atoi(es) == 4 && P.gather && fast && pbytes == 4) ? 4u : 1u;
+        if (sub == 4 && 3u * kGroups * kTile * pbytes * sub > (227u * 1024u) * 3u / 5u) sub = 1;
+        P.sub = sub;
+    }
+    P.tile_rows = kTile * P.sub;
     P.n_tiles = (c.n_rows + P.tile_rows - 1) / P.tile_rows;
     P.n_full_tiles = (uint32_t)(c.n_rows / P.tile_rows);
     // staged columns: predicate columns, plus key columns when there is no predicate
@@ -495,7 +526,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     for (uint32_t q = 0; q < P.n_preds; ++q)
         if (P.pred[q].kind != PR_R32) kw = 0;
     if (getenv("COMPASS_SCAN_KW0")) kw = 0;   // experiments / parity of the generic variant
-    const void *kern = pick_kernel(P.n_keys, P.n_preds, kw, fast);
+    const void *kern = pick_kernel(P.n_keys, P.n_preds, kw, fast, (int)P.sub);
     const int threads = kThreads;
     if (getenv("COMPASS_SCAN_DEBUG"))
         fprintf(stderr, "k_scan plan: keys %u preds %u kw %d fast %d stages %u hh_log2 %u cap %u smem %u (ring %u, counters %u)\n",

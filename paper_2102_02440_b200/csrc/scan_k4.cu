@@ -6,25 +6,25 @@ namespace {
 typedef void (*ScanKernel)(const SParams);
 
 template <int NK, int NP>
-static ScanKernel pick_kw(int kw, bool fast) {
+static ScanKernel pick_kw(int kw, bool fast, int sub) {
     if constexpr (NK <= 2 && NP <= 2) {
         if (fast) {
-            if (NP == 0) return k_scan<NK, NP, 0, true>;
-            if (kw == 4) return k_scan<NK, NP, 4, true>;
+            if (NP == 0) return k_scan<NK, NP, 0, true, 1>;
+            if (kw == 4) return sub == 4 ? k_scan<NK, NP, 4, true, 4> : k_scan<NK, NP, 4, true, 1>;
         }
     }
-    if (NP == 0) return k_scan<NK, NP, 0, false>;
-    return kw == 4 ? k_scan<NK, NP, 4, false> : kw == 8 ? k_scan<NK, NP, 8, false> : k_scan<NK, NP, 0, false>;
+    if (NP == 0) return k_scan<NK, NP, 0, false, 1>;
+    return kw == 4 ? k_scan<NK, NP, 4, false, 1> : kw == 8 ? k_scan<NK, NP, 8, false, 1> : k_scan<NK, NP, 0, false, 1>;
 }
 
 template <int NK>
-static ScanKernel pick_np(uint32_t np, int kw, bool fast) {
+static ScanKernel pick_np(uint32_t np, int kw, bool fast, int sub) {
     switch (np) {
-        case 0: return pick_kw<NK, 0>(kw, fast);
-        case 1: return pick_kw<NK, 1>(kw, fast);
-        case 2: return pick_kw<NK, 2>(kw, fast);
-        case 3: return pick_kw<NK, 3>(kw, fast);
-        default: return pick_kw<NK, 4>(kw, fast);
+        case 0: return pick_kw<NK, 0>(kw, fast, sub);
+        case 1: return pick_kw<NK, 1>(kw, fast, sub);
+        case 2: return pick_kw<NK, 2>(kw, fast, sub);
+        case 3: return pick_kw<NK, 3>(kw, fast, sub);
+        default: return pick_kw<NK, 4>(kw, fast, sub);
     }
 }
 
@@ -32,5 +32,5 @@ static ScanKernel pick_np(uint32_t np, int kw, bool fast) {
 
 namespace skb {
 // the kernel as an opaque handle (launched with cudaLaunchKernel by scan.cu)
-const void *scan_pick_nk4(uint32_t np, int kw, bool fast) { return (const void *)pick_np<4>(np, kw, fast); }
+const void *scan_pick_nk4(uint32_t np, int kw, bool fast, int sub) { return (const void *)pick_np<4>(np, kw, fast, sub); }
 }  // namespace skb

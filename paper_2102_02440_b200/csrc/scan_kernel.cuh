@@ -103,7 +103,8 @@ struct SParams {
     uint32_t off_miss, off_missn;   // per-warp miss buffers (x, count) and fill counts
     uint32_t off_hstat;             // per key: heavy-hitter probes, hits, disabled flag (histogram keys)
     uint32_t off_rows;              // per-warp survivor row-offset list (128 x uint16)
-    uint32_t tile_rows;             // rows per ring stage
+    uint32_t tile_rows;             // rows per ring stage (sub * kTile)
+    uint32_t sub;                   // sub-tiles of kTile rows per stage (predicate path; 1 otherwise)
     uint32_t n_full_tiles;          // tiles with tile_rows rows (staged by TMA)
     unsigned long long *survivors;
     // lookup-table path (FAST instances): per key column, the lookup table of its hash family
@@ -707,7 +708,7 @@ __device__ __forceinline__ void drain_batch(const SParams &P, unsigned char *sme
 // KW = 0: generic (any predicate kinds, key widths read at run time); KW = 4 / 8: every
 // predicate is an int32 range and every key column is KW bytes wide (no kind or width
 // branches; survivors' keys are gathered straight from the ballots)
-template <int NK, int NP, int KW, bool FAST>
+template <int NK, int NP, int KW, bool FAST, int SUB>
 __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SParams P) {
     constexpr bool R32 = KW != 0;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -818,22 +819,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
     constexpr int NPX = (NP > 0) ? NP : 1;
     uint32_t s = 0, ph = 0;
     for (uint32_t t = gid; t < n_tiles; t += G) {
-        const uint64_t row0 = uint64_t(t) * kTile;
+        const uint64_t row0 = uint64_t(t) * (SUB * kTile);
         mbar_wait_a(full_a + s * 8, ph);
         const unsigned char *stage = smem + P.off_ring + (grp * kStages + s) * P.stage_bytes;
         const bool full_tile = t < P.n_full_tiles;   // staged by the producer
         if (NP > 0) {
+          // a stage holds SUB sub-tiles of kTile rows (one column after another); each lane
+          // evaluates 4 rows per sub-tile.  SUB > 1 only for predicates the host expects to be
+          // very selective: one ballot then skips a sub-tile without survivors.
+#pragma unroll 1
+          for (int u = 0; u < SUB; ++u) {
+            const int r0u = r0 + (int)u * kTile;
             bool m[4];
-            if (full_tile) eval_preds<NPX, R32, true>(pr, stage, row0, r0, 4, m);
+            if (full_tile) eval_preds<NPX, R32, true>(pr, stage, row0, r0u, 4, m);
             else {
-                const int64_t rem = (int64_t)P.n_rows - (int64_t)(row0 + r0);
-                eval_preds<NPX, R32, false>(pr, stage, row0, r0, rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem), m);
+                const int64_t rem = (int64_t)P.n_rows - (int64_t)(row0 + r0u);
+                eval_preds<NPX, R32, false>(pr, stage, row0, r0u, rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem), m);
+            }
+            if (SUB > 1) {
+                // the ballot orders every lane's shared reads of stage s before lane 0 releases
+                // it after the last sub-tile
+                const uint32_t any = __ballot_sync(0xffffffffu, m[0] | m[1] | m[2] | m[3]);
+                if (u + 1 == SUB && lane == 0) mbar_arrive_a(empty_a + s * 8);
+                if (!any) continue;   // nothing appended: no cp.async group for this sub-tile
             }
             // one ballot per row slot; the ballots also order every lane's shared reads of
             // stage s before lane 0 releases it
             const uint32_t B0 = __ballot_sync(0xffffffffu, m[0]), B1 = __ballot_sync(0xffffffffu, m[1]);
             const uint32_t B2 = __ballot_sync(0xffffffffu, m[2]), B3 = __ballot_sync(0xffffffffu, m[3]);
-            if (lane == 0) mbar_arrive_a(empty_a + s * 8);
+            if (SUB == 1 && lane == 0) mbar_arrive_a(empty_a + s * 8);
             const uint32_t c0 = __popc(B0), c1 = __popc(B1), c2 = __popc(B2), c3 = __popc(B3);
             const uint32_t wtot = c0 + c1 + c2 + c3;
             surv += wtot;
@@ -846,7 +860,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                     const unsigned char *kb[NK];
 #pragma unroll
                     for (int k = 0; k < NK; ++k)
-                        kb[k] = reinterpret_cast<const unsigned char *>(kptr[k]) + (row0 + r0) * (uint64_t)(KW ? KW : 8);
+                        kb[k] = reinterpret_cast<const unsigned char *>(kptr[k]) + (row0 + r0u) * (uint64_t)(KW ? KW : 8);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {   // predicated copies: no branches
                         const uint32_t dst = q_a + ((pb[j] + __popc(bj[j] & lt)) & (cap - 1)) * (NK * 8);
@@ -858,11 +872,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                 } else {
                     // generic / ring-full path: each survivor's tile offset goes to the warp's
                     // row list (same slot-major order), then the gathers run converged over the
-                    // list, in rounds that fit the ring (a tile may hold more survivors than it)
-                    if (m[0]) sts_u16(rl_a + 2 * __popc(B0 & lt), r0);
-                    if (m[1]) sts_u16(rl_a + 2 * (c0 + __popc(B1 & lt)), r0 + 1);
-                    if (m[2]) sts_u16(rl_a + 2 * (c0 + c1 + __popc(B2 & lt)), r0 + 2);
-                    if (m[3]) sts_u16(rl_a + 2 * (c0 + c1 + c2 + __popc(B3 & lt)), r0 + 3);
+                    // list, in rounds that fit the ring (a sub-tile may hold more survivors than it)
+                    if (m[0]) sts_u16(rl_a + 2 * __popc(B0 & lt), r0u);
+                    if (m[1]) sts_u16(rl_a + 2 * (c0 + __popc(B1 & lt)), r0u + 1);
+                    if (m[2]) sts_u16(rl_a + 2 * (c0 + c1 + __popc(B2 & lt)), r0u + 2);
+                    if (m[3]) sts_u16(rl_a + 2 * (c0 + c1 + c2 + __popc(B3 & lt)), r0u + 3);
                     __syncwarp();
                     for (uint32_t e0 = 0; e0 < wtot;) {
                         if (tail - head == cap || (e0 == 0 && tail - head + wtot > cap)) {
@@ -896,8 +910,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                     __syncwarp();
                 }
             }
-            // one cp.async group per tile (possibly empty): wait_group kLag then guarantees the
-            // entries appended kLag tiles ago (t3) have landed; the latency hides behind 3 tiles
+            // one cp.async group per sub-tile with survivors: wait_group kLag then guarantees
+            // the entries appended kLag such sub-tiles ago have landed
             cp_commit();
             const uint32_t ready_end = tl[kLag - 1];
 #pragma unroll
@@ -908,6 +922,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                 __syncwarp();
                 while (ready_end - head >= 32) { drain_batch<NK, FAST>(P, smem, q, kbytes, head, 32, fs); head += 32; }
             }
+          }
         } else {
             // keys are staged (no predicate): aggregate and update straight from the stage
             const int64_t rem = (int64_t)P.n_rows - (int64_t)(row0 + r0);

@@ -34,7 +34,8 @@ struct UpdPred {
 struct UpdTarget {
     int64_t *counters;
     uint32_t ndim, d, wmask0, wmask1, lw1;  // lw1 = log2(w1)
-    uint32_t key0, key1;
+    uint32_t wmask2, lw2;                   // 3-D tensors: lw2 = log2(w2)
+    uint32_t key0, key1, key2;
     int32_t smem_off;     // int32 offset of the privatised copy, -1 = global atomics
     uint32_t cells;       // w0 or w0*w1
     uint32_t seed_off;    // uint64 offset into the shared seed table
@@ -100,17 +101,23 @@ __global__ void __launch_bounds__(512) k_update_generic(const __grid_constant__ 
             const UpdTarget &tg = p.tgt[t];
             const uint64_t *s0 = sseed + tg.seed_off;
             const uint64_t x = canon61(load_val(p, tg.key0, row));
-            uint64_t y = 0;
-            const uint64_t *s1 = s0 + tg.d * 6;
-            if (tg.ndim == 2) y = canon61(load_val(p, tg.key1, row));
+            uint64_t y = 0, z = 0;
+            const uint64_t *s1 = s0 + tg.d * 6, *s2 = s1 + tg.d * 6;
+            if (tg.ndim >= 2) y = canon61(load_val(p, tg.key1, row));
+            if (tg.ndim == 3) z = canon61(load_val(p, tg.key2, row));
             for (uint32_t r = 0; r < tg.d; ++r) {
                 const uint64_t *a = s0 + r * 6;
                 uint32_t cell = (uint32_t)(hash_g61(a[4], a[5], x) & tg.wmask0);
                 int sign = xi_sign61(a, x);
-                if (tg.ndim == 2) {
+                if (tg.ndim >= 2) {
                     const uint64_t *b = s1 + r * 6;
                     cell = (cell << tg.lw1) | (uint32_t)(hash_g61(b[4], b[5], y) & tg.wmask1);
                     sign *= xi_sign61(b, y);
+                }
+                if (tg.ndim == 3) {   // cell [h0][h1][h2] += xi0 xi1 xi2
+                    const uint64_t *c = s2 + r * 6;
+                    cell = (cell << tg.lw2) | (uint32_t)(hash_g61(c[4], c[5], z) & tg.wmask2);
+                    sign *= xi_sign61(c, z);
                 }
                 const uint64_t idx = uint64_t(r) * tg.cells + cell;
                 if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + idx], sign);
@@ -219,11 +226,14 @@ extern "C" sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_co
         tg.ndim = sk->ndim;
         tg.d = sk->d;
         tg.wmask0 = sk->w[0] - 1;
-        tg.wmask1 = sk->ndim == 2 ? sk->w[1] - 1 : 0;
-        tg.lw1 = sk->ndim == 2 ? (uint32_t)__builtin_ctz(sk->w[1]) : 0;
+        tg.wmask1 = sk->ndim >= 2 ? sk->w[1] - 1 : 0;
+        tg.lw1 = sk->ndim >= 2 ? (uint32_t)__builtin_ctz(sk->w[1]) : 0;
+        tg.wmask2 = sk->ndim == 3 ? sk->w[2] - 1 : 0;
+        tg.lw2 = sk->ndim == 3 ? (uint32_t)__builtin_ctz(sk->w[2]) : 0;
         tg.key0 = targets[t].key_col[0];
-        tg.key1 = sk->ndim == 2 ? targets[t].key_col[1] : 0;
-        tg.cells = sk->ndim == 2 ? sk->w[0] * sk->w[1] : sk->w[0];
+        tg.key1 = sk->ndim >= 2 ? targets[t].key_col[1] : 0;
+        tg.key2 = sk->ndim == 3 ? targets[t].key_col[2] : 0;
+        tg.cells = (uint32_t)(sk->n_counters / sk->d);
         tg.seed_off = soff;
         soff += sk->ndim * sk->d * 6;
         p.seeds[t] = sk->seeds_dev;
@@ -244,7 +254,9 @@ extern "C" sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_co
     if (n_rows == 0) { release(); return SK_OK; }
     // optimised persistent scan (scan.cu) unless disabled or outside its envelope
     const char *mode = getenv("COMPASS_SCAN");
-    if (!(mode && strcmp(mode, "generic") == 0)) {
+    bool has3d = false;   // 3-D tensor targets are built by the grid-stride kernel
+    for (uint32_t t = 0; t < n_targets; ++t) has3d |= targets[t].sketch->ndim == 3;
+    if (!(mode && strcmp(mode, "generic") == 0) && !has3d) {
         ScanCall sc;
         sc.n_cols = n_cols;
         for (uint32_t c = 0; c < n_cols; ++c) {

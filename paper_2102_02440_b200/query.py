@@ -14,23 +14,37 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import JoinGraph, Sketch, sketch_update_filtered
+from . import JoinGraph, Sketch, sketch_update_filtered, sketch_wire_pack, sketch_wire_unpack
 
 
 def packed_layout(q):
-    """Layout of the packed int64 buffer of one query: survivors[n_tables] first, then
-    every sketch's counters (row-major [d][w0](w1)), each starting 16-byte aligned.
-    Returns (total_len, [(offset, count) per sketch])."""
+    """Layout of the packed int64 buffer of one query: survivors[n_tables] first, then every
+    sketch's counters (row-major [d][w0](w1)) grouped by table in table order, each starting
+    16-byte aligned, so one table's sketches form one contiguous slice (per-table all-reduce).
+    Returns (total_len, [(offset, count) per sketch, in q.sketches order])."""
     off = len(q.tables)
     off += off & 1
-    out = []
-    for s in q.sketches:
-        n = s.d
-        for w in s.w:
-            n *= w
-        out.append((off, n))
-        off += n + (n & 1)
+    out = [None] * len(q.sketches)
+    for t in q.tables:
+        for i, s in enumerate(q.sketches):
+            if s.table != t.name:
+                continue
+            n = s.d
+            for w in s.w:
+                n *= w
+            out[i] = (off, n)
+            off += n + (n & 1)
     return off, out
+
+
+def table_slices(q):
+    """{table: (start, end)} of each table's sketches in the packed buffer."""
+    _, lay = packed_layout(q)
+    sl = {}
+    for (o, n), s in zip(lay, q.sketches):
+        a, b = sl.get(s.table, (o, o + n))
+        sl[s.table] = (min(a, o), max(b, o + n + (n & 1)))
+    return sl
 
 
 def allreduce_packed(buffer: torch.Tensor, group=None):
@@ -41,8 +55,70 @@ def allreduce_packed(buffer: torch.Tensor, group=None):
     return buffer
 
 
+class PackedMerge:
+    """Cross-GPU merge of one query's packed buffer, when a
+    process group of > 1 rank is initialised:
+      wire="i64": the slices are summed with NCCL as int64;
+      wire="i32": each slice is packed to int32 (pack(src64, dst32): the library's
+                  sketch_wire_pack), summed, and unpacked (exact while every table has < 2^31
+                  rows, which the caller checks; lever i);
+      overlap=True: each table's slice is all-reduced asynchronously as soon as its scan is
+                  enqueued (reduce_table), on NCCL's stream, while the next table scans (lever
+                  ii); finish() then only merges the survivor counts and waits.
+    Host logic only (the packing kernels are passed in), so it runs under gloo on CPU too."""
+
+    def __init__(self, buffer, n_tables, slices, wire="i64", overlap=False, group=None, pack=None, unpack=None):
+        assert wire in ("i64", "i32")
+        self.buffer, self.slices, self.wire, self.overlap, self.group = buffer, slices, wire, overlap, group
+        self.n_s = n_tables + (n_tables & 1)
+        self.pack, self.unpack = pack, unpack
+        self.wire_buf = torch.empty(buffer.numel(), dtype=torch.int32, device=buffer.device) if wire == "i32" else None
+        self.pending = []
+
+    def world(self) -> int:
+        if dist.is_available() and dist.is_initialized():
+            return dist.get_world_size(self.group)
+        return 1
+
+    def _reduce(self, a: int, b: int, async_op: bool):
+        if self.wire == "i32":
+            w = self.wire_buf[a:b]
+            self.pack(self.buffer[a:b], w)
+            return (dist.all_reduce(w, op=dist.ReduceOp.SUM, group=self.group, async_op=async_op), a, b)
+        return (dist.all_reduce(self.buffer[a:b], op=dist.ReduceOp.SUM, group=self.group, async_op=async_op), None, None)
+
+    def _wait(self, item):
+        work, a, b = item
+        if work is not None:
+            work.wait()
+        if a is not None:
+            self.unpack(self.wire_buf[a:b], self.buffer[a:b])
+
+    def reduce_table(self, name: str):
+        """Called right after table `name`'s scan was enqueued."""
+        if self.overlap and name in self.slices and self.world() > 1:
+            a, b = self.slices[name]
+            self.pending.append(self._reduce(a, b, async_op=True))
+
+    def finish(self):
+        """Every partial merged: the pending per-table reductions (overlap) or the whole sketch
+        region, then the survivor counts (int64)."""
+        if self.world() <= 1:
+            self.pending = []
+            return
+        if self.overlap:
+            for item in self.pending:
+                self._wait(item)
+            self.pending = []
+        else:
+            self._wait(self._reduce(self.n_s, self.buffer.numel(), async_op=False))
+        dist.all_reduce(self.buffer[:self.n_s], op=dist.ReduceOp.SUM, group=self.group)
+
+
 class QueryRun:
-    def __init__(self, q, device="cuda", use_domains=True):
+    """One query's sketches in one packed int64 buffer; cross-GPU merge by PackedMerge."""
+
+    def __init__(self, q, device="cuda", use_domains=True, wire="i64", overlap=False, group=None):
         self.q = q
         self.use_domains = use_domains
         self.device = torch.device(device)
@@ -59,6 +135,10 @@ class QueryRun:
             view = self.buffer[o:o + n].view(s.d, *s.w)
             self.sketches.append(Sketch(s.d, s.w, s.edge_ids, q.master_seed, self.device, counters=view))
         self.sketch_bytes = sum(sizes) * 8
+        if wire == "i32" and any(t.n_rows >= (1 << 31) for t in q.tables):
+            wire = "i64"   # int32 partial/merged counters need < 2^31 rows per table
+        self.merge = PackedMerge(self.buffer, len(self.tnames), table_slices(q), wire, overlap, group,
+                                 pack=lambda a, b: sketch_wire_pack(a, b), unpack=lambda a, b: sketch_wire_unpack(a, b))
 
     def zero_(self):
         self.buffer.zero_()
@@ -76,14 +156,15 @@ class QueryRun:
         domains = [getattr(c, "domain", 0) or 0 for c in t.cols] if self.use_domains else None
         sketch_update_filtered(cols, n_rows, pr, targets, survivors=self.survivors[ti:ti + 1], stream=stream,
                                domains=domains)
+        self.merge.reduce_table(name)
 
     def build(self, data: dict, preds: dict, stream=None):
         for name in self.tnames:
             self.build_table(name, data[name], preds[name], stream=stream)
 
-    def allreduce(self, group=None):
-        """Cross-GPU merge of all partial sketches and survivor counts: one int64 SUM (NCCL)."""
-        allreduce_packed(self.buffer, group)
+    def allreduce(self):
+        """Cross-GPU merge of all partial sketches and survivor counts (NCCL SUM)."""
+        self.merge.finish()
 
     def sketch_of(self, table: str, edge_ids) -> Sketch:
         for s, sk in zip(self.q.sketches, self.sketches):
@@ -112,7 +193,7 @@ class QueryRun:
             edges.append((tix[u], tix[v], self.sketch_of(u, [eid]), self.sketch_of(v, [eid])))
         mats = []
         for s, sk in zip(self.q.sketches, self.sketches):
-            if len(s.edge_ids) == 2:
+            if len(s.edge_ids) >= 2:   # matrices and 3-D tensors
                 eids = [e[0] for e in self.q.edges]
                 mats.append((tix[s.table], eids.index(s.edge_ids[0]), eids.index(s.edge_ids[1]), sk))
         return JoinGraph(gnames, [surv_by[n] for n in gnames], edges, mats)

@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cfg, out_path):
+def _worker(rank, world, port, cfg, mode, out_path):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
@@ -32,7 +32,7 @@ def _worker(rank, world, port, cfg, out_path):
     import datagen
     from paper_2102_02440_b200.query import QueryRun
     ws = getattr(datagen, cfg[0])(**cfg[1])
-    run = QueryRun(ws, dev)
+    run = QueryRun(ws, dev, wire=mode[0], overlap=mode[1])
     for t in ws.tables:
         data = datagen.generate_table(ws, t.name, dev, rank=rank, world=world)
         run.build_table(t.name, data, datagen.resolve_preds(ws, t.name))
@@ -65,14 +65,16 @@ def _oracle_packed(ws):
 
 @pytest.mark.parametrize("cfg", [("c1", {}), ("c5", {"scale": 2e-4, "w": 128, "wm": 64}),
                                  ("c4", {"scale": 0.002})])
-def test_nccl_ranks_merge_equals_oracle_build(cfg, tmp_path):
+@pytest.mark.parametrize("mode", [("i64", False), ("i32", True)])
+def test_nccl_ranks_merge_equals_oracle_build(cfg, mode, tmp_path):
     world = torch.cuda.device_count()
     if world < 2:
         pytest.skip("needs >= 2 GPUs")
     world = min(world, 8)
     import datagen
     out = str(tmp_path / "merged.pt")
-    mp.start_processes(_worker, args=(world, _free_port(), cfg, out), nprocs=world, join=True, start_method="spawn")
+    mp.start_processes(_worker, args=(world, _free_port(), cfg, mode, out), nprocs=world, join=True,
+                       start_method="spawn")
     res = torch.load(out)
     ws = getattr(datagen, cfg[0])(**cfg[1])
     assert np.array_equal(res["buf"].numpy(), _oracle_packed(ws))

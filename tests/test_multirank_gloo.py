@@ -65,3 +65,38 @@ def test_two_rank_allreduce_equals_single_build(cfg, tmp_path):
     single, _ = _build_packed(ws, 0, 1)
     assert torch.equal(merged, single)
     assert int(merged[0]) > 0
+
+
+def _worker_merge(rank, world, port, cfg, mode, out_path):
+    """PackedMerge host logic (per-table asynchronous slices, int32 wire) under gloo: the
+    int32 packing kernels are replaced by plain dtype conversions on CPU."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import datagen
+    from paper_2102_02440_b200.query import PackedMerge, table_slices
+    ws = getattr(datagen, cfg[0])(**cfg[1])
+    buf, _ = _build_packed(ws, rank, world)
+    wire, overlap = mode
+    m = PackedMerge(buf, len(ws.tables), table_slices(ws), wire, overlap,
+                    pack=lambda a, b: b.copy_(a.to(torch.int32)), unpack=lambda a, b: b.copy_(a.to(torch.int64)))
+    for t in ws.tables:
+        m.reduce_table(t.name)
+    m.finish()
+    if rank == 0:
+        torch.save(buf, out_path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", [("i64", True), ("i32", False), ("i32", True)])
+def test_two_rank_per_table_and_int32_wire_merge(mode, tmp_path):
+    import datagen
+    cfg = ("c5", {"scale": 5e-5, "w": 64, "wm": 32})
+    world = 2
+    out = str(tmp_path / "merged.pt")
+    mp.start_processes(_worker_merge, args=(world, _free_port(), cfg, mode, out), nprocs=world, join=True,
+                       start_method="spawn")
+    merged = torch.load(out)
+    ws = getattr(datagen, cfg[0])(**cfg[1])
+    single, _ = _build_packed(ws, 0, 1)
+    assert torch.equal(merged, single)

@@ -207,3 +207,110 @@ def test_lookup_table_scan_equals_oracle(n, skew, preds, fast, capfd, monkeypatc
     assert gs == os_
     for t, (x, y) in enumerate(zip(g, o)):
         assert np.array_equal(x, y), f"target {t} differs"
+
+
+def test_wire_pack_unpack_roundtrip_and_overflow_flag():
+    """sketch_wire_pack / sketch_wire_unpack (int32 wire format of the merge, SURVEY §8(e) i)."""
+    rng = np.random.default_rng(1)
+    v = rng.integers(-(1 << 31), 1 << 31, 100_003, dtype=np.int64)
+    src = torch.from_numpy(v).to(_dev())
+    wire = torch.empty(v.size, dtype=torch.int32, device=_dev())
+    flag = torch.zeros(1, dtype=torch.int32, device=_dev())
+    pb.sketch_wire_pack(src, wire, flag)
+    back = torch.empty_like(src)
+    pb.sketch_wire_unpack(wire, back)
+    torch.cuda.synchronize()
+    assert torch.equal(back, src) and int(flag.item()) == 0
+    src[7] = 1 << 31                      # outside int32
+    pb.sketch_wire_pack(src, wire, flag)
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 1
+
+
+# ------------------------------------------------------------------ §8(f) 3: 3-D partitioned tensors
+T3_TARGETS = [  # (key cols, d, w, edge ids in canonical order)
+    (["x", "y", "z"], 5, [16, 8, 32], ["A.x|C.x", "B.y|C.y", "C.z|D.z"]),
+    (["x"], 5, [256], ["A.x|C.x"]),
+    (["y", "y", "x"], 3, [4, 4, 64], ["A.y|C.y", "B.y|C.y", "C.x|E.x"]),   # one column on two dims
+]
+
+
+@pytest.mark.parametrize("n", [1, 4097, 300_001])
+@pytest.mark.parametrize("preds", [[], [("p", pb.RANGE, 10, 60)]])
+def test_tensor3_build_equals_oracle(n, preds):
+    """3-D partitioned tensor sketches built by sketch_update_filtered next to a
+    1-D sketch in one scan: counters bit-exact against the oracle's tuple-by-tuple build."""
+    rng = np.random.default_rng(n)
+    cols = {"x": rng.integers(-(1 << 40), 1 << 40, n, dtype=np.int64), "y": rng.zipf(1.3, n).astype(np.int32),
+            "z": rng.integers(0, 1000, n).astype(np.int64), "p": rng.integers(0, 100, n).astype(np.int32)}
+    g, gs = _build(cols, preds, T3_TARGETS)
+    o, os_ = _oracle(cols, preds, T3_TARGETS)
+    assert gs == os_
+    for a, b in zip(g, o):
+        assert np.array_equal(a, b)
+
+
+def _t3_star_graph(rng, d, wv, wt, vmax):
+    """centre C with a 3-D tensor over (A.x|C.x, B.y|C.y, C.z|D.z) and leaf vectors; returns
+    (oracle graph, JoinGraph)."""
+    es = ["A.x|C.x", "B.y|C.y", "C.z|D.z"]
+    names = ["A", "B", "C", "D"]
+    vec = {("A", es[0]): rng.integers(-vmax, vmax + 1, (d, wv)), ("B", es[1]): rng.integers(-vmax, vmax + 1, (d, wv)),
+           ("D", es[2]): rng.integers(-vmax, vmax + 1, (d, wv))}
+    for e in es:
+        vec[("C", e)] = rng.integers(-vmax, vmax + 1, (d, wv))
+    vec = {k: v.astype(np.int64) for k, v in vec.items()}
+    ten = rng.integers(-vmax, vmax + 1, (d, wt, wt, wt)).astype(np.int64)
+    edges = [(es[0], "A", "C"), (es[1], "B", "C"), (es[2], "C", "D")]
+    surv = {t: int(rng.integers(1, 100)) for t in names}
+    og = oracle.Graph(surv, edges, vec, {("C", tuple(es)): ten})
+    sk = {k: pb.Sketch(d, [wv], [k[1]], 42, _dev(), counters=torch.from_numpy(v).to(_dev())) for k, v in vec.items()}
+    tsk = pb.Sketch(d, [wt] * 3, es, 42, _dev(), counters=torch.from_numpy(ten).to(_dev()))
+    jedges = [(names.index(u), names.index(v), sk[(u, e)], sk[(v, e)]) for e, u, v in edges]
+    jg = pb.JoinGraph(names, [surv[t] for t in names], jedges, [(2, 0, 1, tsk)])
+    return og, jg
+
+
+@pytest.mark.parametrize("vmax", [3, 1 << 20])
+def test_tensor3_estimates_equal_oracle(vmax):
+    """Sub-plans through a 3-D tensor node (the star centre with all three edges, vectors folded
+    to the tensor width) and without it (merged views): exact per row, plans identical."""
+    rng = np.random.default_rng(vmax)
+    og, jg = _t3_star_graph(rng, 5, 64, 16, vmax)
+    for s in oracle.connected_subplans(og):
+        assert jg.estimate_join_exact(s) == oracle.estimate_rows(og, s), s
+    assert tuple(jg.plan_greedy()) == tuple(oracle.plan_greedy(og))
+
+
+def test_c3t_scaled_all_subplans_and_plan():
+    """C3 with 3-D tensors for MK and CI and a matrix for T (datagen.c3t): the generalised
+    partitioned estimator on the paper's running-example shape; counters and
+    all 14 sub-plans exact, greedy plan identical."""
+    ws = datagen.c3t(scale=0.005, w=256, wt=16)
+    dev = _dev()
+    run = QueryRun(ws, dev)
+    data_h, preds = {}, {}
+    for t in ws.tables:
+        dd = datagen.generate_table(ws, t.name, dev)
+        data_h[t.name] = {k: v.cpu().numpy() for k, v in dd.items()}
+        preds[t.name] = datagen.resolve_preds(ws, t.name)
+        run.build_table(t.name, dd, preds[t.name])
+    torch.cuda.synchronize()
+    vec, mat, surv = {}, {}, {}
+    for t in ws.tables:
+        mask, cnt = oracle.filter_mask(data_h[t.name], preds[t.name])
+        surv[t.name] = cnt
+        for s in ws.sketches_of(t.name):
+            arr = oracle.build([data_h[t.name][k] for k in s.key_cols], mask, s.d, s.w, s.edge_ids, master=ws.master_seed)
+            if len(s.w) == 1:
+                vec[(t.name, s.edge_ids[0])] = arr
+            else:
+                mat[(t.name, tuple(s.edge_ids))] = arr
+    og = oracle.Graph(surv, ws.edges, vec, mat)
+    for s, sk in zip(ws.sketches, run.sketches):
+        want = vec[(s.table, s.edge_ids[0])] if len(s.w) == 1 else mat[(s.table, tuple(s.edge_ids))]
+        assert np.array_equal(sk.counters.cpu().numpy(), want), (s.table, s.edge_ids)
+    jg = run.graph()
+    for s in oracle.connected_subplans(og):
+        assert jg.estimate_join_exact(s) == oracle.estimate_rows(og, s), s
+    assert tuple(jg.plan_greedy()) == tuple(oracle.plan_greedy(og))

@@ -22,7 +22,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import datagen  # noqa: E402
-from paper_2102_02440_b200 import accuracy  # noqa: E402
+import evaluation as accuracy  # noqa: E402
 from paper_2102_02440_b200.query import QueryRun  # noqa: E402
 
 
@@ -39,7 +39,7 @@ def main():
     run.build(data, preds)
     torch.cuda.synchronize()
     tables, edges, names = accuracy.join_data(ws, data, preds)
-    subs = accuracy.acyclic_connected_subplans(names, edges)
+    subs = accuracy.connected_subplans(names, edges)
     t0 = time.perf_counter()
     truths = accuracy.exact_counts(tables, edges, names, subs)
     t_exact = time.perf_counter() - t0
@@ -50,7 +50,8 @@ def main():
         print(json.dumps({"workload": ws.name, "scale": args.scale, "subplan_tables": size, "subplans": len(ratios),
                           "ratio_median": statistics.median(fin) if fin else None,
                           "ratio_min": min(fin) if fin else None, "ratio_max": max(fin) if fin else None,
-                          "l1_normalised": l1, "exact_ms_total": round(t_exact * 1e3, 1)}))
+                          "l1_normalised": l1, "exact_ms_total": round(t_exact * 1e3, 1),
+                          "no_truth": [list(s) for s, v in truths.items() if v is None and len(s) == size]}))
 
 
 if __name__ == "__main__":
