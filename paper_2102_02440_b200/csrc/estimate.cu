@@ -26,6 +26,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <array>
 #include <deque>
 #include <map>
 #include <tuple>
@@ -192,6 +193,8 @@ struct Node {
     const uint64_t *sabs;       // merged: [d][w_qc]
     const int64_t *csorted;     // merged: constituent qc in |c|-sorted order [d][w_qc]
     const int32_t *out_perm;    // parent message written at out_perm[r][o] (the parent's sorted order), or null
+    const uint32_t *rank[3];    // merged: per other leg q, [d][w_q] = #{|c| < |v|} | #{|c| <= |v|} << 16 of
+                                // its constituent values v against the contracted leg's sorted |c| (or null)
     uint64_t *out;              // parent message [K][d][out_bm][w_p], or root partials [K][d][B][tiles]
     int out_bm;
     int B, tiles, d;
@@ -318,6 +321,49 @@ __device__ __forceinline__ int count_le(const uint64_t *S, int w, uint64_t t) {
     int lo = 0, hi = w;
     while (lo < hi) { const int mid = (lo + hi) >> 1; if (S[mid] <= t) lo = mid + 1; else hi = mid; }
     return lo;
+}
+
+// L, R and their threshold positions in the contracted leg's sorted |c|: from the per-leg rank
+// tables when present (L and R are each one constituent value, so its precomputed ranks are
+// the thresholds; two independent loads), else by binary search over S
+__device__ __forceinline__ void merged_thr(const Node &n, int r, int qc, int qf, int qo, int qi, int64_t b, int o, int i,
+                                           const uint64_t *S, int wq, bool &hasL, int64_t &L, bool &hasR, int64_t &R,
+                                           int &nless, int &nle) {
+    hasL = hasR = false;
+    L = R = 0;
+    int qL = -1, qR = -1;
+    int64_t xL = 0, xR = 0;
+    for (int q = 0; q < n.nl; ++q) {
+        if (q == qc) continue;
+        const int64_t ix = (q == qf) ? b : (q == qo ? o : i);
+        const int64_t v = n.data[q][uint64_t(r) * n.w[q] + ix];
+        if (q < qc) { if (!hasL || !(uabs(L) <= uabs(v))) { L = v; qL = q; xL = ix; } hasL = true; }
+        else { if (!hasR || !(uabs(R) <= uabs(v))) { R = v; qR = q; xR = ix; } hasR = true; }
+    }
+    if (n.rank[0] || n.rank[1] || n.rank[2]) {
+        nless = hasL ? (int)(n.rank[qL][uint64_t(r) * n.w[qL] + xL] & 0xffffu) : 0;
+        nle = hasR ? (int)(n.rank[qR][uint64_t(r) * n.w[qR] + xR] >> 16) : 0;
+    } else {
+        nless = hasL ? count_lt(S, wq, uabs(L)) : 0;
+        nle = hasR ? count_le(S, wq, uabs(R)) : 0;
+    }
+}
+
+// per row and every other leg q of a merged node: the ranks of its constituent values in the
+// contracted leg's sorted |c| (computed once per node, shared by every conditioned bucket,
+// every outer index and every modulus).  out[q] = [d][w_q]
+__global__ void k_merged_rank(const __grid_constant__ Node n, uint32_t *out0, uint32_t *out1, uint32_t *out2) {
+    const int r = blockIdx.y;
+    const int wq = n.w[n.qc];
+    const uint64_t *S = n.sabs + uint64_t(r) * wq;
+    uint32_t *outs[3] = {out0, out1, out2};
+    for (int q = 0; q < n.nl; ++q) {
+        if (q == n.qc || !outs[q]) continue;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n.w[q]; i += gridDim.x * blockDim.x) {
+            const uint64_t v = uabs(n.data[q][uint64_t(r) * n.w[q] + i]);
+            outs[q][uint64_t(r) * n.w[q] + i] = (uint32_t)count_lt(S, wq, v) | ((uint32_t)count_le(S, wq, v) << 16);
+        }
+    }
 }
 
 // sum_i x_i fold(L, c_i, R) mod m from the prefix sums P1 (x) and P2 (x*c)
@@ -680,16 +726,8 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
         for (int i = 0; i < wi; ++i) {
             bool hasL, hasR;
             int64_t L, R;
-            merged_LR(n, r, qc, qf, qo, qi, b, o, i, hasL, L, hasR, R);
             int nless, nle;
-            if (pos_pre) {
-                const uint32_t pv = pos_pre[uint64_t(r) * wo + o];
-                nless = (int)(pv & 0xffffu);
-                nle = (int)(pv >> 16);
-            } else {
-                nless = hasL ? count_lt(S, wq, uabs(L)) : 0;
-                nle = hasR ? count_le(S, wq, uabs(R)) : 0;
-            }
+            merged_thr(n, r, qc, qf, qo, qi, b, o, i, S, wq, hasL, L, hasR, R, nless, nle);
             W V = o9_value_x<W>(P1, P2, wq, hasL, L, hasR, R, nless, nle);
             if (xi2) V *= (W)xi2[i];
             sacc += V;
@@ -753,9 +791,8 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_m(const __grid_constant__ 
             if (pos_pre) { pos[o - o_begin] = pos_pre[uint64_t(r) * wo + o]; continue; }
             bool hasL, hasR;
             int64_t L, R;
-            merged_LR(n, r, qc, qf, qo, qi, b, o, 0, hasL, L, hasR, R);
-            const int nless = hasL ? count_lt(S, wq, uabs(L)) : 0;
-            const int nle = hasR ? count_le(S, wq, uabs(R)) : 0;
+            int nless, nle;
+            merged_thr(n, r, qc, qf, qo, qi, b, o, 0, S, wq, hasL, L, hasR, R, nless, nle);
             pos[o - o_begin] = (uint32_t)nless | ((uint32_t)nle << 16);
         }
     }
@@ -810,15 +847,14 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_m(const __grid_constant__ 
             for (int i = 0; i < wi; ++i) {
                 bool hasL, hasR;
                 int64_t L, R;
-                merged_LR(n, r, qc, qf, qo, qi, b, o, i, hasL, L, hasR, R);
                 int nless, nle;
                 if (cache_pos) {
+                    merged_LR(n, r, qc, qf, qo, qi, b, o, i, hasL, L, hasR, R);
                     const uint32_t pv = pos[o - o_begin];
                     nless = (int)(pv & 0xffffu);
                     nle = (int)(pv >> 16);
                 } else {
-                    nless = hasL ? count_lt(S, wq, uabs(L)) : 0;
-                    nle = hasR ? count_le(S, wq, uabs(R)) : 0;
+                    merged_thr(n, r, qc, qf, qo, qi, b, o, i, S, wq, hasL, L, hasR, R, nless, nle);
                 }
                 uint64_t V = o9_value(P1, P2, wq, hasL, L, hasR, R, nless, nle, m, mu);
                 if (xi2) V = mm_mul(V, xi2[i], m, mu);
@@ -1760,6 +1796,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
     std::vector<const int32_t *> ord_of(NT, nullptr);
     std::vector<const uint64_t *> sabs_of(NT, nullptr);
     std::vector<const int64_t *> csorted_of(NT, nullptr);
+    std::vector<std::array<const uint32_t *, 3>> rank_of(NT, {nullptr, nullptr, nullptr});
     std::vector<const int32_t *> perm_of_edge(E, nullptr);   // messages delivered in the parent's sorted order
     for (int i = 0; i < NT; ++i) {
         const TabT &t = P.T[i];
@@ -1788,6 +1825,27 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
         qc_of[i] = qc;
         ord_of[i] = (const int32_t *)o;
         sabs_of[i] = (const uint64_t *)sa;
+        if (absb || getenv("COMPASS_EST_NO_RANK")) continue;
+        // ranks of every other leg's constituent values in this sorted order (thresholds of the
+        // O9 identity by lookup instead of a binary search per output)
+        Node rn;
+        memset(&rn, 0, sizeof(rn));
+        rn.nl = (int)t.legs.size();
+        rn.qc = qc;
+        rn.sabs = sabs_of[i];
+        uint32_t *ro[3] = {nullptr, nullptr, nullptr};
+        int wmax = 1;
+        for (int q = 0; q < rn.nl; ++q) {
+            rn.w[q] = P.width[t.legs[q]];
+            rn.data[q] = data[i][q];
+            if (q == qc) continue;
+            void *rb;
+            if ((st = dalloc(pool, size_t(d) * rn.w[q] * 4, stream, &rb))) return st;
+            ro[q] = (uint32_t *)rb;
+            wmax = std::max(wmax, rn.w[q]);
+        }
+        k_merged_rank<<<dim3((wmax + 255) / 256, d), 256, 0, stream>>>(rn, ro[0], ro[1], ro[2]); count_launch();
+        for (int q = 0; q < 3; ++q) rank_of[i][q] = ro[q];
     }
     // ---- chunking of the conditioned bucket
     const int64_t Btot = P.cond >= 0 ? P.width[P.cond] : 1;
@@ -1857,6 +1915,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                     n.ord = ord_of[i];
                     n.sabs = sabs_of[i];
                     n.csorted = csorted_of[i];
+                    for (int q = 0; q < 3; ++q) n.rank[q] = rank_of[i][q];
                     int wo_max = 1;
                     for (int q = 0; q < n.nl; ++q)
                         if (q != n.qc && n.role[q] != RFIXED) wo_max = std::max(wo_max, n.w[q]);
@@ -1878,6 +1937,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                     n.ord = ord_of[i];
                     n.sabs = sabs_of[i];
                     n.csorted = csorted_of[i];
+                    for (int q = 0; q < 3; ++q) n.rank[q] = rank_of[i][q];
                     // outer leg: the parent, else the first other child (as in the kernel)
                     int wo_max = 1, qo = -1, nother = 0;
                     bool fixed = false;
@@ -1951,6 +2011,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                 n.ord = ord_of[i];
                 n.sabs = sabs_of[i];
                 n.csorted = csorted_of[i];
+                for (int q = 0; q < 3; ++q) n.rank[q] = rank_of[i][q];
                 int wo_max = 1, qo = -1, nother = 0;
                 bool fixed = false;
                 for (int q = 0; q < n.nl; ++q) {
