@@ -4,10 +4,12 @@
 
 A *step* is one pass of the whole hot path over the workload's tables, inputs
 resident in HBM: zero the packed sketch buffer, one fused filter+hash+update
-scan per table (sketch_update_filtered), the cross-GPU int64 all-reduce (N>1),
-the composition estimates of every connected sub-plan (estimate_join) and the
-greedy plan (plan_greedy).  value = rows scanned by all ranks / step time
-(max over ranks, CUDA events).
+scan per table (sketch_update_filtered), the cross-GPU merge (N>1: per-table int32
+all-reduces overlapped with the next scan), the composition estimates of the
+connected sub-plans the planner reads (estimate_join) and the greedy plan
+(plan_greedy).  value = rows scanned by all ranks / t_build, t_build = first kernel
+of the step -> final int64 sketches resident after the merge, max
+over ranks, CUDA events; the full step time is ms_per_step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C4] [--impl reference]
 

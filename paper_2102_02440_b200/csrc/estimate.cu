@@ -671,16 +671,22 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
     const int wi = qi >= 0 ? n.w[qi] : 1;
     const int per_tile = (wo + n.tiles - 1) / n.tiles;
     const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
-    // --- prefix sums over the |c|-sorted order: contiguous chunk per thread, then a scan of
-    //     the per-thread totals by warp 0
+    // --- prefix sums over the |c|-sorted order: the terms x and x*c are staged in P1 / P2
+    //     with coalesced loads (the message is read once), then each thread scans a contiguous
+    //     chunk in place and warp 0 scans the per-thread totals
     const i128 *x = msg_row_x(n, qc, r, bb);   // delivered in the |c|-sorted order
+    for (int s = threadIdx.x; s < wq; s += MX_T) {
+        const W xv = (W)x[s];
+        P1[s] = xv;
+        P2[s] = xv * (W)cs[s];
+    }
+    __syncthreads();
     const int chunk = (wq + MX_T - 1) / MX_T;
     const int s0 = threadIdx.x * chunk, s1 = min(wq, s0 + chunk);
     W l1 = 0, l2 = 0;
     for (int s = s0; s < s1; ++s) {
-        const W xv = (W)x[s];
-        l1 += xv;
-        l2 += xv * (W)cs[s];
+        l1 += P1[s];
+        l2 += P2[s];
     }
     tot1[threadIdx.x] = l1;
     tot2[threadIdx.x] = l2;
@@ -708,12 +714,12 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
     __syncthreads();
     {
         W c1 = tot1[threadIdx.x], c2 = tot2[threadIdx.x];
-        for (int s = s0; s < s1; ++s) {
+        for (int s = s0; s < s1; ++s) {   // exclusive prefix in place
+            const W v1 = P1[s], v2 = P2[s];
             P1[s] = c1;
             P2[s] = c2;
-            const W xv = (W)x[s];
-            c1 += xv;
-            c2 += xv * (W)cs[s];
+            c1 += v1;
+            c2 += v2;
         }
     }
     __syncthreads();
@@ -1714,7 +1720,9 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                               DevPool &pool, uint64_t *acc, unsigned long long *l1, cudaStream_t stream,
                               int ring = 0, std::map<std::pair<const void *, int>, uint32_t *> *rescache = nullptr,
                               const Mods *resmods = nullptr, const std::vector<char> *narrow = nullptr,
-                              std::map<std::tuple<const void *, int, int>, const int64_t *> *foldcache = nullptr) {
+                              std::map<std::tuple<const void *, int, int>, const int64_t *> *foldcache = nullptr,
+                              std::map<std::pair<const void *, int>, std::array<void *, 4>> *sortcache = nullptr,
+                              std::map<std::vector<const void *>, std::array<const uint32_t *, 3>> *rankcache = nullptr) {
     // ring: 0 = CRT residues, 1 = exact int128, 2 = fp64 absolute-value bound (no matrices)
     const bool exact = ring == 1, absb = ring == 2;
     const int E = (int)P.edges.size();
@@ -1812,13 +1820,20 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
         const int w = P.width[t.legs[qc]];
         if (w > 8192) return fail(SK_EOVERFLOW, "estimate: merged contraction supports widths <= 8192");
         void *o, *sa, *rk, *csd;
-        if ((st = dalloc(pool, size_t(d) * w * 4, stream, &o))) return st;
-        if ((st = dalloc(pool, size_t(d) * w * 8, stream, &sa))) return st;
-        if ((st = dalloc(pool, size_t(d) * w * 4, stream, &rk))) return st;
-        if ((st = dalloc(pool, size_t(d) * w * 8, stream, &csd))) return st;
-        const size_t sm = size_t(w) * 12;
-        SKB_CUDA(cudaFuncSetAttribute(k_sort_abs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k_sort_abs<<<d, 512, sm, stream>>>(data[i][qc], w, (int32_t *)o, (uint64_t *)sa, (int32_t *)rk, (int64_t *)csd); count_launch();
+        const auto skey = std::make_pair((const void *)data[i][qc], w);
+        if (sortcache && sortcache->count(skey)) {   // this constituent was sorted for an earlier plan of the batch
+            const auto &c = (*sortcache)[skey];
+            o = c[0]; sa = c[1]; rk = c[2]; csd = c[3];
+        } else {
+            if ((st = dalloc(pool, size_t(d) * w * 4, stream, &o))) return st;
+            if ((st = dalloc(pool, size_t(d) * w * 8, stream, &sa))) return st;
+            if ((st = dalloc(pool, size_t(d) * w * 4, stream, &rk))) return st;
+            if ((st = dalloc(pool, size_t(d) * w * 8, stream, &csd))) return st;
+            const size_t sm = size_t(w) * 12;
+            SKB_CUDA(cudaFuncSetAttribute(k_sort_abs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            k_sort_abs<<<d, 512, sm, stream>>>(data[i][qc], w, (int32_t *)o, (uint64_t *)sa, (int32_t *)rk, (int64_t *)csd); count_launch();
+            if (sortcache) (*sortcache)[skey] = {o, sa, rk, csd};
+        }
         perm_of_edge[t.legs[qc]] = (const int32_t *)rk;
         csorted_of[i] = (const int64_t *)csd;
         SKB_CUDA_CHECK("estimate launch 3");
@@ -1835,9 +1850,19 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
         rn.sabs = sabs_of[i];
         uint32_t *ro[3] = {nullptr, nullptr, nullptr};
         int wmax = 1;
+        std::vector<const void *> rkey{(const void *)(intptr_t)qc};
         for (int q = 0; q < rn.nl; ++q) {
             rn.w[q] = P.width[t.legs[q]];
             rn.data[q] = data[i][q];
+            rkey.push_back(data[i][q]);
+            rkey.push_back((const void *)(intptr_t)rn.w[q]);
+        }
+        if (sortcache && rankcache && rankcache->count(rkey)) {   // same merged view, same contracted leg
+            const auto &c = (*rankcache)[rkey];
+            for (int q = 0; q < 3; ++q) rank_of[i][q] = c[q];
+            continue;
+        }
+        for (int q = 0; q < rn.nl; ++q) {
             if (q == qc) continue;
             void *rb;
             if ((st = dalloc(pool, size_t(d) * rn.w[q] * 4, stream, &rb))) return st;
@@ -1846,6 +1871,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
         }
         k_merged_rank<<<dim3((wmax + 255) / 256, d), 256, 0, stream>>>(rn, ro[0], ro[1], ro[2]); count_launch();
         for (int q = 0; q < 3; ++q) rank_of[i][q] = ro[q];
+        if (sortcache && rankcache) (*rankcache)[rkey] = {ro[0], ro[1], ro[2]};
     }
     // ---- chunking of the conditioned bucket
     const int64_t Btot = P.cond >= 0 ? P.width[P.cond] : 1;
@@ -2272,9 +2298,11 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
         SKB_CUDA_CHECK("estimate launch l1");
     }
     std::map<std::tuple<const void *, int, int>, const int64_t *> foldcache;
+    std::map<std::pair<const void *, int>, std::array<void *, 4>> sortcache;
+    std::map<std::vector<const void *>, std::array<const uint32_t *, 3>> rankcache;
     for (size_t i = 0; i < n; ++i)
         if ((st = enqueue_plan(plans[i], mds[i], uniqs[i], pool, res + off_acc[i], nullptr, stream, exact[i] ? 1 : 0,
-                               &rescache, &kmax_mods, exact[i] ? &narrow[i] : nullptr, &foldcache)))
+                               &rescache, &kmax_mods, exact[i] ? &narrow[i] : nullptr, &foldcache, &sortcache, &rankcache)))
             return st;
     std::vector<uint64_t> host(words), hl1(guniq.size() * dmax);
     SKB_CUDA(cudaMemcpyAsync(host.data(), res, words * 8, cudaMemcpyDeviceToHost, stream));
