@@ -727,6 +727,44 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
     const i128 *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row_x(n, qo, r, bb) : nullptr;
     const i128 *xi2 = qi >= 0 ? msg_row_x(n, qi, r, bb) : nullptr;
     W acc = 0;
+    // no inner leg and rank tables present (the common case): the fixed leg's value and rank
+    // are loop invariants, only the outer leg's constituent varies per output
+    const bool ranked = n.rank[0] || n.rank[1] || n.rank[2];
+    if (qi < 0 && ranked) {
+        const bool hasF = qf >= 0, fL = hasF && qf < qc, oL = qo >= 0 && qo < qc;
+        const int64_t vf = hasF ? n.data[qf][uint64_t(r) * n.w[qf] + b] : 0;
+        const uint32_t rf = hasF ? n.rank[qf][uint64_t(r) * n.w[qf] + b] : 0u;
+        const int64_t *dO = qo >= 0 ? n.data[qo] + uint64_t(r) * wo : nullptr;
+        const uint32_t *rO = qo >= 0 ? n.rank[qo] + uint64_t(r) * wo : nullptr;
+        const bool f_first = hasF && qo >= 0 && qf < qo;   // fold order when both sit on one side
+        for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
+            int64_t vo = 0;
+            uint32_t ro = 0;
+            if (qo >= 0) { vo = dO[o]; ro = rO[o]; }
+            bool hasL = false, hasR = false;
+            int64_t L = 0, R = 0;
+            uint32_t rL = 0, rR = 0;
+            if (hasF && qo >= 0 && fL == oL) {   // both on one side: left fold in leg order
+                const int64_t a = f_first ? vf : vo, c = f_first ? vo : vf;
+                const uint32_t ra = f_first ? rf : ro, rc = f_first ? ro : rf;
+                const bool keep = uabs(a) <= uabs(c);
+                if (fL) { hasL = true; L = keep ? a : c; rL = keep ? ra : rc; }
+                else { hasR = true; R = keep ? a : c; rR = keep ? ra : rc; }
+            } else {
+                if (hasF) { if (fL) { hasL = true; L = vf; rL = rf; } else { hasR = true; R = vf; rR = rf; } }
+                if (qo >= 0) { if (oL) { hasL = true; L = vo; rL = ro; } else { hasR = true; R = vo; rR = ro; } }
+            }
+            const int nless = hasL ? (int)(rL & 0xffffu) : 0, nle = hasR ? (int)(rR >> 16) : 0;
+            W sacc = o9_value_x<W>(P1, P2, wq, hasL, L, hasR, R, nless, nle);
+            if (qp >= 0) {
+                const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
+                reinterpret_cast<i128 *>(n.out)[(uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = (i128)sacc;
+            } else {
+                if (xo) sacc *= (W)xo[o];
+                acc += sacc;
+            }
+        }
+    } else
     for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
         W sacc = 0;
         for (int i = 0; i < wi; ++i) {

@@ -122,6 +122,16 @@ struct SParams {
     uint32_t pair_log2, pair_t;
 };
 
+// Debug builds (-DCOMPASS_CHECKS, tools/build_variant.sh): device-side bounds checks on ring
+// positions, staged-tile offsets and lookup-table counter indices; a violated check traps
+// (a CUDA error at the next synchronisation), standing in for compute-sanitizer, which the
+// gpurun pool does not allow.
+#ifdef COMPASS_CHECKS
+#define SCAN_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define SCAN_CHECK(cond) do { } while (0)
+#endif
+
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -522,6 +532,7 @@ __device__ __forceinline__ void process_fast(const SParams &P, unsigned char *sm
             for (int r = 0; r < 8; ++r)
                 if (r < (int)tp.d) {
                     const uint32_t f = lut_fld(q, r);
+                    SCAN_CHECK((f >> 1) < tp.d * tp.cells && (f >> 1) / tp.cells == (uint32_t)r);
                     atomicAdd(base + (f >> 1), (f & 1u) ? -cnt : cnt);
                 }
         } else {
@@ -597,6 +608,7 @@ __device__ __forceinline__ void eval_preds(const PR (&pr)[NP], const unsigned ch
     for (int q = 0; q < NP; ++q) {
         if (R32 || pr[q].kind == PR_R32) {
             int4 v;
+            SCAN_CHECK(!FULL || (pr[q].soff >= 0 && (r0 & 3) == 0));
             if (FULL) v = *reinterpret_cast<const int4 *>(stage + pr[q].soff + r0 * 4);
             else {
                 const int *g = reinterpret_cast<const int *>(pr[q].p) + row0 + r0;
@@ -684,6 +696,7 @@ __device__ __forceinline__ void drain_batch(const SParams &P, unsigned char *sme
 #endif
     const int lane = threadIdx.x & 31;
     const bool valid = (uint32_t)lane < n;
+    SCAN_CHECK(n <= 32);
     if (FAST) {   // int32 keys: load this batch's table entries, then apply the pending batch
         int32_t xr[NK];
         const unsigned char *e = q + ((head + lane) & (P.cap - 1)) * (NK * 8);
@@ -762,6 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                 const uint64_t row0 = t * P.tile_rows;
                 const bool fulltile = row0 + P.tile_rows <= P.n_rows;
                 if (fulltile && P.stage_bytes) {
+                    SCAN_CHECK(P.off_ring + ((grp + 1) * kStages) * P.stage_bytes <= P.off_kbuf);
                     mbar_arrive_tx(&full[s], P.stage_bytes);
                     unsigned char *stage = smem + P.off_ring + (grp * kStages + s) * P.stage_bytes;
                     for (uint32_t c = 0; c < P.n_cols; ++c) {
@@ -910,6 +924,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                     __syncwarp();
                 }
             }
+            SCAN_CHECK(tail - head <= cap);
             // one cp.async group per sub-tile with survivors: wait_group kLag then guarantees
             // the entries appended kLag such sub-tiles ago have landed
             cp_commit();
