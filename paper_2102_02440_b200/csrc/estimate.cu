@@ -390,7 +390,8 @@ __device__ __forceinline__ uint64_t o9_value(const uint64_t *P1, const uint64_t 
 // products (< 2^52) accumulate exactly in 64 bits (IMAD.WIDE.U32) for 4096 steps between
 // Barrett reductions.  Tile 32 b x 64 j x 32 i, 8 outputs per thread.
 constexpr int GBM = 32, GBN = 64, GBK = 32;
-__global__ void __launch_bounds__(256) k_node_mat_gemm(const __grid_constant__ Node n, const __grid_constant__ Mods md, int qc) {
+__global__ void __launch_bounds__(256) k_node_mat_gemm(const __grid_constant__ Node n, const __grid_constant__ Mods md, int qc,
+                                                       const uint32_t *Rc) {
     __shared__ uint32_t Xs[GBK][GBM + 1];
     __shared__ uint32_t Ms[GBK][GBN + 4];
     const int k = blockIdx.x / n.d, r = blockIdx.x % n.d;
@@ -410,6 +411,14 @@ __global__ void __launch_bounds__(256) k_node_mat_gemm(const __grid_constant__ N
             const int b = b0 + bl, i = i0 + ii;
             Xs[ii][bl] = (b < n.B && i < wi) ? (uint32_t)msg_row(n, qc, k, r, b, 0)[i] : 0u;
         }
+        if (Rc) {   // residues of this matrix in this orientation, precomputed once per batch
+            const uint32_t *R = Rc + (uint64_t(k) * n.d + r) * (uint64_t(wi) * wj);
+            for (int e = tid; e < GBK * GBN; e += 256) {
+                const int jj = e % GBN, ii = e / GBN;
+                const int i = i0 + ii, j = j0 + jj;
+                Ms[ii][jj] = (i < wi && j < wj) ? __ldg(R + uint64_t(i) * wj + j) : 0u;
+            }
+        } else
         for (int e = tid; e < GBK * GBN; e += 256) {
             int ii, jj;
             if (qc == 0) { jj = e % GBN; ii = e / GBN; } else { ii = e % GBK; jj = e / GBK; }
@@ -604,6 +613,12 @@ __device__ __forceinline__ i128 shfl_up_w(i128 v, int o) { return shfl_up_i128(v
 __device__ __forceinline__ int64_t shfl_up_w(int64_t v, int o) { return __shfl_up_sync(0xffffffffu, (long long)v, o); }
 __device__ __forceinline__ i128 shfl_xor_w(i128 v, int o) { return shfl_xor_i128(v, o); }
 __device__ __forceinline__ int64_t shfl_xor_w(int64_t v, int o) { return __shfl_xor_sync(0xffffffffu, (long long)v, o); }
+__device__ __forceinline__ int64_t shfl_idx_w(int64_t v, int l) { return __shfl_sync(0xffffffffu, (long long)v, l); }
+__device__ __forceinline__ i128 shfl_idx_w(i128 v, int l) {
+    const uint64_t lo = __shfl_sync(0xffffffffu, (unsigned long long)(uint64_t)v, l);
+    const uint64_t hi = __shfl_sync(0xffffffffu, (unsigned long long)(uint64_t)((unsigned __int128)v >> 64), l);
+    return (i128)(((unsigned __int128)hi << 64) | lo);
+}
 template <typename W>
 __device__ __forceinline__ W block_sum_w(W v, W *red) {
     for (int o = 16; o > 0; o >>= 1) v += shfl_xor_w(v, o);
@@ -672,8 +687,9 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
     const int per_tile = (wo + n.tiles - 1) / n.tiles;
     const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
     // --- prefix sums over the |c|-sorted order: the terms x and x*c are staged in P1 / P2
-    //     with coalesced loads (the message is read once), then each thread scans a contiguous
-    //     chunk in place and warp 0 scans the per-thread totals
+    //     with coalesced loads (the message is read once); each warp then scans its segment in
+    //     lane-consecutive rounds of 32 (warp shuffles, no bank conflicts), warp 0 scans the
+    //     warp totals, and each warp adds its offset
     const i128 *x = msg_row_x(n, qc, r, bb);   // delivered in the |c|-sorted order
     for (int s = threadIdx.x; s < wq; s += MX_T) {
         const W xv = (W)x[s];
@@ -681,46 +697,42 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
         P2[s] = xv * (W)cs[s];
     }
     __syncthreads();
-    const int chunk = (wq + MX_T - 1) / MX_T;
-    const int s0 = threadIdx.x * chunk, s1 = min(wq, s0 + chunk);
-    W l1 = 0, l2 = 0;
-    for (int s = s0; s < s1; ++s) {
-        l1 += P1[s];
-        l2 += P2[s];
-    }
-    tot1[threadIdx.x] = l1;
-    tot2[threadIdx.x] = l2;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        constexpr int per = MX_T / 32;
-        const int lane = threadIdx.x;
-        W a1 = 0, a2 = 0;
-        for (int t = 0; t < per; ++t) { a1 += tot1[lane * per + t]; a2 += tot2[lane * per + t]; }
-        W i1 = a1, i2 = a2;   // inclusive warp scan
-        for (int o = 1; o < 32; o <<= 1) {
-            const W u1 = shfl_up_w(i1, o), u2 = shfl_up_w(i2, o);
-            if (lane >= o) { i1 += u1; i2 += u2; }
-        }
-        W e1 = i1 - a1, e2 = i2 - a2;   // exclusive
-        for (int t = 0; t < per; ++t) {
-            const W v1 = tot1[lane * per + t], v2 = tot2[lane * per + t];
-            tot1[lane * per + t] = e1;
-            tot2[lane * per + t] = e2;
-            e1 += v1;
-            e2 += v2;
-        }
-        if (lane == 31) { P1[wq] = i1; P2[wq] = i2; }
-    }
-    __syncthreads();
     {
-        W c1 = tot1[threadIdx.x], c2 = tot2[threadIdx.x];
-        for (int s = s0; s < s1; ++s) {   // exclusive prefix in place
-            const W v1 = P1[s], v2 = P2[s];
-            P1[s] = c1;
-            P2[s] = c2;
-            c1 += v1;
-            c2 += v2;
+        constexpr int NW = MX_T / 32;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        const int seg = ((wq + NW - 1) / NW + 31) & ~31;
+        const int a = wid * seg, e = min(wq, a + seg);
+        W c1 = 0, c2 = 0;   // running totals of this warp's segment (warp-uniform)
+        for (int base = a; base < e; base += 32) {
+            const int s = base + lane;
+            const W v1 = s < e ? P1[s] : (W)0, v2 = s < e ? P2[s] : (W)0;
+            W i1 = v1, i2 = v2;
+            for (int o = 1; o < 32; o <<= 1) {
+                const W u1 = shfl_up_w(i1, o), u2 = shfl_up_w(i2, o);
+                if (lane >= o) { i1 += u1; i2 += u2; }
+            }
+            if (s < e) { P1[s] = c1 + i1 - v1; P2[s] = c2 + i2 - v2; }   // exclusive within the segment
+            c1 += shfl_idx_w(i1, 31);
+            c2 += shfl_idx_w(i2, 31);
         }
+        if (lane == 0) { tot1[wid] = c1; tot2[wid] = c2; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            W e1 = 0, e2 = 0;
+            for (int w = 0; w < NW; ++w) {
+                const W t1 = tot1[w], t2 = tot2[w];
+                tot1[w] = e1;
+                tot2[w] = e2;
+                e1 += t1;
+                e2 += t2;
+            }
+            P1[wq] = e1;
+            P2[wq] = e2;
+        }
+        __syncthreads();
+        const W o1 = tot1[wid], o2 = tot2[wid];
+        if (wid > 0)
+            for (int s = a + lane; s < e; s += 32) { P1[s] += o1; P2[s] += o2; }
     }
     __syncthreads();
     // --- outputs
@@ -2069,7 +2081,23 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
             } else if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB >= 16) {
                 const int nbt = (nB + GBM - 1) / GBM;
                 const int njt = (P.width[pe] + GBN - 1) / GBN;
-                k_node_mat_gemm<<<dim3(K * d, nbt * njt), 256, 0, stream>>>(n, md, qchild); count_launch();
+                const uint32_t *Rc = nullptr;   // residues shared with the chain mat-vecs of the batch
+                if (rescache && resmods && md.K <= resmods->K) {
+                    const auto key = std::make_pair((const void *)n.data[0], qchild);
+                    auto it = rescache->find(key);
+                    if (it == rescache->end()) {
+                        void *rb;
+                        const size_t cells = size_t(n.w[0]) * n.w[1];
+                        if ((st = dalloc(pool, size_t(resmods->K) * d * cells * 4, stream, &rb))) return st;
+                        k_mat_residues<<<1184, 256, 0, stream>>>(n.data[0], d, n.w[0], n.w[1], qchild, *resmods, (uint32_t *)rb);
+                        count_launch();
+                        (*rescache)[key] = (uint32_t *)rb;
+                        Rc = (uint32_t *)rb;
+                    } else {
+                        Rc = it->second;
+                    }
+                }
+                k_node_mat_gemm<<<dim3(K * d, nbt * njt), 256, 0, stream>>>(n, md, qchild, Rc); count_launch();
             } else if (t.kind == KG && qc_of[i] >= 0) {
                 n.qc = qc_of[i];
                 n.ord = ord_of[i];
