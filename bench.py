@@ -283,7 +283,7 @@ def _max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
-def _oracle_pass(ws, cols_by_table, preds_by_table, threads: int) -> float:
+def _oracle_pass(ws, cols_by_table, preds_by_table, threads: int, out: dict | None = None) -> float:
     """One timed oracle pass (O1 filter + O2/O3 builds, SURVEY.md §8(d) "Oracle timing
     beside it") over the sampled rows.  threads > 1: the rows of every table are split into
     `threads` contiguous ranges, each thread filters and builds private sketches for its range
@@ -308,6 +308,8 @@ def _oracle_pass(ws, cols_by_table, preds_by_table, threads: int) -> float:
             for p_ in parts[1:]:
                 for m, q in zip(merged, p_):
                     m += q
+            if out is not None:
+                out[t.name] = merged
     return time.perf_counter() - t0
 
 
