@@ -214,6 +214,14 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
             }
         fam_t[k] = best;
     }
+    if (fast) {   // matrix targets of the lookup-table path (both dims on the two key columns)
+        P.n_mat = 0;
+        for (uint32_t t = 0; t < c.n_targets; ++t)
+            if (c.tgt_ndim[t] == 2) {
+                if (P.n_mat == 2 || c.tgt_key[t][0] == c.tgt_key[t][1]) fast = false;
+                else P.mat_t[P.n_mat++] = t;
+            }
+    }
     if (fast) {
         int dev_f = 0, sms_f = 148;
         cudaGetDevice(&dev_f);

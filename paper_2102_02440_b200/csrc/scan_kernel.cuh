@@ -113,6 +113,7 @@ struct SParams {
     // sketch (the widest 1-D sketch of the family) and the other 1-D sketches on the column
     const uint4 *klut[kMaxKeys];
     uint64_t klut_dom[kMaxKeys];
+    uint32_t n_mat, mat_t[2];        // matrix targets of the lookup-table path
     uint32_t kprim[kMaxKeys];
     uint32_t kothers[kMaxKeys];
     // skewed key pairs of one L2-backed matrix (target pair_t): a two-choice table of
@@ -490,6 +491,22 @@ __device__ __forceinline__ void fast_load(const SParams &P, bool valid, const in
     }
 }
 
+// out-of-domain keys on the lookup-table path (rare): hashed by the polynomials (inlined: an
+// out-of-line call made the kernel spill around it)
+__device__ __forceinline__ void fast_slow_1d(const SParams &P, unsigned char *smem, uint32_t k, int32_t xr, int cnt) {
+    int32_t *sc = reinterpret_cast<int32_t *>(smem + P.off_sc);
+    const uint64_t *seeds = reinterpret_cast<const uint64_t *>(smem + P.off_seed);
+    for (uint32_t tm = P.key[k].priv1d | P.key[k].glob1d; tm; tm &= tm - 1) {
+        const STarget &tg = P.tgt[__ffs(tm) - 1];
+        update_1d(tg, seeds + tg.seed_off, sc, canon61(xr), cnt);
+    }
+}
+__device__ __forceinline__ void fast_slow_2d(const SParams &P, unsigned char *smem, uint32_t t, int32_t xa, int32_t xb, int cnt) {
+    const STarget &tg = P.tgt[t];
+    update_2d(tg, reinterpret_cast<const uint64_t *>(smem + P.off_seed) + tg.seed_off,
+              reinterpret_cast<int32_t *>(smem + P.off_sc), canon61(xa), canon61(xb), cnt);
+}
+
 // apply one pending batch (all 32 lanes converged).  Key aggregation (match_any on the raw
 // int32 keys, exact by linearity) is adaptive per warp: sampled once every 32
 // batches and kept while at least 1/8 of the batch's lanes repeat a key (skewed columns).
@@ -518,10 +535,7 @@ __device__ __forceinline__ void process_fast(const SParams &P, unsigned char *sm
         if (!P.key[k].has1d || lane != __ffs(grp[k]) - 1) continue;
         const int cnt = __popc(grp[k]);
         if ((uint32_t)b.x[k] >= P.klut_dom[k]) {   // outside the hinted domain: hash
-            for (uint32_t tm = P.key[k].priv1d | P.key[k].glob1d; tm; tm &= tm - 1) {
-                const STarget &tg = P.tgt[__ffs(tm) - 1];
-                update_1d(tg, seeds + tg.seed_off, sc, canon61(b.x[k]), cnt);
-            }
+            fast_slow_1d(P, smem, (uint32_t)k, b.x[k], cnt);
             continue;
         }
         const uint4 q = b.e[k];
@@ -556,32 +570,44 @@ __device__ __forceinline__ void process_fast(const SParams &P, unsigned char *sm
                 }
         }
     }
-    if (!P.has2d) return;
-    for (uint32_t t = 0; t < P.n_targets; ++t) {
+    for (uint32_t mi = 0; mi < P.n_mat; ++mi) {   // the matrix targets (at most two on this path)
+        const uint32_t t = P.mat_t[mi];
         const STarget &tg = P.tgt[t];
-        if (tg.ndim != 2) continue;
-        const uint32_t g = pick<NK>(grp, tg.k0) & pick<NK>(grp, tg.k1);
+        // NK <= 2 and a matrix spans both key columns (k0 = 0, k1 = 1 or the reverse)
+        const bool swap = NK > 1 && tg.k0 != 0;
+        const uint32_t g = NK > 1 ? (grp[0] & grp[NK - 1]) : grp[0];
         if (lane != __ffs(g) - 1) continue;
         const int cnt = __popc(g);
-        const int32_t xa = pick<NK>(b.x, tg.k0), xb = pick<NK>(b.x, tg.k1);
+        const int32_t xa = swap ? b.x[NK - 1] : b.x[0], xb = swap ? b.x[0] : b.x[NK - 1];
         if ((uint32_t)xa >= P.klut_dom[tg.k0] || (uint32_t)xb >= P.klut_dom[tg.k1]) {
-            update_2d(tg, seeds + tg.seed_off, sc, canon61(xa), canon61(xb), cnt);
+            fast_slow_2d(P, smem, t, xa, xb, cnt);
             continue;
         }
         if (agg && cnt > 1 && P.pairhh_off >= 0 && t == P.pair_t &&
             hh_add(smem + P.pairhh_off, P.pair_log2, ((uint64_t)(uint32_t)xa << 32) | (uint32_t)xb, cnt))
             continue;   // absorbed by the CTA's pair table (flushed once per distinct pair)
-        const uint4 qa = pick<NK>(b.e, tg.k0), qb = pick<NK>(b.e, tg.k1);
+        const uint4 qa = swap ? b.e[NK - 1] : b.e[0], qb = swap ? b.e[0] : b.e[NK - 1];
+        const uint32_t wm0 = tg.wmask0, wm1 = tg.wmask1, lw1 = tg.lw1, d = tg.d;
         // (r * w + b) & (w_m - 1) = b & (w_m - 1): the family's bucket at the matrix width
+        if (tg.smem_off >= 0) {
+            int32_t *row = sc + tg.smem_off;
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
-            if (r < (int)tg.d) {
+            for (int r = 0; r < 8; ++r) {
+                if (r >= (int)d) break;
                 const uint32_t fa = lut_fld(qa, r), fb = lut_fld(qb, r);
-                const uint32_t cell = (((fa >> 1) & tg.wmask0) << tg.lw1) | ((fb >> 1) & tg.wmask1);
-                const int v = ((fa ^ fb) & 1u) ? -cnt : cnt;
-                if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
-                else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
+                atomicAdd(row + ((((fa >> 1) & wm0) << lw1) | ((fb >> 1) & wm1)), ((fa ^ fb) & 1u) ? -cnt : cnt);
+                row += tg.cells;
             }
+        } else {
+            int64_t *row = tg.counters;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                if (r >= (int)d) break;
+                const uint32_t fa = lut_fld(qa, r), fb = lut_fld(qb, r);
+                red_add_s64(row + ((((fa >> 1) & wm0) << lw1) | ((fb >> 1) & wm1)), ((fa ^ fb) & 1u) ? -cnt : cnt);
+                row += tg.cells;
+            }
+        }
     }
 }
 

@@ -67,9 +67,11 @@ class PackedMerge:
                   ii); finish() then only merges the survivor counts and waits.
     Host logic only (the packing kernels are passed in), so it runs under gloo on CPU too."""
 
-    def __init__(self, buffer, n_tables, slices, wire="i64", overlap=False, group=None, pack=None, unpack=None):
+    def __init__(self, buffer, n_tables, slices, wire="i64", overlap=False, group=None, pack=None, unpack=None,
+                 always=False):
         assert wire in ("i64", "i32")
         self.buffer, self.slices, self.wire, self.overlap, self.group = buffer, slices, wire, overlap, group
+        self.always = always   # run the collectives even for a group of one rank (tests)
         self.n_s = n_tables + (n_tables & 1)
         self.pack, self.unpack = pack, unpack
         self.wire_buf = torch.empty(buffer.numel(), dtype=torch.int32, device=buffer.device) if wire == "i32" else None
@@ -77,7 +79,8 @@ class PackedMerge:
 
     def world(self) -> int:
         if dist.is_available() and dist.is_initialized():
-            return dist.get_world_size(self.group)
+            n = dist.get_world_size(self.group)
+            return 2 if (self.always and n == 1) else n
         return 1
 
     def _reduce(self, a: int, b: int, async_op: bool):
@@ -118,7 +121,7 @@ class PackedMerge:
 class QueryRun:
     """One query's sketches in one packed int64 buffer; cross-GPU merge by PackedMerge."""
 
-    def __init__(self, q, device="cuda", use_domains=True, wire="i64", overlap=False, group=None):
+    def __init__(self, q, device="cuda", use_domains=True, wire="i64", overlap=False, group=None, always_merge=False):
         self.q = q
         self.use_domains = use_domains
         self.device = torch.device(device)
@@ -138,7 +141,8 @@ class QueryRun:
         if wire == "i32" and any(t.n_rows >= (1 << 31) for t in q.tables):
             wire = "i64"   # int32 partial/merged counters need < 2^31 rows per table
         self.merge = PackedMerge(self.buffer, len(self.tnames), table_slices(q), wire, overlap, group,
-                                 pack=lambda a, b: sketch_wire_pack(a, b), unpack=lambda a, b: sketch_wire_unpack(a, b))
+                                 pack=lambda a, b: sketch_wire_pack(a, b), unpack=lambda a, b: sketch_wire_unpack(a, b),
+                                 always=always_merge)
 
     def zero_(self):
         self.buffer.zero_()

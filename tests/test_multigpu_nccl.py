@@ -79,3 +79,32 @@ def test_nccl_ranks_merge_equals_oracle_build(cfg, mode, tmp_path):
     ws = getattr(datagen, cfg[0])(**cfg[1])
     assert np.array_equal(res["buf"].numpy(), _oracle_packed(ws))
     assert all(p == res["plans"][0] for p in res["plans"])
+
+
+def _worker_one(rank, world, port, mode, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    import datagen
+    from paper_2102_02440_b200.query import QueryRun
+    ws = datagen.c5(scale=2e-4, w=128, wm=64)
+    run = QueryRun(ws, dev, wire=mode[0], overlap=mode[1], always_merge=True)
+    for t in ws.tables:
+        run.build_table(t.name, datagen.generate_table(ws, t.name, dev), datagen.resolve_preds(ws, t.name))
+    run.allreduce()
+    torch.cuda.synchronize()
+    torch.save({"buf": run.buffer.cpu()}, out_path)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", [("i64", False), ("i32", True)])
+def test_nccl_merge_path_on_one_gpu(mode, tmp_path):
+    """The merge code path on the device with a one-rank NCCL group (the pool has one GPU):
+    per-table int32 packing by the library, NCCL all-reduces on NCCL's stream (asynchronous,
+    overlapping the next scan), unpacking — the packed buffer equals the oracle's build."""
+    import datagen
+    out = str(tmp_path / "one.pt")
+    mp.start_processes(_worker_one, args=(1, _free_port(), mode, out), nprocs=1, join=True, start_method="spawn")
+    res = torch.load(out)
+    assert np.array_equal(res["buf"].numpy(), _oracle_packed(datagen.c5(scale=2e-4, w=128, wm=64)))
