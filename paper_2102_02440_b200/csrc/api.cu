@@ -164,7 +164,7 @@ extern "C" sk_status sketch_destroy(sk_sketch *sk) {
     cudaDeviceSynchronize();
     if (sk->owned && sk->counters) cudaFree(sk->counters);
     if (sk->seeds_dev) cudaFree(sk->seeds_dev);
-    for (int q = 0; q < 2; ++q)
+    for (int q = 0; q < 3; ++q)
         if (sk->lut[q]) cudaFree(sk->lut[q]);
     if (sk->lutx) cudaFree(sk->lutx);
     if (sk->lut_ready) cudaEventDestroy(sk->lut_ready);

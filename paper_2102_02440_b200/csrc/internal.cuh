@@ -28,8 +28,8 @@ struct sk_sketch {
     // lut[q][x * dp + r] = (h_r(x) & (w_q - 1)) << 1 | (xi_r(x) < 0), dp = d rounded up to a
     // multiple of 4 (d <= 8); built on first use
     // (the seeds never change), freed with the sketch
-    uint32_t *lut[2] = {nullptr, nullptr};
-    uint64_t lut_dom[2] = {0, 0};
+    uint32_t *lut[3] = {nullptr, nullptr, nullptr};
+    uint64_t lut_dom[3] = {0, 0, 0};
     // 1-D sketches: lookup table over a hinted key domain [0, lutx_dom) for the scan's
     // lookup-table path (d <= 8, d * w <= 2^15): lutx[x] holds 8 uint16 fields, field r =
     // ((r * w + (h_r(x) & (w - 1))) << 1) | (xi_r(x) < 0) for r < d (H3/H4), i.e. the

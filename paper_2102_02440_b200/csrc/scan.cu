@@ -131,11 +131,16 @@ static const void *pick_kernel(uint32_t nk, uint32_t np, int kw, bool fast, int 
 
 namespace skb {
 
+static sk_status decline(const char *why) {
+    if (getenv("COMPASS_SCAN_DEBUG")) fprintf(stderr, "k_scan declined: %s\n", why);
+    return SK_OK;
+}
+
 // Returns SK_OK and sets *launched if the optimised scan handled the call; leaves
 // *launched false (and returns SK_OK) when the call is outside its envelope.
 sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     *launched = false;
-    if (c.n_cols > kMaxSCols || c.n_preds > 4 || c.n_targets > kMaxSTargets || c.n_rows == 0) return SK_OK;
+    if (c.n_cols > kMaxSCols || c.n_preds > 4 || c.n_targets > kMaxSTargets || c.n_rows == 0) return decline("call size");
     SParams P;
     memset(&P, 0, sizeof(P));
     P.n_cols = c.n_cols;
@@ -144,14 +149,14 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         P.col[i].p = c.col_ptr[i];
         P.col[i].bytes = c.col_bytes[i];
         P.col[i].soff = -1;
-        if (((uintptr_t)c.col_ptr[i]) & 15) return SK_OK;   // bulk copies need 16-byte alignment
+        if (((uintptr_t)c.col_ptr[i]) & 15) return decline("column alignment");   // bulk copies need 16-byte alignment
     }
     // distinct key columns
     std::vector<uint32_t> keys;
     for (uint32_t t = 0; t < c.n_targets; ++t)
         for (uint32_t q = 0; q < c.tgt_ndim[t]; ++q)
             if (std::find(keys.begin(), keys.end(), c.tgt_key[t][q]) == keys.end()) keys.push_back(c.tgt_key[t][q]);
-    if (keys.size() > (size_t)kMaxKeys) return SK_OK;
+    if (keys.size() > (size_t)kMaxKeys) return decline("key columns");
     P.n_keys = (uint32_t)keys.size();
     // histogram mode for key columns with a small hinted domain feeding 1-D sketches
     const char *env_hist = getenv("COMPASS_HIST");
@@ -217,7 +222,8 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     if (fast) {   // matrix targets of the lookup-table path (both dims on the two key columns)
         P.n_mat = 0;
         for (uint32_t t = 0; t < c.n_targets; ++t)
-            if (c.tgt_ndim[t] == 2) {
+            if (c.tgt_ndim[t] == 3) fast = false;   // 3-D tensors take the hashing drain
+            else if (c.tgt_ndim[t] == 2) {
                 if (P.n_mat == 2 || c.tgt_key[t][0] == c.tgt_key[t][1]) fast = false;
                 else P.mat_t[P.n_mat++] = t;
             }
@@ -308,7 +314,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         cudaPointerAttributes pa;
         if (cudaPointerGetAttributes(&pa, c.col_ptr[ci]) != cudaSuccess || pa.type != cudaMemoryTypeDevice) {
             cudaGetLastError();
-            return SK_OK;
+            return decline("staged column not device memory");
         }
     }
     // ---- shared-memory plan (227 KB): barriers | TMA ring (stages x stage) | per-warp key
@@ -336,7 +342,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     const uint32_t ring_stage = kGroups * P.stage_bytes;   // one stage of every group's ring
     const uint32_t fixed = kBarBytes + min_stages * ring_stage + ring_warps * P.kb_bytes + seed_bytes + miss_bytes +
                            kWarps * 128 * 2 + 256;
-    if (fixed > kBudget) return SK_OK;
+    if (fixed > kBudget) return decline("fixed smem");
     uint32_t avail = kBudget - fixed;
     // privatise targets in declaration order while they fit
     P.n_targets = c.n_targets;
@@ -348,11 +354,16 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         tg.ndim = c.tgt_ndim[t];
         tg.d = c.tgt_d[t];
         tg.wmask0 = c.tgt_w[t][0] - 1;
-        tg.wmask1 = tg.ndim == 2 ? c.tgt_w[t][1] - 1 : 0;
-        tg.lw1 = tg.ndim == 2 ? (uint32_t)__builtin_ctz(c.tgt_w[t][1]) : 0;
+        tg.wmask1 = tg.ndim >= 2 ? c.tgt_w[t][1] - 1 : 0;
+        tg.lw1 = tg.ndim >= 2 ? (uint32_t)__builtin_ctz(c.tgt_w[t][1]) : 0;
+        tg.wmask2 = tg.ndim == 3 ? c.tgt_w[t][2] - 1 : 0;
+        tg.lw2 = tg.ndim == 3 ? (uint32_t)__builtin_ctz(c.tgt_w[t][2]) : 0;
         tg.k0 = (uint32_t)(std::find(keys.begin(), keys.end(), c.tgt_key[t][0]) - keys.begin());
-        tg.k1 = tg.ndim == 2 ? (uint32_t)(std::find(keys.begin(), keys.end(), c.tgt_key[t][1]) - keys.begin()) : 0;
-        tg.cells = tg.ndim == 2 ? c.tgt_w[t][0] * c.tgt_w[t][1] : c.tgt_w[t][0];
+        tg.k1 = tg.ndim >= 2 ? (uint32_t)(std::find(keys.begin(), keys.end(), c.tgt_key[t][1]) - keys.begin()) : 0;
+        tg.k2 = tg.ndim == 3 ? (uint32_t)(std::find(keys.begin(), keys.end(), c.tgt_key[t][2]) - keys.begin()) : 0;
+        const uint64_t cells64 = uint64_t(c.tgt_w[t][0]) * (tg.ndim >= 2 ? c.tgt_w[t][1] : 1) * (tg.ndim == 3 ? c.tgt_w[t][2] : 1);
+        if (cells64 * tg.d >= (1ULL << 31)) return decline("tensor cells");   // 32-bit cell arithmetic in the drain
+        tg.cells = (uint32_t)cells64;
         tg.seed_off = seed_off;
         seed_off += tg.ndim * tg.d * 6;
         P.seeds[t] = c.tgt_seeds[t];
@@ -364,7 +375,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         } else {
             tg.smem_off = -1;
         }
-        if (tg.ndim == 2) P.has2d = 1;
+        if (tg.ndim >= 2) P.has2d = 1;
         if (tg.ndim == 1) {
             P.key[tg.k0].has1d = 1;
             if (tg.smem_off >= 0) P.key[tg.k0].priv1d |= 1u << t;
@@ -398,17 +409,21 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         cudaDeviceGetAttribute(&sms_l, cudaDevAttrMultiProcessorCount, dev_l);
         for (uint32_t t = 0; t < c.n_targets; ++t) {
             STarget &tg = P.tgt[t];
-            tg.lut0 = tg.lut1 = nullptr;
-            if (tg.ndim != 2 || !c.tgt_sketch[t]) continue;
+            tg.lut0 = tg.lut1 = tg.lut2 = nullptr;
+            if (tg.ndim < 2 || !c.tgt_sketch[t]) continue;
             sk_sketch *sk = c.tgt_sketch[t];
-            const uint64_t dom[2] = {c.col_domain[c.tgt_key[t][0]], c.col_domain[c.tgt_key[t][1]]};
+            const int nd = (int)tg.ndim;
+            uint64_t dom[3] = {0, 0, 0};
             bool ok = true;
             const uint64_t dp = (sk->d + 3) & ~3u;
-            for (int q = 0; q < 2; ++q) ok &= sk->d <= 8 && dom[q] > 0 && dom[q] <= (1ULL << 31) && dom[q] * dp * 4 <= (64ULL << 20);
+            for (int q = 0; q < nd; ++q) {
+                dom[q] = c.col_domain[c.tgt_key[t][q]];
+                ok &= sk->d <= 8 && dom[q] > 0 && dom[q] <= (1ULL << 31) && dom[q] * dp * 4 <= (64ULL << 20);
+            }
             if (!ok) continue;
             std::lock_guard<std::mutex> lk(sk->lut_mu);
             bool built = false;
-            for (int q = 0; q < 2; ++q) {
+            for (int q = 0; q < nd; ++q) {
                 if (sk->lut[q] && sk->lut_dom[q] >= dom[q]) continue;
                 if (sk->lut[q]) {   // a wider table replaces it: no reader of the old one may be in flight
                     SKB_CUDA(cudaDeviceSynchronize());
@@ -431,8 +446,10 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
             }
             tg.lut0 = sk->lut[0];
             tg.lut1 = sk->lut[1];
+            tg.lut2 = sk->lut[2];
             tg.lut_dom0 = dom[0];
             tg.lut_dom1 = dom[1];
+            tg.lut_dom2 = dom[2];
         }
     }
     // trio detection: matrix M whose dimension-q hash rows equal those of a privatised 1-D
@@ -504,7 +521,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     off = P.off_hstat + kMaxKeys * 4 * 4;
     P.off_seed = (off + 15) & ~15u;
     off = P.off_seed + seed_bytes;
-    if (off > kBudget) return SK_OK;
+    if (off > kBudget) return decline("smem plan");
     P.survivors = c.survivors;
 
     int dev = 0, sms = 148;
@@ -512,8 +529,8 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     uint64_t grid = std::min<uint64_t>((uint64_t)sms, (P.n_tiles + kGroups - 1) / kGroups);
     // int32 privatised counts stay exact: rows per CTA < 2^31
-    if ((P.n_tiles + grid * kGroups - 1) / (grid * kGroups) * P.tile_rows * kGroups >= (1ULL << 31)) return SK_OK;
-    if (P.n_keys == 0) return SK_OK;
+    if ((P.n_tiles + grid * kGroups - 1) / (grid * kGroups) * P.tile_rows * kGroups >= (1ULL << 31)) return decline("rows per CTA");
+    if (P.n_keys == 0) return decline("no key column");
     std::vector<void *> hists;
     for (uint32_t k = 0; k < P.n_keys; ++k) {
         P.key[k].hist = nullptr;

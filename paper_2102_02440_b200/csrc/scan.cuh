@@ -20,7 +20,7 @@ struct ScanCall {
     uint32_t pred_n[8];
     uint32_t n_targets = 0;
     int64_t *tgt_counters[16];
-    uint32_t tgt_ndim[16], tgt_d[16], tgt_w[16][2], tgt_key[16][2];
+    uint32_t tgt_ndim[16], tgt_d[16], tgt_w[16][3], tgt_key[16][3];
     const uint64_t *tgt_seeds[16];
     const uint64_t *tgt_seeds_host[16];   // host copies [ndim][d][6] (hash-unit sharing)
     sk_sketch *tgt_sketch[16];             // target handles (per-sketch hash lookup tables)

@@ -69,13 +69,13 @@ struct SKey {
 };
 struct STarget {
     int64_t *counters;
-    uint32_t ndim, d, wmask0, wmask1, lw1;
-    uint32_t k0, k1;      // indices into keys[]
+    uint32_t ndim, d, wmask0, wmask1, lw1, wmask2, lw2;
+    uint32_t k0, k1, k2;  // indices into keys[]
     int32_t smem_off;     // int32 offset of privatised copy, -1 = global
     uint32_t cells;
     uint32_t seed_off;
-    const uint32_t *lut0, *lut1;   // matrices: per-dimension hash lookup tables (or null)
-    uint64_t lut_dom0, lut_dom1;
+    const uint32_t *lut0, *lut1, *lut2;   // matrices / tensors: per-dimension hash lookup tables (or null)
+    uint64_t lut_dom0, lut_dom1, lut_dom2;
 };
 struct SParams {
     SCol col[kMaxSCols];
@@ -291,6 +291,50 @@ __device__ __forceinline__ void update_2d(const STarget &tg, const uint64_t *see
     else update_2d_t<false>(tg, seed, sc, x, y, cnt);
 }
 
+// 3-D tensor target t: row r gets cnt * xi0(x) xi1(y) xi2(z) at cell
+// [h0(x)][h1(y)][h2(z)], dimensions in the sketch's canonical edge order
+template <bool N>
+__device__ __forceinline__ void update_3d_t(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, uint64_t y,
+                                            uint64_t z, int cnt) {
+    const uint64_t *s1 = seed + tg.d * 6, *s2 = s1 + tg.d * 6;
+    for (uint32_t r = 0; r < tg.d; ++r) {
+        const uint64_t *a = seed + r * 6, *b = s1 + r * 6, *c = s2 + r * 6;
+        const uint32_t cell = ((((uint32_t)(hash_g61_t<N>(a[4], a[5], x) & tg.wmask0) << tg.lw1) |
+                                (uint32_t)(hash_g61_t<N>(b[4], b[5], y) & tg.wmask1)) << tg.lw2) |
+                              (uint32_t)(hash_g61_t<N>(c[4], c[5], z) & tg.wmask2);
+        const int v = xi_sign61_t<N>(a, x) * xi_sign61_t<N>(b, y) * xi_sign61_t<N>(c, z) * cnt;
+        if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
+        else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
+    }
+}
+__device__ __forceinline__ void update_3d(const STarget &tg, const uint64_t *seed, int32_t *sc, uint64_t x, uint64_t y,
+                                          uint64_t z, int cnt) {
+    if (tg.lut0 && x < tg.lut_dom0 && y < tg.lut_dom1 && z < tg.lut_dom2) {
+        // (bucket, sign) of every row of every dimension from the lookup tables, all loads
+        // issued before the first update (same layout as update_2d)
+        const uint32_t dp = (tg.d + 3) & ~3u;
+        const uint4 *la = reinterpret_cast<const uint4 *>(tg.lut0 + x * dp), *lb = reinterpret_cast<const uint4 *>(tg.lut1 + y * dp),
+                    *lc = reinterpret_cast<const uint4 *>(tg.lut2 + z * dp);
+        uint4 va[2], vb[2], vc[2];
+        va[0] = __ldg(la); vb[0] = __ldg(lb); vc[0] = __ldg(lc);
+        if (dp > 4) { va[1] = __ldg(la + 1); vb[1] = __ldg(lb + 1); vc[1] = __ldg(lc + 1); }
+        for (uint32_t r = 0; r < tg.d && r < 8; ++r) {
+            const uint4 &qa = va[r >> 2], &qb = vb[r >> 2], &qc = vc[r >> 2];
+            const uint32_t j = r & 3;
+            const uint32_t ea = j == 0 ? qa.x : j == 1 ? qa.y : j == 2 ? qa.z : qa.w;
+            const uint32_t eb = j == 0 ? qb.x : j == 1 ? qb.y : j == 2 ? qb.z : qb.w;
+            const uint32_t ec = j == 0 ? qc.x : j == 1 ? qc.y : j == 2 ? qc.z : qc.w;
+            const uint32_t cell = ((((ea >> 1) << tg.lw1) | (eb >> 1)) << tg.lw2) | (ec >> 1);
+            const int v = ((ea ^ eb ^ ec) & 1u) ? -cnt : cnt;
+            if (tg.smem_off >= 0) atomicAdd(&sc[tg.smem_off + r * tg.cells + cell], v);
+            else red_add_s64(tg.counters + uint64_t(r) * tg.cells + cell, (int64_t)v);
+        }
+        return;
+    }
+    if ((x | y | z) < (1ULL << 32)) update_3d_t<true>(tg, seed, sc, x, y, z, cnt);
+    else update_3d_t<false>(tg, seed, sc, x, y, z, cnt);
+}
+
 // x[idx] with compile-time indexing only (keeps the key array in registers)
 template <int NK, typename T>
 __device__ __forceinline__ T pick(const T (&x)[NK], uint32_t idx) {
@@ -416,8 +460,14 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
     if (valid && P.has2d) {
         for (uint32_t t = 0; t < P.n_targets; ++t) {
             const STarget &tg = P.tgt[t];
-            if (tg.ndim != 2 || (P.trio_on && t == P.trio_m)) continue;
+            if (tg.ndim < 2 || (P.trio_on && t == P.trio_m)) continue;
             const uint64_t xa = pick<NK>(x, tg.k0), xb = pick<NK>(x, tg.k1);
+            if (tg.ndim == 3) {   // 3-D tensor: equal key triples aggregated
+                const uint64_t xc = pick<NK>(x, tg.k2);
+                const uint32_t grp = __match_any_sync(act, xa) & __match_any_sync(act, xb) & __match_any_sync(act, xc);
+                if (lane == __ffs(grp) - 1) update_3d(tg, seeds + tg.seed_off, sc, xa, xb, xc, __popc(grp));
+                continue;
+            }
             const uint32_t grp = __match_any_sync(act, xa) & __match_any_sync(act, xb);
             if (lane == __ffs(grp) - 1) update_2d(tg, seeds + tg.seed_off, sc, xa, xb, __popc(grp));
         }

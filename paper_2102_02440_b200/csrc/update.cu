@@ -254,9 +254,7 @@ extern "C" sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_co
     if (n_rows == 0) { release(); return SK_OK; }
     // optimised persistent scan (scan.cu) unless disabled or outside its envelope
     const char *mode = getenv("COMPASS_SCAN");
-    bool has3d = false;   // 3-D tensor targets are built by the grid-stride kernel
-    for (uint32_t t = 0; t < n_targets; ++t) has3d |= targets[t].sketch->ndim == 3;
-    if (!(mode && strcmp(mode, "generic") == 0) && !has3d) {
+    if (!(mode && strcmp(mode, "generic") == 0)) {
         ScanCall sc;
         sc.n_cols = n_cols;
         for (uint32_t c = 0; c < n_cols; ++c) {
@@ -281,9 +279,11 @@ extern "C" sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_co
             sc.tgt_ndim[t] = sk->ndim;
             sc.tgt_d[t] = sk->d;
             sc.tgt_w[t][0] = sk->w[0];
-            sc.tgt_w[t][1] = sk->ndim == 2 ? sk->w[1] : 1;
             sc.tgt_key[t][0] = targets[t].key_col[0];
-            sc.tgt_key[t][1] = sk->ndim == 2 ? targets[t].key_col[1] : 0;
+            for (uint32_t q = 1; q < 3; ++q) {
+                sc.tgt_w[t][q] = q < sk->ndim ? sk->w[q] : 1;
+                sc.tgt_key[t][q] = q < sk->ndim ? targets[t].key_col[q] : 0;
+            }
             sc.tgt_seeds[t] = sk->seeds_dev;
             sc.tgt_seeds_host[t] = sk->seeds_host.data();
             sc.tgt_sketch[t] = const_cast<sk_sketch *>(sk);

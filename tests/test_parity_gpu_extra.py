@@ -250,6 +250,37 @@ def test_tensor3_build_equals_oracle(n, preds):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("n", [4097, 1_000_003])
+@pytest.mark.parametrize("mode", ["scan", "scan_lut", "generic"])
+def test_tensor3_scan_paths_equal_oracle(n, mode, capfd, monkeypatch):
+    """3-D tensors inside the persistent scan (k_scan drain: hashing, or the per-dimension
+    lookup tables when every key column has a domain hint) and in the grid-stride kernel:
+    bit-exact counters next to a 1-D sketch and a matrix, keys partly outside the hints."""
+    monkeypatch.setenv("COMPASS_SCAN_DEBUG", "1")
+    if mode == "generic":
+        monkeypatch.setenv("COMPASS_SCAN", "generic")
+    rng = np.random.default_rng(n + len(mode))
+    a = (rng.zipf(1.3, n) % 3000).astype(np.int32)
+    b = rng.integers(0, 5000, n).astype(np.int32)
+    a[::89] = 3000 + rng.integers(0, 10**6, a[::89].shape[0]).astype(np.int32)   # above the hint
+    cols = {"a": a, "b": b, "p": rng.integers(0, 100, n).astype(np.int32)}
+    targets = [(["a", "a", "b"], 7, [64, 16, 32], ["C.a|E.a", "C.a|G.a", "C.b|F.b"]),
+               (["a", "b"], 7, [64, 64], ["C.a|E.a", "C.b|F.b"]),
+               (["a"], 7, [1024], ["C.a|E.a"])]
+    preds = [("p", pb.RANGE, 10, 70)]
+    dom = {"a": 3000, "b": 5000} if mode == "scan_lut" else None
+    g, gs = _build(cols, preds, targets, domains=dom)
+    err = capfd.readouterr().err
+    if mode == "generic":
+        assert "k_scan plan" not in err
+    else:
+        assert "k_scan plan: keys 2 preds 1" in err, err
+    o, os_ = _oracle(cols, preds, targets)
+    assert gs == os_
+    for t, (x, y) in enumerate(zip(g, o)):
+        assert np.array_equal(x, y), f"target {t} differs"
+
+
 def _t3_star_graph(rng, d, wv, wt, vmax):
     """centre C with a 3-D tensor over (A.x|C.x, B.y|C.y, C.z|D.z) and leaf vectors; returns
     (oracle graph, JoinGraph)."""
@@ -314,3 +345,4 @@ def test_c3t_scaled_all_subplans_and_plan():
     for s in oracle.connected_subplans(og):
         assert jg.estimate_join_exact(s) == oracle.estimate_rows(og, s), s
     assert tuple(jg.plan_greedy()) == tuple(oracle.plan_greedy(og))
+

@@ -8,7 +8,7 @@ Variants: generic KW=0 (int64 range + subset predicates), KW=4 / KW=8 specialise
 ring-overflow rounds (100 % selectivity, two key columns), histogram mode with heavy-hitter
 tables (hinted key domain), the lookup-table path (int32 keys with hints, matrix + pair
 table), sub-tiled stages (very selective predicate), the staged no-predicate path, 3-D
-tensors (grid-stride kernel), and the estimate kernels (two-way, merged views, CRT).
+tensors (k_scan drain), and the estimate kernels (two-way, merged views, CRT).
 Each build is checked against the oracle so a silent corruption also fails.
 """
 import os
