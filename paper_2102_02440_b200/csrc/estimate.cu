@@ -459,6 +459,202 @@ __global__ void __launch_bounds__(256) k_node_mat_gemm(const __grid_constant__ N
     }
 }
 
+// ---------------------------------------------------------------- tensor-core modular GEMM
+// The same product as k_node_mat_gemm, out[b][j] = sum_i x[b][i] M(i, j) mod m, on the
+// 5th-generation tensor cores (tcgen05.mma kind::i8, u8 x u8 -> s32 in TMEM).  Residues
+// (< 2^26) are split into 4 byte planes, x = sum_a 2^(8a) x_a and M = sum_c 2^(8c) M_c; the
+// 16 byte-plane products with a + c = s accumulate in one of 7 int32 TMEM accumulators
+// D_s (every entry <= 4 * w_i * 255^2 < 2^31 for w_i <= 8192, exact), and the epilogue forms
+// sum_s D_s * (2^(8s) mod m) (< 2^60) and reduces it once.  The result is the same integer
+// residue as the CUDA-core kernel's, by construction.
+//
+// CTA tile 128 b x 64 j, k-blocks of 64 i; 3-stage smem ring of byte planes (A: 4 x 128 x
+// 64 B, B: 4 x 64 x 64 B) filled by all 256 threads (residues -> bytes, canonical K-major
+// no-swizzle core-matrix layout: 8 rows x 16 B per core matrix, SBO = 128 B between 8-row
+// groups, LBO = rows x 16 B between 16-byte K chunks), one elected thread issues the 32
+// MMAs (128 x 64 x 32) of a stage and commits them to the stage's mbarrier; 512 TMEM
+// columns (7 x 64 used), one CTA per SM.
+constexpr int TC_M = 128, TC_N = 64, TC_KB = 64, TC_ST = 3;
+constexpr int TC_A_PLANE = TC_M * TC_KB, TC_B_PLANE = TC_N * TC_KB;          // bytes
+constexpr int TC_STAGE = 4 * TC_A_PLANE + 4 * TC_B_PLANE;                    // 48 KB
+constexpr int TC_SMEM = TC_ST * TC_STAGE + 64;                               // + barriers, TMEM slot
+
+__device__ __forceinline__ uint64_t tc_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    // SM100 shared-memory matrix descriptor: start >> 4 [0,14), LBO >> 4 [16,30), SBO >> 4
+    // [32,46), version 1 [46,48), base offset 0, layout SWIZZLE_NONE (0) [61,64)
+    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ void tc_mbar_wait(uint32_t a, uint32_t ph) {
+    asm volatile("{\n.reg .pred p;\nW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W;\n}\n" ::"r"(a),
+                 "r"(ph) : "memory");
+}
+
+__global__ void __launch_bounds__(256, 1) k_node_mat_gemm_tc(const __grid_constant__ Node n, const __grid_constant__ Mods md,
+                                                             int qc, const uint32_t *Rc) {
+    extern __shared__ __align__(1024) unsigned char tsm[];
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tsm);
+    const uint32_t bar0 = sbase + TC_ST * TC_STAGE;     // TC_ST mbarriers, then the TMEM address slot
+    const uint32_t slot = bar0 + 8 * TC_ST;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int k = blockIdx.x / n.d, r = blockIdx.x % n.d;
+    const uint64_t m = md.m[k], mu = md.mu[k];
+    const int nbt = (n.B + TC_M - 1) / TC_M;
+    const int b0 = (blockIdx.y % nbt) * TC_M, j0 = (blockIdx.y / nbt) * TC_N;
+    const int qp = 1 - qc;
+    const int wi = n.w[qc], wj = n.w[qp];
+    const uint32_t *R = Rc + (uint64_t(k) * n.d + r) * (uint64_t(wi) * wj);
+
+    if (tid == 0) {
+        for (int s = 0; s < TC_ST; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * s) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(slot) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    uint32_t tmem;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(tmem) : "r"(slot) : "memory");
+
+    // instruction descriptor: D s32 [4,6) = 2, A/B u8, K-major, N >> 3 at [17,23), M >> 4 at [24,29)
+    const uint32_t idesc = (2u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+    const int nkb = (wi + TC_KB - 1) / TC_KB;
+    for (int kb = 0; kb < nkb; ++kb) {
+        const int st = kb % TC_ST;
+        if (kb >= TC_ST) tc_mbar_wait(bar0 + 8 * st, (uint32_t)((kb / TC_ST - 1) & 1));   // MMAs of kb - TC_ST done
+        unsigned char *A = tsm + st * TC_STAGE, *Bp = A + 4 * TC_A_PLANE;
+        const int i0 = kb * TC_KB;
+        // A: 128 rows x 4 chunks of 16 i; one item = 16 residues of one row -> 16 B per plane
+        for (int e = tid; e < TC_M * 4; e += 256) {
+            const int row = e % TC_M, c = e / TC_M;
+            const int b = b0 + row, ib = i0 + c * 16;
+            uint32_t w[4][4];
+            if (b < n.B && ib + 16 <= wi) {
+                const uint64_t *x = msg_row(n, qc, k, r, b, 0) + ib;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t v[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) v[t] = (uint32_t)__ldg(reinterpret_cast<const unsigned long long *>(x) + q * 4 + t);
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+                        w[a][q] = ((v[0] >> (8 * a)) & 0xFF) | (((v[1] >> (8 * a)) & 0xFF) << 8) |
+                                  (((v[2] >> (8 * a)) & 0xFF) << 16) | (((v[3] >> (8 * a)) & 0xFF) << 24);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t v[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int i = ib + q * 4 + t;
+                        v[t] = (b < n.B && i < wi) ? (uint32_t)msg_row(n, qc, k, r, b, 0)[i] : 0u;
+                    }
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+                        w[a][q] = ((v[0] >> (8 * a)) & 0xFF) | (((v[1] >> (8 * a)) & 0xFF) << 8) |
+                                  (((v[2] >> (8 * a)) & 0xFF) << 16) | (((v[3] >> (8 * a)) & 0xFF) << 24);
+                }
+            }
+            const int off = c * (TC_M * 16) + (row >> 3) * 128 + (row & 7) * 16;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+                *reinterpret_cast<uint4 *>(A + a * TC_A_PLANE + off) = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
+        }
+        // B (K-major: row j holds M(i, j) for the 64 i of the block): 64 rows x 4 chunks
+        for (int e = tid; e < TC_N * 4; e += 256) {
+            const int jr = e % TC_N, c = e / TC_N;
+            const int j = j0 + jr, ib = i0 + c * 16;
+            uint32_t w[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t v[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int i = ib + q * 4 + t;
+                    v[t] = (j < wj && i < wi) ? __ldg(R + uint64_t(i) * wj + j) : 0u;
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+                    w[a][q] = ((v[0] >> (8 * a)) & 0xFF) | (((v[1] >> (8 * a)) & 0xFF) << 8) |
+                              (((v[2] >> (8 * a)) & 0xFF) << 16) | (((v[3] >> (8 * a)) & 0xFF) << 24);
+            }
+            const int off = c * (TC_N * 16) + (jr >> 3) * 128 + (jr & 7) * 16;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+                *reinterpret_cast<uint4 *>(Bp + a * TC_B_PLANE + off) = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
+        }
+        // generic-proxy smem writes -> visible to the tensor core (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t a_s = sbase + st * TC_STAGE, b_s = a_s + 4 * TC_A_PLANE;
+            for (int a = 0; a < 4; ++a)
+                for (int c = 0; c < 4; ++c) {
+                    const int s = a + c;
+                    const uint32_t dt = tmem + (uint32_t)(s * TC_N);
+                    for (int ks = 0; ks < TC_KB / 32; ++ks) {
+                        // first write of D_s: (kb, ks) == (0, 0) and the first (a, c) with a + c = s
+                        const bool first = kb == 0 && ks == 0 && (s <= 3 ? a == 0 : c == 3);
+                        const uint64_t ad = tc_sdesc(a_s + a * TC_A_PLANE + ks * 2 * (TC_M * 16), TC_M * 16, 128);
+                        const uint64_t bd = tc_sdesc(b_s + c * TC_B_PLANE + ks * 2 * (TC_N * 16), TC_N * 16, 128);
+                        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+                                     "l"(ad), "l"(bd), "r"(idesc), "r"(first ? 0u : 1u) : "memory");
+                    }
+                }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar0 + 8 * st)
+                         : "memory");
+        }
+    }
+    // the last commit covers every MMA issued before it
+    {
+        const int st = (nkb - 1) % TC_ST;
+        tc_mbar_wait(bar0 + 8 * st, (uint32_t)(((nkb - 1) / TC_ST) & 1));
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. (rows b), column half w / 4
+    uint64_t pw[7];
+    pw[0] = 1 % m;
+    for (int s = 1; s < 7; ++s) pw[s] = mm_red(pw[s - 1] << 8, m, mu);
+    const int lq = warp & 3, half = warp >> 2;
+    const int b = b0 + lq * 32 + lane;
+    for (int cc = 0; cc < 2; ++cc) {
+        const int col = half * 32 + cc * 16;
+        uint64_t acc[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) acc[t] = 0;
+#pragma unroll
+        for (int s = 0; s < 7; ++s) {
+            uint32_t v[16];
+            const uint32_t ta = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(s * TC_N + col);
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                         : "r"(ta));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int t = 0; t < 16; ++t) acc[t] += (uint64_t)v[t] * pw[s];
+        }
+        if (b < n.B) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                const int j = j0 + col + t;
+                if (j >= wj) continue;
+                const int jo = n.out_perm ? n.out_perm[uint64_t(r) * wj + j] : j;
+                n.out[((uint64_t(k) * n.d + r) * n.out_bm + (n.out_bm > 1 ? b : 0)) * wj + jo] = mm_red(acc[t], m, mu);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
 // Matrix node with one child leg and one parent leg, one conditioned bucket (chains, PAPER.md
 // :222-225): out[k][r][o] = sum_i x[k][r][i] * M(i, o) mod m_k for every modulus k in one pass
 // over the matrix (each element is reduced once per modulus; the int64 matrix is read once per
@@ -2097,7 +2293,22 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                         Rc = it->second;
                     }
                 }
-                k_node_mat_gemm<<<dim3(K * d, nbt * njt), 256, 0, stream>>>(n, md, qchild, Rc); count_launch();
+                const char *ge = getenv("COMPASS_GEMM");
+                if (Rc && n.w[qchild] <= 8192 && !(ge && strcmp(ge, "cuda") == 0)) {
+                    // tensor cores (tcgen05 kind::i8 on byte planes), same residues
+                    static bool attr_set = false;
+                    if (!attr_set) {
+                        SKB_CUDA(cudaFuncSetAttribute(k_node_mat_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+                        attr_set = true;
+                    }
+                    const int tbt = (nB + TC_M - 1) / TC_M, tjt = (P.width[pe] + TC_N - 1) / TC_N;
+                    if (getenv("COMPASS_EST_DEBUG"))
+                        fprintf(stderr, "gemm tc: K %d d %d B %d wi %d wj %d\n", K, d, nB, n.w[qchild], P.width[pe]);
+                    k_node_mat_gemm_tc<<<dim3(K * d, tbt * tjt), 256, TC_SMEM, stream>>>(n, md, qchild, Rc);
+                } else {
+                    k_node_mat_gemm<<<dim3(K * d, nbt * njt), 256, 0, stream>>>(n, md, qchild, Rc);
+                }
+                count_launch();
             } else if (t.kind == KG && qc_of[i] >= 0) {
                 n.qc = qc_of[i];
                 n.ord = ord_of[i];

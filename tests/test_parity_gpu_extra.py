@@ -346,3 +346,58 @@ def test_c3t_scaled_all_subplans_and_plan():
         assert jg.estimate_join_exact(s) == oracle.estimate_rows(og, s), s
     assert tuple(jg.plan_greedy()) == tuple(oracle.plan_greedy(og))
 
+
+# ------------------------------------------------------------------ tensor-core modular GEMM (cycles)
+def _matrix_ring(rng, T, w, d, vmax):
+    """ring of T tables, every table a w x w matrix over its two edges (the conditioned-cycle
+    path batches one modular GEMM per interior matrix over the w buckets of the cut edge)."""
+    names = [f"t{i}" for i in range(T)]
+    eids = [f"{names[i]}.c|{names[(i + 1) % T]}.c" if i + 1 < T else f"{names[0]}.c{i}|{names[i]}.c{i}" for i in range(T)]
+    topo = [(i, (i + 1) % T) for i in range(T)]
+    vec_np, mat_np = {}, {}
+    for i, (u, v) in enumerate(topo):
+        for t in (u, v):
+            vec_np[(names[t], eids[i])] = rng.integers(-vmax, vmax + 1, (d, w)).astype(np.int64)
+    for t in range(T):
+        inc = sorted(eids[i] for i, e in enumerate(topo) if t in e)
+        mat_np[(names[t], tuple(inc))] = rng.integers(-vmax, vmax + 1, (d, w, w)).astype(np.int64)
+    og = oracle.Graph({n: int(rng.integers(1, 1000)) for n in names}, [(eids[i], names[u], names[v]) for i, (u, v) in enumerate(topo)],
+                      vec_np, mat_np)
+    sk = {}
+    for key, arr in vec_np.items():
+        s = pb.Sketch(d, [w], [key[1]], 42, _dev(), counters=torch.from_numpy(arr).to(_dev()))
+        sk[key] = s
+    mats = []
+    for (t, inc), arr in mat_np.items():
+        s = pb.Sketch(d, [w, w], list(inc), 42, _dev(), counters=torch.from_numpy(arr).to(_dev()))
+        mats.append((names.index(t), eids.index(inc[0]), eids.index(inc[1]), s))
+    edges = [(u, v, sk[(names[u], eids[i])], sk[(names[v], eids[i])]) for i, (u, v) in enumerate(topo)]
+    return og, pb.JoinGraph(names, [og.tables[n] for n in names], edges, mats), names
+
+
+@pytest.mark.parametrize("T,w,vmax", [(4, 16, 3), (5, 32, 1 << 20), (4, 64, 1 << 40)])
+def test_cycle_gemm_tensor_cores_equal_oracle(T, w, vmax, capfd, monkeypatch):
+    """Matrix rings (every table a matrix): the conditioned-cycle estimate runs the modular
+    GEMM on tcgen05 (kind::i8 byte planes); every row equals the oracle's exact value."""
+    monkeypatch.setenv("COMPASS_EST_DEBUG", "1")
+    rng = np.random.default_rng(T * 1000 + w)
+    og, jg, names = _matrix_ring(rng, T, w, 3, vmax)
+    full = tuple(names)
+    got = jg.estimate_join_exact(full)
+    assert "gemm tc:" in capfd.readouterr().err
+    assert got == oracle.estimate_rows(og, full)
+
+
+@pytest.mark.parametrize("T,w", [(4, 128), (6, 256), (4, 512)])
+def test_cycle_gemm_tensor_cores_equal_cuda_cores(T, w, capfd, monkeypatch):
+    """Full-size tiles and several tiles per GEMM (w = 128..512): the tensor-core GEMM and the
+    CUDA-core GEMM give identical exact estimates on every row of every cyclic sub-plan."""
+    rng = np.random.default_rng(T * 7 + w)
+    og, jg, names = _matrix_ring(rng, T, w, 5, 1 << 30)
+    full = tuple(names)
+    monkeypatch.setenv("COMPASS_EST_DEBUG", "1")
+    tc = jg.estimate_join_exact(full)
+    assert "gemm tc:" in capfd.readouterr().err
+    monkeypatch.setenv("COMPASS_GEMM", "cuda")
+    og2, jg2, _ = _matrix_ring(np.random.default_rng(T * 7 + w), T, w, 5, 1 << 30)
+    assert jg2.estimate_join_exact(full) == tc
