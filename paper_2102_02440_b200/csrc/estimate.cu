@@ -655,6 +655,193 @@ __global__ void __launch_bounds__(256, 1) k_node_mat_gemm_tc(const __grid_consta
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
+// Byte-plane operands in global memory, pre-tiled in the canonical UMMA K-major layout so the
+// GEMM streams them with 1-D bulk copies (TMA engine, no register traffic): one 32 KB chunk
+// per (modulus k, row r, 128-row b tile, 64-i block) for x (4 planes x 128 x 64 B) and one
+// 16 KB chunk per (k, r, 64-column j tile, 64-i block) for M (4 planes x 64 x 64 B).
+__global__ void k_planes_x(const __grid_constant__ Node n, int qc, int K, int nbt, int nkb, unsigned char *out) {
+    const int wi = n.w[qc];
+    const uint64_t items = uint64_t(K) * n.d * nbt * TC_M * (nkb * 4);   // (kr, row, 16-i chunk)
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < items; e += uint64_t(gridDim.x) * blockDim.x) {
+        const int row = (int)(e % TC_M);
+        uint64_t t = e / TC_M;
+        const int c16 = (int)(t % (nkb * 4));
+        t /= (nkb * 4);
+        const int bt = (int)(t % nbt);
+        const int kr = (int)(t / nbt);
+        const int k = kr / n.d, r = kr % n.d;
+        const int b = bt * TC_M + row, ib = c16 * 16;
+        uint32_t w[4][4];
+        const uint64_t *x = (b < n.B) ? msg_row(n, qc, k, r, b, 0) : nullptr;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = ib + q * 4 + u;
+                v[u] = (x && i < wi) ? (uint32_t)__ldg(reinterpret_cast<const unsigned long long *>(x) + i) : 0u;
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+                w[a][q] = ((v[0] >> (8 * a)) & 0xFF) | (((v[1] >> (8 * a)) & 0xFF) << 8) | (((v[2] >> (8 * a)) & 0xFF) << 16) |
+                          (((v[3] >> (8 * a)) & 0xFF) << 24);
+        }
+        const int kb = c16 >> 2, c = c16 & 3;
+        unsigned char *chunk = out + ((uint64_t(kr) * nbt + bt) * nkb + kb) * (4 * TC_A_PLANE);
+        const int off = c * (TC_M * 16) + (row >> 3) * 128 + (row & 7) * 16;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+            *reinterpret_cast<uint4 *>(chunk + a * TC_A_PLANE + off) = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
+    }
+}
+__global__ void k_planes_m(const uint32_t *Rc, int Kd, int wi, int wj, int njt, int nkb, unsigned char *out) {
+    const uint64_t items = uint64_t(Kd) * njt * TC_N * (nkb * 4);   // (kr, j, 16-i chunk); j fastest (coalesced reads)
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < items; e += uint64_t(gridDim.x) * blockDim.x) {
+        const int jr = (int)(e % TC_N);
+        uint64_t t = e / TC_N;
+        const int jt = (int)(t % njt);
+        t /= njt;
+        const int c16 = (int)(t % (nkb * 4));
+        const int kr = (int)(t / (nkb * 4));
+        const int j = jt * TC_N + jr, ib = c16 * 16;
+        const uint32_t *R = Rc + uint64_t(kr) * wi * wj;
+        uint32_t w[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = ib + q * 4 + u;
+                v[u] = (j < wj && i < wi) ? __ldg(R + uint64_t(i) * wj + j) : 0u;
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+                w[a][q] = ((v[0] >> (8 * a)) & 0xFF) | (((v[1] >> (8 * a)) & 0xFF) << 8) | (((v[2] >> (8 * a)) & 0xFF) << 16) |
+                          (((v[3] >> (8 * a)) & 0xFF) << 24);
+        }
+        const int kb = c16 >> 2, c = c16 & 3;
+        unsigned char *chunk = out + ((uint64_t(kr) * njt + jt) * nkb + kb) * (4 * TC_B_PLANE);
+        const int off = c * (TC_N * 16) + (jr >> 3) * 128 + (jr & 7) * 16;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+            *reinterpret_cast<uint4 *>(chunk + a * TC_B_PLANE + off) = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
+    }
+}
+
+// The tensor-core GEMM fed by bulk copies: warp 0 (one lane) streams the pre-tiled x and M
+// chunks of each 64-i block into a 4-stage ring (mbarrier full[s], expect_tx 48 KB), warp 1
+// (one lane) waits full[s], issues the 32 MMAs and commits them to empty[s]; after the last
+// block all four warps read the 7 accumulators back from TMEM (epilogue as above).
+constexpr int TC_ST2 = 4;
+constexpr int TC_SMEM2 = TC_ST2 * TC_STAGE + 128;
+__global__ void __launch_bounds__(128, 1) k_node_mat_gemm_bulk(const __grid_constant__ Node n, const __grid_constant__ Mods md,
+                                                               int qc, const unsigned char *Xp, const unsigned char *Mp,
+                                                               int nbt, int njt, int nkb, int kr_m0) {
+    extern __shared__ __align__(1024) unsigned char tsm[];
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tsm);
+    const uint32_t full0 = sbase + TC_ST2 * TC_STAGE, empty0 = full0 + 8 * TC_ST2, done = empty0 + 8 * TC_ST2;
+    const uint32_t slot = done + 8;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int kr = blockIdx.x, k = kr / n.d, r = kr % n.d;
+    const uint64_t m = md.m[k], mu = md.mu[k];
+    const int bt = blockIdx.y % nbt, jt = blockIdx.y / nbt;
+    const int b0 = bt * TC_M, j0 = jt * TC_N;
+    const int wj = n.w[1 - qc];
+    if (tid == 0) {
+        for (int s = 0; s < TC_ST2; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * s) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(empty0 + 8 * s) : "memory");
+        }
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(done) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(slot) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    uint32_t tmem;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(tmem) : "r"(slot) : "memory");
+
+    const unsigned char *xa = Xp + (uint64_t(kr) * nbt + bt) * nkb * (4 * TC_A_PLANE);
+    const unsigned char *mb = Mp + (uint64_t(kr_m0 + kr) * njt + jt) * nkb * (4 * TC_B_PLANE);
+    if (warp == 0 && lane == 0) {   // producer
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int st = kb % TC_ST2;
+            if (kb >= TC_ST2) tc_mbar_wait(empty0 + 8 * st, (uint32_t)((kb / TC_ST2 - 1) & 1));
+            const uint32_t fb = full0 + 8 * st, dst = sbase + st * TC_STAGE;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"((uint32_t)TC_STAGE) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                         "l"(xa + uint64_t(kb) * (4 * TC_A_PLANE)), "r"((uint32_t)(4 * TC_A_PLANE)), "r"(fb) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + 4 * TC_A_PLANE),
+                         "l"(mb + uint64_t(kb) * (4 * TC_B_PLANE)), "r"((uint32_t)(4 * TC_B_PLANE)), "r"(fb) : "memory");
+        }
+    } else if (warp == 1 && lane == 0) {   // MMA issuer
+        const uint32_t idesc = (2u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int st = kb % TC_ST2;
+            tc_mbar_wait(full0 + 8 * st, (uint32_t)((kb / TC_ST2) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t a_s = sbase + st * TC_STAGE, b_s = a_s + 4 * TC_A_PLANE;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int s = a + c;
+#pragma unroll
+                    for (int ks = 0; ks < TC_KB / 32; ++ks) {
+                        const bool first = kb == 0 && ks == 0 && (s <= 3 ? a == 0 : c == 3);
+                        const uint64_t ad = tc_sdesc(a_s + a * TC_A_PLANE + ks * 2 * (TC_M * 16), TC_M * 16, 128);
+                        const uint64_t bd = tc_sdesc(b_s + c * TC_B_PLANE + ks * 2 * (TC_N * 16), TC_N * 16, 128);
+                        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(s * TC_N)),
+                                     "l"(ad), "l"(bd), "r"(idesc), "r"(first ? 0u : 1u) : "memory");
+                    }
+                }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty0 + 8 * st) : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(done) : "memory");
+    }
+    __syncwarp();
+    tc_mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    uint64_t pw[7];
+    pw[0] = 1 % m;
+    for (int s = 1; s < 7; ++s) pw[s] = mm_red(pw[s - 1] << 8, m, mu);
+    const int b = b0 + warp * 32 + lane;
+    for (int col = 0; col < TC_N; col += 16) {
+        uint64_t acc[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) acc[t] = 0;
+#pragma unroll
+        for (int s = 0; s < 7; ++s) {
+            uint32_t v[16];
+            const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(s * TC_N + col);
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                         : "r"(ta));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int t = 0; t < 16; ++t) acc[t] += (uint64_t)v[t] * pw[s];
+        }
+        if (b < n.B) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                const int j = j0 + col + t;
+                if (j >= wj) continue;
+                const int jo = n.out_perm ? n.out_perm[uint64_t(r) * wj + j] : j;
+                n.out[((uint64_t(k) * n.d + r) * n.out_bm + (n.out_bm > 1 ? b : 0)) * wj + jo] = mm_red(acc[t], m, mu);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
 // Matrix node with one child leg and one parent leg, one conditioned bucket (chains, PAPER.md
 // :222-225): out[k][r][o] = sum_i x[k][r][i] * M(i, o) mod m_k for every modulus k in one pass
 // over the matrix (each element is reduced once per modulus; the int64 matrix is read once per
@@ -1329,15 +1516,15 @@ __global__ void k_mat_residues(const int64_t *T, int d, int w0, int w1, int qc, 
 // 16 slices of the child index per block, combined in shared memory.
 constexpr int MR_SL = 16;
 __global__ void __launch_bounds__(512) k_node_matvec_r(const __grid_constant__ Node n, const __grid_constant__ Mods md,
-                                                       int qc, const uint32_t *Rc) {
+                                                       int qc, const uint32_t *Rc, int G) {
     __shared__ uint64_t part[MR_SL][MV_G][MV_OUT];
     const int r = blockIdx.x;
     const int qp = 1 - qc;
     const int wi = n.w[qc], wo = n.w[qp];
     const int lane = threadIdx.x & 31, sl = threadIdx.x >> 5;
     const int o = blockIdx.y * MV_OUT + lane;
-    const int g0 = blockIdx.z * MV_G;
-    const int ng = min(MV_G, md.K - g0);
+    const int g0 = blockIdx.z * G;   // G <= MV_G moduli per CTA
+    const int ng = min(G, md.K - g0);
     const uint64_t cells = uint64_t(wi) * wo;
     const int chunk = (wi + MR_SL - 1) / MR_SL;
     const int i0 = sl * chunk, i1 = min(wi, i0 + chunk);
@@ -2142,6 +2329,8 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
     if ((st = dalloc(pool, size_t(K) * d * Bc * tiles_root * 8, stream, &part))) return st;
     for (int64_t b0 = 0; b0 < Btot; b0 += Bc) {
         const int B = (int)std::min<int64_t>(Bc, Btot - b0);
+        uint64_t *dense_root_part = nullptr;   // modular dense root split over tiles
+        int dense_root_slots = 0;
         for (int i : order) {
             const TabT &t = P.T[i];
             const int pe = parent_edge[i];
@@ -2269,8 +2458,11 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                 } else {
                     Rc = it->second;
                 }
-                k_node_matvec_r<<<dim3(d, (P.width[pe] + MV_OUT - 1) / MV_OUT, (md.K + MV_G - 1) / MV_G), 512, 0, stream>>>(
-                    n, md, qchild, Rc);
+                // one modulus per CTA unless that makes the grid very large (more CTAs in
+                // flight hide the latency of the residue loads)
+                const int nto = (P.width[pe] + MV_OUT - 1) / MV_OUT;
+                const int G = (d * nto * md.K <= 4096) ? 1 : MV_G;
+                k_node_matvec_r<<<dim3(d, nto, (md.K + G - 1) / G), 512, 0, stream>>>(n, md, qchild, Rc, G);
                 count_launch();
             } else if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB == 1 && !getenv("COMPASS_EST_NO_MATVEC")) {
                 k_node_matvec<<<dim3(d, (P.width[pe] + MV_OUT - 1) / MV_OUT), 256, 0, stream>>>(n, md, qchild); count_launch();
@@ -2294,7 +2486,39 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                     }
                 }
                 const char *ge = getenv("COMPASS_GEMM");
-                if (Rc && n.w[qchild] <= 8192 && !(ge && strcmp(ge, "cuda") == 0)) {
+                if (Rc && n.w[qchild] <= 8192 && !(ge && (strcmp(ge, "cuda") == 0 || strcmp(ge, "tc") == 0))) {
+                    // tensor cores fed by bulk copies of pre-tiled byte planes: x planes per
+                    // node, M planes cached per batch with the residues
+                    const int wi = n.w[qchild], wj = P.width[pe];
+                    const int tbt = (nB + TC_M - 1) / TC_M, tjt = (wj + TC_N - 1) / TC_N, tkb = (wi + TC_KB - 1) / TC_KB;
+                    const int Kres = resmods->K;
+                    const auto pkey = std::make_pair((const void *)n.data[0], qchild + 16);
+                    auto pit = rescache->find(pkey);
+                    unsigned char *Mp;
+                    if (pit == rescache->end()) {
+                        void *pm;
+                        if ((st = dalloc(pool, size_t(Kres) * d * tjt * tkb * (4 * TC_B_PLANE), stream, &pm))) return st;
+                        k_planes_m<<<1184, 256, 0, stream>>>(Rc, Kres * d, wi, wj, tjt, tkb, (unsigned char *)pm);
+                        count_launch();
+                        (*rescache)[pkey] = (uint32_t *)pm;
+                        Mp = (unsigned char *)pm;
+                    } else {
+                        Mp = (unsigned char *)pit->second;
+                    }
+                    void *px;
+                    if ((st = dalloc(pool, size_t(K) * d * tbt * tkb * (4 * TC_A_PLANE), stream, &px))) return st;
+                    k_planes_x<<<1184, 256, 0, stream>>>(n, qchild, K, tbt, tkb, (unsigned char *)px);
+                    count_launch();
+                    static bool attr2 = false;
+                    if (!attr2) {
+                        SKB_CUDA(cudaFuncSetAttribute(k_node_mat_gemm_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM2));
+                        attr2 = true;
+                    }
+                    if (getenv("COMPASS_EST_DEBUG"))
+                        fprintf(stderr, "gemm tc bulk: K %d d %d B %d wi %d wj %d\n", K, d, nB, wi, wj);
+                    k_node_mat_gemm_bulk<<<dim3(K * d, tbt * tjt), 128, TC_SMEM2, stream>>>(n, md, qchild, (const unsigned char *)px,
+                                                                                           Mp, tbt, tjt, tkb, 0);
+                } else if (Rc && n.w[qchild] <= 8192 && !(ge && strcmp(ge, "cuda") == 0)) {
                     // tensor cores (tcgen05 kind::i8 on byte planes), same residues
                     static bool attr_set = false;
                     if (!attr_set) {
@@ -2344,13 +2568,33 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                 SKB_CUDA(cudaFuncSetAttribute(k_node_merged_m, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
                 k_node_merged_m<<<dim3(d * nB, n.tiles), MX_T, sm, stream>>>(n, md, pos); count_launch();
             } else {
+                if (pe < 0) {
+                    // root: the outer leg is split over enough CTAs to fill the GPU, partials per
+                    // tile in their own buffer (reduced below)
+                    int qo = -1;
+                    for (int q = 0; q < n.nl && qo < 0; ++q)
+                        if (n.role[q] == RCHILD) qo = q;
+                    const int wo_r = qo >= 0 ? n.w[qo] : 1;
+                    int rt = 1;
+                    while (blocks_xy * rt < 592 && rt * 256 < wo_r && rt < 64) rt *= 2;
+                    if (rt > 1) {
+                        void *pd;
+                        if ((st = dalloc(pool, size_t(K) * d * nB * rt * 8, stream, &pd))) return st;
+                        n.out = (uint64_t *)pd;
+                        n.tiles = tiles = rt;
+                        dense_root_part = (uint64_t *)pd;
+                        dense_root_slots = nB * rt;
+                    }
+                }
                 k_node_dense<<<dim3(blocks_xy, tiles), 256, 0, stream>>>(n, md); count_launch();
             }
             SKB_CUDA_CHECK("estimate launch 4");
         }
         if (exact) { k_root_reduce_x<<<d, 256, 0, stream>>>((const i128 *)part, (i128 *)acc, B * tiles_root); count_launch(); }
         else if (absb) { k_root_reduce_abs<<<d, 256, 0, stream>>>((const double *)part, (double *)acc, B * tiles_root); count_launch(); }
-        else { k_root_reduce<<<K * d, 256, 0, stream>>>((const uint64_t *)part, acc, B * tiles_root, d, md); count_launch(); }
+        else if (dense_root_part) {
+            k_root_reduce<<<K * d, 256, 0, stream>>>(dense_root_part, acc, dense_root_slots, d, md); count_launch();
+        } else { k_root_reduce<<<K * d, 256, 0, stream>>>((const uint64_t *)part, acc, B * tiles_root, d, md); count_launch(); }
         SKB_CUDA_CHECK("estimate launch 5");
     }
     return SK_OK;

@@ -376,28 +376,35 @@ def _matrix_ring(rng, T, w, d, vmax):
 
 
 @pytest.mark.parametrize("T,w,vmax", [(4, 16, 3), (5, 32, 1 << 20), (4, 64, 1 << 40)])
-def test_cycle_gemm_tensor_cores_equal_oracle(T, w, vmax, capfd, monkeypatch):
+@pytest.mark.parametrize("feed", ["bulk", "tc"])
+def test_cycle_gemm_tensor_cores_equal_oracle(T, w, vmax, feed, capfd, monkeypatch):
     """Matrix rings (every table a matrix): the conditioned-cycle estimate runs the modular
-    GEMM on tcgen05 (kind::i8 byte planes); every row equals the oracle's exact value."""
+    GEMM on tcgen05 (kind::i8 byte planes; fed by bulk copies of pre-tiled planes, or by
+    register stores); every row equals the oracle's exact value."""
     monkeypatch.setenv("COMPASS_EST_DEBUG", "1")
+    if feed == "tc":
+        monkeypatch.setenv("COMPASS_GEMM", "tc")
     rng = np.random.default_rng(T * 1000 + w)
     og, jg, names = _matrix_ring(rng, T, w, 3, vmax)
     full = tuple(names)
     got = jg.estimate_join_exact(full)
-    assert "gemm tc:" in capfd.readouterr().err
+    assert ("gemm tc bulk:" if feed == "bulk" else "gemm tc:") in capfd.readouterr().err
     assert got == oracle.estimate_rows(og, full)
 
 
 @pytest.mark.parametrize("T,w", [(4, 128), (6, 256), (4, 512)])
-def test_cycle_gemm_tensor_cores_equal_cuda_cores(T, w, capfd, monkeypatch):
-    """Full-size tiles and several tiles per GEMM (w = 128..512): the tensor-core GEMM and the
+@pytest.mark.parametrize("feed", ["bulk", "tc"])
+def test_cycle_gemm_tensor_cores_equal_cuda_cores(T, w, feed, capfd, monkeypatch):
+    """Full-size tiles and several tiles per GEMM (w = 128..512): the tensor-core GEMMs and the
     CUDA-core GEMM give identical exact estimates on every row of every cyclic sub-plan."""
     rng = np.random.default_rng(T * 7 + w)
     og, jg, names = _matrix_ring(rng, T, w, 5, 1 << 30)
     full = tuple(names)
     monkeypatch.setenv("COMPASS_EST_DEBUG", "1")
+    if feed == "tc":
+        monkeypatch.setenv("COMPASS_GEMM", "tc")
     tc = jg.estimate_join_exact(full)
-    assert "gemm tc:" in capfd.readouterr().err
+    assert ("gemm tc bulk:" if feed == "bulk" else "gemm tc:") in capfd.readouterr().err
     monkeypatch.setenv("COMPASS_GEMM", "cuda")
     og2, jg2, _ = _matrix_ring(np.random.default_rng(T * 7 + w), T, w, 5, 1 << 30)
     assert jg2.estimate_join_exact(full) == tc
