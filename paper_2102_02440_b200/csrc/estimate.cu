@@ -767,7 +767,10 @@ __global__ void __launch_bounds__(128, 1) k_node_mat_gemm_bulk(const __grid_cons
 
     const unsigned char *xa = Xp + (uint64_t(kr) * nbt + bt) * nkb * (4 * TC_A_PLANE);
     const unsigned char *mb = Mp + (uint64_t(kr_m0 + kr) * njt + jt) * nkb * (4 * TC_B_PLANE);
-    if (warp == 0 && lane == 0) {   // producer
+    // the producer and the MMA issuer each run on one lane of their own warp; the other lanes
+    // of those warps park at __syncwarp (no spinning lanes competing with the issuing lane)
+    if (warp == 0) {
+      if (lane == 0) {   // producer
         for (int kb = 0; kb < nkb; ++kb) {
             const int st = kb % TC_ST2;
             if (kb >= TC_ST2) tc_mbar_wait(empty0 + 8 * st, (uint32_t)((kb / TC_ST2 - 1) & 1));
@@ -778,7 +781,10 @@ __global__ void __launch_bounds__(128, 1) k_node_mat_gemm_bulk(const __grid_cons
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + 4 * TC_A_PLANE),
                          "l"(mb + uint64_t(kb) * (4 * TC_B_PLANE)), "r"((uint32_t)(4 * TC_B_PLANE)), "r"(fb) : "memory");
         }
-    } else if (warp == 1 && lane == 0) {   // MMA issuer
+      }
+      __syncwarp();
+    } else if (warp == 1) {
+      if (lane == 0) {   // MMA issuer
         const uint32_t idesc = (2u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
         for (int kb = 0; kb < nkb; ++kb) {
             const int st = kb % TC_ST2;
@@ -803,8 +809,9 @@ __global__ void __launch_bounds__(128, 1) k_node_mat_gemm_bulk(const __grid_cons
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty0 + 8 * st) : "memory");
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(done) : "memory");
+      }
+      __syncwarp();
     }
-    __syncwarp();
     tc_mbar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     uint64_t pw[7];
@@ -1516,7 +1523,7 @@ __global__ void k_mat_residues(const int64_t *T, int d, int w0, int w1, int qc, 
 // 16 slices of the child index per block, combined in shared memory.
 constexpr int MR_SL = 16;
 __global__ void __launch_bounds__(512) k_node_matvec_r(const __grid_constant__ Node n, const __grid_constant__ Mods md,
-                                                       int qc, const uint32_t *Rc, int G) {
+                                                       int qc, const uint32_t *Rc, int G, uint64_t *root_part) {
     __shared__ uint64_t part[MR_SL][MV_G][MV_OUT];
     const int r = blockIdx.x;
     const int qp = 1 - qc;
@@ -1546,12 +1553,26 @@ __global__ void __launch_bounds__(512) k_node_matvec_r(const __grid_constant__ N
 #pragma unroll
     for (int g = 0; g < MV_G; ++g) part[sl][g][lane] = g < ng ? mm_red(acc[g], md.m[g0 + g], md.mu[g0 + g]) : 0;
     __syncthreads();
-    if (sl < ng && o < wo) {
+    if (!root_part && sl < ng && o < wo) {
         const int k = g0 + sl;
         uint64_t t = 0;
         for (int s2 = 0; s2 < MR_SL; ++s2) t = mm_add(t, part[s2][sl][lane], md.m[k]);
         const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
         n.out[(uint64_t(k) * n.d + r) * n.out_bm * wo + oo] = t;
+    }
+    if (root_part && sl < ng) {
+        // root matrix with two child legs: sum_o x_o (M y)_o, this CTA's 32 outputs reduced
+        // by warp sl for modulus g0 + sl into the root partial of its output tile
+        const int k = g0 + sl;
+        const uint64_t m = md.m[k], mu = md.mu[k];
+        uint64_t v = 0;
+        if (o < wo) {
+            uint64_t t = 0;
+            for (int s2 = 0; s2 < MR_SL; ++s2) t = mm_add(t, part[s2][sl][lane], m);
+            v = mm_mul(t, msg_row(n, qp, k, r, 0, 0)[o], m, mu);
+        }
+        for (int off = 16; off > 0; off >>= 1) v = mm_add(v, __shfl_xor_sync(0xffffffffu, v, off), m);
+        if (lane == 0) root_part[(uint64_t(k) * n.d + r) * gridDim.y + blockIdx.y] = v;
     }
 }
 
@@ -2441,7 +2462,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                     n.tiles = (pe >= 0) ? xt : 1;
                     k_node_dense_x<<<dim3(d * nB, n.tiles), 256, 0, stream>>>(n); count_launch();
                 }
-            } else if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB == 1 && rescache && resmods &&
+            } else if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB == 1 && rescache && resmods && !getenv("COMPASS_EST_NO_RES") &&
                        md.K <= resmods->K && !getenv("COMPASS_EST_NO_MATVEC")) {
                 // residues of this (folded) matrix in this orientation: once per batch
                 const auto key = std::make_pair((const void *)n.data[0], qchild);
@@ -2462,8 +2483,35 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                 // flight hide the latency of the residue loads)
                 const int nto = (P.width[pe] + MV_OUT - 1) / MV_OUT;
                 const int G = (d * nto * md.K <= 4096) ? 1 : MV_G;
-                k_node_matvec_r<<<dim3(d, nto, (md.K + G - 1) / G), 512, 0, stream>>>(n, md, qchild, Rc, G);
+                k_node_matvec_r<<<dim3(d, nto, (md.K + G - 1) / G), 512, 0, stream>>>(n, md, qchild, Rc, G, nullptr);
                 count_launch();
+            } else if (t.kind == KM && pe < 0 && nchild == 2 && !hasfixed && nB == 1 && rescache && resmods &&
+                       !getenv("COMPASS_EST_NO_RES") && md.K <= resmods->K && !getenv("COMPASS_EST_NO_MATVEC")) {
+                // root matrix with two child legs: the mat-vec over leg 1 (residues cached per
+                // batch), dotted with the leg-0 message inside the same kernel
+                const int qc = 1, qo = 0;
+                const auto key = std::make_pair((const void *)n.data[0], qc);
+                auto it = rescache->find(key);
+                uint32_t *Rc;
+                if (it == rescache->end()) {
+                    void *rb;
+                    const size_t cells = size_t(n.w[0]) * n.w[1];
+                    if ((st = dalloc(pool, size_t(resmods->K) * d * cells * 4, stream, &rb))) return st;
+                    k_mat_residues<<<1184, 256, 0, stream>>>(n.data[0], d, n.w[0], n.w[1], qc, *resmods, (uint32_t *)rb);
+                    count_launch();
+                    Rc = (uint32_t *)rb;
+                    (*rescache)[key] = Rc;
+                } else {
+                    Rc = it->second;
+                }
+                const int nto = (n.w[qo] + MV_OUT - 1) / MV_OUT;
+                const int G = (d * nto * md.K <= 4096) ? 1 : MV_G;
+                void *pr;
+                if ((st = dalloc(pool, size_t(K) * d * nto * 8, stream, &pr))) return st;
+                k_node_matvec_r<<<dim3(d, nto, (md.K + G - 1) / G), 512, 0, stream>>>(n, md, qc, Rc, G, (uint64_t *)pr);
+                count_launch();
+                dense_root_part = (uint64_t *)pr;
+                dense_root_slots = nto;
             } else if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB == 1 && !getenv("COMPASS_EST_NO_MATVEC")) {
                 k_node_matvec<<<dim3(d, (P.width[pe] + MV_OUT - 1) / MV_OUT), 256, 0, stream>>>(n, md, qchild); count_launch();
             } else if (t.kind == KM && pe >= 0 && nchild == 1 && !hasfixed && nB >= 16) {
