@@ -728,31 +728,33 @@ __global__ void k_planes_m(const uint32_t *Rc, int Kd, int wi, int wj, int njt, 
     }
 }
 
-// The tensor-core GEMM fed by bulk copies: warp 0 (one lane) streams the pre-tiled x and M
-// chunks of each 64-i block into a 4-stage ring (mbarrier full[s], expect_tx 48 KB), warp 1
-// (one lane) waits full[s], issues the 32 MMAs and commits them to empty[s]; after the last
-// block all four warps read the 7 accumulators back from TMEM (epilogue as above).
+// The tensor-core GEMM fed by bulk copies, persistent: one CTA per SM walks the (k r, b tile,
+// j tile) tiles with a static stride.  Warp 4 (one lane) streams the pre-tiled x and M chunks
+// of every 64-i block of every tile into a 4-stage ring (mbarrier full[s], expect_tx 48 KB),
+// running ahead across tile boundaries; warp 5 (one lane) waits full[s], issues the 32 MMAs
+// and commits them to empty[s], and after a tile's last block commits tmem_full; warps 0-3
+// drain the 7 accumulators (tcgen05.ld, one TMEM lane quarter each), form the residues, store
+// them (16-byte vector stores when the row is contiguous) and release TMEM (tmem_empty) for
+// the next tile's MMAs.
 constexpr int TC_ST2 = 4;
 constexpr int TC_SMEM2 = TC_ST2 * TC_STAGE + 128;
-__global__ void __launch_bounds__(128, 1) k_node_mat_gemm_bulk(const __grid_constant__ Node n, const __grid_constant__ Mods md,
+__global__ void __launch_bounds__(192, 1) k_node_mat_gemm_bulk(const __grid_constant__ Node n, const __grid_constant__ Mods md,
                                                                int qc, const unsigned char *Xp, const unsigned char *Mp,
                                                                int nbt, int njt, int nkb, int kr_m0) {
     extern __shared__ __align__(1024) unsigned char tsm[];
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tsm);
-    const uint32_t full0 = sbase + TC_ST2 * TC_STAGE, empty0 = full0 + 8 * TC_ST2, done = empty0 + 8 * TC_ST2;
-    const uint32_t slot = done + 8;
+    const uint32_t full0 = sbase + TC_ST2 * TC_STAGE, empty0 = full0 + 8 * TC_ST2;
+    const uint32_t tfull = empty0 + 8 * TC_ST2, tempty = tfull + 8, slot = tempty + 8;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int kr = blockIdx.x, k = kr / n.d, r = kr % n.d;
-    const uint64_t m = md.m[k], mu = md.mu[k];
-    const int bt = blockIdx.y % nbt, jt = blockIdx.y / nbt;
-    const int b0 = bt * TC_M, j0 = jt * TC_N;
     const int wj = n.w[1 - qc];
+    const int ntiles = n.d * md.K * nbt * njt;
     if (tid == 0) {
         for (int s = 0; s < TC_ST2; ++s) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * s) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(empty0 + 8 * s) : "memory");
         }
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(done) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tfull) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(tempty) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -765,82 +767,110 @@ __global__ void __launch_bounds__(128, 1) k_node_mat_gemm_bulk(const __grid_cons
     uint32_t tmem;
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(tmem) : "r"(slot) : "memory");
 
-    const unsigned char *xa = Xp + (uint64_t(kr) * nbt + bt) * nkb * (4 * TC_A_PLANE);
-    const unsigned char *mb = Mp + (uint64_t(kr_m0 + kr) * njt + jt) * nkb * (4 * TC_B_PLANE);
-    // the producer and the MMA issuer each run on one lane of their own warp; the other lanes
-    // of those warps park at __syncwarp (no spinning lanes competing with the issuing lane)
-    if (warp == 0) {
-      if (lane == 0) {   // producer
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int st = kb % TC_ST2;
-            if (kb >= TC_ST2) tc_mbar_wait(empty0 + 8 * st, (uint32_t)((kb / TC_ST2 - 1) & 1));
-            const uint32_t fb = full0 + 8 * st, dst = sbase + st * TC_STAGE;
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"((uint32_t)TC_STAGE) : "memory");
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                         "l"(xa + uint64_t(kb) * (4 * TC_A_PLANE)), "r"((uint32_t)(4 * TC_A_PLANE)), "r"(fb) : "memory");
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + 4 * TC_A_PLANE),
-                         "l"(mb + uint64_t(kb) * (4 * TC_B_PLANE)), "r"((uint32_t)(4 * TC_B_PLANE)), "r"(fb) : "memory");
+    if (warp == 4) {
+        if (lane == 0) {   // producer
+            uint32_t g = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int jt = t % njt, bt = (t / njt) % nbt, kr = t / (njt * nbt);
+                const unsigned char *xa = Xp + (uint64_t(kr) * nbt + bt) * nkb * (4 * TC_A_PLANE);
+                const unsigned char *mb = Mp + (uint64_t(kr_m0 + kr) * njt + jt) * nkb * (4 * TC_B_PLANE);
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const uint32_t st = g % TC_ST2;
+                    if (g >= TC_ST2) tc_mbar_wait(empty0 + 8 * st, ((g / TC_ST2) - 1) & 1);
+                    const uint32_t fb = full0 + 8 * st, dst = sbase + st * TC_STAGE;
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"((uint32_t)TC_STAGE) : "memory");
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                                 "l"(xa + uint64_t(kb) * (4 * TC_A_PLANE)), "r"((uint32_t)(4 * TC_A_PLANE)), "r"(fb) : "memory");
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst + 4 * TC_A_PLANE),
+                                 "l"(mb + uint64_t(kb) * (4 * TC_B_PLANE)), "r"((uint32_t)(4 * TC_B_PLANE)), "r"(fb) : "memory");
+                }
+            }
         }
-      }
-      __syncwarp();
-    } else if (warp == 1) {
-      if (lane == 0) {   // MMA issuer
-        const uint32_t idesc = (2u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int st = kb % TC_ST2;
-            tc_mbar_wait(full0 + 8 * st, (uint32_t)((kb / TC_ST2) & 1));
+        __syncwarp();
+    } else if (warp == 5) {
+        if (lane == 0) {   // MMA issuer
+            const uint32_t idesc = (2u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+            uint32_t g = 0, li = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++li) {
+                if (li > 0) tc_mbar_wait(tempty, (li - 1) & 1);   // the epilogue has read the previous tile
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const uint32_t st = g % TC_ST2;
+                    tc_mbar_wait(full0 + 8 * st, (g / TC_ST2) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t a_s = sbase + st * TC_STAGE, b_s = a_s + 4 * TC_A_PLANE;
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const int s = a + c;
+#pragma unroll
+                            for (int ks = 0; ks < TC_KB / 32; ++ks) {
+                                const bool first = kb == 0 && ks == 0 && (s <= 3 ? a == 0 : c == 3);
+                                const uint64_t ad = tc_sdesc(a_s + a * TC_A_PLANE + ks * 2 * (TC_M * 16), TC_M * 16, 128);
+                                const uint64_t bd = tc_sdesc(b_s + c * TC_B_PLANE + ks * 2 * (TC_N * 16), TC_N * 16, 128);
+                                asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                             "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(s * TC_N)),
+                                             "l"(ad), "l"(bd), "r"(idesc), "r"(first ? 0u : 1u) : "memory");
+                            }
+                        }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty0 + 8 * st) : "memory");
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(tfull) : "memory");
+            }
+        }
+        __syncwarp();
+    } else {   // epilogue: warps 0-3, TMEM lanes 32 w .. 32 w + 31 = rows b
+        uint32_t li = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++li) {
+            const int jt = t % njt, bt = (t / njt) % nbt, kr = t / (njt * nbt);
+            const int k = kr / n.d, r = kr % n.d;
+            const uint64_t m = md.m[k], mu = md.mu[k];
+            uint64_t pw[7];
+            pw[0] = 1 % m;
+            for (int s = 1; s < 7; ++s) pw[s] = mm_red(pw[s - 1] << 8, m, mu);
+            const int b = bt * TC_M + warp * 32 + lane, j0 = jt * TC_N;
+            tc_mbar_wait(tfull, li & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t a_s = sbase + st * TC_STAGE, b_s = a_s + 4 * TC_A_PLANE;
+            uint64_t *orow = n.out + ((uint64_t(k) * n.d + r) * n.out_bm + (n.out_bm > 1 ? b : 0)) * wj;
+            for (int col = 0; col < TC_N; col += 16) {
+                uint64_t acc[16];
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
+                for (int u = 0; u < 16; ++u) acc[u] = 0;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const int s = a + c;
+                for (int s = 0; s < 7; ++s) {
+                    uint32_t v[16];
+                    const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(s * TC_N + col);
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                                 : "r"(ta));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                    for (int ks = 0; ks < TC_KB / 32; ++ks) {
-                        const bool first = kb == 0 && ks == 0 && (s <= 3 ? a == 0 : c == 3);
-                        const uint64_t ad = tc_sdesc(a_s + a * TC_A_PLANE + ks * 2 * (TC_M * 16), TC_M * 16, 128);
-                        const uint64_t bd = tc_sdesc(b_s + c * TC_B_PLANE + ks * 2 * (TC_N * 16), TC_N * 16, 128);
-                        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(s * TC_N)),
-                                     "l"(ad), "l"(bd), "r"(idesc), "r"(first ? 0u : 1u) : "memory");
+                    for (int u = 0; u < 16; ++u) acc[u] += (uint64_t)v[u] * pw[s];
+                }
+                if (col + 16 == TC_N) {   // every accumulator column read: release TMEM early
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty) : "memory");
+                }
+                if (b < n.B) {
+                    const int jb = j0 + col;
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) acc[u] = mm_red(acc[u], m, mu);
+                    if (!n.out_perm && jb + 16 <= wj) {
+#pragma unroll
+                        for (int u = 0; u < 16; u += 2)
+                            *reinterpret_cast<ulonglong2 *>(orow + jb + u) = make_ulonglong2(acc[u], acc[u + 1]);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) {
+                            const int j = jb + u;
+                            if (j >= wj) continue;
+                            orow[n.out_perm ? n.out_perm[uint64_t(r) * wj + j] : j] = acc[u];
+                        }
                     }
                 }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty0 + 8 * st) : "memory");
-        }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(done) : "memory");
-      }
-      __syncwarp();
-    }
-    tc_mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    uint64_t pw[7];
-    pw[0] = 1 % m;
-    for (int s = 1; s < 7; ++s) pw[s] = mm_red(pw[s - 1] << 8, m, mu);
-    const int b = b0 + warp * 32 + lane;
-    for (int col = 0; col < TC_N; col += 16) {
-        uint64_t acc[16];
-#pragma unroll
-        for (int t = 0; t < 16; ++t) acc[t] = 0;
-#pragma unroll
-        for (int s = 0; s < 7; ++s) {
-            uint32_t v[16];
-            const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(s * TC_N + col);
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                         : "r"(ta));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-            for (int t = 0; t < 16; ++t) acc[t] += (uint64_t)v[t] * pw[s];
-        }
-        if (b < n.B) {
-#pragma unroll
-            for (int t = 0; t < 16; ++t) {
-                const int j = j0 + col + t;
-                if (j >= wj) continue;
-                const int jo = n.out_perm ? n.out_perm[uint64_t(r) * wj + j] : j;
-                n.out[((uint64_t(k) * n.d + r) * n.out_bm + (n.out_bm > 1 ? b : 0)) * wj + jo] = mm_red(acc[t], m, mu);
             }
         }
     }
@@ -1022,21 +1052,25 @@ __device__ __forceinline__ W block_sum_w(W v, W *red) {
     return t;
 }
 
+// prefix arrays of the exact merged kernel are padded by one slot every 8 entries (index s
+// lives at PXI(s)), so each thread's contiguous chunk is read without bank conflicts
+__device__ __forceinline__ int PXI(int s) { return s + (s >> 3); }
+
 template <typename W>
 __device__ __forceinline__ W o9_value_x(const W *P1, const W *P2, int wq, bool hasL, int64_t L, bool hasR,
                                         int64_t R, int nless, int nle) {
     W V;
     if (hasL) {
         const int64_t win = (hasR && !(uabs(L) <= uabs(R))) ? R : L;
-        V = (W)win * (P1[wq] - P1[nless]);
+        V = (W)win * (P1[PXI(wq)] - P1[PXI(nless)]);
         int endB = nless;
         if (hasR && nle < endB) {
-            V += (W)R * (P1[endB] - P1[nle]);
+            V += (W)R * (P1[PXI(endB)] - P1[PXI(nle)]);
             endB = nle;
         }
-        V += P2[endB];
+        V += P2[PXI(endB)];
     } else {
-        V = (W)R * (P1[wq] - P1[nle]) + P2[nle];
+        V = (W)R * (P1[PXI(wq)] - P1[PXI(nle)]) + P2[PXI(nle)];
     }
     return V;
 }
@@ -1052,7 +1086,7 @@ template <typename W>
 __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ Node n, const uint32_t *pos_pre) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ W red[32];
-    __shared__ W tot1[MX_T], tot2[MX_T];
+    __shared__ W tot1[32], tot2[32];
     const int B = n.B;
     const int bb = blockIdx.x % B;
     const int r = blockIdx.x / B;
@@ -1060,7 +1094,7 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
     const int qc = n.qc;
     const int wq = n.w[qc];
     W *P1 = reinterpret_cast<W *>(sm);
-    W *P2 = P1 + (wq + 1);
+    W *P2 = P1 + (PXI(wq) + 1);
     const int64_t *cs = n.csorted + uint64_t(r) * wq;
     const uint64_t *S = n.sabs + uint64_t(r) * wq;
     int qp = -1, qf = -1, oc[2] = {-1, -1}, noc = 0;
@@ -1077,52 +1111,51 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
     const int per_tile = (wo + n.tiles - 1) / n.tiles;
     const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
     // --- prefix sums over the |c|-sorted order: the terms x and x*c are staged in P1 / P2
-    //     with coalesced loads (the message is read once); each warp then scans its segment in
-    //     lane-consecutive rounds of 32 (warp shuffles, no bank conflicts), warp 0 scans the
-    //     warp totals, and each warp adds its offset
+    //     with coalesced loads (the message is read once); thread t then scans its contiguous
+    //     chunk in registers, one warp shuffle scan combines the thread totals, thread 0 scans
+    //     the warp totals, and each thread writes its chunk's exclusive prefixes back
     const i128 *x = msg_row_x(n, qc, r, bb);   // delivered in the |c|-sorted order
     for (int s = threadIdx.x; s < wq; s += MX_T) {
         const W xv = (W)x[s];
-        P1[s] = xv;
-        P2[s] = xv * (W)cs[s];
+        P1[PXI(s)] = xv;
+        P2[PXI(s)] = xv * (W)cs[s];
     }
     __syncthreads();
     {
         constexpr int NW = MX_T / 32;
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        const int seg = ((wq + NW - 1) / NW + 31) & ~31;
-        const int a = wid * seg, e = min(wq, a + seg);
-        W c1 = 0, c2 = 0;   // running totals of this warp's segment (warp-uniform)
-        for (int base = a; base < e; base += 32) {
-            const int s = base + lane;
-            const W v1 = s < e ? P1[s] : (W)0, v2 = s < e ? P2[s] : (W)0;
-            W i1 = v1, i2 = v2;
-            for (int o = 1; o < 32; o <<= 1) {
-                const W u1 = shfl_up_w(i1, o), u2 = shfl_up_w(i2, o);
-                if (lane >= o) { i1 += u1; i2 += u2; }
-            }
-            if (s < e) { P1[s] = c1 + i1 - v1; P2[s] = c2 + i2 - v2; }   // exclusive within the segment
-            c1 += shfl_idx_w(i1, 31);
-            c2 += shfl_idx_w(i2, 31);
+        const int ch = (wq + MX_T - 1) / MX_T;
+        const int s0 = min(wq, (int)threadIdx.x * ch), s1 = min(wq, s0 + ch);
+        W t1 = 0, t2 = 0;
+        for (int s = s0; s < s1; ++s) { t1 += P1[PXI(s)]; t2 += P2[PXI(s)]; }
+        W i1 = t1, i2 = t2;
+        for (int o = 1; o < 32; o <<= 1) {
+            const W u1 = shfl_up_w(i1, o), u2 = shfl_up_w(i2, o);
+            if (lane >= o) { i1 += u1; i2 += u2; }
         }
-        if (lane == 0) { tot1[wid] = c1; tot2[wid] = c2; }
+        if (lane == 31) { tot1[wid] = i1; tot2[wid] = i2; }
         __syncthreads();
         if (threadIdx.x == 0) {
             W e1 = 0, e2 = 0;
             for (int w = 0; w < NW; ++w) {
-                const W t1 = tot1[w], t2 = tot2[w];
+                const W a1 = tot1[w], a2 = tot2[w];
                 tot1[w] = e1;
                 tot2[w] = e2;
-                e1 += t1;
-                e2 += t2;
+                e1 += a1;
+                e2 += a2;
             }
-            P1[wq] = e1;
-            P2[wq] = e2;
+            P1[PXI(wq)] = e1;
+            P2[PXI(wq)] = e2;
         }
         __syncthreads();
-        const W o1 = tot1[wid], o2 = tot2[wid];
-        if (wid > 0)
-            for (int s = a + lane; s < e; s += 32) { P1[s] += o1; P2[s] += o2; }
+        W c1 = tot1[wid] + i1 - t1, c2 = tot2[wid] + i2 - t2;   // exclusive prefix at s0
+        for (int s = s0; s < s1; ++s) {
+            const W v1 = P1[PXI(s)], v2 = P2[PXI(s)];
+            P1[PXI(s)] = c1;
+            P2[PXI(s)] = c2;
+            c1 += v1;
+            c2 += v2;
+        }
     }
     __syncthreads();
     // --- outputs
@@ -1139,10 +1172,13 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
         const int64_t *dO = qo >= 0 ? n.data[qo] + uint64_t(r) * wo : nullptr;
         const uint32_t *rO = qo >= 0 ? n.rank[qo] + uint64_t(r) * wo : nullptr;
         const bool f_first = hasF && qo >= 0 && qf < qo;   // fold order when both sit on one side
+        // read-only loads (ld.global.nc) so the loads of later outputs are not held behind this
+        // thread's message stores; unrolled for several outputs in flight
+#pragma unroll 4
         for (int o = o_begin + threadIdx.x; o < o_end; o += blockDim.x) {
             int64_t vo = 0;
             uint32_t ro = 0;
-            if (qo >= 0) { vo = dO[o]; ro = rO[o]; }
+            if (qo >= 0) { vo = __ldg(reinterpret_cast<const long long *>(dO) + o); ro = __ldg(rO + o); }
             bool hasL = false, hasR = false;
             int64_t L = 0, R = 0;
             uint32_t rL = 0, rR = 0;
@@ -1159,10 +1195,13 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
             const int nless = hasL ? (int)(rL & 0xffffu) : 0, nle = hasR ? (int)(rR >> 16) : 0;
             W sacc = o9_value_x<W>(P1, P2, wq, hasL, L, hasR, R, nless, nle);
             if (qp >= 0) {
-                const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
+                const int oo = n.out_perm ? __ldg(n.out_perm + uint64_t(r) * wo + o) : o;
                 reinterpret_cast<i128 *>(n.out)[(uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = (i128)sacc;
             } else {
-                if (xo) sacc *= (W)xo[o];
+                if (xo) {
+                    const longlong2 xv = __ldg(reinterpret_cast<const longlong2 *>(xo) + o);
+                    sacc *= (W)(((i128)xv.y << 64) | (i128)(unsigned long long)xv.x);
+                }
                 acc += sacc;
             }
         }
@@ -2446,7 +2485,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                     while (d * nB * mtiles < 296 && mtiles * MX_T < wo_max) mtiles *= 2;
                     n.tiles = (pe >= 0) ? mtiles : 1;
                     const bool nw = narrow && (*narrow)[i] && !getenv("COMPASS_EST_NO_NARROW");
-                    const size_t sm = size_t(2) * (n.w[n.qc] + 1) * (nw ? 8 : 16);
+                    const size_t sm = size_t(2) * (n.w[n.qc] + (n.w[n.qc] >> 3) + 1) * (nw ? 8 : 16);   // padded prefixes
                     if (sm + 2 * MX_T * 16 + 1024 > 227 * 1024) return fail(SK_EOVERFLOW, "estimate: merged contraction too wide");
                     if (nw) {
                         SKB_CUDA(cudaFuncSetAttribute(k_node_merged_x<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -2564,8 +2603,12 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                     }
                     if (getenv("COMPASS_EST_DEBUG"))
                         fprintf(stderr, "gemm tc bulk: K %d d %d B %d wi %d wj %d\n", K, d, nB, wi, wj);
-                    k_node_mat_gemm_bulk<<<dim3(K * d, tbt * tjt), 128, TC_SMEM2, stream>>>(n, md, qchild, (const unsigned char *)px,
-                                                                                           Mp, tbt, tjt, tkb, 0);
+                    int dev_g = 0, sms_g = 148;
+                    cudaGetDevice(&dev_g);
+                    cudaDeviceGetAttribute(&sms_g, cudaDevAttrMultiProcessorCount, dev_g);
+                    const int ntl = K * d * tbt * tjt;
+                    k_node_mat_gemm_bulk<<<std::min(ntl, sms_g), 192, TC_SMEM2, stream>>>(n, md, qchild, (const unsigned char *)px,
+                                                                                         Mp, tbt, tjt, tkb, 0);
                 } else if (Rc && n.w[qchild] <= 8192 && !(ge && strcmp(ge, "cuda") == 0)) {
                     // tensor cores (tcgen05 kind::i8 on byte planes), same residues
                     static bool attr_set = false;
