@@ -197,6 +197,8 @@ struct Node {
                                 // its constituent values v against the contracted leg's sorted |c| (or null)
     uint64_t *out;              // parent message [K][d][out_bm][w_p], or root partials [K][d][B][tiles]
     int out_bm;
+    int m64;                    // exact engine: bit q = leg q's child message is stored as int64
+    int out64;                  // exact engine: this node's parent message is stored as int64
     int B, tiles, d;
     int64_t b0;
 };
@@ -959,9 +961,28 @@ __device__ __forceinline__ i128 block_sum_i128(i128 v, i128 *red) {
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
     return t;
 }
-__device__ __forceinline__ const i128 *msg_row_x(const Node &n, int q, int r, int bb) {
+// exact messages: int128, or int64 when the producing node's bound is <= 2^61 (narrow merged
+// nodes; half the bytes written and read).  Read-only within a kernel (ld.global.nc).
+struct MsgX {
+    const void *p;
+    bool w64;
+    __device__ __forceinline__ i128 operator[](uint64_t i) const {
+        if (w64) return (i128)__ldg(reinterpret_cast<const long long *>(p) + i);
+        const longlong2 v = __ldg(reinterpret_cast<const longlong2 *>(p) + i);
+        return (i128)(((unsigned __int128)(unsigned long long)v.y << 64) | (unsigned long long)v.x);
+    }
+    __device__ __forceinline__ explicit operator bool() const { return p != nullptr; }
+};
+__device__ __forceinline__ MsgX msg_row_x(const Node &n, int q, int r, int bb) {
     const int bm = n.bm[q];
-    return reinterpret_cast<const i128 *>(n.msg[q]) + (uint64_t(r) * bm + (bm > 1 ? bb : 0)) * (uint64_t)n.w[q];
+    const uint64_t off = (uint64_t(r) * bm + (bm > 1 ? bb : 0)) * (uint64_t)n.w[q];
+    const bool w64 = (n.m64 >> q) & 1;
+    return MsgX{w64 ? (const void *)(reinterpret_cast<const int64_t *>(n.msg[q]) + off)
+                    : (const void *)(reinterpret_cast<const i128 *>(n.msg[q]) + off), w64};
+}
+__device__ __forceinline__ void store_msg_x(const Node &n, uint64_t idx, i128 v) {
+    if (n.out64) reinterpret_cast<int64_t *>(n.out)[idx] = (int64_t)v;
+    else reinterpret_cast<i128 *>(n.out)[idx] = v;
 }
 
 // VEC / MAT node or merged leaf, exact.  blockIdx.x = r*B + bb, blockIdx.y = tile.
@@ -982,8 +1003,8 @@ __global__ void k_node_dense_x(const __grid_constant__ Node n) {
     const int qi = qp >= 0 ? qc0 : qc1;
     const int wo = qo >= 0 ? n.w[qo] : 1;
     const int wi = qi >= 0 ? n.w[qi] : 1;
-    const i128 *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row_x(n, qo, r, bb) : nullptr;
-    const i128 *xi = (qi >= 0) ? msg_row_x(n, qi, r, bb) : nullptr;
+    const MsgX xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row_x(n, qo, r, bb) : MsgX{nullptr, false};
+    const MsgX xi = (qi >= 0) ? msg_row_x(n, qi, r, bb) : MsgX{nullptr, false};
     i128 acc = 0;
     const int per_tile = (wo + n.tiles - 1) / n.tiles;
     const int o_begin = blockIdx.y * per_tile, o_end = min(wo, o_begin + per_tile);
@@ -1000,7 +1021,7 @@ __global__ void k_node_dense_x(const __grid_constant__ Node n) {
         }
         if (qp >= 0) {
             const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
-            reinterpret_cast<i128 *>(n.out)[(uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = s;
+            store_msg_x(n, (uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo, s);
         } else {
             if (xo) s *= xo[o];
             acc += s;
@@ -1114,7 +1135,7 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
     //     with coalesced loads (the message is read once); thread t then scans its contiguous
     //     chunk in registers, one warp shuffle scan combines the thread totals, thread 0 scans
     //     the warp totals, and each thread writes its chunk's exclusive prefixes back
-    const i128 *x = msg_row_x(n, qc, r, bb);   // delivered in the |c|-sorted order
+    const MsgX x = msg_row_x(n, qc, r, bb);   // delivered in the |c|-sorted order
     for (int s = threadIdx.x; s < wq; s += MX_T) {
         const W xv = (W)x[s];
         P1[PXI(s)] = xv;
@@ -1159,8 +1180,8 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
     }
     __syncthreads();
     // --- outputs
-    const i128 *xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row_x(n, qo, r, bb) : nullptr;
-    const i128 *xi2 = qi >= 0 ? msg_row_x(n, qi, r, bb) : nullptr;
+    const MsgX xo = (qo >= 0 && n.role[qo] == RCHILD) ? msg_row_x(n, qo, r, bb) : MsgX{nullptr, false};
+    const MsgX xi2 = qi >= 0 ? msg_row_x(n, qi, r, bb) : MsgX{nullptr, false};
     W acc = 0;
     // no inner leg and rank tables present (the common case): the fixed leg's value and rank
     // are loop invariants, only the outer leg's constituent varies per output
@@ -1196,12 +1217,9 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
             W sacc = o9_value_x<W>(P1, P2, wq, hasL, L, hasR, R, nless, nle);
             if (qp >= 0) {
                 const int oo = n.out_perm ? __ldg(n.out_perm + uint64_t(r) * wo + o) : o;
-                reinterpret_cast<i128 *>(n.out)[(uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = (i128)sacc;
+                store_msg_x(n, (uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo, (i128)sacc);
             } else {
-                if (xo) {
-                    const longlong2 xv = __ldg(reinterpret_cast<const longlong2 *>(xo) + o);
-                    sacc *= (W)(((i128)xv.y << 64) | (i128)(unsigned long long)xv.x);
-                }
+                if (xo) sacc *= (W)xo[o];
                 acc += sacc;
             }
         }
@@ -1219,7 +1237,7 @@ __global__ void __launch_bounds__(MX_T) k_node_merged_x(const __grid_constant__ 
         }
         if (qp >= 0) {
             const int oo = n.out_perm ? n.out_perm[uint64_t(r) * wo + o] : o;
-            reinterpret_cast<i128 *>(n.out)[(uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo] = (i128)sacc;
+            store_msg_x(n, (uint64_t(r) * n.out_bm + (n.out_bm > 1 ? bb : 0)) * wo + oo, (i128)sacc);
         } else {
             if (xo) sacc *= (W)xo[o];
             acc += sacc;
@@ -2376,6 +2394,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
     // message buffers per local edge
     std::vector<uint64_t *> msg(E, nullptr);
     std::vector<int> msg_bm(E, 1);
+    std::vector<char> msg64(E, 0);   // exact engine: the edge's message is stored as int64
     for (int i : order) {
         const int pe = parent_edge[i];
         if (pe < 0) continue;
@@ -2405,7 +2424,11 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                 const int le = t.legs[q];
                 n.w[q] = P.width[le];
                 n.role[q] = (le == P.cond) ? RFIXED : (le == pe ? RPARENT : RCHILD);
-                if (n.role[q] == RCHILD) { n.msg[q] = msg[le]; n.bm[q] = msg_bm[le]; }
+                if (n.role[q] == RCHILD) {
+                    n.msg[q] = msg[le];
+                    n.bm[q] = msg_bm[le];
+                    if (msg64[le]) n.m64 |= 1 << q;
+                }
                 n.data[q] = (t.kind == KG) ? data[i][q] : data[i][0];
             }
             // nodes whose message does not depend on b are computed once (first chunk)
@@ -2485,6 +2508,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                     while (d * nB * mtiles < 296 && mtiles * MX_T < wo_max) mtiles *= 2;
                     n.tiles = (pe >= 0) ? mtiles : 1;
                     const bool nw = narrow && (*narrow)[i] && !getenv("COMPASS_EST_NO_NARROW");
+                    if (nw && pe >= 0) { n.out64 = 1; msg64[pe] = 1; }   // |message| <= node bound <= 2^61
                     const size_t sm = size_t(2) * (n.w[n.qc] + (n.w[n.qc] >> 3) + 1) * (nw ? 8 : 16);   // padded prefixes
                     if (sm + 2 * MX_T * 16 + 1024 > 227 * 1024) return fail(SK_EOVERFLOW, "estimate: merged contraction too wide");
                     if (nw) {
