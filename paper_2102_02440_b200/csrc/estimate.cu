@@ -721,12 +721,16 @@ __global__ void k_planes_m(const uint32_t *Rc, int Kd, int wi, int wj, int njt, 
                 w[a][q] = ((v[0] >> (8 * a)) & 0xFF) | (((v[1] >> (8 * a)) & 0xFF) << 8) | (((v[2] >> (8 * a)) & 0xFF) << 16) |
                           (((v[3] >> (8 * a)) & 0xFF) << 24);
         }
+        // the 4 limb planes stacked along N (row a * 64 + j of one 256-row K-major operand,
+        // 16-byte K chunks 4096 B apart): one N = 256 MMA per x limb covers all 4 M limbs
         const int kb = c16 >> 2, c = c16 & 3;
         unsigned char *chunk = out + ((uint64_t(kr) * njt + jt) * nkb + kb) * (4 * TC_B_PLANE);
-        const int off = c * (TC_N * 16) + (jr >> 3) * 128 + (jr & 7) * 16;
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
-            *reinterpret_cast<uint4 *>(chunk + a * TC_B_PLANE + off) = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
+        for (int a = 0; a < 4; ++a) {
+            const int jj = a * TC_N + jr;
+            *reinterpret_cast<uint4 *>(chunk + c * (4 * TC_N * 16) + (jj >> 3) * 128 + (jj & 7) * 16) =
+                make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
+        }
     }
 }
 
@@ -791,10 +795,14 @@ __global__ void __launch_bounds__(192, 1) k_node_mat_gemm_bulk(const __grid_cons
         __syncwarp();
     } else if (warp == 5) {
         if (lane == 0) {   // MMA issuer
-            const uint32_t idesc = (2u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+            // x limb a times all 4 M limbs in one N = 256 MMA: columns [64 a, 64 a + 256) of TMEM
+            // are exactly D_a .. D_{a+3}, so every product lands on its shift s = a + c
+            const uint32_t idesc = (2u << 4) | ((uint32_t)((4 * TC_N) >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+            const uint32_t idesc3 = (2u << 4) | ((uint32_t)((3 * TC_N) >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+            const uint32_t idesc1 = (2u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
             uint32_t g = 0, li = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++li) {
-                if (li > 0) tc_mbar_wait(tempty, (li - 1) & 1);   // the epilogue has read the previous tile
+                tc_mbar_wait(tempty, li & 1);   // the epilogue has read the previous tile
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 for (int kb = 0; kb < nkb; ++kb, ++g) {
                     const uint32_t st = g % TC_ST2;
@@ -804,16 +812,25 @@ __global__ void __launch_bounds__(192, 1) k_node_mat_gemm_bulk(const __grid_cons
 #pragma unroll
                     for (int a = 0; a < 4; ++a)
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            const int s = a + c;
-#pragma unroll
-                            for (int ks = 0; ks < TC_KB / 32; ++ks) {
-                                const bool first = kb == 0 && ks == 0 && (s <= 3 ? a == 0 : c == 3);
-                                const uint64_t ad = tc_sdesc(a_s + a * TC_A_PLANE + ks * 2 * (TC_M * 16), TC_M * 16, 128);
-                                const uint64_t bd = tc_sdesc(b_s + c * TC_B_PLANE + ks * 2 * (TC_N * 16), TC_N * 16, 128);
+                        for (int ks = 0; ks < TC_KB / 32; ++ks) {
+                            const uint64_t ad = tc_sdesc(a_s + a * TC_A_PLANE + ks * 2 * (TC_M * 16), TC_M * 16, 128);
+                            const uint32_t bs = b_s + ks * 2 * (4 * TC_N * 16);
+                            const uint32_t dt = tmem + (uint32_t)(a * TC_N);
+                            if (kb == 0 && ks == 0 && a > 0) {
+                                // first touch of D_{a+3}: M limbs 0-2 accumulate into D_a..D_{a+2},
+                                // limb 3 overwrites D_{a+3} (no zeroing pass needed)
                                 asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                                             "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + (uint32_t)(s * TC_N)),
-                                             "l"(ad), "l"(bd), "r"(idesc), "r"(first ? 0u : 1u) : "memory");
+                                             "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+                                             "l"(ad), "l"(tc_sdesc(bs, 4 * TC_N * 16, 128)), "r"(idesc3), "r"(1u) : "memory");
+                                asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                             "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt + (uint32_t)(3 * TC_N)),
+                                             "l"(ad), "l"(tc_sdesc(bs + (3 * TC_N / 8) * 128, 4 * TC_N * 16, 128)), "r"(idesc1), "r"(0u)
+                                             : "memory");
+                            } else {
+                                asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                             "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+                                             "l"(ad), "l"(tc_sdesc(bs, 4 * TC_N * 16, 128)), "r"(idesc),
+                                             "r"((kb == 0 && ks == 0) ? 0u : 1u) : "memory");
                             }
                         }
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(empty0 + 8 * st) : "memory");
@@ -823,6 +840,13 @@ __global__ void __launch_bounds__(192, 1) k_node_mat_gemm_bulk(const __grid_cons
         }
         __syncwarp();
     } else {   // epilogue: warps 0-3, TMEM lanes 32 w .. 32 w + 31 = rows b
+        // release TMEM to the issuer (initially, then after each tile's last read)
+        auto release_acc = [&]() {
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty) : "memory");
+        };
+        release_acc();
         uint32_t li = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++li) {
             const int jt = t % njt, bt = (t / njt) % nbt, kr = t / (njt * nbt);
@@ -839,23 +863,28 @@ __global__ void __launch_bounds__(192, 1) k_node_mat_gemm_bulk(const __grid_cons
                 uint64_t acc[16];
 #pragma unroll
                 for (int u = 0; u < 16; ++u) acc[u] = 0;
+                // the 7 loads of this column chunk in flight together, one wait; the empty asm
+                // ties the registers to the wait so no use is scheduled before it
+                uint32_t v[7][16];
 #pragma unroll
                 for (int s = 0; s < 7; ++s) {
-                    uint32_t v[16];
                     const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(s * TC_N + col);
                     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                                 : "=r"(v[s][0]), "=r"(v[s][1]), "=r"(v[s][2]), "=r"(v[s][3]), "=r"(v[s][4]), "=r"(v[s][5]),
+                                   "=r"(v[s][6]), "=r"(v[s][7]), "=r"(v[s][8]), "=r"(v[s][9]), "=r"(v[s][10]), "=r"(v[s][11]),
+                                   "=r"(v[s][12]), "=r"(v[s][13]), "=r"(v[s][14]), "=r"(v[s][15])
                                  : "r"(ta));
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) acc[u] += (uint64_t)v[u] * pw[s];
+                for (int s = 0; s < 7; ++s) {
+                    asm volatile("" : "+r"(v[s][0]), "+r"(v[s][1]), "+r"(v[s][2]), "+r"(v[s][3]), "+r"(v[s][4]), "+r"(v[s][5]),
+                                      "+r"(v[s][6]), "+r"(v[s][7]), "+r"(v[s][8]), "+r"(v[s][9]), "+r"(v[s][10]), "+r"(v[s][11]),
+                                      "+r"(v[s][12]), "+r"(v[s][13]), "+r"(v[s][14]), "+r"(v[s][15]));
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) acc[u] += (uint64_t)v[s][u] * pw[s];
                 }
-                if (col + 16 == TC_N) {   // every accumulator column read: release TMEM early
-                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                    __syncwarp();
-                    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty) : "memory");
-                }
+                if (col + 16 == TC_N) release_acc();   // every accumulator column read
                 if (b < n.B) {
                     const int jb = j0 + col;
 #pragma unroll
