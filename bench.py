@@ -383,6 +383,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--wire", default="i32", choices=["i32", "i64"], help="all-reduce wire format (N > 1)")
     ap.add_argument("--no-overlap", action="store_true", help="one trailing all-reduce instead of per-table ones")
+    ap.add_argument("--row-shard", action="store_true",
+                    help="reduce-scatter by sketch row + row-sharded composition instead of the all-reduce (graph workloads)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(_relaunch(args.gpus))
@@ -422,6 +424,15 @@ def main():
             run.build_table(t.name, data[t.name], preds[t.name], stream=stream)
             if record:
                 kev.append((a, ev()))
+        if args.row_shard and subplans is not None:
+            # lever iii: reduce-scatter by sketch row, row-sharded composition, one all-gather
+            # of the per-row exact values per greedy level
+            shards, own = run.merge_rows()
+            s1 = ev() if record else None
+            plan = run.plan_greedy_rowshard(shards, own)
+            if record:
+                pev.append((s0, s1, ev()))
+            return None, plan
         run.allreduce()
         s1 = ev() if record else None
         g = run.graph()
@@ -502,9 +513,10 @@ def main():
                        "sketches": [f"{s.table}:{'x'.join(map(str, s.w))}xd{s.d}" for s in ws.sketches],
                        "subplans": len(subplans) if subplans else len(ests),
                        "l2": "inputs larger than L2 (no flush)" if ab["full"] > 4 * 126e6 else "inputs L2-resident",
-                       "parallelism": f"row-sharded x{world}" + (f" + NCCL SUM all-reduce ({run.merge.wire} wire, "
-                                                                  f"{'per-table overlapped' if run.merge.overlap else 'one trailing'})"
-                                                                  if world > 1 else "")},
+                       "parallelism": f"row-sharded x{world}" + (
+                           " + NCCL reduce-scatter by sketch row, row-sharded composition" if (args.row_shard and subplans)
+                           else (f" + NCCL SUM all-reduce ({run.merge.wire} wire, "
+                                 f"{'per-table overlapped' if run.merge.overlap else 'one trailing'})" if world > 1 else ""))},
             "roofline": roof, "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "survivors": run.survivors.tolist(), "estimates": ests[:8] if ests else None,

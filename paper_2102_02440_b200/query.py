@@ -176,9 +176,13 @@ class QueryRun:
                 return sk
         raise KeyError((table, edge_ids))
 
-    def graph(self, survivors=None) -> JoinGraph:
+    def graph(self, survivors=None, sketches=None) -> JoinGraph:
+        """JoinGraph over the merged sketches (or `sketches`, one per q.sketches entry, e.g.
+        the row shards of merge_rows)."""
         if survivors is None:
             survivors = self.survivors.tolist()
+        if sketches is None:
+            sketches = self.sketches
         # graph vertices in alias order: index order is the tie-break order of plan_greedy
         gnames = sorted(self.tnames)
         surv_by = dict(zip(self.tnames, survivors))
@@ -187,20 +191,64 @@ class QueryRun:
         if getattr(self.q, "kind", "graph") == "selfjoin":
             # self-join size per key sketch (F2): the sketch meets itself on one edge
             names, surv, mats = [], [], []
-            for s, sk in zip(self.q.sketches, self.sketches):
+            for s, sk in zip(self.q.sketches, sketches):
                 i = len(names)
                 names += [f"{s.table}.{s.key_cols[0]}", f"{s.table}.{s.key_cols[0]}'"]
                 surv += [surv_by[s.table]] * 2
                 edges.append((i, i + 1, sk, sk))
             return JoinGraph(names, surv, edges, mats)
+        def sk_of(table, eids):
+            for s, sk in zip(self.q.sketches, sketches):
+                if s.table == table and list(s.edge_ids) == list(eids):
+                    return sk
+            raise KeyError((table, eids))
         for eid, u, v in self.q.edges:
-            edges.append((tix[u], tix[v], self.sketch_of(u, [eid]), self.sketch_of(v, [eid])))
+            edges.append((tix[u], tix[v], sk_of(u, [eid]), sk_of(v, [eid])))
         mats = []
-        for s, sk in zip(self.q.sketches, self.sketches):
+        for s, sk in zip(self.q.sketches, sketches):
             if len(s.edge_ids) >= 2:   # matrices and 3-D tensors
                 eids = [e[0] for e in self.q.edges]
                 mats.append((tix[s.table], eids.index(s.edge_ids[0]), eids.index(s.edge_ids[1]), sk))
         return JoinGraph(gnames, [surv_by[n] for n in gnames], edges, mats)
+
+    # ---- row-sharded merge and composition (SURVEY.md §8(e) lever iii; rowshard.py)
+    def merge_rows(self, group=None):
+        """Reduce-scatter by sketch row instead of the all-reduce: this rank receives the
+        merged rows row_ranges(d, N)[rank] of every sketch (plus zero rows up to an odd count)
+        and the merged survivor counts.  Returns (row-shard Sketch per q.sketches entry,
+        own row count)."""
+        import torch.distributed as dist
+        from . import rowshard as rs
+        d = self.q.sketches[0].d
+        assert all(s.d == d for s in self.q.sketches), "row sharding needs one d for the query"
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        chunk = rs.reduce_scatter_rows([sk.counters for sk in self.sketches], d, group)
+        if world > 1:
+            dist.all_reduce(self.survivors, op=dist.ReduceOp.SUM, group=group)
+        R = rs.shard_rows(d, world)
+        cells = [sk.counters[0].numel() for sk in self.sketches]
+        _, offs = rs.chunk_layout(cells, R)
+        shards = []
+        for s, o, n in zip(self.q.sketches, offs, cells):
+            shards.append(Sketch(R, s.w, s.edge_ids, self.q.master_seed, self.device,
+                                 counters=chunk[o:o + R * n].view(R, *s.w)))
+        self._row_chunk = chunk   # keeps the views alive
+        r0, r1 = rs.row_ranges(d, world)[rank]
+        return shards, r1 - r0
+
+    def plan_greedy_rowshard(self, shards, own_rows: int, group=None):
+        """Greedy plan from row-sharded estimates: each level's candidate sub-plans are
+        evaluated on this rank's rows (exact per-row values), one all-gather per level."""
+        from . import rowshard as rs
+        surv = dict(zip(self.tnames, self.survivors.tolist()))
+        g = self.graph(survivors=[surv[n] for n in self.tnames], sketches=shards)
+
+        def rows_of_batch(subsets):
+            if own_rows == 0:
+                return [[] for _ in subsets]
+            return [g.estimate_join_exact(S)[:own_rows] for S in subsets]
+        return rs.plan_greedy_gathered(surv, self.q.edges, rows_of_batch, rs.gather_objects(group))
 
     def close(self):
         for sk in self.sketches:

@@ -108,3 +108,56 @@ def test_nccl_merge_path_on_one_gpu(mode, tmp_path):
     mp.start_processes(_worker_one, args=(1, _free_port(), mode, out), nprocs=1, join=True, start_method="spawn")
     res = torch.load(out)
     assert np.array_equal(res["buf"].numpy(), _oracle_packed(datagen.c5(scale=2e-4, w=128, wm=64)))
+
+
+def _worker_rows(rank, world, port, cycle, out_path):
+    """Row-sharded merge over NCCL (reduce-scatter by sketch row) and the greedy over gathered
+    per-row values; on one GPU the group has one rank (the collectives still run)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    gpu = rank if torch.cuda.device_count() > 1 else 0
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    import datagen
+    from paper_2102_02440_b200.query import QueryRun
+    ws = datagen.c5(scale=2e-4, w=128, wm=64, cycle=cycle)
+    run = QueryRun(ws, dev)
+    for t in ws.tables:
+        run.build_table(t.name, datagen.generate_table(ws, t.name, dev, rank=rank, world=world),
+                        datagen.resolve_preds(ws, t.name))
+    shards, own = run.merge_rows()
+    plan = run.plan_greedy_rowshard(shards, own)
+    plans = [None] * world
+    dist.all_gather_object(plans, plan)
+    if rank == 0:
+        torch.save({"plans": plans}, out_path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cycle", [False, True])
+def test_nccl_row_sharded_plan_equals_oracle(cycle, tmp_path):
+    """SURVEY.md §8(e) lever iii on NCCL: every rank's plan equals the oracle's greedy plan on
+    the single-process build (all visible GPUs, at least a one-rank group)."""
+    import datagen
+    import oracle
+    from paper_2102_02440_b200.query import packed_layout
+    world = max(1, min(torch.cuda.device_count(), 8))
+    out = str(tmp_path / "rows.pt")
+    mp.start_processes(_worker_rows, args=(world, _free_port(), cycle, out), nprocs=world, join=True,
+                       start_method="spawn")
+    res = torch.load(out)
+    ws = datagen.c5(scale=2e-4, w=128, wm=64, cycle=cycle)
+    buf = _oracle_packed(ws)
+    _, lay = packed_layout(ws)
+    vec, mat = {}, {}
+    for (o, n), s in zip(lay, ws.sketches):
+        arr = buf[o:o + n].reshape(s.d, *s.w)
+        if len(s.w) == 1:
+            vec[(s.table, s.edge_ids[0])] = arr
+        else:
+            mat[(s.table, tuple(s.edge_ids))] = arr
+    og = oracle.Graph({t.name: int(buf[i]) for i, t in enumerate(ws.tables)}, ws.edges, vec, mat)
+    o_order, o_pre, _ = oracle.plan_greedy(og)
+    for order, pre, _ in res["plans"]:
+        assert tuple(order) == tuple(o_order) and pre == o_pre

@@ -100,3 +100,100 @@ def test_two_rank_per_table_and_int32_wire_merge(mode, tmp_path):
     ws = getattr(datagen, cfg[0])(**cfg[1])
     single, _ = _build_packed(ws, 0, 1)
     assert torch.equal(merged, single)
+
+
+# ------------------------------------------------------------------ row-sharded merge + composition (§8(e) iii)
+def _worker_rowshard(rank, world, port, cfg, out_path):
+    """Partial sketches of this rank's table rows -> reduce-scatter by sketch row -> exact
+    per-row values of this rank's rows from its shard only -> greedy over gathered rows."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import datagen
+    import oracle
+    from paper_2102_02440_b200 import rowshard as rs
+    from paper_2102_02440_b200.query import packed_layout
+    ws = getattr(datagen, cfg[0])(**cfg[1])
+    buf, names = _build_packed(ws, rank, world)
+    _, lay = packed_layout(ws)
+    d = ws.sketches[0].d
+    views = [buf[o:o + n].view(s.d, *s.w) for (o, n), s in zip(lay, ws.sketches)]
+    chunk = rs.reduce_scatter_rows(views, d)
+    surv = buf[:len(names)].clone()
+    dist.all_reduce(surv, op=dist.ReduceOp.SUM)
+    R = rs.shard_rows(d, world)
+    cells = [v[0].numel() for v in views]
+    _, offs = rs.chunk_layout(cells, R)
+    r0, r1 = rs.row_ranges(d, world)[rank]
+    vec, mat = {}, {}
+    for s, o, n in zip(ws.sketches, offs, cells):
+        arr = chunk[o:o + R * n].view(R, *s.w).numpy()
+        if len(s.w) == 1:
+            vec[(s.table, s.edge_ids[0])] = arr
+        else:
+            mat[(s.table, tuple(s.edge_ids))] = arr
+    tables = dict(zip(names, [int(x) for x in surv.tolist()]))
+    shard_graph = oracle.Graph(tables, ws.edges, vec, mat)
+
+    def rows_of_batch(subsets):
+        return [oracle.estimate_rows(shard_graph, S)[:r1 - r0] for S in subsets]
+    plan = rs.plan_greedy_gathered(tables, ws.edges, rows_of_batch, rs.gather_objects())
+    # this rank's rows of every 2- and 3-table connected sub-plan, for the parent's check
+    subs = [S for S in oracle.connected_subplans(shard_graph) if 2 <= len(S) <= 3]
+    mine = {S: oracle.estimate_rows(shard_graph, S)[:r1 - r0] for S in subs}
+    allp = [None] * world
+    dist.all_gather_object(allp, (r0, r1, mine))
+    if rank == 0:
+        torch.save({"plan": plan, "rows": allp}, out_path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("cfg", [("c5", {"scale": 5e-5, "w": 64, "wm": 32}),
+                                 ("c5", {"scale": 5e-5, "w": 64, "wm": 32, "cycle": True}),
+                                 ("c2", {"scale": 2e-4})])
+def test_row_sharded_merge_and_greedy_equal_single_device(cfg, world, tmp_path):
+    """Reduce-scatter by sketch row + row-sharded composition (SURVEY.md §8(e) lever iii):
+    every rank's rows of every sub-plan equal the single-device oracle's rows, and the
+    greedy plan from gathered rows equals oracle.plan_greedy on the merged sketches."""
+    import datagen
+    import oracle
+    from paper_2102_02440_b200.query import packed_layout
+    out = str(tmp_path / "rs.pt")
+    mp.start_processes(_worker_rowshard, args=(world, _free_port(), cfg, out), nprocs=world, join=True,
+                       start_method="spawn")
+    res = torch.load(out)
+    ws = getattr(datagen, cfg[0])(**cfg[1])
+    single, names = _build_packed(ws, 0, 1)
+    _, lay = packed_layout(ws)
+    vec, mat = {}, {}
+    for (o, n), s in zip(lay, ws.sketches):
+        arr = single[o:o + n].view(s.d, *s.w).numpy()
+        if len(s.w) == 1:
+            vec[(s.table, s.edge_ids[0])] = arr
+        else:
+            mat[(s.table, tuple(s.edge_ids))] = arr
+    og = oracle.Graph(dict(zip(names, [int(x) for x in single[:len(names)].tolist()])), ws.edges, vec, mat)
+    for r0, r1, mine in res["rows"]:
+        for S, rows in mine.items():
+            assert rows == oracle.estimate_rows(og, S)[r0:r1], (S, r0, r1)
+    assert tuple(res["plan"][0]) == tuple(oracle.plan_greedy(og)[0])
+    assert res["plan"][1] == oracle.plan_greedy(og)[1]
+
+
+def test_row_ranges_and_pack_layout():
+    from paper_2102_02440_b200 import rowshard as rs
+    for d in (1, 5, 7, 9):
+        for world in (1, 2, 3, 8):
+            rr = rs.row_ranges(d, world)
+            assert rr[0][0] == 0 and rr[-1][1] == d and all(a[1] == b[0] for a, b in zip(rr, rr[1:]))
+            assert max(b - a for a, b in rr) - min(b - a for a, b in rr) <= 1
+            R = rs.shard_rows(d, world)
+            assert R % 2 == 1 and R >= max(b - a for a, b in rr)
+    c = [torch.arange(5 * 4).view(5, 4), 100 + torch.arange(5 * 6).view(5, 2, 3)]
+    send = rs.pack_rows(c, 5, 2)   # ranks get rows [0,3) and [3,5); R = 3
+    clen = send.numel() // 2
+    assert clen == 3 * 4 + 3 * 6
+    assert torch.equal(send[:12], c[0][0:3].reshape(-1)) and torch.equal(send[12:30], c[1][0:3].reshape(-1))
+    assert torch.equal(send[30:38], c[0][3:5].reshape(-1)) and torch.equal(send[38:42], torch.zeros(4, dtype=send.dtype))
+    assert torch.equal(send[42:54], c[1][3:5].reshape(-1)) and torch.equal(send[54:60], torch.zeros(6, dtype=send.dtype))

@@ -408,3 +408,51 @@ def test_cycle_gemm_tensor_cores_equal_cuda_cores(T, w, feed, capfd, monkeypatch
     monkeypatch.setenv("COMPASS_GEMM", "cuda")
     og2, jg2, _ = _matrix_ring(np.random.default_rng(T * 7 + w), T, w, 5, 1 << 30)
     assert jg2.estimate_join_exact(full) == tc
+
+
+# ------------------------------------------------------------------ row-sharded composition on the device (§8(e) iii)
+@pytest.mark.parametrize("cycle", [False, True])
+def test_row_shard_estimates_and_plan_on_device(cycle):
+    """The row-shard sketches of rowshard.pack_rows (as 2 and 3 ranks would receive them
+    after the reduce-scatter) evaluated by the library's exact estimator: the rows of every
+    connected sub-plan concatenate to the full sketches' rows, and merge_rows +
+    plan_greedy_rowshard (one process) give plan_greedy's plan."""
+    from paper_2102_02440_b200 import rowshard as rs
+    ws = datagen.c5(scale=2e-4, cycle=cycle, w=128, wm=64)
+    dev = _dev()
+    run = QueryRun(ws, dev)
+    data = {t.name: datagen.generate_table(ws, t.name, dev) for t in ws.tables}
+    preds = {t.name: datagen.resolve_preds(ws, t.name) for t in ws.tables}
+    run.build(data, preds)
+    torch.cuda.synchronize()
+    full = run.graph()
+    d = ws.sketches[0].d
+    adj = {t.name: set() for t in ws.tables}
+    for _, u, v in ws.edges:
+        adj[u].add(v)
+        adj[v].add(u)
+    subs, frontier = set(), {(t.name,) for t in ws.tables}
+    while frontier:   # connected sub-plans, grown one neighbour at a time
+        subs |= frontier
+        frontier = {tuple(sorted(S + (x,))) for S in frontier for a in S for x in adj[a] if x not in S} - subs
+    want = {S: full.estimate_join_exact(S) for S in subs if len(S) > 1}
+    counters = [sk.counters for sk in run.sketches]
+    for world in (2, 3):
+        send = rs.pack_rows(counters, d, world)
+        clen = send.numel() // world
+        R = rs.shard_rows(d, world)
+        cells = [c[0].numel() for c in counters]
+        _, offs = rs.chunk_layout(cells, R)
+        got = {S: [] for S in want}
+        for rank, (r0, r1) in enumerate(rs.row_ranges(d, world)):
+            chunk = send[rank * clen:(rank + 1) * clen]
+            shards = [pb.Sketch(R, s.w, s.edge_ids, ws.master_seed, dev, counters=chunk[o:o + R * n].view(R, *s.w))
+                      for s, o, n in zip(ws.sketches, offs, cells)]
+            g = run.graph(sketches=shards)
+            for S in want:
+                got[S] += g.estimate_join_exact(S)[:r1 - r0]
+        assert got == want, world
+    shards, own = run.merge_rows()
+    order, pre, cost = run.plan_greedy_rowshard(shards, own)
+    o2, p2, c2 = full.plan_greedy()
+    assert (tuple(order), pre, cost) == (tuple(o2), p2, c2)
