@@ -1590,18 +1590,39 @@ __global__ void k_root_reduce_x(const i128 *part, i128 *acc, int slots) {
 // shared by every chain sub-plan through that matrix.
 __global__ void k_mat_residues(const int64_t *T, int d, int w0, int w1, int qc, const __grid_constant__ Mods md,
                                uint32_t *Rc) {
-    const uint64_t cells = uint64_t(w0) * w1, total = cells * d;
+    // 32 x 32 tiles of row r (blockIdx.z) of the matrix, staged through shared memory so the
+    // int64 reads and the K uint32 writes per element are both coalesced in either
+    // orientation (Rc[k][r][i][o], i = the contracted leg); widths are powers of two
+    __shared__ int64_t tile[32][33];
     const int wi = qc == 0 ? w0 : w1, wo = qc == 0 ? w1 : w0;
-    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t r = e / cells, c = e % cells;
-        const int i = (int)(c / wo), o = (int)(c % wo);
-        const int64_t v = qc == 0 ? T[r * cells + uint64_t(i) * w1 + o] : T[r * cells + uint64_t(o) * w1 + i];
-        const uint64_t av = uabs(v);
-        for (int k = 0; k < md.K; ++k) {
-            uint64_t rv = mm_red(av, md.m[k], md.mu[k]);
-            if (v < 0 && rv) rv = md.m[k] - rv;
-            Rc[(uint64_t(k) * d + r) * cells + c] = (uint32_t)rv;
+    const uint64_t cells = uint64_t(w0) * w1;
+    const int r = blockIdx.z;
+    const int64_t *Tr = T + uint64_t(r) * cells;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 256 threads: 32 x 8
+    const int ntx = (wo + 31) / 32;
+    for (int tb = blockIdx.x; tb < ntx * ((wi + 31) / 32); tb += gridDim.x) {
+        const int i0 = (tb / ntx) * 32, o0 = (tb % ntx) * 32;
+        // load the T block in its storage order (row-major [w0][w1]), coalesced along w1
+        for (int y = ty; y < 32; y += 8) {
+            int a, b;   // storage coordinates (row, col) of tile element (y, tx)
+            if (qc == 0) { a = i0 + y; b = o0 + tx; }   // T[i][o]
+            else { a = o0 + y; b = i0 + tx; }           // T[o][i]
+            tile[y][tx] = (a < w0 && b < w1) ? Tr[uint64_t(a) * w1 + b] : 0;
         }
+        __syncthreads();
+        for (int y = ty; y < 32; y += 8) {
+            const int i = i0 + y, o = o0 + tx;
+            if (i >= wi || o >= wo) continue;
+            const int64_t v = qc == 0 ? tile[y][tx] : tile[tx][y];
+            const uint64_t av = uabs(v);
+            const uint64_t c = uint64_t(i) * wo + o;
+            for (int k = 0; k < md.K; ++k) {
+                uint64_t rv = mm_red(av, md.m[k], md.mu[k]);
+                if (v < 0 && rv) rv = md.m[k] - rv;
+                Rc[(uint64_t(k) * d + r) * cells + c] = (uint32_t)rv;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -2564,7 +2585,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                     void *rb;
                     const size_t cells = size_t(n.w[0]) * n.w[1];
                     if ((st = dalloc(pool, size_t(resmods->K) * d * cells * 4, stream, &rb))) return st;
-                    k_mat_residues<<<1184, 256, 0, stream>>>(n.data[0], d, n.w[0], n.w[1], qchild, *resmods, (uint32_t *)rb);
+                    k_mat_residues<<<dim3(std::max(1, 1184 / d), 1, d), 256, 0, stream>>>(n.data[0], d, n.w[0], n.w[1], qchild, *resmods, (uint32_t *)rb);
                     count_launch();
                     Rc = (uint32_t *)rb;
                     (*rescache)[key] = Rc;
@@ -2589,7 +2610,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                     void *rb;
                     const size_t cells = size_t(n.w[0]) * n.w[1];
                     if ((st = dalloc(pool, size_t(resmods->K) * d * cells * 4, stream, &rb))) return st;
-                    k_mat_residues<<<1184, 256, 0, stream>>>(n.data[0], d, n.w[0], n.w[1], qc, *resmods, (uint32_t *)rb);
+                    k_mat_residues<<<dim3(std::max(1, 1184 / d), 1, d), 256, 0, stream>>>(n.data[0], d, n.w[0], n.w[1], qc, *resmods, (uint32_t *)rb);
                     count_launch();
                     Rc = (uint32_t *)rb;
                     (*rescache)[key] = Rc;
@@ -2617,7 +2638,7 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                         void *rb;
                         const size_t cells = size_t(n.w[0]) * n.w[1];
                         if ((st = dalloc(pool, size_t(resmods->K) * d * cells * 4, stream, &rb))) return st;
-                        k_mat_residues<<<1184, 256, 0, stream>>>(n.data[0], d, n.w[0], n.w[1], qchild, *resmods, (uint32_t *)rb);
+                        k_mat_residues<<<dim3(std::max(1, 1184 / d), 1, d), 256, 0, stream>>>(n.data[0], d, n.w[0], n.w[1], qchild, *resmods, (uint32_t *)rb);
                         count_launch();
                         (*rescache)[key] = (uint32_t *)rb;
                         Rc = (uint32_t *)rb;
