@@ -29,10 +29,10 @@
 #include "scan_kernel.cuh"
 
 namespace skb {
-const void *scan_pick_nk1(uint32_t np, int kw, bool fast, int sub);   // scan_k1.cu
-const void *scan_pick_nk2(uint32_t np, int kw, bool fast, int sub);   // scan_k2.cu
-const void *scan_pick_nk3(uint32_t np, int kw, bool fast, int sub);   // scan_k3.cu
-const void *scan_pick_nk4(uint32_t np, int kw, bool fast, int sub);   // scan_k4.cu
+const void *scan_pick_nk1(uint32_t np, int kw, bool fast, int sub, bool t3);   // scan_k1.cu
+const void *scan_pick_nk2(uint32_t np, int kw, bool fast, int sub, bool t3);   // scan_k2.cu
+const void *scan_pick_nk3(uint32_t np, int kw, bool fast, int sub, bool t3);   // scan_k3.cu
+const void *scan_pick_nk4(uint32_t np, int kw, bool fast, int sub, bool t3);   // scan_k4.cu
 }  // namespace skb
 
 namespace {
@@ -118,12 +118,12 @@ __global__ void k_lutx_build(const uint64_t *seeds, uint32_t d, uint32_t w, uint
     }
 }
 
-static const void *pick_kernel(uint32_t nk, uint32_t np, int kw, bool fast, int sub) {
+static const void *pick_kernel(uint32_t nk, uint32_t np, int kw, bool fast, int sub, bool t3) {
     switch (nk) {
-        case 1: return skb::scan_pick_nk1(np, kw, fast, sub);
-        case 2: return skb::scan_pick_nk2(np, kw, fast, sub);
-        case 3: return skb::scan_pick_nk3(np, kw, fast, sub);
-        default: return skb::scan_pick_nk4(np, kw, fast, sub);
+        case 1: return skb::scan_pick_nk1(np, kw, fast, sub, t3);
+        case 2: return skb::scan_pick_nk2(np, kw, fast, sub, t3);
+        case 3: return skb::scan_pick_nk3(np, kw, fast, sub, t3);
+        default: return skb::scan_pick_nk4(np, kw, fast, sub, t3);
     }
 }
 
@@ -551,7 +551,11 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     for (uint32_t q = 0; q < P.n_preds; ++q)
         if (P.pred[q].kind != PR_R32) kw = 0;
     if (getenv("COMPASS_SCAN_KW0")) kw = 0;   // experiments / parity of the generic variant
-    const void *kern = pick_kernel(P.n_keys, P.n_preds, kw, fast, (int)P.sub);
+    // 3-D tensor targets: the T3 instances (generic KW = 0, hashing drain) carry the tensor code
+    bool t3 = false;
+    for (uint32_t t = 0; t < c.n_targets; ++t) t3 = t3 || c.tgt_ndim[t] == 3;
+    if (t3) kw = 0;
+    const void *kern = pick_kernel(P.n_keys, P.n_preds, kw, fast && !t3, (int)P.sub, t3);
     const int threads = kThreads;
     if (getenv("COMPASS_SCAN_DEBUG"))
         fprintf(stderr, "k_scan plan: keys %u preds %u kw %d fast %d stages %u hh_log2 %u cap %u smem %u (ring %u, counters %u)\n",

@@ -362,7 +362,7 @@ __device__ __forceinline__ void flush_misses(const SParams &P, const uint64_t *s
 }
 
 // one warp-wide batch: lanes with `valid` hold one surviving tuple each, canonical keys x[k]
-template <int NK>
+template <int NK, bool T3>
 __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *smem, bool valid, const uint64_t (&x)[NK]) {
     const uint32_t act = __ballot_sync(0xffffffffu, valid);
     if (!act) return;
@@ -462,7 +462,10 @@ __device__ __forceinline__ void process_batch(const SParams &P, unsigned char *s
             const STarget &tg = P.tgt[t];
             if (tg.ndim < 2 || (P.trio_on && t == P.trio_m)) continue;
             const uint64_t xa = pick<NK>(x, tg.k0), xb = pick<NK>(x, tg.k1);
-            if (tg.ndim == 3) {   // 3-D tensor: equal key triples aggregated
+            // 3-D tensor: equal key triples aggregated.  Only the T3 instances (launched when a
+            // tensor target is present) carry this code: compiled into every hashing-drain
+            // instance, it slowed the C4 scan (k_scan<2,3,8,0,1>, no tensor) from 2.9 to 5.0 ms
+            if (T3 && tg.ndim == 3) {
                 const uint64_t xc = pick<NK>(x, tg.k2);
                 const uint32_t grp = __match_any_sync(act, xa) & __match_any_sync(act, xb) & __match_any_sync(act, xc);
                 if (lane == __ffs(grp) - 1) update_3d(tg, seeds + tg.seed_off, sc, xa, xb, xc, __popc(grp));
@@ -764,7 +767,7 @@ struct FastState {
     uint32_t actr;
 };
 
-template <int NK, bool FAST>
+template <int NK, bool FAST, bool T3>
 __device__ __forceinline__ void drain_batch(const SParams &P, unsigned char *smem, const unsigned char *q,
                                             const uint32_t (&kbytes)[NK], uint32_t head, uint32_t n, FastState<NK> &fs) {
 #ifdef SCAN_NOHASH   // timing experiments only (tools/build_variant.sh): results are wrong
@@ -791,13 +794,14 @@ __device__ __forceinline__ void drain_batch(const SParams &P, unsigned char *sme
         xk[k] = valid ? canon61(kbytes[k] == 8 ? *reinterpret_cast<const int64_t *>(e + k * 8)
                                                : (int64_t) * reinterpret_cast<const int32_t *>(e + k * 8))
                       : 0;
-    process_batch<NK>(P, smem, valid, xk);
+    process_batch<NK, T3>(P, smem, valid, xk);
 }
 
 // KW = 0: generic (any predicate kinds, key widths read at run time); KW = 4 / 8: every
 // predicate is an int32 range and every key column is KW bytes wide (no kind or width
-// branches; survivors' keys are gathered straight from the ballots)
-template <int NK, int NP, int KW, bool FAST, int SUB>
+// branches; survivors' keys are gathered straight from the ballots).  T3: the hashing drain
+// also serves 3-D tensor targets (KW = 0 instances, launched only when a tensor is present)
+template <int NK, int NP, int KW, bool FAST, int SUB, bool T3>
 __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SParams P) {
     constexpr bool R32 = KW != 0;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -977,7 +981,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                             __syncwarp();
                             while (tail != head) {
                                 const uint32_t n = min(32u, tail - head);
-                                drain_batch<NK, FAST>(P, smem, q, kbytes, head, n, fs);
+                                drain_batch<NK, FAST, T3>(P, smem, q, kbytes, head, n, fs);
                                 head += n;
                             }
 #pragma unroll
@@ -1011,7 +1015,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             if (ready_end - head >= 32) {
                 cp_wait_lag();
                 __syncwarp();
-                while (ready_end - head >= 32) { drain_batch<NK, FAST>(P, smem, q, kbytes, head, 32, fs); head += 32; }
+                while (ready_end - head >= 32) { drain_batch<NK, FAST, T3>(P, smem, q, kbytes, head, 32, fs); head += 32; }
             }
           }
         } else {
@@ -1055,7 +1059,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
                 }
             } else {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) process_batch<NK>(P, smem, (bits >> j) & 1u, xs[j]);
+                for (int j = 0; j < 4; ++j) process_batch<NK, T3>(P, smem, (bits >> j) & 1u, xs[j]);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive_a(empty_a + s * 8);
@@ -1067,7 +1071,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
         __syncwarp();
         while (tail - head > 0) {
             const uint32_t n = min(32u, tail - head);
-            drain_batch<NK, FAST>(P, smem, q, kbytes, head, n, fs);
+            drain_batch<NK, FAST, T3>(P, smem, q, kbytes, head, n, fs);
             head += n;
         }
     }
