@@ -263,6 +263,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         }
     }
     P.gather = c.n_preds > 0 ? 1u : 0u;
+    double sel_est = -1.0;   // expected selectivity of the predicates from the value-domain hints (-1: no hint)
     // predicate path: stages of up to 4 sub-tiles, ~10 KB of predicate columns per stage and
     // group (a single int32 column gets 4 sub-tiles: the per-stage work is amortised over more
     // rows); COMPASS_SUB overrides (experiments)
@@ -275,9 +276,11 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         // from the columns' value-domain hints (uniform reading of each predicate's share of
         // the domain; no hint = 1) must be below 1 %
         double est = 1.0;
+        bool hinted = false;
         for (uint32_t q = 0; q < c.n_preds; ++q) {
             const double dom = (double)c.col_domain[c.pred_col[q]];
             if (dom <= 0) continue;
+            hinted = true;
             double f = 1.0;
             if (c.pred_kind[q] == SK_PRED_SUBSET) f = c.pred_n[q] / dom;
             else {
@@ -287,6 +290,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
             }
             est *= std::min(1.0, f);
         }
+        if (hinted) sel_est = est;
         // 4 sub-tiles (instances exist for the lookup-table path with an int32 predicate
         // column: ~10 KB per stage and group, three stages within 3/5 of the budget), else 1
         uint32_t sub = (P.gather && fast && pbytes == 4 && est < 0.01) ? 4u : 1u;
@@ -332,16 +336,35 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     P.cap = 0;
     P.kb_bytes = 0;
     const uint32_t ring_warps = kWarps;                 // warps owning a survivor-key ring
-    if (P.gather) {
-        P.cap = P.n_keys == 1 ? 256 : SCAN_CAP2;              // >= one tile-slice of survivors (128); overflow drains
-        P.kb_bytes = P.cap * P.n_keys * 8;
-    }
     const uint32_t min_stages = 3;
     const uint32_t miss_bytes = kWarps * P.n_keys * 32 * 12 + ((kWarps * P.n_keys * 4 + 15) & ~15u) + kMaxKeys * 16 + 16;
     const uint32_t kBarBytes = 2 * kGroups * kMaxStages * 8;
     const uint32_t ring_stage = kGroups * P.stage_bytes;   // one stage of every group's ring
-    const uint32_t fixed = kBarBytes + min_stages * ring_stage + ring_warps * P.kb_bytes + seed_bytes + miss_bytes +
-                           kWarps * 128 * 2 + 256;
+    auto fixed_for = [&](uint32_t kb) {
+        return kBarBytes + min_stages * ring_stage + ring_warps * kb + seed_bytes + miss_bytes + kWarps * 128 * 2 + 256;
+    };
+    if (P.gather) {
+        // survivor-key ring per warp: >= one tile slice of survivors (128).  Depth measured on
+        // the C5 tables (tools/r02_p48.sh; per-table ms at ring 64 / 128 / 256 / 512): one key
+        // column at >= 25 % expected selectivity (C5 T10, 50 %) 1.29 / 1.12 / 1.08 / 0.89 -> 512;
+        // two key columns at 2-15 % (T8, 7.5 %) 0.97 / 0.72 / 0.73 -> 128, while at 19 % (T9,
+        // uniform keys) 1.53 / 1.87 / 1.98 and at 50 % (cycle T10) 3.53 / 3.40 / 4.45 the
+        // 64-entry ring is best or within 4 %.  Only with value-domain hints on the predicates.
+        const uint32_t base = P.n_keys == 1 ? 256 : SCAN_CAP2;
+        uint32_t cap = base;
+        if (sel_est >= 0) {
+            if (P.n_keys == 1 && sel_est >= 0.25) cap = 512;
+            if (P.n_keys >= 2 && sel_est >= 0.02 && sel_est < 0.15) cap = 128;
+        }
+        uint64_t sc1d = 0;
+        for (uint32_t t = 0; t < c.n_targets; ++t)
+            if (c.tgt_ndim[t] == 1) sc1d += uint64_t(c.tgt_d[t]) * c.tgt_w[t][0] * 4;
+        while (cap > base && fixed_for(cap * P.n_keys * 8) + sc1d > kBudget) cap /= 2;
+        if (const char *ec = getenv("COMPASS_CAP")) cap = std::max<uint32_t>(64, 1u << (31 - __builtin_clz(std::max(1, atoi(ec)))));
+        P.cap = cap;
+        P.kb_bytes = P.cap * P.n_keys * 8;
+    }
+    const uint32_t fixed = fixed_for(P.kb_bytes);
     if (fixed > kBudget) return decline("fixed smem");
     uint32_t avail = kBudget - fixed;
     // privatise targets in declaration order while they fit
