@@ -326,7 +326,11 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     //      (COMPASS_STAGES, COMPASS_HH_LOG2) for experiments only.
     const uint32_t kBudget = 227 * 1024;
     const char *env_st = getenv("COMPASS_STAGES"), *env_hh = getenv("COMPASS_HH_LOG2");
-    const uint32_t want_stages = env_st ? (uint32_t)atoi(env_st) : 6;
+    // two key columns at >= 5 % expected selectivity: 3 stages (the rest of the budget is left
+    // to the L1 carve-out; tools/sweep_scan.py, r02 s4d/s4e: C5 T8 0.75 -> 0.70 ms, T9 1.53 ->
+    // 1.43, cycle T10 3.52 -> 3.31), else 6 and up to the budget
+    const bool few_stages = !env_st && c.n_preds > 0 && P.n_keys >= 2 && sel_est >= 0.05;
+    const uint32_t want_stages = env_st ? (uint32_t)atoi(env_st) : (few_stages ? 3u : 6u);
     const uint32_t max_hh = env_hh ? (uint32_t)atoi(env_hh) : 11;
     uint32_t seed_words = 0;
     for (uint32_t t = 0; t < c.n_targets; ++t) seed_words += c.tgt_ndim[t] * c.tgt_d[t] * 6;
@@ -347,14 +351,18 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         // survivor-key ring per warp: >= one tile slice of survivors (128).  Depth measured on
         // the C5 tables (tools/r02_p48.sh; per-table ms at ring 64 / 128 / 256 / 512): one key
         // column at >= 25 % expected selectivity (C5 T10, 50 %) 1.29 / 1.12 / 1.08 / 0.89 -> 512;
-        // two key columns at 2-15 % (T8, 7.5 %) 0.97 / 0.72 / 0.73 -> 128, while at 19 % (T9,
-        // uniform keys) 1.53 / 1.87 / 1.98 and at 50 % (cycle T10) 3.53 / 3.40 / 4.45 the
-        // 64-entry ring is best or within 4 %.  Only with value-domain hints on the predicates.
+        // two key columns at 2-5 % (T7) -> 128.  With 3 stages (tools/sweep_scan.py, r02 s4d /
+        // s4e; ring 64 / 128 / 256): T8 (7.5 %) 1.07 / 0.70 / 0.69 and T9 (19 %, uniform keys)
+        // 1.47 / 1.89 / 1.43 -> 256; cycle T10 (50 %) 3.45 / 3.31 / 3.92 -> 128 (512 entries
+        // push the 1-D sketches out of shared memory: 2.9 / 4.9 / 12.2 ms).  Only with
+        // value-domain hints on the predicates.
         const uint32_t base = P.n_keys == 1 ? 256 : SCAN_CAP2;
         uint32_t cap = base;
         if (sel_est >= 0) {
             if (P.n_keys == 1 && sel_est >= 0.25) cap = 512;
-            if (P.n_keys >= 2 && sel_est >= 0.02 && sel_est < 0.15) cap = 128;
+            if (P.n_keys >= 2 && sel_est >= 0.02 && sel_est < 0.05) cap = 128;
+            if (P.n_keys >= 2 && sel_est >= 0.05 && sel_est < 0.3) cap = 256;   // T8 7.5 %, T9 19 %
+            if (P.n_keys >= 2 && sel_est >= 0.3) cap = 128;                      // cycle T10 50 %
         }
         uint64_t sc1d = 0;
         for (uint32_t t = 0; t < c.n_targets; ++t)
@@ -513,7 +521,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
         if (nhh * (12u << l) <= avail) { P.hh_log2 = l; break; }
     if (P.hh_log2) avail -= nhh * (12u << P.hh_log2);
     while (stages < want_stages && stages < kMaxStages && avail >= ring_stage) { ++stages; avail -= ring_stage; }
-    while (stages < kMaxStages && !env_st && avail >= ring_stage && nhh == 0) { ++stages; avail -= ring_stage; }
+    while (stages < kMaxStages && !env_st && !few_stages && avail >= ring_stage && nhh == 0) { ++stages; avail -= ring_stage; }
     P.stages = stages;
     uint32_t off = (kBarBytes + 127) & ~127u;            // full + empty mbarriers per group
     P.off_ring = off;
@@ -550,6 +558,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (const char *es = getenv("COMPASS_SCAN_CTAS")) sms = std::max(1, std::min(sms, atoi(es)));   // experiments
     uint64_t grid = std::min<uint64_t>((uint64_t)sms, (P.n_tiles + kGroups - 1) / kGroups);
     // int32 privatised counts stay exact: rows per CTA < 2^31
     if ((P.n_tiles + grid * kGroups - 1) / (grid * kGroups) * P.tile_rows * kGroups >= (1ULL << 31)) return decline("rows per CTA");
