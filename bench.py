@@ -106,22 +106,63 @@ def _sectors_hit(mask: torch.Tensor, elem_bytes: int) -> int:
 def algorithmic_bytes(ws, data, preds, run) -> dict:
     """SURVEY.md §8(d) B_alg: predicate columns in full + key-column 32-B sectors holding
     >= 1 survivor + the final int64 sketch bytes; each column counted once per scan."""
-    total, full = 0, 0
+    total, full, per = 0, 0, {}
     for t in ws.tables:
         cols = data[t.name]
         pcols = {p[0] for p in preds[t.name]}
         kcols = {k for s in ws.sketches_of(t.name) for k in s.key_cols} - pcols
         mask = _torch_mask(cols, preds[t.name]) if preds[t.name] else None
+        tb = 0
         for c in pcols:
-            total += cols[c].numel() * cols[c].element_size()
+            tb += cols[c].numel() * cols[c].element_size()
         for c in kcols:
             eb = cols[c].element_size()
-            total += cols[c].numel() * eb if mask is None else 32 * _sectors_hit(mask, eb)
+            tb += cols[c].numel() * eb if mask is None else 32 * _sectors_hit(mask, eb)
         for c in pcols | kcols:
             full += cols[c].numel() * cols[c].element_size()
-    total += run.sketch_bytes
+        for s in ws.sketches_of(t.name):
+            cells = 1
+            for w in s.w:
+                cells *= w
+            tb += 8 * s.d * cells
+        per[t.name] = tb
+        total += tb
     full += run.sketch_bytes
-    return {"alg": total, "full": full}
+    return {"alg": total, "full": full, "per_table": per}
+
+
+def binding_roof(ws, survivors, per_table_bytes, kernel_ms, hbm_gbs, roofs) -> dict | None:
+    """Per-table binding roof of the scans: sum over tables of max(HBM time of the table's
+    algorithmic bytes, its naive counter-update time, its naive hash time) with the measured
+    roofs (MEASURED_ROOFS.json).  The lookup-table path (int32 keys with domain hints
+    <= 2^22) does no hashing, so its tables take no hash term.  A table whose scan is
+    update-bound (C5 T9, cycle T10: every survivor costs d shared atomics per 1-D sketch and
+    d L2 red per matrix) cannot reach the HBM roof; this is the roof it can reach."""
+    if not roofs:
+        return None
+    tot, per = 0.0, {}
+    for tb, sv in zip(ws.tables, survivors):
+        keys = {k for s in ws.sketches_of(tb.name) for k in s.key_cols}
+        cmap = {c.name: c for c in tb.cols}
+        lut = len(keys) <= 2 and all(cmap[k].dtype == "int32" and 0 < (getattr(cmap[k], "domain", 0) or 0) <= (1 << 22)
+                                     for k in keys)
+        wide = any(cmap[k].dtype == "int64" for k in keys)
+        t_upd = t_hash = 0.0
+        for s in ws.sketches_of(tb.name):
+            cells = 1
+            for w in s.w:
+                cells *= w
+            u = sv * s.d
+            t_upd += u / (roofs["atoms_smem_per_s"] if s.d * cells * 4 <= 96 * 1024 else roofs["red_l2_u64_mat10mb_per_s"])
+            if not lut:
+                t_hash += u * len(s.w) / (roofs["hash_wide_pairs_per_s"] if wide else roofs["hash_narrow_pairs_per_s"])
+        t_hbm = per_table_bytes[tb.name] / (hbm_gbs * 1e9)
+        terms = {"hbm": t_hbm, "update": t_upd, "hash": t_hash}
+        b = max(terms, key=terms.get)
+        per[tb.name] = {"bound": b, "roof_ms": round(terms[b] * 1e3, 4)}
+        tot += terms[b]
+    return {"roof_time_ms": round(tot * 1e3, 4), "frac": round(tot * 1e3 / kernel_ms, 4), "per_table": per,
+            "how": "sum over tables of max(t_hbm, t_update, t_hash) (naive counts, measured roofs)"}
 
 
 class ClockSampler:
@@ -377,7 +418,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C4", choices=["C1", "C2", "C3", "C3t", "C4", "C5", "C5-cycle"])
     ap.add_argument("--scale", type=float, default=1.0)
-    ap.add_argument("--cpu-rows", type=int, default=150_000_000)
+    ap.add_argument("--cpu-rows", type=int, default=300_000_000)
     ap.add_argument("--ref-rows", type=int, default=20_000_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -502,6 +543,9 @@ def main():
         roof["read_stream_gbs"] = read_peak
         roof["frac_of_read_stream"] = round(achieved / read_peak, 4)
     roof.update(_int_update_roofs(ws, run.survivors.tolist(), kms, roofs))
+    br = binding_roof(ws, run.survivors.tolist(), ab["per_table"], kms, peak, roofs)
+    if br:
+        roof["binding"] = br
     line = {"metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
             "timing": {"value_is": "rows of all ranks / t_build (SURVEY.md 8(d)): zero + fused scans + "

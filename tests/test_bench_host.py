@@ -54,3 +54,23 @@ def test_threaded_oracle_baseline_merges_private_sketches():
     for t in ws.tables:
         for a, b in zip(one[t.name], four[t.name]):
             assert np.array_equal(a, b)
+
+
+def test_binding_roof_by_hand():
+    """Per-table binding roof: max(HBM, update, hash) per table, summed; lookup-table tables
+    (int32 keys with small hinted domains) take no hash term."""
+    ws = datagen.c5(scale=1e-6)
+    roofs = {"hash_narrow_pairs_per_s": 1e11, "hash_wide_pairs_per_s": 5e10, "atoms_smem_per_s": 1e12,
+             "red_l2_u64_mat10mb_per_s": 2e11}
+    names = [t.name for t in ws.tables]
+    surv = [0] * len(names)
+    surv[8] = 10_000_000                          # T9: two 1-D sketches (smem) + one 512^2 matrix (L2)
+    per_bytes = {n: 1_000_000_000 for n in names}  # 1 GB each -> 1/6 ms at 6000 GB/s
+    r = bench.binding_roof(ws, surv, per_bytes, 10.0, 6000.0, roofs)
+    t_hbm = 1e9 / 6e12
+    t9 = 2 * 10_000_000 * 5 / 1e12 + 10_000_000 * 5 / 2e11      # 0.1 ms + 0.25 ms
+    assert r["per_table"]["T9"]["bound"] == "update"
+    assert abs(r["per_table"]["T9"]["roof_ms"] - t9 * 1e3) < 1e-3
+    assert r["per_table"]["T1"]["bound"] == "hbm"
+    assert abs(r["roof_time_ms"] - (9 * t_hbm + t9) * 1e3) < 1e-3
+    assert abs(r["frac"] - r["roof_time_ms"] / 10.0) < 1e-4
