@@ -426,6 +426,9 @@ def main():
     ap.add_argument("--no-overlap", action="store_true", help="one trailing all-reduce instead of per-table ones")
     ap.add_argument("--row-shard", action="store_true",
                     help="reduce-scatter by sketch row + row-sharded composition instead of the all-reduce (graph workloads)")
+    ap.add_argument("--merge", default="nccl", choices=["nccl", "peer"],
+                    help="cross-GPU merge: NCCL all-reduce, or pushes over peer memory fused into the scans "
+                         "(SURVEY.md 8(f) 4, P2P variant)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(_relaunch(args.gpus))
@@ -446,7 +449,7 @@ def main():
     torch.cuda.synchronize()
     # N > 1: int32 wire and per-table all-reduces overlapped with the next table's scan
     # (SURVEY.md §8(e) levers i and ii); N = 1 has no collective
-    run = QueryRun(ws, dev, wire=args.wire, overlap=not args.no_overlap)
+    run = QueryRun(ws, dev, wire=args.wire, overlap=not args.no_overlap, merge=args.merge)
     subplans = _subplans(ws) if ws.kind == "graph" else None
     stream = torch.cuda.current_stream()
     kev = []  # (start, end) events around each fused-scan launch
@@ -459,7 +462,7 @@ def main():
 
     def step(record=False):
         s0 = ev() if record else None
-        run.zero_()
+        run.zero_(stream)
         for t in ws.tables:
             a = ev() if record else None
             run.build_table(t.name, data[t.name], preds[t.name], stream=stream)
@@ -559,6 +562,7 @@ def main():
                        "l2": "inputs larger than L2 (no flush)" if ab["full"] > 4 * 126e6 else "inputs L2-resident",
                        "parallelism": f"row-sharded x{world}" + (
                            " + NCCL reduce-scatter by sketch row, row-sharded composition" if (args.row_shard and subplans)
+                           else " + pushes over peer memory fused into the scans (CUDA IPC, red.add)" if args.merge == "peer"
                            else (f" + NCCL SUM all-reduce ({run.merge.wire} wire, "
                                  f"{'per-table overlapped' if run.merge.overlap else 'one trailing'})" if world > 1 else ""))},
             "roofline": roof, "gpu_launches": int(launches),

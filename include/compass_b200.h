@@ -165,6 +165,48 @@ SK_API sk_status sketch_wire_pack(const int64_t *counters_dev, int32_t *wire_dev
 SK_API sk_status sketch_wire_unpack(const int32_t *wire_dev, int64_t *counters_dev, uint64_t n, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * Cross-GPU merge over peer memory (SURVEY.md §8(f) 4, P2P variant of the fused flush +
+ * all-reduce; "partition, sketch, merge").  Each rank owns a MERGED buffer with
+ * the query's packed layout, allocated with sk_ipc_alloc and mapped into every other rank's
+ * process with sk_ipc_open (handles exchanged by the caller, e.g. torch.distributed).  A push
+ * adds this rank's partial slice into the same slice of every rank's merged buffer (own
+ * included) with red.add over NVLink; once every rank's pushes have completed (caller: stream
+ * synchronize + a host barrier), every merged buffer holds the sum of all partials — exact,
+ * order-independent integer addition.  The merged buffers must be zeroed on every rank before
+ * any rank pushes (caller: zero, synchronize, barrier).
+ *   src:     this rank's partial slice (device, 16-byte aligned, n int64)
+ *   dst:     host array of n_peers device pointers (1 <= n_peers <= 8): the slice in every
+ *            rank's merged buffer as mapped in this process (16-byte aligned)
+ * sketch_update_filtered_push: sketch_update_filtered, then the push of `src` — FUSED into the
+ *   scan when the optimised kernel runs without a histogram epilogue: a cooperative launch
+ *   whose CTAs, after a grid barrier that follows the last flush, push the slice (no separate
+ *   kernel, no NCCL); otherwise one k_peer_push launch after the scan.  `src` must cover the
+ *   counters of every target (the table's slice of the partial buffer).
+ * sketch_peer_push: the push alone (e.g. the survivor counts).
+ * Errors: SK_EINVAL (NULL pointers, misalignment, n_peers out of range), SK_ECUDA. */
+typedef struct {
+    const int64_t *src;
+    int64_t *const *dst;
+    uint32_t n_peers;
+    uint64_t n;
+} sk_peer_push;
+SK_API sk_status sketch_update_filtered_push(const sk_column *cols, uint32_t n_cols, uint64_t n_rows,
+                                             const sk_pred *preds, uint32_t n_preds,
+                                             const sk_target *targets, uint32_t n_targets,
+                                             int64_t *survivors_dev, const sk_peer_push *push, void *stream);
+SK_API sk_status sketch_peer_push(const sk_peer_push *push, void *stream);
+
+/* CUDA IPC for the merged buffers.  sk_ipc_alloc: `bytes` of zeroed device memory on `device`
+ * (library-owned until sk_ipc_free) and its SK_IPC_HANDLE_BYTES-byte handle.  sk_ipc_open:
+ * map another process's buffer (never this process's own) on `device`; sk_ipc_close unmaps.
+ * SK_EINVAL on NULL arguments, SK_ENOMEM, SK_ECUDA. */
+#define SK_IPC_HANDLE_BYTES 64
+SK_API sk_status sk_ipc_alloc(uint64_t bytes, int device, void **dev_ptr, unsigned char *handle);
+SK_API sk_status sk_ipc_free(void *dev_ptr);
+SK_API sk_status sk_ipc_open(const unsigned char *handle, int device, void **dev_ptr);
+SK_API sk_status sk_ipc_close(void *dev_ptr);
+
+/* ---------------------------------------------------------------------------
  * Join graph of one query: tables are vertices carrying their
  * exact post-selection cardinality; edge e joins tables edge_u[e] and edge_v[e]
  * and carries one 1-D sketch per side (vec_u[e] built on table edge_u[e]'s join

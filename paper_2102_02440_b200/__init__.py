@@ -53,6 +53,14 @@ class sk_target(ctypes.Structure):
     _fields_ = [("sketch", ctypes.c_void_p), ("key_col", ctypes.c_uint32 * 3)]
 
 
+class sk_peer_push(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_void_p), ("dst", ctypes.POINTER(ctypes.c_void_p)), ("n_peers", ctypes.c_uint32),
+                ("n", ctypes.c_uint64)]
+
+
+SK_IPC_HANDLE_BYTES = 64
+
+
 class sk_graph(ctypes.Structure):
     _fields_ = [("n_tables", ctypes.c_uint32), ("survivors", ctypes.POINTER(ctypes.c_int64)),
                 ("n_edges", ctypes.c_uint32), ("edge_u", ctypes.POINTER(ctypes.c_uint32)),
@@ -65,7 +73,8 @@ class sk_graph(ctypes.Structure):
 # every symbol include/compass_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = ["sketch_create", "sketch_destroy", "sketch_counters", "sketch_zero", "sketch_update_filtered",
            "sketch_merge", "sketch_wire_pack", "sketch_wire_unpack", "estimate_join", "estimate_join_exact", "estimate_subplans", "plan_greedy",
-           "plan_enumerate", "exact_join_size", "sk_last_error", "sk_version", "sk_kernel_launches"]
+           "plan_enumerate", "exact_join_size", "sk_last_error", "sk_version", "sk_kernel_launches",
+           "sketch_update_filtered_push", "sketch_peer_push", "sk_ipc_alloc", "sk_ipc_free", "sk_ipc_open", "sk_ipc_close"]
 
 # Algorithm 1 search-space settings
 ENUM_GREEDY, ENUM_FULL_GREEDY, ENUM_LIMIT, ENUM_EXHAUSTIVE = range(4)
@@ -143,6 +152,20 @@ def lib() -> ctypes.CDLL:
         L.exact_join_size.restype = st
         L.exact_join_size.argtypes = [ctypes.POINTER(sk_join_data), u64, ctypes.c_char_p, u32,
                                       ctypes.POINTER(ctypes.c_double), vp]
+        if hasattr(L, "sketch_peer_push"):   # (experimental builds of older revisions lack it)
+            L.sketch_update_filtered_push.restype = st
+            L.sketch_update_filtered_push.argtypes = [ctypes.POINTER(sk_column), u32, u64, ctypes.POINTER(sk_pred), u32,
+                                                      ctypes.POINTER(sk_target), u32, vp, ctypes.POINTER(sk_peer_push), vp]
+            L.sketch_peer_push.restype = st
+            L.sketch_peer_push.argtypes = [ctypes.POINTER(sk_peer_push), vp]
+            L.sk_ipc_alloc.restype = st
+            L.sk_ipc_alloc.argtypes = [u64, ctypes.c_int, ctypes.POINTER(vp), ctypes.c_char_p]
+            L.sk_ipc_free.restype = st
+            L.sk_ipc_free.argtypes = [vp]
+            L.sk_ipc_open.restype = st
+            L.sk_ipc_open.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(vp)]
+            L.sk_ipc_close.restype = st
+            L.sk_ipc_close.argtypes = [vp]
         L.sk_last_error.restype = ctypes.c_char_p
         L.sk_last_error.argtypes = []
         L.sk_kernel_launches.restype = ctypes.c_uint64
@@ -214,10 +237,12 @@ class Sketch:
 
 
 def sketch_update_filtered(columns, n_rows: int, preds, targets, survivors: torch.Tensor | None = None, stream=None,
-                           domains=None):
+                           domains=None, push=None):
     """One fused scan.  columns: list of int32/int64 CUDA tensors; preds: list of
     (col_index, kind, lo, hi, set_values); targets: list of (Sketch, [key col indices]);
-    domains: optional per-column key-domain hints (0 = unknown)."""
+    domains: optional per-column key-domain hints (0 = unknown); push: optional
+    (src int64 CUDA tensor, [dst device pointers]) — the cross-GPU merge over peer memory
+    (sketch_update_filtered_push), fused into the scan where the library can."""
     ncol = len(columns)
     cols = (sk_column * max(1, ncol))()
     for i, c in enumerate(columns):
@@ -244,8 +269,71 @@ def sketch_update_filtered(columns, n_rows: int, preds, targets, survivors: torc
         for q, k in enumerate(keys):
             tg[i].key_col[q] = k
     sp = ctypes.c_void_p(survivors.data_ptr()) if survivors is not None else None
+    if push is not None:
+        pp = _peer_push_desc(*push)
+        _check(lib().sketch_update_filtered_push(cols, ncol, n_rows, pr, len(preds), tg, len(targets), sp,
+                                                 ctypes.byref(pp), ctypes.c_void_p(_stream_ptr(stream))))
+        return
     _check(lib().sketch_update_filtered(cols, ncol, n_rows, pr, len(preds), tg, len(targets), sp,
                                         ctypes.c_void_p(_stream_ptr(stream))))
+
+
+def _peer_push_desc(src: torch.Tensor, dst_ptrs) -> "sk_peer_push":
+    assert src.dtype == torch.int64 and src.is_cuda and src.is_contiguous()
+    pp = sk_peer_push()
+    pp.src = src.data_ptr()
+    arr = (ctypes.c_void_p * max(1, len(dst_ptrs)))(*[int(p) for p in dst_ptrs])
+    pp._keep = arr
+    pp.dst = ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
+    pp.n_peers = len(dst_ptrs)
+    pp.n = src.numel()
+    return pp
+
+
+def sketch_peer_push(src: torch.Tensor, dst_ptrs, stream=None):
+    """Add `src` (this rank's partial slice) into every rank's merged slice (device pointers
+    mapped in this process, own included): the cross-GPU merge over peer memory."""
+    pp = _peer_push_desc(src, dst_ptrs)
+    _check(lib().sketch_peer_push(ctypes.byref(pp), ctypes.c_void_p(_stream_ptr(stream))))
+
+
+class IpcBuffer:
+    """A library-allocated, zeroed int64 device buffer that other processes can map (CUDA IPC):
+    `.tensor` is a torch view of it, `.handle` the bytes to send to the peers."""
+
+    def __init__(self, numel: int, device: torch.device):
+        self.device = torch.device(device)
+        ptr = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(SK_IPC_HANDLE_BYTES)
+        _check(lib().sk_ipc_alloc(numel * 8, self.device.index or 0, ctypes.byref(ptr), h))
+        self.ptr, self.numel, self.handle = ptr.value, numel, h.raw
+        self.tensor = _tensor_at(self.ptr, numel, self.device)
+
+    def close(self):
+        if self.ptr:
+            self.tensor = None
+            _check(lib().sk_ipc_free(ctypes.c_void_p(self.ptr)))
+            self.ptr = None
+
+
+def ipc_open(handle: bytes, device: torch.device) -> int:
+    """Map another process's IpcBuffer; returns its device pointer in this process."""
+    ptr = ctypes.c_void_p()
+    _check(lib().sk_ipc_open(handle, torch.device(device).index or 0, ctypes.byref(ptr)))
+    return ptr.value
+
+
+def ipc_close(ptr: int):
+    _check(lib().sk_ipc_close(ctypes.c_void_p(ptr)))
+
+
+def _tensor_at(ptr: int, numel: int, device: torch.device) -> torch.Tensor:
+    """A torch int64 tensor over existing device memory (the library owns it)."""
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (numel,), "typestr": "<i8", "data": (ptr, False), "version": 3,
+                                    "strides": None}
+    with torch.cuda.device(device):
+        return torch.as_tensor(_Arr(), device=device)
 
 
 def _columns(columns, domains=None):

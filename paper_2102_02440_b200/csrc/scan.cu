@@ -138,8 +138,9 @@ static sk_status decline(const char *why) {
 
 // Returns SK_OK and sets *launched if the optimised scan handled the call; leaves
 // *launched false (and returns SK_OK) when the call is outside its envelope.
-sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
+sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched, bool *pushed) {
     *launched = false;
+    *pushed = false;
     if (c.n_cols > kMaxSCols || c.n_preds > 4 || c.n_targets > kMaxSTargets || c.n_rows == 0) return decline("call size");
     SParams P;
     memset(&P, 0, sizeof(P));
@@ -594,8 +595,25 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched) {
                 P.n_keys, P.n_preds, kw, (int)fast, P.stages, P.hh_log2, P.cap, off, P.stages * kGroups * P.stage_bytes,
                 P.smem_counters * 4);
     SKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)off));
+    // fused cross-GPU merge: only when no histogram epilogue has to run after the scan (its
+    // counts must be in the partial before the push); a cooperative launch guarantees that
+    // every CTA is co-resident for the tail's grid barrier
+    bool fuse = c.push.peers > 0 && hists.empty();
+    void *bar = nullptr;
+    if (fuse) {
+        P.push = c.push;
+        SKB_CUDA(cudaMallocAsync(&bar, 16, stream));
+        SKB_CUDA(cudaMemsetAsync(bar, 0, 16, stream));
+        P.push_bar = (unsigned int *)bar;
+    }
     void *kargs[] = {&P};
-    SKB_CUDA(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(threads), kargs, off, stream));
+    if (fuse) {
+        SKB_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(threads), kargs, off, stream));
+        SKB_CUDA(cudaFreeAsync(bar, stream));
+        *pushed = true;
+    } else {
+        SKB_CUDA(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(threads), kargs, off, stream));
+    }
     count_launch();
     // histogram -> sketches, then release the histograms (stream-ordered).  Every 1-D target
     // on a histogram key gets its in-domain counts only here, so all of them must be served:

@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include "compass_b200.h"
+#include "peer.cuh"
 
 namespace skb {
 
@@ -25,9 +26,15 @@ struct ScanCall {
     const uint64_t *tgt_seeds_host[16];   // host copies [ndim][d][6] (hash-unit sharing)
     sk_sketch *tgt_sketch[16];             // target handles (per-sketch hash lookup tables)
     unsigned long long *survivors = nullptr;
+    PeerPush push{};                       // cross-GPU merge over peer memory (peers = 0: none)
 };
 
-// Launch the optimised persistent scan if the call fits its envelope (sets *launched).
-sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched);
+// Launch the optimised persistent scan if the call fits its envelope (sets *launched); with
+// c.push.peers, *pushed says whether the push was fused into the scan (else the caller runs
+// peer_push_launch after it).
+sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched, bool *pushed);
+
+// Stand-alone push of a partial slice into every rank's merged slice (peer.cuh).
+sk_status peer_push_launch(const PeerPush &pp, cudaStream_t stream);
 
 }  // namespace skb

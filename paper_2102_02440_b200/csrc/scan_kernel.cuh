@@ -14,6 +14,7 @@
 
 #include "hash.cuh"
 #include "internal.cuh"
+#include "peer.cuh"
 #include "scan.cuh"
 
 using namespace skb;
@@ -107,6 +108,10 @@ struct SParams {
     uint32_t sub;                   // sub-tiles of kTile rows per stage (predicate path; 1 otherwise)
     uint32_t n_full_tiles;          // tiles with tile_rows rows (staged by TMA)
     unsigned long long *survivors;
+    // fused cross-GPU merge (peer.cuh): after every CTA has flushed, the table's partial slice
+    // is added into every rank's merged buffer (push.peers > 0 only in a cooperative launch)
+    PeerPush push;
+    unsigned int *push_bar;
     // lookup-table path (FAST instances): per key column, the lookup table of its hash family
     // over the hinted domain [0, klut_dom) (16 bytes per key: 8 uint16 fields, field r =
     // counter index r * w + bucket of the family's primary sketch << 1 | sign), the primary
@@ -1149,6 +1154,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan(const __grid_constant__ SP
             const int32_t v = sc[tg.smem_off + qq];
             if (v) red_add_s64(tg.counters + qq, (int64_t)v);
         }
+    }
+    if (P.push.peers) {
+        // fused merge: once every CTA's flush has landed (grid barrier of the cooperative
+        // launch), the consumers of all CTAs push the table's partial slice to every rank
+        consumer_sync();
+        if (tid == 0) grid_arrive_wait(P.push_bar, gridDim.x);
+        consumer_sync();
+        peer_push_range(P.push, uint64_t(blockIdx.x) * kConsumers + tid, uint64_t(gridDim.x) * kConsumers);
     }
 }
 

@@ -144,10 +144,9 @@ __global__ void __launch_bounds__(512) k_update_generic(const __grid_constant__ 
 
 }  // namespace
 
-extern "C" sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_cols, uint64_t n_rows,
-                                            const sk_pred *preds, uint32_t n_preds,
-                                            const sk_target *targets, uint32_t n_targets,
-                                            int64_t *survivors_dev, void *stream_) {
+static sk_status update_impl(const sk_column *cols, uint32_t n_cols, uint64_t n_rows, const sk_pred *preds,
+                             uint32_t n_preds, const sk_target *targets, uint32_t n_targets, int64_t *survivors_dev,
+                             const PeerPush *push, void *stream_) {
     cudaStream_t stream = (cudaStream_t)stream_;
     if (n_cols > kMaxCols || n_preds > kMaxPreds || n_targets > kMaxTargets)
         return fail(SK_EINVAL, "sketch_update_filtered: too many cols/preds/targets (%u/%u/%u)", n_cols, n_preds, n_targets);
@@ -251,7 +250,10 @@ extern "C" sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_co
     size_t smem = p.seeds_byte_off + size_t(seed_words) * 8;
     p.survivors = reinterpret_cast<unsigned long long *>(survivors_dev);
 
-    if (n_rows == 0) { release(); return SK_OK; }
+    if (n_rows == 0) {
+        release();
+        return push ? peer_push_launch(*push, stream) : SK_OK;
+    }
     // optimised persistent scan (scan.cu) unless disabled or outside its envelope
     const char *mode = getenv("COMPASS_SCAN");
     if (!(mode && strcmp(mode, "generic") == 0)) {
@@ -289,10 +291,12 @@ extern "C" sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_co
             sc.tgt_sketch[t] = const_cast<sk_sketch *>(sk);
         }
         sc.survivors = p.survivors;
-        bool launched = false;
-        sk_status st = scan_launch(sc, stream, &launched);
+        if (push) sc.push = *push;
+        bool launched = false, pushed = false;
+        sk_status st = scan_launch(sc, stream, &launched, &pushed);
         if (st != SK_OK || launched) {
             release();
+            if (st == SK_OK && push && !pushed) st = peer_push_launch(*push, stream);
             return st;
         }
     }
@@ -314,5 +318,46 @@ extern "C" sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_co
     e = cudaGetLastError();
     release();
     if (e != cudaSuccess) return cuda_fail(e, "k_update_generic launch");
+    return push ? peer_push_launch(*push, stream) : SK_OK;
+}
+
+extern "C" sk_status sketch_update_filtered(const sk_column *cols, uint32_t n_cols, uint64_t n_rows,
+                                            const sk_pred *preds, uint32_t n_preds,
+                                            const sk_target *targets, uint32_t n_targets,
+                                            int64_t *survivors_dev, void *stream) {
+    return update_impl(cols, n_cols, n_rows, preds, n_preds, targets, n_targets, survivors_dev, nullptr, stream);
+}
+
+// checks a push description and copies it into the kernel-side form
+static sk_status push_desc(const sk_peer_push *push, PeerPush *pp) {
+    if (!push) return fail(SK_EINVAL, "peer push: NULL description");
+    if (push->n_peers == 0 || push->n_peers > kMaxPeers) return fail(SK_EINVAL, "peer push: n_peers %u not in 1..%u", push->n_peers, kMaxPeers);
+    if (push->n && (!push->src || !push->dst)) return fail(SK_EINVAL, "peer push: NULL src or dst");
+    if ((uintptr_t)push->src & 15) return fail(SK_EINVAL, "peer push: src not 16-byte aligned");
+    memset(pp, 0, sizeof(*pp));
+    pp->src = push->src;
+    pp->n = push->n;
+    pp->peers = push->n_peers;
+    for (uint32_t q = 0; q < push->n_peers; ++q) {
+        if (push->n && (!push->dst[q] || ((uintptr_t)push->dst[q] & 15))) return fail(SK_EINVAL, "peer push: dst %u NULL or not 16-byte aligned", q);
+        pp->dst[q] = push->dst[q];
+    }
     return SK_OK;
+}
+
+extern "C" sk_status sketch_update_filtered_push(const sk_column *cols, uint32_t n_cols, uint64_t n_rows,
+                                                 const sk_pred *preds, uint32_t n_preds,
+                                                 const sk_target *targets, uint32_t n_targets,
+                                                 int64_t *survivors_dev, const sk_peer_push *push, void *stream) {
+    PeerPush pp;
+    sk_status st = push_desc(push, &pp);
+    if (st != SK_OK) return st;
+    return update_impl(cols, n_cols, n_rows, preds, n_preds, targets, n_targets, survivors_dev, pp.n ? &pp : nullptr, stream);
+}
+
+extern "C" sk_status sketch_peer_push(const sk_peer_push *push, void *stream) {
+    PeerPush pp;
+    sk_status st = push_desc(push, &pp);
+    if (st != SK_OK) return st;
+    return peer_push_launch(pp, (cudaStream_t)stream);
 }

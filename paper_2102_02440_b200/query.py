@@ -14,7 +14,8 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import JoinGraph, Sketch, sketch_update_filtered, sketch_wire_pack, sketch_wire_unpack
+from . import (IpcBuffer, JoinGraph, Sketch, ipc_close, ipc_open, sketch_peer_push, sketch_update_filtered,
+               sketch_wire_pack, sketch_wire_unpack)
 
 
 def packed_layout(q):
@@ -118,10 +119,82 @@ class PackedMerge:
         dist.all_reduce(self.buffer[:self.n_s], op=dist.ReduceOp.SUM, group=self.group)
 
 
+class PeerMerge:
+    """Cross-GPU merge over peer memory (SURVEY.md §8(f) 4, P2P variant of the fused flush +
+    all-reduce).  Every rank owns a merged buffer with the packed layout, allocated
+    by the library for CUDA IPC and mapped into every other rank's process (handles exchanged
+    with all_gather_object).  Each table's scan is launched with a push of its partial slice
+    into that slice of every rank's merged buffer — fused into the scan's cooperative launch
+    (after a grid barrier behind the last CTA's flush) where the library can — and finish()
+    pushes the survivor counts, waits for the stream, and after a barrier (every rank's pushes
+    complete) copies the merged buffer into the partial buffer, so the sketch handles read the
+    sums.  No NCCL kernel; exact integer addition in any order."""
+
+    def __init__(self, buffer, n_tables, slices, group=None):
+        self.buffer, self.slices, self.group = buffer, slices, group
+        self.n_s = n_tables + (n_tables & 1)
+        self.init = dist.is_available() and dist.is_initialized()
+        self.world_n = dist.get_world_size(group) if self.init else 1
+        rank = dist.get_rank(group) if self.init else 0
+        assert self.world_n <= 8, "peer merge: at most 8 ranks"
+        self.final = IpcBuffer(buffer.numel(), buffer.device)
+        handles = [None] * self.world_n
+        if self.world_n > 1:
+            dist.all_gather_object(handles, self.final.handle, group=group)
+        self.opened = []
+        self.ptrs = []
+        for r in range(self.world_n):
+            if r == rank:
+                self.ptrs.append(self.final.ptr)
+            else:
+                p_ = ipc_open(handles[r], buffer.device)
+                self.opened.append(p_)
+                self.ptrs.append(p_)
+        self.stream = None
+
+    def world(self) -> int:
+        return self.world_n
+
+    def _barrier(self, stream):
+        if self.world_n > 1:
+            (stream or torch.cuda.current_stream(self.buffer.device)).synchronize()
+            dist.barrier(group=self.group)
+
+    def zero_(self, stream=None):
+        """Zero the partial and this rank's merged buffer; no rank pushes before every rank
+        has zeroed (barrier)."""
+        self.buffer.zero_()
+        self.final.tensor.zero_()
+        self._barrier(stream)
+
+    def push_for(self, name: str, stream=None):
+        self.stream = stream
+        a, b = self.slices[name]
+        return self.buffer[a:b], [p + 8 * a for p in self.ptrs]
+
+    def reduce_table(self, name: str):
+        pass   # the push travels with the scan
+
+    def finish(self):
+        s = self.stream
+        sketch_peer_push(self.buffer[:self.n_s], list(self.ptrs), stream=s)
+        self._barrier(s)
+        cur = s or torch.cuda.current_stream(self.buffer.device)
+        with torch.cuda.stream(cur):
+            self.buffer.copy_(self.final.tensor)
+
+    def close(self):
+        for p_ in self.opened:
+            ipc_close(p_)
+        self.opened = []
+        self.final.close()
+
+
 class QueryRun:
     """One query's sketches in one packed int64 buffer; cross-GPU merge by PackedMerge."""
 
-    def __init__(self, q, device="cuda", use_domains=True, wire="i64", overlap=False, group=None, always_merge=False):
+    def __init__(self, q, device="cuda", use_domains=True, wire="i64", overlap=False, group=None, always_merge=False,
+                 merge="nccl"):
         self.q = q
         self.use_domains = use_domains
         self.device = torch.device(device)
@@ -140,12 +213,20 @@ class QueryRun:
         self.sketch_bytes = sum(sizes) * 8
         if wire == "i32" and any(t.n_rows >= (1 << 31) for t in q.tables):
             wire = "i64"   # int32 partial/merged counters need < 2^31 rows per table
-        self.merge = PackedMerge(self.buffer, len(self.tnames), table_slices(q), wire, overlap, group,
-                                 pack=lambda a, b: sketch_wire_pack(a, b), unpack=lambda a, b: sketch_wire_unpack(a, b),
-                                 always=always_merge)
+        assert merge in ("nccl", "peer")
+        self.peer = merge == "peer"
+        if self.peer:
+            self.merge = PeerMerge(self.buffer, len(self.tnames), table_slices(q), group)
+        else:
+            self.merge = PackedMerge(self.buffer, len(self.tnames), table_slices(q), wire, overlap, group,
+                                     pack=lambda a, b: sketch_wire_pack(a, b),
+                                     unpack=lambda a, b: sketch_wire_unpack(a, b), always=always_merge)
 
-    def zero_(self):
-        self.buffer.zero_()
+    def zero_(self, stream=None):
+        if self.peer:
+            self.merge.zero_(stream)
+        else:
+            self.buffer.zero_()
 
     def build_table(self, name: str, columns: dict, preds, stream=None):
         """Fused filter + sketch update for every sketch of table `name` (one scan)."""
@@ -158,8 +239,9 @@ class QueryRun:
                    for s, sk in zip(self.q.sketches, self.sketches) if s.table == name]
         ti = self.tnames.index(name)
         domains = [getattr(c, "domain", 0) or 0 for c in t.cols] if self.use_domains else None
+        push = self.merge.push_for(name, stream) if (self.peer and name in self.merge.slices) else None
         sketch_update_filtered(cols, n_rows, pr, targets, survivors=self.survivors[ti:ti + 1], stream=stream,
-                               domains=domains)
+                               domains=domains, push=push)
         self.merge.reduce_table(name)
 
     def build(self, data: dict, preds: dict, stream=None):
@@ -253,3 +335,5 @@ class QueryRun:
     def close(self):
         for sk in self.sketches:
             sk.close()
+        if self.peer:
+            self.merge.close()
