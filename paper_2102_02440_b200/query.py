@@ -157,7 +157,8 @@ class PeerMerge:
 
     def _barrier(self, stream):
         if self.world_n > 1:
-            (stream or torch.cuda.current_stream(self.buffer.device)).synchronize()
+            if self.buffer.is_cuda:
+                (stream or torch.cuda.current_stream(self.buffer.device)).synchronize()
             dist.barrier(group=self.group)
 
     def zero_(self, stream=None):
@@ -179,8 +180,10 @@ class PeerMerge:
         s = self.stream
         sketch_peer_push(self.buffer[:self.n_s], list(self.ptrs), stream=s)
         self._barrier(s)
-        cur = s or torch.cuda.current_stream(self.buffer.device)
-        with torch.cuda.stream(cur):
+        if not self.buffer.is_cuda:   # (host logic tests with emulated peer buffers)
+            self.buffer.copy_(self.final.tensor)
+            return
+        with torch.cuda.stream(s or torch.cuda.current_stream(self.buffer.device)):
             self.buffer.copy_(self.final.tensor)
 
     def close(self):

@@ -197,3 +197,101 @@ def test_row_ranges_and_pack_layout():
     assert torch.equal(send[:12], c[0][0:3].reshape(-1)) and torch.equal(send[12:30], c[1][0:3].reshape(-1))
     assert torch.equal(send[30:38], c[0][3:5].reshape(-1)) and torch.equal(send[38:42], torch.zeros(4, dtype=send.dtype))
     assert torch.equal(send[42:54], c[1][3:5].reshape(-1)) and torch.equal(send[54:60], torch.zeros(6, dtype=send.dtype))
+
+
+# ---- merge over peer memory (query.PeerMerge, SURVEY.md §8(f) 4 P2P variant): host logic with
+# the library's IPC buffers and push emulated by file-backed shared tensors.  A "device
+# pointer" is (rank + 1) << 40 plus a byte offset, so the slice arithmetic of PeerMerge
+# (ptr + 8 * offset) is exercised as on the device.
+class _FakeIpc:
+    def __init__(self, numel, device, root, rank):
+        self.numel = numel
+        path = os.path.join(root, f"merged{rank}.bin")
+        self.tensor = torch.from_file(path, shared=True, size=numel, dtype=torch.int64)
+        self.tensor.zero_()
+        self.ptr = (rank + 1) << 40
+        self.handle = path.encode()
+        _LOCKS[self.ptr] = path + ".lock"
+
+    def close(self):
+        pass
+
+
+def _fake_open(handle, device, numel):
+    path = handle.decode()
+    rank = int(os.path.basename(path)[len("merged"):-len(".bin")])
+    _FAKE[(rank + 1) << 40] = torch.from_file(path, shared=True, size=numel, dtype=torch.int64)
+    _LOCKS[(rank + 1) << 40] = path + ".lock"
+    return (rank + 1) << 40
+
+
+_FAKE = {}
+
+
+def _fake_push(src, dst_ptrs, stream=None):
+    """red.add emulation: the read-modify-write of another process's buffer under a file lock
+    (the device's atomics need none)."""
+    import fcntl
+    for p in dst_ptrs:
+        base = (p >> 40) << 40
+        off = (p - base) // 8
+        with open(_LOCKS[base], "a") as lk:
+            fcntl.flock(lk, fcntl.LOCK_EX)
+            _FAKE[base][off:off + src.numel()] += src
+            fcntl.flock(lk, fcntl.LOCK_UN)
+
+
+_LOCKS = {}
+
+
+def _worker_peer(rank, world, port, cfg, root, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import datagen
+    from paper_2102_02440_b200 import query
+    from paper_2102_02440_b200.query import PeerMerge, table_slices
+    ws = getattr(datagen, cfg[0])(**cfg[1])
+    part, _ = _build_packed(ws, rank, world)
+    numel = part.numel()
+
+    def fake_ipc(n, device):
+        b = _FakeIpc(n, device, root, rank)
+        _FAKE[b.ptr] = b.tensor
+        return b
+
+    query.IpcBuffer = fake_ipc
+    query.ipc_open = lambda h, device: _fake_open(h, device, numel)
+    query.ipc_close = lambda p: None
+    query.sketch_peer_push = _fake_push
+    buf = torch.zeros_like(part)
+    m = PeerMerge(buf, len(ws.tables), table_slices(ws))
+    outs = []
+    for _ in range(2):   # two steps: zero + barrier, per-table pushes (as the fused scan does), finish
+        m.zero_()
+        buf.copy_(part)
+        for t in ws.tables:
+            if t.name in m.slices:
+                src, dsts = m.push_for(t.name)
+                _fake_push(src, dsts)
+        m.finish()
+        outs.append(buf.clone())
+    if rank == 0:
+        torch.save(outs, out_path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("cfg", [("c1", {"scale": 0.2}), ("c5", {"scale": 5e-5, "w": 64, "wm": 32})])
+def test_peer_merge_host_logic_equals_single_build(cfg, world, tmp_path):
+    """Every rank's merged buffer after the pushes == the single-process build, two steps in a
+    row (the merged buffers are re-zeroed behind a barrier)."""
+    import datagen
+    out = str(tmp_path / "peer.pt")
+    mp.start_processes(_worker_peer, args=(world, _free_port(), cfg, str(tmp_path), out), nprocs=world, join=True,
+                       start_method="spawn")
+    outs = torch.load(out)
+    ws = getattr(datagen, cfg[0])(**cfg[1])
+    full, _ = _build_packed(ws, 0, 1)
+    for b in outs:
+        assert torch.equal(b, full)
