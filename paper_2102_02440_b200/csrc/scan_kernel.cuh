@@ -190,6 +190,11 @@ __device__ __forceinline__ void cp_commit_wait_all() { asm volatile("cp.async.wa
 #define SCAN_LAG 3
 #endif
 constexpr int kLag = SCAN_LAG;   // a tile's gathered keys are consumed kLag tiles later
+// L2 prefetch size of the survivor-key gathers (experiments: tools/build_variant.sh
+// -DSCAN_L2HINT='""')
+#ifndef SCAN_L2HINT
+#define SCAN_L2HINT ".L2::64B"
+#endif
 __device__ __forceinline__ void cp_wait_lag() { asm volatile("cp.async.wait_group %0;" ::"n"(kLag) : "memory"); }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 __device__ __forceinline__ void red_add_u32(uint32_t *p, uint32_t v) {
@@ -740,19 +745,19 @@ __device__ __forceinline__ void eval_preds(const PR (&pr)[NP], const unsigned ch
 __device__ __forceinline__ void cp_async_key(uint32_t dst, const void *src, uint32_t is8) {
     asm volatile(
         "{\n\t.reg .pred p8;\n\tsetp.ne.u32 p8, %2, 0;\n\t"
-        "@p8 cp.async.ca.shared.global.L2::64B [%0], [%1], 8;\n\t"
-        "@!p8 cp.async.ca.shared.global.L2::64B [%0], [%1], 4;\n}" ::"r"(dst), "l"(src), "r"(is8)
+        "@p8 cp.async.ca.shared.global" SCAN_L2HINT " [%0], [%1], 8;\n\t"
+        "@!p8 cp.async.ca.shared.global" SCAN_L2HINT " [%0], [%1], 4;\n}" ::"r"(dst), "l"(src), "r"(is8)
         : "memory");
 }
 template <int W>
 __device__ __forceinline__ void cp_async_fixed_if(bool on, uint32_t dst, const void *src) {
     if (W == 8)
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
-                     "@p cp.async.ca.shared.global.L2::64B [%0], [%1], 8;\n}" ::"r"(dst), "l"(src), "r"((int)on)
+                     "@p cp.async.ca.shared.global" SCAN_L2HINT " [%0], [%1], 8;\n}" ::"r"(dst), "l"(src), "r"((int)on)
                      : "memory");
     else
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
-                     "@p cp.async.ca.shared.global.L2::64B [%0], [%1], 4;\n}" ::"r"(dst), "l"(src), "r"((int)on)
+                     "@p cp.async.ca.shared.global" SCAN_L2HINT " [%0], [%1], 4;\n}" ::"r"(dst), "l"(src), "r"((int)on)
                      : "memory");
 }
 __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
