@@ -203,6 +203,10 @@ __device__ __forceinline__ void red_add_u32(uint32_t *p, uint32_t v) {
 __device__ __forceinline__ void red_add_s64(int64_t *p, int64_t v) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// shared-memory int32 add at a 32-bit shared address (no generic-to-shared conversion per update)
+__device__ __forceinline__ void red_shared_s32(uint32_t a, int v) {
+    asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ bool in_set(const int64_t *s, uint32_t n, int64_t v) {
     uint32_t lo = 0, hi = n;
@@ -604,14 +608,23 @@ __device__ __forceinline__ void process_fast(const SParams &P, unsigned char *sm
         const uint4 q = b.e[k];
         const STarget &tp = P.tgt[P.kprim[k]];   // field >> 1 is its counter index
         if (tp.smem_off >= 0) {
-            int32_t *base = sc + tp.smem_off;
+            const uint32_t base = smem_u32(sc + tp.smem_off);
+            if (tp.d == 5) {   // the common depth: no per-row bound checks
 #pragma unroll
-            for (int r = 0; r < 8; ++r)
-                if (r < (int)tp.d) {
+                for (int r = 0; r < 5; ++r) {
                     const uint32_t f = lut_fld(q, r);
                     SCAN_CHECK((f >> 1) < tp.d * tp.cells && (f >> 1) / tp.cells == (uint32_t)r);
-                    atomicAdd(base + (f >> 1), (f & 1u) ? -cnt : cnt);
+                    red_shared_s32(base + (f >> 1) * 4u, (f & 1u) ? -cnt : cnt);
                 }
+            } else {
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    if (r < (int)tp.d) {
+                        const uint32_t f = lut_fld(q, r);
+                        SCAN_CHECK((f >> 1) < tp.d * tp.cells && (f >> 1) / tp.cells == (uint32_t)r);
+                        red_shared_s32(base + (f >> 1) * 4u, (f & 1u) ? -cnt : cnt);
+                    }
+            }
         } else {
 #pragma unroll
             for (int r = 0; r < 8; ++r)
