@@ -266,7 +266,7 @@ def _relaunch(n: int) -> int:
     """`bench.py --gpus N` run as one process: re-executes itself under torchrun with N ranks
     on this node (one process per GPU, NCCL over NVLink), rendezvous on 127.0.0.1."""
     import socket
-    if torch.cuda.device_count() < n:
+    if torch.cuda.device_count() < n and not os.environ.get("COMPASS_BENCH_SHARED_GPU"):
         print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {torch.cuda.device_count()}", file=sys.stderr)
         return 2
     with socket.socket() as so:
@@ -284,6 +284,12 @@ def _setup_dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and os.environ.get("COMPASS_BENCH_SHARED_GPU"):
+        # functional test of the multi-rank bench logic on a one-GPU box (tests/test_bench_ranks_gpu.py):
+        # every rank on cuda:0, gloo collectives; the numbers of such a run are not measurements
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+        return world, rank, 0
     if world > 1:
         # NCCL's communicator line (rank count, NVLS / channels) is kept so the JSON line can
         # show the collective really spanned every rank
