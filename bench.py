@@ -425,7 +425,7 @@ def main():
     ap.add_argument("--workload", default="C4", choices=["C1", "C2", "C3", "C3t", "C4", "C5", "C5-cycle"])
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--cpu-rows", type=int, default=300_000_000)
-    ap.add_argument("--ref-rows", type=int, default=20_000_000)
+    ap.add_argument("--ref-rows", type=int, default=100_000_000)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--wire", default="i32", choices=["i32", "i64"], help="all-reduce wire format (N > 1)")

@@ -3,6 +3,7 @@
 The oracle cannot replay 10^9-row builds in a test, so at full size the CUDA path is checked
 through properties that hold at any size and through independent device paths:
   * linearity (PAPER.md:86): the table built in 8 row shards == built in one call, bit-exact;
+  * the same builds with the merge over peer memory fused into every scan == the plain builds;
   * the persistent scan == the grid-stride kernel (`COMPASS_SCAN=generic`, a separate
     implementation of filter + update) counter for counter;
   * survivor counts == a plain torch evaluation of the predicates;
@@ -60,6 +61,17 @@ def test_full_size_build_linearity_and_independent_kernel(name, monkeypatch):
     eight, s8 = _counters(_build(ws, data, preds, dev, shards=8))
     assert torch.equal(s1, s8) and all(torch.equal(a, b) for a, b in zip(one, eight))
     assert s1.tolist() == [_torch_survivors(data[t.name], preds[t.name]) for t in ws.tables]
+    # the timed launch configuration with the merge over peer memory fused into each scan
+    # (bench.py --merge peer; one rank: the merged buffer is the rank's own)
+    peer = QueryRun(ws, dev, merge="peer")
+    peer.zero_()
+    for t in ws.tables:
+        peer.build_table(t.name, data[t.name], preds[t.name])
+    peer.allreduce()
+    torch.cuda.synchronize()
+    pc, ps = _counters(peer)
+    assert torch.equal(s1, ps) and all(torch.equal(a, b) for a, b in zip(one, pc))
+    peer.close()
     monkeypatch.setenv("COMPASS_SCAN", "generic")
     gen, sg = _counters(_build(ws, data, preds, dev))
     assert torch.equal(s1, sg)
