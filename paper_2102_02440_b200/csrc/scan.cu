@@ -608,9 +608,18 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched, bo
     }
     void *kargs[] = {&P};
     if (fuse) {
-        SKB_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(threads), kargs, off, stream));
+        // COMPASS_SCAN_NOCOOP: take the fallback below (tests)
+        const cudaError_t e = getenv("COMPASS_SCAN_NOCOOP") ? cudaErrorCooperativeLaunchTooLarge
+                              : cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(threads), kargs, off, stream);
+        if (e == cudaSuccess) {
+            *pushed = true;
+        } else {   // co-residency not available (e.g. a restricted grid): plain scan, the caller pushes after it
+            cudaGetLastError();
+            memset(&P.push, 0, sizeof(P.push));
+            P.push_bar = nullptr;
+            SKB_CUDA(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(threads), kargs, off, stream));
+        }
         SKB_CUDA(cudaFreeAsync(bar, stream));
-        *pushed = true;
     } else {
         SKB_CUDA(cudaLaunchKernel(kern, dim3((unsigned)grid), dim3(threads), kargs, off, stream));
     }

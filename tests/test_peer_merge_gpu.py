@@ -107,6 +107,33 @@ def test_peer_merge_one_process_unfused(monkeypatch):
     run.close()
 
 
+def test_peer_merge_cooperative_launch_fallback(monkeypatch):
+    """Without a cooperative launch (COMPASS_SCAN_NOCOOP stands in for a refused one) the scan
+    runs plain and one k_peer_push follows it: same merged buffer, one more launch per table."""
+    import datagen
+    import paper_2102_02440_b200 as pb
+    from paper_2102_02440_b200.query import QueryRun
+    dev = torch.device("cuda", 0)
+    ws = datagen.c5(scale=2e-4, w=128, wm=64)
+    data = {t.name: datagen.generate_table(ws, t.name, dev) for t in ws.tables}
+    counts = {}
+    for mode in ("coop", "fallback"):
+        if mode == "fallback":
+            monkeypatch.setenv("COMPASS_SCAN_NOCOOP", "1")
+        run = QueryRun(ws, dev, merge="peer")
+        for _ in range(2):   # second pass: lookup tables cached
+            run.zero_()
+            l0 = pb.kernel_launches()
+            for t in ws.tables:
+                run.build_table(t.name, data[t.name], datagen.resolve_preds(ws, t.name))
+            counts[mode] = pb.kernel_launches() - l0
+            run.allreduce()
+        torch.cuda.synchronize()
+        assert np.array_equal(run.buffer.cpu().numpy(), _oracle_packed(ws))
+        run.close()
+    assert counts["fallback"] == counts["coop"] + len(ws.tables)
+
+
 def test_peer_push_histogram_epilogue_not_fused():
     """A hinted key domain sends the 1-D sketches through the histogram epilogue after the
     scan: the push must follow the epilogue (not fused), and the merged counters are exact."""
