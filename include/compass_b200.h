@@ -180,8 +180,9 @@ SK_API sk_status sketch_wire_unpack(const int32_t *wire_dev, int64_t *counters_d
  * sketch_update_filtered_push: sketch_update_filtered, then the push of `src` — FUSED into the
  *   scan when the optimised kernel runs without a histogram epilogue: a cooperative launch
  *   whose CTAs, after a grid barrier that follows the last flush, push the slice (no separate
- *   kernel, no NCCL); otherwise one k_peer_push launch after the scan.  `src` must cover the
- *   counters of every target (the table's slice of the partial buffer).
+ *   kernel, no NCCL); otherwise (grid-stride kernel, histogram epilogue, or a refused
+ *   cooperative launch) one k_peer_push launch after the scan.  `src` must cover the counters
+ *   of every target (the table's slice of the partial buffer).
  * sketch_peer_push: the push alone (e.g. the survivor counts).
  * Errors: SK_EINVAL (NULL pointers, misalignment, n_peers out of range), SK_ECUDA. */
 typedef struct {
