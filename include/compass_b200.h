@@ -109,6 +109,7 @@ SK_API sk_status sketch_zero(sk_sketch *sk, void *stream);
  *   For every surviving tuple and every target t, row r of t's sketch gets
  *       ndim 1: sk[r][h_r(k0)]              += xi_r(k0)
  *       ndim 2: M[r][h0_r(k0)][h1_r(k1)]     += xi0_r(k0) * xi1_r(k1)
+ *       ndim 3: T[r][h0_r(k0)][h1_r(k1)][h2_r(k2)] += xi0_r(k0) xi1_r(k1) xi2_r(k2)
  *   with kq = cols[target.key_col[q]][i].
  *   *survivors_dev (device int64, may be NULL) += number of surviving tuples
  *   (the exact selection cardinality).
@@ -123,10 +124,14 @@ typedef struct {
     const void *data;   /* device pointer */
     uint32_t dtype;     /* sk_dtype */
     uint64_t domain;    /* optional hint: key values lie in [0, domain); 0 = unknown.  With a
-                           hint <= 2^22 the 1-D sketches of this key column are built by
-                           histogram-then-sketch (one L2 atomic per surviving tuple, hashing once
-                           per distinct key; exact by linearity).  Values outside
-                           the hinted domain are still counted exactly (direct path). */
+                           hint <= 2^22: int32 key columns (<= 2 keys, <= 2 predicates) take the
+                           lookup-table path (one 16-byte table entry holds the (bucket, sign) of
+                           every row of the key's hash family; matrices reuse it); otherwise the
+                           1-D sketches of the column are built by histogram-then-sketch (one L2
+                           atomic per surviving tuple, hashing once per distinct key).  Both are
+                           exact by linearity; values outside the hinted domain
+                           are still counted exactly (hashed directly).  A predicate column's
+                           hint also sets the expected selectivity the scan is tuned for. */
 } sk_column;
 
 typedef enum { SK_PRED_POINT = 0, SK_PRED_RANGE = 1, SK_PRED_SUBSET = 2 } sk_pred_kind;
