@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <array>
 #include <deque>
+#include <set>
 #include <map>
 #include <tuple>
 #include <string>
@@ -2275,11 +2276,40 @@ static void node_logbounds(const Plan &P, const std::vector<double> &logF, std::
     }
 }
 
+// Residues (and tensor-core M planes) of matrices per (matrix pointer, orientation): computed
+// once per batch, or once per planning call for the sketches' own counters (BatchShare: their
+// contents cannot change while plan_greedy / plan_enumerate runs; one map per modulus count)
+using ResKey = std::pair<const void *, int>;
+struct BatchShare {
+    DevPool pool;
+    std::map<int, std::map<ResKey, uint32_t *>> by_K;
+    std::set<const void *> stable;
+    explicit BatchShare(const sk_graph *g) {
+        if (!g) return;
+        for (uint32_t m = 0; m < g->n_mats; ++m)
+            if (g->mat && g->mat[m]) stable.insert(g->mat[m]->counters);
+    }
+};
+struct ResCache {
+    std::map<ResKey, uint32_t *> map;
+    std::map<ResKey, uint32_t *> *shared = nullptr;
+    DevPool *spool = nullptr;
+    const std::set<const void *> *stable = nullptr;
+    bool is_shared(const void *p) const { return shared && stable && stable->count(p); }
+    uint32_t *find(const ResKey &k) const {
+        const auto &m = is_shared(k.first) ? *shared : map;
+        auto it = m.find(k);
+        return it == m.end() ? nullptr : it->second;
+    }
+    void put(const ResKey &k, uint32_t *p) { (is_shared(k.first) ? *shared : map)[k] = p; }
+    DevPool &pool_for(const void *p, DevPool &batch) { return is_shared(p) ? *spool : batch; }
+};
+
 // Enqueue every kernel of one sub-plan on `stream` (no host synchronisation): per-row
 // residues -> acc[K][d] (zeroed by the caller), per-sketch-row L1 norms -> l1[n_uniq][d].
 static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const sk_sketch *> &uniq,
                               DevPool &pool, uint64_t *acc, unsigned long long *l1, cudaStream_t stream,
-                              int ring = 0, std::map<std::pair<const void *, int>, uint32_t *> *rescache = nullptr,
+                              int ring = 0, ResCache *rescache = nullptr,
                               const Mods *resmods = nullptr, const std::vector<char> *narrow = nullptr,
                               std::map<std::tuple<const void *, int, int>, const int64_t *> *foldcache = nullptr,
                               std::map<std::pair<const void *, int>, std::array<void *, 4>> *sortcache = nullptr,
@@ -2579,18 +2609,15 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                        md.K <= resmods->K && !getenv("COMPASS_EST_NO_MATVEC")) {
                 // residues of this (folded) matrix in this orientation: once per batch
                 const auto key = std::make_pair((const void *)n.data[0], qchild);
-                auto it = rescache->find(key);
-                uint32_t *Rc;
-                if (it == rescache->end()) {
+                uint32_t *Rc = rescache->find(key);
+                if (!Rc) {
                     void *rb;
                     const size_t cells = size_t(n.w[0]) * n.w[1];
-                    if ((st = dalloc(pool, size_t(resmods->K) * d * cells * 4, stream, &rb))) return st;
+                    if ((st = dalloc(rescache->pool_for(key.first, pool), size_t(resmods->K) * d * cells * 4, stream, &rb))) return st;
                     k_mat_residues<<<dim3(std::max(1, 1184 / d), 1, d), 256, 0, stream>>>(n.data[0], d, n.w[0], n.w[1], qchild, *resmods, (uint32_t *)rb);
                     count_launch();
                     Rc = (uint32_t *)rb;
-                    (*rescache)[key] = Rc;
-                } else {
-                    Rc = it->second;
+                    rescache->put(key, Rc);
                 }
                 // one modulus per CTA unless that makes the grid very large (more CTAs in
                 // flight hide the latency of the residue loads)
@@ -2604,18 +2631,15 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                 // batch), dotted with the leg-0 message inside the same kernel
                 const int qc = 1, qo = 0;
                 const auto key = std::make_pair((const void *)n.data[0], qc);
-                auto it = rescache->find(key);
-                uint32_t *Rc;
-                if (it == rescache->end()) {
+                uint32_t *Rc = rescache->find(key);
+                if (!Rc) {
                     void *rb;
                     const size_t cells = size_t(n.w[0]) * n.w[1];
-                    if ((st = dalloc(pool, size_t(resmods->K) * d * cells * 4, stream, &rb))) return st;
+                    if ((st = dalloc(rescache->pool_for(key.first, pool), size_t(resmods->K) * d * cells * 4, stream, &rb))) return st;
                     k_mat_residues<<<dim3(std::max(1, 1184 / d), 1, d), 256, 0, stream>>>(n.data[0], d, n.w[0], n.w[1], qc, *resmods, (uint32_t *)rb);
                     count_launch();
                     Rc = (uint32_t *)rb;
-                    (*rescache)[key] = Rc;
-                } else {
-                    Rc = it->second;
+                    rescache->put(key, Rc);
                 }
                 const int nto = (n.w[qo] + MV_OUT - 1) / MV_OUT;
                 const int G = (d * nto * md.K <= 4096) ? 1 : MV_G;
@@ -2633,17 +2657,15 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                 const uint32_t *Rc = nullptr;   // residues shared with the chain mat-vecs of the batch
                 if (rescache && resmods && md.K <= resmods->K) {
                     const auto key = std::make_pair((const void *)n.data[0], qchild);
-                    auto it = rescache->find(key);
-                    if (it == rescache->end()) {
+                    Rc = rescache->find(key);
+                    if (!Rc) {
                         void *rb;
                         const size_t cells = size_t(n.w[0]) * n.w[1];
-                        if ((st = dalloc(pool, size_t(resmods->K) * d * cells * 4, stream, &rb))) return st;
+                        if ((st = dalloc(rescache->pool_for(key.first, pool), size_t(resmods->K) * d * cells * 4, stream, &rb))) return st;
                         k_mat_residues<<<dim3(std::max(1, 1184 / d), 1, d), 256, 0, stream>>>(n.data[0], d, n.w[0], n.w[1], qchild, *resmods, (uint32_t *)rb);
                         count_launch();
-                        (*rescache)[key] = (uint32_t *)rb;
+                        rescache->put(key, (uint32_t *)rb);
                         Rc = (uint32_t *)rb;
-                    } else {
-                        Rc = it->second;
                     }
                 }
                 const char *ge = getenv("COMPASS_GEMM");
@@ -2654,17 +2676,14 @@ static sk_status enqueue_plan(const Plan &P, const Mods &md, std::vector<const s
                     const int tbt = (nB + TC_M - 1) / TC_M, tjt = (wj + TC_N - 1) / TC_N, tkb = (wi + TC_KB - 1) / TC_KB;
                     const int Kres = resmods->K;
                     const auto pkey = std::make_pair((const void *)n.data[0], qchild + 16);
-                    auto pit = rescache->find(pkey);
-                    unsigned char *Mp;
-                    if (pit == rescache->end()) {
+                    unsigned char *Mp = (unsigned char *)rescache->find(pkey);
+                    if (!Mp) {
                         void *pm;
-                        if ((st = dalloc(pool, size_t(Kres) * d * tjt * tkb * (4 * TC_B_PLANE), stream, &pm))) return st;
+                        if ((st = dalloc(rescache->pool_for(pkey.first, pool), size_t(Kres) * d * tjt * tkb * (4 * TC_B_PLANE), stream, &pm))) return st;
                         k_planes_m<<<1184, 256, 0, stream>>>(Rc, Kres * d, wi, wj, tjt, tkb, (unsigned char *)pm);
                         count_launch();
-                        (*rescache)[pkey] = (uint32_t *)pm;
+                        rescache->put(pkey, (uint32_t *)pm);
                         Mp = (unsigned char *)pm;
-                    } else {
-                        Mp = (unsigned char *)pit->second;
                     }
                     void *px;
                     if ((st = dalloc(pool, size_t(K) * d * tbt * tkb * (4 * TC_A_PLANE), stream, &px))) return st;
@@ -2823,7 +2842,7 @@ static sk_status run_two_way(std::vector<Plan> &plans, const std::vector<size_t>
 }
 
 static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vector<std::vector<SBig>> &rows,
-                           cudaStream_t stream, bool no_two_way = false) {
+                           cudaStream_t stream, bool no_two_way = false, BatchShare *share = nullptr) {
     const size_t n = plans.size();
     rows.assign(n, {});
     if (!n) return SK_OK;
@@ -2844,7 +2863,7 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
             if (rest_idx.empty()) return SK_OK;
             for (size_t i : rest_idx) rest.push_back(std::move(plans[i]));
             std::vector<std::vector<SBig>> rrows;
-            st = run_batch(g, rest, rrows, stream, /*no_two_way=*/true);
+            st = run_batch(g, rest, rrows, stream, /*no_two_way=*/true, share);
             for (size_t j = 0; j < rest_idx.size(); ++j) {
                 plans[rest_idx[j]] = std::move(rest[j]);
                 rows[rest_idx[j]] = std::move(rrows[j]);
@@ -2934,7 +2953,12 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
     kmax_mods.K = 0;
     for (size_t i = 0; i < n; ++i)
         if (!exact[i] && mds[i].K > kmax_mods.K) kmax_mods = mds[i];
-    std::map<std::pair<const void *, int>, uint32_t *> rescache;
+    ResCache rescache;
+    if (share) {
+        rescache.shared = &share->by_K[kmax_mods.K];
+        rescache.spool = &share->pool;
+        rescache.stable = &share->stable;
+    }
     // exact plans: 64-bit merged nodes where the survivor-based node bound is <= 2^61
     // (re-checked below with the measured L1 norms)
     std::vector<std::vector<char>> narrow(n);
@@ -3057,7 +3081,7 @@ namespace skb {
 
 // Batched evaluation: masks[i] -> est[i] (median, fp64), optional per-row values.
 sk_status estimate_batch(const sk_graph *g, const uint64_t *masks, uint32_t n, double *est,
-                         std::vector<std::vector<SBig>> *rows_out, cudaStream_t stream) {
+                         std::vector<std::vector<SBig>> *rows_out, cudaStream_t stream, BatchShare *share = nullptr) {
     if (!g) return fail(SK_EINVAL, "estimate: NULL graph");
     std::vector<Plan> plans;
     std::vector<uint32_t> which;
@@ -3084,7 +3108,7 @@ sk_status estimate_batch(const sk_graph *g, const uint64_t *masks, uint32_t n, d
     cudaGetDevice(&prev);
     SKB_CUDA(cudaSetDevice(plans[0].device));
     std::vector<std::vector<SBig>> rows;
-    sk_status st = run_batch(g, plans, rows, stream);
+    sk_status st = run_batch(g, plans, rows, stream, false, share);
     cudaSetDevice(prev);
     if (st) return st;
     for (size_t j = 0; j < plans.size(); ++j) {
@@ -3149,7 +3173,8 @@ struct CardCache {
     std::map<uint64_t, double> cache;
     sk_status err = SK_OK;
     uint64_t calls = 0;
-    CardCache(const sk_graph *g_, cudaStream_t s) : g(g_), stream(s) {}
+    BatchShare share;   // matrix residues shared by the batches of this planning call
+    CardCache(const sk_graph *g_, cudaStream_t s) : g(g_), stream(s), share(g_) {}
     sk_status prefetch() {
         const uint32_t n = g->n_tables;
         if (n > 16) return SK_OK;
@@ -3174,7 +3199,7 @@ struct CardCache {
         }
         if (masks.size() > 512) return SK_OK;
         std::vector<double> est(masks.size());
-        sk_status st = estimate_batch(g, masks.data(), (uint32_t)masks.size(), est.data(), nullptr, stream);
+        sk_status st = estimate_batch(g, masks.data(), (uint32_t)masks.size(), est.data(), nullptr, stream, &share);
         if (st) return st;
         for (size_t i = 0; i < masks.size(); ++i) cache[masks[i]] = std::max(est[i], 0.0);
         return SK_OK;
@@ -3189,7 +3214,7 @@ struct CardCache {
                 masks.push_back(m);
         if (masks.empty()) return SK_OK;
         std::vector<double> est(masks.size());
-        sk_status st = estimate_batch(g, masks.data(), (uint32_t)masks.size(), est.data(), nullptr, stream);
+        sk_status st = estimate_batch(g, masks.data(), (uint32_t)masks.size(), est.data(), nullptr, stream, &share);
         if (st) return st;
         for (size_t i = 0; i < masks.size(); ++i) cache[masks[i]] = std::max(est[i], 0.0);
         return SK_OK;
