@@ -2284,6 +2284,7 @@ struct BatchShare {
     DevPool pool;
     std::map<int, std::map<ResKey, uint32_t *>> by_K;
     std::set<const void *> stable;
+    std::map<const sk_sketch *, std::vector<uint64_t>> l1;   // per-row L1 norms (host)
     explicit BatchShare(const sk_graph *g) {
         if (!g) return;
         for (uint32_t m = 0; m < g->n_mats; ++m)
@@ -2990,15 +2991,20 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
             if (!gidx.count(sk)) { gidx[sk] = guniq.size(); guniq.push_back(sk); }
     int dmax = 1;
     for (auto &P : plans) dmax = std::max(dmax, P.d);
+    // norms already measured by an earlier batch of this planning call are reused (the
+    // sketches cannot change while it runs); the rest are measured now
+    std::vector<const sk_sketch *> l1todo;
+    for (auto *sk : guniq)
+        if (!(share && share->l1.count(sk))) l1todo.push_back(sk);
     void *dl1;
-    if ((st = dalloc(pool, guniq.size() * dmax * 8 + 8, stream, &dl1))) return st;
-    SKB_CUDA(cudaMemsetAsync(dl1, 0, guniq.size() * dmax * 8 + 8, stream));
-    for (size_t b0 = 0; b0 < guniq.size(); b0 += kMaxL1Items) {
+    if ((st = dalloc(pool, l1todo.size() * dmax * 8 + 8, stream, &dl1))) return st;
+    SKB_CUDA(cudaMemsetAsync(dl1, 0, l1todo.size() * dmax * 8 + 8, stream));
+    for (size_t b0 = 0; b0 < l1todo.size(); b0 += kMaxL1Items) {
         L1Items items;
-        items.n = (int)std::min<size_t>(kMaxL1Items, guniq.size() - b0);
+        items.n = (int)std::min<size_t>(kMaxL1Items, l1todo.size() - b0);
         uint32_t maxcells = 1;
         for (int j = 0; j < items.n; ++j) {
-            const sk_sketch *sk = guniq[b0 + j];
+            const sk_sketch *sk = l1todo[b0 + j];
             items.it[j] = {sk->counters, sk->d, (uint32_t)(sk->n_counters / sk->d)};
             maxcells = std::max(maxcells, items.it[j].cells);
         }
@@ -3014,10 +3020,19 @@ static sk_status run_batch(const sk_graph *g, std::vector<Plan> &plans, std::vec
         if ((st = enqueue_plan(plans[i], mds[i], uniqs[i], pool, res + off_acc[i], nullptr, stream, exact[i] ? 1 : 0,
                                &rescache, &kmax_mods, exact[i] ? &narrow[i] : nullptr, &foldcache, &sortcache, &rankcache)))
             return st;
-    std::vector<uint64_t> host(words), hl1(guniq.size() * dmax);
+    std::vector<uint64_t> host(words), hl1(guniq.size() * dmax), hnew(l1todo.size() * dmax);
     SKB_CUDA(cudaMemcpyAsync(host.data(), res, words * 8, cudaMemcpyDeviceToHost, stream));
-    if (!hl1.empty()) SKB_CUDA(cudaMemcpyAsync(hl1.data(), dl1, hl1.size() * 8, cudaMemcpyDeviceToHost, stream));
+    if (!hnew.empty()) SKB_CUDA(cudaMemcpyAsync(hnew.data(), dl1, hnew.size() * 8, cudaMemcpyDeviceToHost, stream));
     SKB_CUDA(cudaStreamSynchronize(stream));
+    for (size_t j = 0; j < l1todo.size(); ++j) {
+        std::copy(hnew.begin() + j * dmax, hnew.begin() + (j + 1) * dmax, hl1.begin() + gidx[l1todo[j]] * dmax);
+        if (share) share->l1[l1todo[j]] = std::vector<uint64_t>(hnew.begin() + j * dmax, hnew.begin() + (j + 1) * dmax);
+    }
+    if (share)
+        for (size_t j = 0; j < guniq.size(); ++j) {
+            const auto &v = share->l1[guniq[j]];
+            for (int r = 0; r < dmax && r < (int)v.size(); ++r) hl1[j * dmax + r] = v[r];
+        }
     for (size_t i = 0; i < n; ++i)   // each plan's L1 slots, as enqueue_plan would have written them
         for (size_t u = 0; u < uniqs[i].size(); ++u)
             for (int r = 0; r < plans[i].d; ++r) host[off_l1[i] + u * plans[i].d + r] = hl1[gidx[uniqs[i][u]] * dmax + r];
