@@ -195,12 +195,25 @@ typedef struct {
     int64_t *const *dst;
     uint32_t n_peers;
     uint64_t n;
+    /* owner_mode 1 (reduce-scatter over peer memory): the merged buffer of `total` elements is
+     * split into n_peers contiguous ranges (range o starts at floor(total*o/n_peers) rounded
+     * down to even); element i of src (merged-buffer index offset+i, offset even) is added
+     * into its owner's buffer only, so each rank sends its partial once; after every rank's
+     * pushes (caller barrier) sketch_peer_gather copies the other owners' ranges into this
+     * rank's buffer (P2P reads).  owner_mode 0: added into every rank's buffer (one shot). */
+    uint32_t owner_mode;
+    uint32_t rank;      /* this rank (index into dst) */
+    uint64_t offset;    /* owner_mode: element offset of src in the merged buffer */
+    uint64_t total;     /* owner_mode: elements of the merged buffer */
 } sk_peer_push;
 SK_API sk_status sketch_update_filtered_push(const sk_column *cols, uint32_t n_cols, uint64_t n_rows,
                                              const sk_pred *preds, uint32_t n_preds,
                                              const sk_target *targets, uint32_t n_targets,
                                              int64_t *survivors_dev, const sk_peer_push *push, void *stream);
 SK_API sk_status sketch_peer_push(const sk_peer_push *push, void *stream);
+/* After an owner-mode merge: dst[rank][i] = dst[owner(i)][i] for every i < total owned by
+ * another rank (dst = every rank's merged-buffer base as mapped here; src, n, offset unused). */
+SK_API sk_status sketch_peer_gather(const sk_peer_push *push, void *stream);
 
 /* CUDA IPC for the merged buffers.  sk_ipc_alloc: `bytes` of zeroed device memory on `device`
  * (library-owned until sk_ipc_free) and its SK_IPC_HANDLE_BYTES-byte handle.  sk_ipc_open:

@@ -55,7 +55,8 @@ class sk_target(ctypes.Structure):
 
 class sk_peer_push(ctypes.Structure):
     _fields_ = [("src", ctypes.c_void_p), ("dst", ctypes.POINTER(ctypes.c_void_p)), ("n_peers", ctypes.c_uint32),
-                ("n", ctypes.c_uint64)]
+                ("n", ctypes.c_uint64), ("owner_mode", ctypes.c_uint32), ("rank", ctypes.c_uint32),
+                ("offset", ctypes.c_uint64), ("total", ctypes.c_uint64)]
 
 
 SK_IPC_HANDLE_BYTES = 64
@@ -74,7 +75,7 @@ class sk_graph(ctypes.Structure):
 EXPORTS = ["sketch_create", "sketch_destroy", "sketch_counters", "sketch_zero", "sketch_update_filtered",
            "sketch_merge", "sketch_wire_pack", "sketch_wire_unpack", "estimate_join", "estimate_join_exact", "estimate_subplans", "plan_greedy",
            "plan_enumerate", "exact_join_size", "sk_last_error", "sk_version", "sk_kernel_launches",
-           "sketch_update_filtered_push", "sketch_peer_push", "sk_ipc_alloc", "sk_ipc_free", "sk_ipc_open", "sk_ipc_close"]
+           "sketch_update_filtered_push", "sketch_peer_push", "sketch_peer_gather", "sk_ipc_alloc", "sk_ipc_free", "sk_ipc_open", "sk_ipc_close"]
 
 # Algorithm 1 search-space settings
 ENUM_GREEDY, ENUM_FULL_GREEDY, ENUM_LIMIT, ENUM_EXHAUSTIVE = range(4)
@@ -158,6 +159,8 @@ def lib() -> ctypes.CDLL:
                                                       ctypes.POINTER(sk_target), u32, vp, ctypes.POINTER(sk_peer_push), vp]
             L.sketch_peer_push.restype = st
             L.sketch_peer_push.argtypes = [ctypes.POINTER(sk_peer_push), vp]
+            L.sketch_peer_gather.restype = st
+            L.sketch_peer_gather.argtypes = [ctypes.POINTER(sk_peer_push), vp]
             L.sk_ipc_alloc.restype = st
             L.sk_ipc_alloc.argtypes = [u64, ctypes.c_int, ctypes.POINTER(vp), ctypes.c_char_p]
             L.sk_ipc_free.restype = st
@@ -270,7 +273,7 @@ def sketch_update_filtered(columns, n_rows: int, preds, targets, survivors: torc
             tg[i].key_col[q] = k
     sp = ctypes.c_void_p(survivors.data_ptr()) if survivors is not None else None
     if push is not None:
-        pp = _peer_push_desc(*push)
+        pp = _peer_push_desc(push[0], push[1], push[2] if len(push) > 2 else None)
         _check(lib().sketch_update_filtered_push(cols, ncol, n_rows, pr, len(preds), tg, len(targets), sp,
                                                  ctypes.byref(pp), ctypes.c_void_p(_stream_ptr(stream))))
         return
@@ -278,23 +281,35 @@ def sketch_update_filtered(columns, n_rows: int, preds, targets, survivors: torc
                                         ctypes.c_void_p(_stream_ptr(stream))))
 
 
-def _peer_push_desc(src: torch.Tensor, dst_ptrs) -> "sk_peer_push":
-    assert src.dtype == torch.int64 and src.is_cuda and src.is_contiguous()
+def _peer_push_desc(src, dst_ptrs, owner=None) -> "sk_peer_push":
+    """owner = (rank, offset, total): reduce-scatter mode (each element to its owner only)."""
     pp = sk_peer_push()
-    pp.src = src.data_ptr()
+    if src is not None:
+        assert src.dtype == torch.int64 and src.is_cuda and src.is_contiguous()
+        pp.src = src.data_ptr()
+        pp.n = src.numel()
     arr = (ctypes.c_void_p * max(1, len(dst_ptrs)))(*[int(p) for p in dst_ptrs])
     pp._keep = arr
     pp.dst = ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
     pp.n_peers = len(dst_ptrs)
-    pp.n = src.numel()
+    if owner is not None:
+        pp.owner_mode, pp.rank, pp.offset, pp.total = 1, int(owner[0]), int(owner[1]), int(owner[2])
     return pp
 
 
-def sketch_peer_push(src: torch.Tensor, dst_ptrs, stream=None):
+def sketch_peer_push(src: torch.Tensor, dst_ptrs, stream=None, owner=None):
     """Add `src` (this rank's partial slice) into every rank's merged slice (device pointers
-    mapped in this process, own included): the cross-GPU merge over peer memory."""
-    pp = _peer_push_desc(src, dst_ptrs)
+    mapped in this process, own included), or with owner = (rank, offset, total) into the
+    owning rank's only: the cross-GPU merge over peer memory."""
+    pp = _peer_push_desc(src, dst_ptrs, owner)
     _check(lib().sketch_peer_push(ctypes.byref(pp), ctypes.c_void_p(_stream_ptr(stream))))
+
+
+def sketch_peer_gather(dst_ptrs, rank: int, total: int, stream=None):
+    """Owner-mode merge, second half: this rank's merged buffer (dst_ptrs[rank]) receives the
+    ranges owned by the other ranks (dst_ptrs = every rank's merged-buffer base)."""
+    pp = _peer_push_desc(None, dst_ptrs, (rank, 0, total))
+    _check(lib().sketch_peer_gather(ctypes.byref(pp), ctypes.c_void_p(_stream_ptr(stream))))
 
 
 class IpcBuffer:

@@ -17,6 +17,22 @@ __global__ void __launch_bounds__(512) k_peer_push(const __grid_constant__ PeerP
     peer_push_range(pp, uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, uint64_t(gridDim.x) * blockDim.x);
 }
 
+// all-gather half of the owner-mode merge: this rank's merged buffer receives every other
+// owner's range (P2P reads that bypass caches: the owners' buffers were written by remote red)
+__global__ void __launch_bounds__(512) k_peer_gather(const __grid_constant__ PeerPush pp) {
+    const uint64_t pairs = pp.total >> 1;
+    int64_t *own = pp.dst[pp.rank];
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < pairs; e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t o = owner_of(2 * e, pp.total, pp.peers);
+        if (o == pp.rank) continue;
+        reinterpret_cast<longlong2 *>(own)[e] = __ldcv(reinterpret_cast<const longlong2 *>(pp.dst[o]) + e);
+    }
+    if ((pp.total & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint32_t o = owner_of(pp.total - 1, pp.total, pp.peers);
+        if (o != pp.rank) own[pp.total - 1] = __ldcv(reinterpret_cast<const long long *>(pp.dst[o]) + pp.total - 1);
+    }
+}
+
 }  // namespace
 
 namespace skb {
@@ -29,6 +45,19 @@ sk_status peer_push_launch(const PeerPush &pp, cudaStream_t stream) {
     const uint64_t pairs = (pp.n + 1) / 2;
     const unsigned grid = (unsigned)std::min<uint64_t>(uint64_t(sms) * 4, (pairs + 511) / 512);
     k_peer_push<<<std::max(1u, grid), 512, 0, stream>>>(pp);
+    SKB_CUDA(cudaGetLastError());
+    count_launch();
+    return SK_OK;
+}
+
+sk_status peer_gather_launch(const PeerPush &pp, cudaStream_t stream) {
+    if (!pp.peers || !pp.total || pp.peers == 1) return SK_OK;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t pairs = (pp.total + 1) / 2;
+    const unsigned grid = (unsigned)std::min<uint64_t>(uint64_t(sms) * 4, (pairs + 511) / 512);
+    k_peer_gather<<<std::max(1u, grid), 512, 0, stream>>>(pp);
     SKB_CUDA(cudaGetLastError());
     count_launch();
     return SK_OK;

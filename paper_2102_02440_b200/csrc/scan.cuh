@@ -36,5 +36,7 @@ sk_status scan_launch(const ScanCall &c, cudaStream_t stream, bool *launched, bo
 
 // Stand-alone push of a partial slice into every rank's merged slice (peer.cuh).
 sk_status peer_push_launch(const PeerPush &pp, cudaStream_t stream);
+// Owner-mode merge, second half: copy the other owners' ranges into this rank's buffer.
+sk_status peer_gather_launch(const PeerPush &pp, cudaStream_t stream);
 
 }  // namespace skb

@@ -334,10 +334,16 @@ static sk_status push_desc(const sk_peer_push *push, PeerPush *pp) {
     if (push->n_peers == 0 || push->n_peers > kMaxPeers) return fail(SK_EINVAL, "peer push: n_peers %u not in 1..%u", push->n_peers, kMaxPeers);
     if (push->n && (!push->src || !push->dst)) return fail(SK_EINVAL, "peer push: NULL src or dst");
     if ((uintptr_t)push->src & 15) return fail(SK_EINVAL, "peer push: src not 16-byte aligned");
+    if (push->owner_mode && (push->rank >= push->n_peers || (push->offset & 1) || push->offset + push->n > push->total))
+        return fail(SK_EINVAL, "peer push: owner mode needs rank < n_peers, an even offset and offset + n <= total");
     memset(pp, 0, sizeof(*pp));
     pp->src = push->src;
     pp->n = push->n;
     pp->peers = push->n_peers;
+    pp->owner_mode = push->owner_mode ? 1u : 0u;
+    pp->rank = push->rank;
+    pp->offset = push->offset;
+    pp->total = push->total;
     for (uint32_t q = 0; q < push->n_peers; ++q) {
         if (push->n && (!push->dst[q] || ((uintptr_t)push->dst[q] & 15))) return fail(SK_EINVAL, "peer push: dst %u NULL or not 16-byte aligned", q);
         pp->dst[q] = push->dst[q];
@@ -353,6 +359,22 @@ extern "C" sk_status sketch_update_filtered_push(const sk_column *cols, uint32_t
     sk_status st = push_desc(push, &pp);
     if (st != SK_OK) return st;
     return update_impl(cols, n_cols, n_rows, preds, n_preds, targets, n_targets, survivors_dev, pp.n ? &pp : nullptr, stream);
+}
+
+extern "C" sk_status sketch_peer_gather(const sk_peer_push *push, void *stream) {
+    if (!push || !push->dst || push->n_peers == 0 || push->n_peers > kMaxPeers || push->rank >= push->n_peers)
+        return fail(SK_EINVAL, "peer gather: bad description");
+    PeerPush pp;
+    memset(&pp, 0, sizeof(pp));
+    pp.peers = push->n_peers;
+    pp.rank = push->rank;
+    pp.total = push->total;
+    pp.owner_mode = 1;
+    for (uint32_t q = 0; q < push->n_peers; ++q) {
+        if (!push->dst[q] || ((uintptr_t)push->dst[q] & 15)) return fail(SK_EINVAL, "peer gather: dst %u NULL or not 16-byte aligned", q);
+        pp.dst[q] = push->dst[q];
+    }
+    return peer_gather_launch(pp, (cudaStream_t)stream);
 }
 
 extern "C" sk_status sketch_peer_push(const sk_peer_push *push, void *stream) {

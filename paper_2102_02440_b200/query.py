@@ -14,8 +14,8 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import (IpcBuffer, JoinGraph, Sketch, ipc_close, ipc_open, sketch_peer_push, sketch_update_filtered,
-               sketch_wire_pack, sketch_wire_unpack)
+from . import (IpcBuffer, JoinGraph, Sketch, ipc_close, ipc_open, sketch_peer_gather, sketch_peer_push,
+               sketch_update_filtered, sketch_wire_pack, sketch_wire_unpack)
 
 
 def packed_layout(q):
@@ -128,15 +128,24 @@ class PeerMerge:
     (after a grid barrier behind the last CTA's flush) where the library can — and finish()
     pushes the survivor counts, waits for the stream, and after a barrier (every rank's pushes
     complete) copies the merged buffer into the partial buffer, so the sketch handles read the
-    sums.  No NCCL kernel; exact integer addition in any order."""
+    sums.  No NCCL kernel; exact integer addition in any order.
 
-    def __init__(self, buffer, n_tables, slices, group=None):
+    mode "all": every element is added into every rank's buffer (one shot, N x the bytes);
+    mode "owner" (default from 3 ranks): reduce-scatter — each element goes to the rank owning
+    its range of the buffer only — then, after a barrier, every rank reads the other owners'
+    ranges (sketch_peer_gather) and a second barrier keeps the owners' buffers untouched until
+    every rank has read them: 2 (N-1)/N x the bytes, like a ring all-reduce."""
+
+    def __init__(self, buffer, n_tables, slices, group=None, mode=None):
         self.buffer, self.slices, self.group = buffer, slices, group
         self.n_s = n_tables + (n_tables & 1)
         self.init = dist.is_available() and dist.is_initialized()
         self.world_n = dist.get_world_size(group) if self.init else 1
         rank = dist.get_rank(group) if self.init else 0
         assert self.world_n <= 8, "peer merge: at most 8 ranks"
+        self.rank = rank
+        self.mode = mode or ("owner" if self.world_n >= 3 else "all")
+        assert self.mode in ("all", "owner")
         self.final = IpcBuffer(buffer.numel(), buffer.device)
         handles = [None] * self.world_n
         if self.world_n > 1:
@@ -168,18 +177,26 @@ class PeerMerge:
         self.final.tensor.zero_()
         self._barrier(stream)
 
+    def _owner(self, a):
+        return (self.rank, a, self.buffer.numel()) if self.mode == "owner" else None
+
     def push_for(self, name: str, stream=None):
         self.stream = stream
         a, b = self.slices[name]
-        return self.buffer[a:b], [p + 8 * a for p in self.ptrs]
+        src, dst = self.buffer[a:b], [p + 8 * a for p in self.ptrs]
+        own = self._owner(a)
+        return (src, dst) if own is None else (src, dst, own)
 
     def reduce_table(self, name: str):
         pass   # the push travels with the scan
 
     def finish(self):
         s = self.stream
-        sketch_peer_push(self.buffer[:self.n_s], list(self.ptrs), stream=s)
+        sketch_peer_push(self.buffer[:self.n_s], list(self.ptrs), stream=s, owner=self._owner(0))
         self._barrier(s)
+        if self.mode == "owner":
+            sketch_peer_gather(list(self.ptrs), self.rank, self.buffer.numel(), stream=s)
+            self._barrier(s)   # every rank has read the owners' ranges before any rank zeroes
         if not self.buffer.is_cuda:   # (host logic tests with emulated peer buffers)
             self.buffer.copy_(self.final.tensor)
             return
@@ -197,7 +214,7 @@ class QueryRun:
     """One query's sketches in one packed int64 buffer; cross-GPU merge by PackedMerge."""
 
     def __init__(self, q, device="cuda", use_domains=True, wire="i64", overlap=False, group=None, always_merge=False,
-                 merge="nccl"):
+                 merge="nccl", peer_mode=None):
         self.q = q
         self.use_domains = use_domains
         self.device = torch.device(device)
@@ -219,7 +236,7 @@ class QueryRun:
         assert merge in ("nccl", "peer")
         self.peer = merge == "peer"
         if self.peer:
-            self.merge = PeerMerge(self.buffer, len(self.tnames), table_slices(q), group)
+            self.merge = PeerMerge(self.buffer, len(self.tnames), table_slices(q), group, mode=peer_mode)
         else:
             self.merge = PackedMerge(self.buffer, len(self.tnames), table_slices(q), wire, overlap, group,
                                      pack=lambda a, b: sketch_wire_pack(a, b),

@@ -228,23 +228,44 @@ def _fake_open(handle, device, numel):
 _FAKE = {}
 
 
-def _fake_push(src, dst_ptrs, stream=None):
+def _owner_lo(total, peers, o):
+    return total if o >= peers else (total * o // peers) & ~1
+
+
+def _fake_push(src, dst_ptrs, stream=None, owner=None):
     """red.add emulation: the read-modify-write of another process's buffer under a file lock
-    (the device's atomics need none)."""
+    (the device's atomics need none).  owner = (rank, offset, total): each element only to the
+    rank owning its range (the library's owner mode, csrc/peer.cuh)."""
     import fcntl
-    for p in dst_ptrs:
+    n = src.numel()
+    for q, p in enumerate(dst_ptrs):
         base = (p >> 40) << 40
         off = (p - base) // 8
+        a, b = 0, n
+        if owner is not None:   # this rank's share of src owned by rank q
+            _, o0, total = owner
+            a = max(0, _owner_lo(total, len(dst_ptrs), q) - o0)
+            b = min(n, _owner_lo(total, len(dst_ptrs), q + 1) - o0)
+            if a >= b:
+                continue
         with open(_LOCKS[base], "a") as lk:
             fcntl.flock(lk, fcntl.LOCK_EX)
-            _FAKE[base][off:off + src.numel()] += src
+            _FAKE[base][off + a:off + b] += src[a:b]
             fcntl.flock(lk, fcntl.LOCK_UN)
+
+
+def _fake_gather(dst_ptrs, rank, total, stream=None):
+    own = _FAKE[dst_ptrs[rank]]
+    for q, p in enumerate(dst_ptrs):
+        if q != rank:
+            a, b = _owner_lo(total, len(dst_ptrs), q), _owner_lo(total, len(dst_ptrs), q + 1)
+            own[a:b] = _FAKE[p][a:b]
 
 
 _LOCKS = {}
 
 
-def _worker_peer(rank, world, port, cfg, root, out_path):
+def _worker_peer(rank, world, port, cfg, root, out_path, mode):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import datagen
@@ -263,16 +284,16 @@ def _worker_peer(rank, world, port, cfg, root, out_path):
     query.ipc_open = lambda h, device: _fake_open(h, device, numel)
     query.ipc_close = lambda p: None
     query.sketch_peer_push = _fake_push
+    query.sketch_peer_gather = _fake_gather
     buf = torch.zeros_like(part)
-    m = PeerMerge(buf, len(ws.tables), table_slices(ws))
+    m = PeerMerge(buf, len(ws.tables), table_slices(ws), mode=mode)
     outs = []
     for _ in range(2):   # two steps: zero + barrier, per-table pushes (as the fused scan does), finish
         m.zero_()
         buf.copy_(part)
         for t in ws.tables:
             if t.name in m.slices:
-                src, dsts = m.push_for(t.name)
-                _fake_push(src, dsts)
+                _fake_push(*m.push_for(t.name))
         m.finish()
         outs.append(buf.clone())
     if rank == 0:
@@ -281,15 +302,16 @@ def _worker_peer(rank, world, port, cfg, root, out_path):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("mode", ["all", "owner"])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("cfg", [("c1", {"scale": 0.2}), ("c5", {"scale": 5e-5, "w": 64, "wm": 32})])
-def test_peer_merge_host_logic_equals_single_build(cfg, world, tmp_path):
+def test_peer_merge_host_logic_equals_single_build(cfg, world, mode, tmp_path):
     """Every rank's merged buffer after the pushes == the single-process build, two steps in a
     row (the merged buffers are re-zeroed behind a barrier)."""
     import datagen
     out = str(tmp_path / "peer.pt")
-    mp.start_processes(_worker_peer, args=(world, _free_port(), cfg, str(tmp_path), out), nprocs=world, join=True,
-                       start_method="spawn")
+    mp.start_processes(_worker_peer, args=(world, _free_port(), cfg, str(tmp_path), out, mode), nprocs=world,
+                       join=True, start_method="spawn")
     outs = torch.load(out)
     ws = getattr(datagen, cfg[0])(**cfg[1])
     full, _ = _build_packed(ws, 0, 1)

@@ -159,7 +159,7 @@ def test_peer_push_histogram_epilogue_not_fused():
     merged.close()
 
 
-def _worker(rank, world, port, cfg, out_path):
+def _worker(rank, world, port, cfg, out_path, mode):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     gpu = rank if torch.cuda.device_count() >= world else 0
     torch.cuda.set_device(gpu)
@@ -168,7 +168,8 @@ def _worker(rank, world, port, cfg, out_path):
     import datagen
     from paper_2102_02440_b200.query import QueryRun
     ws = getattr(datagen, cfg[0])(**cfg[1])
-    run = QueryRun(ws, dev, merge="peer")
+    run = QueryRun(ws, dev, merge="peer", peer_mode=mode)
+    assert run.merge.mode == mode
     data = {t.name: datagen.generate_table(ws, t.name, dev, rank=rank, world=world) for t in ws.tables}
     bufs = []
     for _ in range(2):   # two steps: zero + barrier, fused scans + pushes, survivors, barrier
@@ -188,14 +189,17 @@ def _worker(rank, world, port, cfg, out_path):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("world,mode", [(2, "all"), (2, "owner"), (3, "owner")])
 @pytest.mark.parametrize("cfg", [("c5", {"scale": 2e-4, "w": 128, "wm": 64}), ("c4", {"scale": 0.002})])
-def test_peer_merge_two_ranks(cfg, tmp_path):
-    """Two ranks (two GPUs, or two processes on the pool's one GPU): each builds its row shard
-    and pushes into both merged buffers; both equal the oracle's full build, plans agree."""
+def test_peer_merge_ranks(cfg, world, mode, tmp_path):
+    """Two or three ranks (one GPU each, or processes sharing the pool's one GPU): each builds
+    its row shard and pushes into every merged buffer ("all") or into the owners' ranges then
+    gathers ("owner", reduce-scatter + all-gather over peer memory); every merged buffer equals
+    the oracle's full build, plans agree."""
     import datagen
-    world = 2
     out = str(tmp_path / "peer.pt")
-    mp.start_processes(_worker, args=(world, _free_port(), cfg, out), nprocs=world, join=True, start_method="spawn")
+    mp.start_processes(_worker, args=(world, _free_port(), cfg, out, mode), nprocs=world, join=True,
+                       start_method="spawn")
     res = torch.load(out)
     ref = _oracle_packed(getattr(datagen, cfg[0])(**cfg[1]))
     for r in res:
